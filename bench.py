@@ -1,0 +1,486 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 hot path (BASELINE.json metric: orderings simulated
+per second at N=10/12, heuristic TG decisions per second).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
+
+Headline workload (BASELINE config 4): one 12-task group (the reference's
+sample_real_tasks("AMD", 12, seed=12), 2-DMA, sigma 0.5); one step = the
+exhaustive search of all 12! = 479,001,600 orderings -> best makespan,
+lowest-rank argmin, worst, mean, geomean.  With N ranks the Lehmer-rank
+space is sharded contiguously and the 48-byte per-rank summaries are
+combined by one NCCL all_gather inside the step (strong scaling).
+
+`value` times the device-resident path (osim_exhaustive_dev: inputs in HBM,
+CUDA events on the launching stream, L2 flushed between steps and excluded).
+`e2e` times the public host API (exhaustive_summary_durs /
+dist.exhaustive_summary_distributed): host buffers, H2D + kernels + D2H +
+combine per step.  `secondary` holds configs 3 (N=10), 2 (100k x 8! batch)
+and 5 (10^6 x 16-task heuristic, three device profiles).
+`--impl reference` times the CPU restatement of the reference algorithm
+(oracle/, the reference itself is pure Python and not buildable) on all host
+cores on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N12 = 12
+TOTAL12 = math.factorial(12)
+SIGMA = 0.5
+DMA = 2
+WORKLOAD = ("C4: one 12-task TG (reference sample_real_tasks('AMD', 12, seed=12)), 2-DMA, sigma 0.5; "
+            "exhaustive search of all 12! = 479001600 orderings -> best/argmin/worst/mean/geomean")
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def op_counts():
+    with open(os.path.join(ROOT, "tests", "golden", "op_counts.json")) as fh:
+        return json.load(fh)
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampled every 100 ms while the timed region runs."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append((float(f[1]), float(f[2]), f[5], f[6], f[7], f[8]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- helpers
+class Dist:
+    def __init__(self, gpus):
+        self.world = env_int("WORLD_SIZE", 1)
+        self.rank = env_int("RANK", 0)
+        self.local = env_int("LOCAL_RANK", 0)
+        self.pg = None
+        if gpus != self.world and self.world > 1:
+            print(f"warning: --gpus {gpus} but WORLD_SIZE={self.world}", file=sys.stderr)
+
+    def init(self):
+        import torch
+
+        torch.cuda.set_device(self.local)
+        if self.world > 1:
+            import torch.distributed as tdist
+
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.pg = tdist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t)
+        return float(t.item())
+
+
+def timed_steps(step, K, W, flush, sync):
+    """W untimed warm-ups, then K steps each bracketed by CUDA events on
+    the current stream; L2 flushed before every step (not timed)."""
+    import torch
+
+    for _ in range(W):
+        step()
+    sync()
+    evs = []
+    for _ in range(K):
+        flush()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record()
+        step(e[1])
+        e[2].record()
+        evs.append(e)
+    torch.cuda.synchronize()
+    kern = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3
+    total = sum(e[0].elapsed_time(e[2]) for e in evs) / 1e3
+    return total, kern
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(a):
+    import ctypes as C
+
+    import torch
+
+    from paper_1806_10113_b200 import _capi, dist as odist, search, synth
+
+    D = Dist(a.gpus)
+    D.init()
+    _capi.set_device(D.local)
+    L = _capi.load()
+    dev = torch.device("cuda", D.local)
+    stream = torch.cuda.current_stream()
+    sp = C.c_void_p(stream.cuda_stream)
+    flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def flush():
+        flush_buf.zero_()
+
+    ops = op_counts()
+    peak_tflops = _capi.fp64_peak_tflops()  # DFMA: 2 flops/instruction
+    peak_ops = peak_tflops / 2.0  # FP64 pipe instructions/s (T/s)
+
+    # ---- headline: C4 ------------------------------------------------------
+    durs = synth.c4_group()
+    fast = int(_capi.fast_eligible(durs, SIGMA))
+    d_durs = torch.from_numpy(durs).to(dev)
+    d_out = torch.zeros(6, dtype=torch.float64, device=dev)
+    gathered = [torch.zeros(6, dtype=torch.float64, device=dev) for _ in range(D.world)]
+    lo, hi = odist.shard(TOTAL12, D.rank, D.world)
+    launches_per_step = 2  # exhaustive kernel + final reduce
+
+    def step(ev_kernel_done=None):
+        _capi.check(L.osim_exhaustive_dev(C.c_void_p(d_durs.data_ptr()), N12, DMA, SIGMA, lo, hi, fast,
+                                          C.c_void_p(d_out.data_ptr()), None, sp))
+        if ev_kernel_done is not None:
+            ev_kernel_done.record()
+        if D.pg:
+            D.pg.all_gather(gathered, d_out)
+
+    D.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(D.local) as clk:
+        t_total, t_kern = timed_steps(step, a.steps, a.warmup, flush, torch.cuda.synchronize)
+    D.barrier()
+    torch.cuda.synchronize()
+    t_max = D.max(t_total)
+    value = TOTAL12 * a.steps / t_max
+    parts = [odist.unpack(g.cpu().numpy()) for g in gathered] if D.pg else [odist.unpack(d_out.cpu().numpy())]
+    res = search.summary_from_dict(odist.combine(parts), N12)
+    assert res.count == TOTAL12, res
+
+    ops_per = ops[f"c4_sigma{SIGMA}"]["ops"]
+    kern_avg = t_kern / a.steps
+    achieved = ops_per * (hi - lo) / kern_avg / 1e12
+    roof = {"bound": "fp64", "achieved": achieved, "peak": peak_ops, "unit": "TFLOP/s", "frac": achieved / peak_ops,
+            "traffic": profile_traffic(),
+            "definition": ("algorithmic FP64 ops per ordering (S+8R+2O = %.1f, tests/golden/op_counts.json, "
+                           "DDIV counted as one op) x orderings per launch / CUDA-event launch time; peak = "
+                           "measured DFMA instructions/s of this GPU (osim_fp64_peak, %.2f TFLOP/s at 2 "
+                           "flops/DFMA), i.e. FP64-pipe issue capacity in ops/s" % (ops_per, peak_tflops)),
+            "kernel": "k_exhaustive_fast<12,2>", "launch_ms": kern_avg * 1e3}
+
+    # ---- e2e through the public API (host buffers) ---------------------------
+    e2e_steps = max(3, a.steps // 2)
+    D.barrier()
+
+    def e2e_call():
+        if D.pg:
+            return odist.exhaustive_summary_distributed(durs, DMA, SIGMA)
+        return search.exhaustive_summary_durs(durs, DMA, SIGMA)
+
+    e2e_call()
+    torch.cuda.synchronize()
+    D.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        r = e2e_call()
+    t_e2e = D.max(time.perf_counter() - t0)
+    assert r.best == res.best and r.best_rank == res.best_rank
+    e2e = {"value": TOTAL12 * e2e_steps / t_e2e, "unit": "orderings/s",
+           "h2d_bytes_per_step": durs.nbytes + (48 if D.pg else 0),
+           "d2h_bytes_per_step": 48 + (48 * D.world if D.pg else 0),
+           "api": "search.exhaustive_summary_durs" if not D.pg else "dist.exhaustive_summary_distributed",
+           "steps": e2e_steps}
+
+    secondary = {} if a.no_secondary else run_secondary(a, D, torch, dev, sp, flush, ops, peak_ops, L)
+
+    cpu = None
+    if D.rank == 0 and D.world == 1 and not a.no_cpu:
+        cpu = cpu_baseline(a.cpu_seconds)
+
+    if D.rank == 0:
+        line = {
+            "metric": "orderings simulated/sec", "value": value, "unit": "orderings/s", "n_gpus": D.world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": t_max / a.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "orderings_per_step": TOTAL12, "n_tasks": N12,
+                       "parallelism": f"Lehmer-rank shards x{D.world}" + (" + NCCL all_gather of 48-B summaries"
+                                                                          if D.pg else ""),
+                       "l2": "256 MiB buffer zeroed before every timed step (excluded from timing); inputs 288 B",
+                       "fast_path": bool(fast)},
+            "result": {"best": res.best, "best_rank": res.best_rank, "best_ordering": list(res.best_ordering),
+                       "worst": res.worst, "mean": res.mean, "geomean": res.geomean},
+            "roofline": roof, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches_per_step * a.steps,
+            "secondary": secondary,
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if D.pg:
+        D.pg.barrier()
+        D.pg.destroy_process_group()
+
+
+def profile_traffic():
+    """dram read+write bytes per launch of the headline kernel from the
+    committed ncu capture summary, if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_headline.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def run_secondary(a, D, torch, dev, sp, flush, ops, peak_ops, L):
+    import ctypes as C
+
+    from paper_1806_10113_b200 import _capi, dist as odist, synth
+
+    out = {}
+    K, W = 3, 1
+    sync = torch.cuda.synchronize
+
+    # C3: one 10-task group, 10! orderings (strong over ranks)
+    d3 = torch.from_numpy(synth.c3_group()).to(dev)
+    o3 = torch.zeros(6, dtype=torch.float64, device=dev)
+    t10 = math.factorial(10)
+    lo, hi = odist.shard(t10, D.rank, D.world)
+    g3 = [torch.zeros(6, dtype=torch.float64, device=dev) for _ in range(D.world)]
+    reps = 20  # one step = 20 back-to-back searches (a single one is ~0.2 ms)
+
+    def s3(ev=None):
+        for _ in range(reps):
+            _capi.check(L.osim_exhaustive_dev(C.c_void_p(d3.data_ptr()), 10, 2, 0.5, lo, hi, 1,
+                                              C.c_void_p(o3.data_ptr()), None, sp))
+        if ev is not None:
+            ev.record()
+        if D.pg:
+            D.pg.all_gather(g3, o3)
+
+    t, tk = timed_steps(s3, K, W, flush, sync)
+    t = D.max(t)
+    out["c3_orderings_per_s"] = {"value": t10 * reps * K / t, "unit": "orderings/s",
+                                 "workload": "C3: K20 seed 10, 10 tasks, 10! orderings x20 per step",
+                                 "frac_fp64": ops["c3"]["ops"] * (hi - lo) * reps * K / tk / 1e12 / peak_ops}
+
+    # C2: 100k x 8-task groups, 8! each (group-range shards, no collective)
+    B2 = 100_000
+    lo2, hi2 = odist.shard(B2, D.rank, D.world)
+    d2 = torch.from_numpy(synth.c2_batch(B2)[lo2:hi2].copy()).to(dev)
+    o2 = torch.zeros((hi2 - lo2) * 6, dtype=torch.float64, device=dev)
+
+    def s2(ev=None):
+        _capi.check(L.osim_exhaustive_batch_dev(C.c_void_p(d2.data_ptr()), hi2 - lo2, 8, 2, 0.5, 1,
+                                                C.c_void_p(o2.data_ptr()), sp))
+        if ev is not None:
+            ev.record()
+
+    t, tk = timed_steps(s2, K, W, flush, sync)
+    t = D.max(t)
+    out["c2_orderings_per_s"] = {"value": B2 * 40320 * K / t, "unit": "orderings/s",
+                                 "workload": "C2: 100000 x 8-task TGs (Table-2 x U(0.5,1.5)), 8! each, 2-DMA 0.5",
+                                 "frac_fp64": ops["c2"]["ops"] * (hi2 - lo2) * 40320 * K / tk / 1e12 / peak_ops}
+    del d2, o2
+
+    # C5: 10^6 x 16-task groups through the heuristic, three device profiles
+    B5 = 1_000_000
+    lo5, hi5 = odist.shard(B5, D.rank, D.world)
+    m = hi5 - lo5
+    for prof, (_, dma, sigma) in synth.PROFILES.items():
+        dh, rh = synth.c5_batch_fast(prof, B5)
+        dd = torch.from_numpy(dh[lo5:hi5].copy()).to(dev)
+        rr = torch.from_numpy(rh[lo5:hi5].copy()).to(dev)
+        oo = torch.empty((m, 16), dtype=torch.uint8, device=dev)
+        mm = torch.empty(m, dtype=torch.float64, device=dev)
+        ns = torch.empty(m, dtype=torch.int32, device=dev)
+
+        def s5(ev=None):
+            _capi.check(L.osim_heuristic_batch_dev(C.c_void_p(dd.data_ptr()), C.c_void_p(rr.data_ptr()), m, 16,
+                                                   dma, sigma, 1 if sys.version_info >= (3, 12) else 0, 1,
+                                                   C.c_void_p(oo.data_ptr()), C.c_void_p(mm.data_ptr()),
+                                                   C.c_void_p(ns.data_ptr()), sp))
+            if ev is not None:
+                ev.record()
+
+        t, tk = timed_steps(s5, K, W, flush, sync)
+        t = D.max(t)
+        out[f"c5_{prof}_decisions_per_s"] = {
+            "value": B5 * K / t, "unit": "TG decisions/s",
+            "workload": f"C5: 10^6 x 16-task TGs, {prof}-style ({dma}-DMA, sigma {sigma}), reorder_batch",
+            "frac_fp64": ops[f"c5_{prof}"]["ops"] * m * K / tk / 1e12 / peak_ops}
+        if prof == "nvidia" and D.world == 1:
+            # e2e through the public array API with host buffers (pinned)
+            pd = torch.from_numpy(dh).pin_memory()
+            pr = torch.from_numpy(rh).pin_memory()
+            po = torch.empty((B5, 16), dtype=torch.uint8).pin_memory()
+            pm = torch.empty(B5, dtype=torch.float64).pin_memory()
+            pn = torch.empty(B5, dtype=torch.int32).pin_memory()
+            args = (pd.numpy(), pr.numpy(), dma, sigma, 1 if sys.version_info >= (3, 12) else 0)
+            _capi.heuristic_batch(*args, order=po.numpy(), makespan=pm.numpy(), n_sims=pn.numpy().view(np.uint32))
+            t0 = time.perf_counter()
+            for _ in range(K):
+                _capi.heuristic_batch(*args, order=po.numpy(), makespan=pm.numpy(),
+                                      n_sims=pn.numpy().view(np.uint32))
+            te = time.perf_counter() - t0
+            out["c5_nvidia_decisions_per_s"]["e2e"] = {
+                "value": B5 * K / te, "unit": "TG decisions/s", "api": "_capi.heuristic_batch (pinned host buffers)",
+                "h2d_bytes_per_step": dh.nbytes + rh.nbytes, "d2h_bytes_per_step": B5 * (16 + 8 + 4)}
+        del dd, rr, oo, mm, ns
+    return out
+
+
+# ---------------------------------------------------------------- CPU legs
+def cpu_rate(seconds):
+    """CPU restatement (oracle/, all host threads) on contiguous C4 ranks,
+    sized to ~`seconds` of wall time."""
+    from oracle import oracle as O
+    from paper_1806_10113_b200 import synth
+
+    threads = os.cpu_count() or 1
+    d = synth.c4_group()
+    probe = 2000 * threads
+    t0 = time.perf_counter()
+    O.exhaustive(d, DMA, SIGMA, 0, probe, threads=threads)
+    rate = probe / (time.perf_counter() - t0)
+    m = int(max(probe, min(TOTAL12 // 2, rate * seconds)))
+    start = TOTAL12 // 3  # a mid-space window
+    t0 = time.perf_counter()
+    O.exhaustive(d, DMA, SIGMA, start, start + m, threads=threads)
+    el = time.perf_counter() - t0
+    return m / el, threads, m, start
+
+
+def cpu_baseline(seconds):
+    v, threads, m, start = cpu_rate(seconds)
+    return {"value": v, "unit": "orderings/s", "cores": threads, "kind": "port",
+            "sample": f"C4 ranks [{start}, {start + m}) ({m} of 12! orderings) through oracle/osim_oracle.c "
+                      f"(C restatement of engine.py/oracle.py; the reference is pure Python) on {threads} threads"}
+
+
+def run_reference(a):
+    if env_int("RANK", 0) != 0:
+        return
+    from oracle import oracle as O
+    from paper_1806_10113_b200 import synth
+
+    threads = os.cpu_count() or 1
+    d = synth.c4_group()
+    v, _, m, start = cpu_rate(2.0)  # calibrate: each step ~2 s of wall time
+    for _ in range(a.warmup):
+        O.exhaustive(d, DMA, SIGMA, start, start + m // 4, threads=threads)
+    t0 = time.perf_counter()
+    for k in range(a.steps):
+        lo = start + k * m
+        O.exhaustive(d, DMA, SIGMA, lo, lo + m, threads=threads)
+    el = time.perf_counter() - t0
+    value = m * a.steps / el
+    sample = (f"C4 ranks [{start}, {start + m * a.steps}) in {a.steps} steps of {m} orderings through "
+              f"oracle/osim_oracle.c on {threads} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": "orderings simulated/sec", "value": value, "unit": "orderings/s",
+        "n_gpus": env_int("WORLD_SIZE", 1), "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": el / a.steps * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "orderings_per_step": m, "n_tasks": N12},
+        "cpu_baseline": {"value": value, "unit": "orderings/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "orderings/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    a = ap.parse_args()
+    if a.warmup < 3:
+        print("note: --warmup raised to 3 (timing rules)", file=sys.stderr)
+        a.warmup = 3
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,132 @@
+/*
+ * offsim_b200.h -- C ABI of liboffsim_b200.so, the B200 (sm_100a) hot path
+ * of the temporal execution model of arXiv 1806.10113.
+ *
+ * The reference (`offsim`, /root/reference/pkg/src/offsim) is a pure-Python
+ * package with no FFI; its public hot-path surface is three functions,
+ * and each entry point below replaces the inner loop of one of them:
+ *
+ *   engine.simulate(tasks, profile)            engine.py:252-263
+ *       -> osim_timeline           (one ordered group, full timeline)
+ *   oracle.exhaustive_search(tasks, profile, cap, seed)   oracle.py:111-136
+ *       -> osim_exhaustive         (every ordering: Lehmer ranks [lo, hi))
+ *       -> osim_eval_perms         (sampled mode: explicit orderings,
+ *                                   oracle.py:98-108,127-129)
+ *       -> osim_exhaustive_batch   (many independent groups, one summary each)
+ *   heuristic.reorder_batch(tg, profile)       heuristic.py:105-125
+ *       -> osim_heuristic_batch    (Algorithm 1 over many groups)
+ *
+ * The summary replaces make_report's reductions (oracle.py:41-57):
+ * best = ms.min(), best_rank = np.argmin(ms) (first of ties = lowest rank),
+ * worst = ms.max(), sum -> mean, sum_log -> geomean = exp(sum_log / count).
+ * The median needs the makespans (pass a `makespans` buffer).
+ *
+ * Durations are the resolved stage times (model.stage_times, model.py:139-160)
+ * of each task as float64 (t_htd, t_k, t_dth) in ms, task-major [n][3];
+ * a stage <= 0 is null (no command, engine.py:129-151).  `dma` is
+ * DeviceProfile.dma_engines (1 or 2), `sigma` its overlap_sigma in (0, 1].
+ * Orderings are task indices 0..n-1 (n <= 16).
+ *
+ * Conventions: every function returns 0 on success or a negative OSIM_E*
+ * code; osim_last_error() gives a thread-local message.  Host buffers are
+ * caller-owned, C-contiguous, used only during the call, never retained.
+ * Device memory and streams are library-owned.  Calls are reentrant
+ * (per-device mutex).  `_dev` variants take device pointers on the calling
+ * thread's current library device, enqueue on `stream` (NULL = the
+ * library's stream) and do not synchronize.
+ */
+#ifndef OFFSIM_B200_H
+#define OFFSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OSIM_OK 0
+#define OSIM_EINVAL (-1)  /* ValueError / UnresolvableDuration in the reference */
+#define OSIM_ENODEV (-2)  /* no CUDA device */
+#define OSIM_ECUDA (-3)   /* CUDA runtime error */
+#define OSIM_ENCCL (-4)   /* reserved: collective failure */
+#define OSIM_ESTALL (-5)  /* "simulation stalled with commands pending", engine.py:239-241 */
+
+/* make_report reduction state (48 bytes). */
+typedef struct {
+    double best;
+    uint64_t best_rank; /* index of the first minimum within the evaluated set */
+    double worst;
+    double sum;
+    double sum_log;
+    uint64_t count;
+} osim_summary;
+
+/* Library version string. */
+const char* osim_version(void);
+/* Thread-local message for the last non-zero return on this thread. */
+const char* osim_last_error(void);
+
+/* Open up to `want_devices` CUDA devices (<= 0: all); *got = opened. */
+int osim_init(int want_devices, int* got);
+int osim_shutdown(void);
+/* Select the library device used by this thread for n_dev <= 1 calls and
+ * for the _dev variants (one process per GPU: pass LOCAL_RANK). */
+int osim_set_device(int device);
+
+/* exhaustive_search's simulate-and-reduce loop (oracle.py:123-135) over
+ * lexicographic ranks [rank_lo, rank_hi) of range(n)'s permutations,
+ * sharded over n_dev devices (<= 1: the current device).  `makespans`
+ * (nullable) receives hi-lo values in rank order. */
+int osim_exhaustive(const double* durs, int n, int dma, double sigma, uint64_t rank_lo,
+                    uint64_t rank_hi, int n_dev, osim_summary* out, double* makespans);
+
+/* Sampled mode: evaluate `cnt` explicit orderings perms[cnt][n]; best_rank
+ * is the index in the list (np.argmin over the sample, oracle.py:47). */
+int osim_eval_perms(const double* durs, int n, int dma, double sigma, const uint8_t* perms,
+                    uint64_t cnt, int n_dev, double* makespans, osim_summary* out);
+
+/* B independent groups durs[B][n][3], all n! orderings each; out[B]. */
+int osim_exhaustive_batch(const double* durs, uint64_t B, int n, int dma, double sigma, int n_dev,
+                          osim_summary* out);
+
+/* reorder_batch (heuristic.py:105-125) for B groups.  id_rank[B][n]: the
+ * position of each task in Python's sorted() order of the ids (the
+ * tie-break of heuristic.py:18-19,29,74).  sum_mode: 1 = CPython >= 3.12
+ * builtin sum (Neumaier), 0 = <= 3.11 naive (heuristic.py:47).
+ * order[B][n] receives the chosen orderings, makespan[B] the simulated
+ * makespan of each, n_sims[B] (nullable) the simulate() calls made. */
+int osim_heuristic_batch(const double* durs, const uint8_t* id_rank, uint64_t B, int n, int dma,
+                         double sigma, int sum_mode, int n_dev, uint8_t* order, double* makespan,
+                         uint32_t* n_sims);
+
+/* engine.simulate for one ordering: start/end[n][3] by task index
+ * (-1 = null stage), makespan, idle[3] = idle_report (HtD, K, DtH). */
+int osim_timeline(const double* durs, int n, int dma, double sigma, const uint8_t* order,
+                  double* start, double* end, double* makespan, double* idle);
+
+/* ---- device-resident variants (inputs already in HBM) ---------------- */
+/* fast = 1 asserts every stage is non-null and every duration and sigma
+ * lies in [2^-60, 2^60] (osim_fast_eligible()); 0 selects the general path. */
+int osim_fast_eligible(const double* durs, uint64_t count /* tasks */, double sigma);
+
+int osim_exhaustive_dev(const double* d_durs, int n, int dma, double sigma, uint64_t rank_lo,
+                        uint64_t rank_hi, int fast, osim_summary* d_out, double* d_makespans,
+                        void* stream);
+int osim_exhaustive_batch_dev(const double* d_durs, uint64_t B, int n, int dma, double sigma,
+                              int fast, osim_summary* d_out, void* stream);
+int osim_heuristic_batch_dev(const double* d_durs, const uint8_t* d_id_rank, uint64_t B, int n,
+                             int dma, double sigma, int sum_mode, int fast, uint8_t* d_order,
+                             double* d_makespan, uint32_t* d_n_sims, void* stream);
+
+/* ---- diagnostics ------------------------------------------------------ */
+/* Compare the fast-path division with IEEE division on `samples` random
+ * operand pairs drawn from the fast-path range; *mismatches = count. */
+int osim_selftest_div(uint64_t samples, uint64_t seed, uint64_t* mismatches);
+/* Measured FP64 FMA-pipe throughput of the current device, TFLOP/s
+ * (2 flops per DFMA). */
+int osim_fp64_peak(double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

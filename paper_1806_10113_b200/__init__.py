@@ -1,0 +1,66 @@
+"""offsim-b200: the B200 (sm_100a) hot path of arXiv 1806.10113's temporal
+execution model, behind the reference package's API (offsim).
+
+Drop-in names (same signatures and semantics as /root/reference's
+offsim/__init__.py:3-55 for the hot path):
+    simulate, exhaustive_search, reorder_batch, select_first_task,
+    select_next_task, select_last_tasks, recompute_overlap, make_report,
+    DeviceProfile, TaskSpec, Command, Timeline, PermutationReport,
+    stage_times, estimate_transfer, estimate_kernel, fit_kernel_model,
+    classify_task
+Batched / summary-mode additions (no reference equivalent; the reference
+only loops in Python):
+    exhaustive_summary, exhaustive_summary_batch, reorder_batch_many,
+    reorder_durs
+Every simulation runs in liboffsim_b200.so; importing the package does not
+load it, the first call does, and fails loudly if it is missing.
+"""
+
+from .engine import KINDS, Command, Timeline, idle_report, recompute_overlap, simulate
+from .heuristic import (
+    SUM_MODE,
+    reorder_batch,
+    reorder_batch_many,
+    reorder_durs,
+    select_first_task,
+    select_last_tasks,
+    select_next_task,
+)
+from .model import (
+    DeviceProfile,
+    Direction,
+    InsufficientSamples,
+    NegativeFitWarning,
+    OffsimError,
+    TaskDominance,
+    TaskSpec,
+    UnresolvableDuration,
+    classify_task,
+    estimate_kernel,
+    estimate_transfer,
+    fit_kernel_model,
+    stage_times,
+)
+from .search import (
+    DEFAULT_CAP,
+    OrderingSummary,
+    PermutationReport,
+    exhaustive_search,
+    exhaustive_summary,
+    exhaustive_summary_batch,
+    exhaustive_summary_durs,
+    make_report,
+    sample_permutations,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Command", "DeviceProfile", "Direction", "InsufficientSamples", "KINDS", "NegativeFitWarning",
+    "OffsimError", "OrderingSummary", "PermutationReport", "SUM_MODE", "TaskDominance", "TaskSpec",
+    "Timeline", "UnresolvableDuration", "classify_task", "DEFAULT_CAP", "estimate_kernel",
+    "estimate_transfer", "exhaustive_search", "exhaustive_summary", "exhaustive_summary_batch",
+    "exhaustive_summary_durs", "fit_kernel_model", "idle_report", "make_report", "recompute_overlap",
+    "reorder_batch", "reorder_batch_many", "reorder_durs", "sample_permutations", "select_first_task",
+    "select_last_tasks", "select_next_task", "simulate", "stage_times",
+]

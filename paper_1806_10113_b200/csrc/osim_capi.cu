@@ -1,0 +1,706 @@
+// osim_capi.cu -- the extern "C" boundary (include/offsim_b200.h): argument
+// validation with the reference's error semantics, device/stream/scratch
+// management, kernel dispatch and multi-device sharding.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "osim_kernels.cuh"
+
+using namespace osim;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_thread_dev = -1;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(OSIM_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_));      \
+    } while (0)
+
+struct DevCtx {
+    int dev = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    int* d_err = nullptr;
+    std::mutex mu;
+};
+
+std::mutex g_init_mu;
+std::vector<DevCtx*> g_devs;
+
+int ensure_init() {
+    std::lock_guard<std::mutex> lk(g_init_mu);
+    if (!g_devs.empty()) return 0;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count <= 0)
+        return fail(OSIM_ENODEV, "no CUDA device available (%s)", cudaGetErrorString(e));
+    for (int d = 0; d < count; ++d) {
+        DevCtx* c = new DevCtx();
+        c->dev = d;
+        CK(cudaSetDevice(d));
+        CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, d));
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaMalloc(&c->d_err, sizeof(int)));
+        CK(cudaMemset(c->d_err, 0, sizeof(int)));
+        g_devs.push_back(c);
+    }
+    return 0;
+}
+
+int cur_dev() {
+    if (g_thread_dev >= 0) return g_thread_dev;
+    int d = 0;
+    cudaGetDevice(&d);
+    return d < (int)g_devs.size() ? d : 0;
+}
+
+// grow-only per-device scratch; caller holds c->mu
+int scratch(DevCtx* c, size_t bytes, void** p) {
+    if (bytes > c->scratch_bytes) {
+        if (c->scratch) cudaFree(c->scratch);
+        c->scratch = nullptr;
+        size_t want = bytes < (1u << 20) ? (1u << 20) : bytes + bytes / 4;
+        CK(cudaMalloc(&c->scratch, want));
+        c->scratch_bytes = want;
+    }
+    *p = c->scratch;
+    return 0;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ---- validation (model.py:63-71, 91-100; engine.py:129-130, 258-259) -----
+int check_common(int n, int dma, double sigma) {
+    if (n < 1) return fail(OSIM_EINVAL, "task group must be non-empty");
+    if (n > kMaxN) return fail(OSIM_EINVAL, "n=%d exceeds the supported maximum of %d tasks", n, kMaxN);
+    if (dma != 1 && dma != 2) return fail(OSIM_EINVAL, "dma_engines must be 1 or 2, got %d", dma);
+    if (!(sigma > 0.0 && sigma <= 1.0)) return fail(OSIM_EINVAL, "overlap_sigma must be in (0, 1]");
+    return 0;
+}
+
+int check_durs(const double* durs, uint64_t tasks) {
+    if (!durs) return fail(OSIM_EINVAL, "durations pointer is NULL");
+    for (uint64_t t = 0; t < tasks; ++t) {
+        const double h = durs[3 * t], k = durs[3 * t + 1], d = durs[3 * t + 2];
+        if (!(h >= 0.0) || !(k >= 0.0) || !(d >= 0.0) || !std::isfinite(h) || !std::isfinite(k) ||
+            !std::isfinite(d))
+            return fail(OSIM_EINVAL, "task %llu: durations must be finite and non-negative",
+                        (unsigned long long)t);
+        if (h <= 0 && k <= 0 && d <= 0)
+            return fail(OSIM_EINVAL, "task %llu has no commands", (unsigned long long)t);
+    }
+    return 0;
+}
+
+uint64_t factorial(int n) {
+    uint64_t f = 1;
+    for (int i = 2; i <= n; ++i) f *= (uint64_t)i;
+    return f;
+}
+
+template <class K>
+int grid_for(K kernel, int threads, size_t smem, const DevCtx* c, uint64_t work_blocks) {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    uint64_t g = (uint64_t)per_sm * c->sms;
+    if (work_blocks < g) g = work_blocks;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+// ---- launchers (stream-ordered, no sync) -------------------------------
+template <int N, int DMA>
+int launch_exh_fast_t(DevCtx* c, cudaStream_t st, const double* d_durs, double sigma, uint64_t lo,
+                      uint64_t hi, Part* parts, int max_parts, double* d_ms, int* grid_out) {
+    auto k = k_exhaustive_fast<N, DMA>;
+    uint64_t blocks = (hi - lo + kBlock - 1) / kBlock;
+    int g = grid_for(k, kBlock, 0, c, blocks);
+    if (g > max_parts) g = max_parts;
+    k<<<g, kBlock, 0, st>>>(d_durs, sigma, lo, hi, parts, d_ms);
+    *grid_out = g;
+    return 0;
+}
+
+template <int DMA>
+int launch_exh_fast(int n, DevCtx* c, cudaStream_t st, const double* d_durs, double sigma,
+                    uint64_t lo, uint64_t hi, Part* parts, int max_parts, double* d_ms, int* g) {
+    switch (n) {
+#define OSIM_CASE(NN) \
+    case NN: return launch_exh_fast_t<NN, DMA>(c, st, d_durs, sigma, lo, hi, parts, max_parts, d_ms, g);
+        OSIM_CASE(1) OSIM_CASE(2) OSIM_CASE(3) OSIM_CASE(4) OSIM_CASE(5) OSIM_CASE(6)
+        OSIM_CASE(7) OSIM_CASE(8) OSIM_CASE(9) OSIM_CASE(10) OSIM_CASE(11) OSIM_CASE(12)
+        OSIM_CASE(13) OSIM_CASE(14) OSIM_CASE(15) OSIM_CASE(16)
+#undef OSIM_CASE
+    }
+    return fail(OSIM_EINVAL, "unsupported n=%d", n);
+}
+
+template <int N, int DMA>
+int launch_batch_fast_t(DevCtx* c, cudaStream_t st, const double* d_durs, uint64_t B, double sigma,
+                        osim_summary* d_out) {
+    auto k = k_exhaustive_batch_fast<N, DMA>;
+    int g = grid_for(k, kBlock, 0, c, B);
+    k<<<g, kBlock, 0, st>>>(d_durs, B, sigma, d_out);
+    return 0;
+}
+
+template <int DMA>
+int launch_batch_fast(int n, DevCtx* c, cudaStream_t st, const double* d_durs, uint64_t B,
+                      double sigma, osim_summary* d_out) {
+    switch (n) {
+#define OSIM_CASE(NN) case NN: return launch_batch_fast_t<NN, DMA>(c, st, d_durs, B, sigma, d_out);
+        OSIM_CASE(1) OSIM_CASE(2) OSIM_CASE(3) OSIM_CASE(4) OSIM_CASE(5) OSIM_CASE(6)
+        OSIM_CASE(7) OSIM_CASE(8) OSIM_CASE(9) OSIM_CASE(10) OSIM_CASE(11) OSIM_CASE(12)
+        OSIM_CASE(13) OSIM_CASE(14) OSIM_CASE(15) OSIM_CASE(16)
+#undef OSIM_CASE
+    }
+    return fail(OSIM_EINVAL, "unsupported n=%d", n);
+}
+
+// Enqueue exhaustive over [lo, hi) and its final reduce into d_out.
+int enqueue_exhaustive(DevCtx* c, cudaStream_t st, const double* d_durs, int n, int dma,
+                       double sigma, uint64_t lo, uint64_t hi, int fast, osim_summary* d_out,
+                       double* d_ms, Part* parts, int max_parts) {
+    int g = 1;
+    int rc = 0;
+    if (hi > lo) {
+        if (fast) {
+            rc = dma == 2 ? launch_exh_fast<2>(n, c, st, d_durs, sigma, lo, hi, parts, max_parts, d_ms, &g)
+                          : launch_exh_fast<1>(n, c, st, d_durs, sigma, lo, hi, parts, max_parts, d_ms, &g);
+        } else {
+            uint64_t blocks = (hi - lo + kBlock - 1) / kBlock;
+            if (dma == 2) {
+                g = grid_for(k_exhaustive_gen<2>, kBlock, 0, c, blocks);
+                if (g > max_parts) g = max_parts;
+                k_exhaustive_gen<2><<<g, kBlock, 0, st>>>(d_durs, n, sigma, lo, hi, parts, d_ms, c->d_err);
+            } else {
+                g = grid_for(k_exhaustive_gen<1>, kBlock, 0, c, blocks);
+                if (g > max_parts) g = max_parts;
+                k_exhaustive_gen<1><<<g, kBlock, 0, st>>>(d_durs, n, sigma, lo, hi, parts, d_ms, c->d_err);
+            }
+        }
+        if (rc) return rc;
+    } else {
+        g = 0;
+    }
+    k_final_reduce<<<1, kBlock, 0, st>>>(parts, g, d_out);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int max_parts_for(const DevCtx* c) { return c->sms * 16; }
+
+int enqueue_batch(DevCtx* c, cudaStream_t st, const double* d_durs, uint64_t B, int n, int dma,
+                  double sigma, int fast, osim_summary* d_out) {
+    if (B == 0) return 0;
+    int rc = 0;
+    if (fast) {
+        rc = dma == 2 ? launch_batch_fast<2>(n, c, st, d_durs, B, sigma, d_out)
+                      : launch_batch_fast<1>(n, c, st, d_durs, B, sigma, d_out);
+    } else if (dma == 2) {
+        int g = grid_for(k_exhaustive_batch_gen<2>, kBlock, 0, c, B);
+        k_exhaustive_batch_gen<2><<<g, kBlock, 0, st>>>(d_durs, B, n, sigma, d_out, c->d_err);
+    } else {
+        int g = grid_for(k_exhaustive_batch_gen<1>, kBlock, 0, c, B);
+        k_exhaustive_batch_gen<1><<<g, kBlock, 0, st>>>(d_durs, B, n, sigma, d_out, c->d_err);
+    }
+    if (rc) return rc;
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int enqueue_heuristic(DevCtx* c, cudaStream_t st, const double* d_durs, const uint8_t* d_idr,
+                      uint64_t B, int n, int dma, double sigma, int sum_mode, int fast,
+                      uint8_t* d_order, double* d_ms, uint32_t* d_ns) {
+    if (B == 0) return 0;
+    const uint64_t grid = (B + kHG - 1) / kHG;
+    if (grid > 0x7fffffffull) return fail(OSIM_EINVAL, "batch too large");
+    const size_t sm = sizeof(HeurShared);
+#define OSIM_HL(D, F) \
+    k_heuristic<D, F><<<(unsigned)grid, kHT, sm, st>>>(d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms, d_ns, c->d_err)
+    if (dma == 2) { if (fast) OSIM_HL(2, true); else OSIM_HL(2, false); }
+    else { if (fast) OSIM_HL(1, true); else OSIM_HL(1, false); }
+#undef OSIM_HL
+    CK(cudaGetLastError());
+    return 0;
+}
+
+// Sync the device's stream and surface a kernel-side stall flag.
+int finish(DevCtx* c, cudaStream_t st) {
+    CK(cudaStreamSynchronize(st));
+    int h_err = 0;
+    CK(cudaMemcpy(&h_err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (h_err) {
+        CK(cudaMemset(c->d_err, 0, sizeof(int)));
+        return fail(h_err, "simulation stalled with commands pending");
+    }
+    return 0;
+}
+
+bool fast_ok(const double* durs, uint64_t tasks, double sigma) {
+    const double lo = std::ldexp(1.0, -60), hi = std::ldexp(1.0, 60);
+    if (!(sigma >= lo)) return false;
+    for (uint64_t i = 0; i < 3 * tasks; ++i)
+        if (!(durs[i] >= lo && durs[i] <= hi)) return false;
+    return true;
+}
+
+void merge_host(osim_summary& a, const osim_summary& b) {
+    if (b.count == 0) return;
+    if (a.count == 0) { a = b; return; }
+    if (b.best < a.best || (b.best == a.best && b.best_rank < a.best_rank)) {
+        a.best = b.best;
+        a.best_rank = b.best_rank;
+    }
+    if (b.worst > a.worst) a.worst = b.worst;
+    a.sum += b.sum;
+    a.sum_log += b.sum_log;
+    a.count += b.count;
+}
+
+struct DevList {
+    std::vector<DevCtx*> v;
+};
+
+int pick_devs(int n_dev, DevList& out) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (n_dev <= 1) {
+        int d = cur_dev();
+        if (d < 0 || d >= (int)g_devs.size()) return fail(OSIM_ENODEV, "device %d not available", d);
+        out.v.push_back(g_devs[d]);
+        return 0;
+    }
+    if (n_dev > (int)g_devs.size())
+        return fail(OSIM_ENODEV, "requested %d devices, %d available", n_dev, (int)g_devs.size());
+    for (int d = 0; d < n_dev; ++d) out.v.push_back(g_devs[d]);
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* osim_version(void) { return "offsim-b200 0.1.0 (sm_100a)"; }
+const char* osim_last_error(void) { return g_err.c_str(); }
+
+int osim_init(int want_devices, int* got) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    int n = (int)g_devs.size();
+    if (want_devices > 0 && want_devices < n) n = want_devices;
+    if (got) *got = n;
+    return 0;
+}
+
+int osim_shutdown(void) {
+    std::lock_guard<std::mutex> lk(g_init_mu);
+    for (DevCtx* c : g_devs) {
+        cudaSetDevice(c->dev);
+        if (c->scratch) cudaFree(c->scratch);
+        if (c->d_err) cudaFree(c->d_err);
+        if (c->stream) cudaStreamDestroy(c->stream);
+        delete c;
+    }
+    g_devs.clear();
+    return 0;
+}
+
+int osim_set_device(int device) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (device < 0 || device >= (int)g_devs.size())
+        return fail(OSIM_ENODEV, "device %d not available (%d visible)", device, (int)g_devs.size());
+    g_thread_dev = device;
+    CK(cudaSetDevice(device));
+    return 0;
+}
+
+int osim_fast_eligible(const double* durs, uint64_t count, double sigma) {
+    if (!durs) return 0;
+    return fast_ok(durs, count, sigma) ? 1 : 0;
+}
+
+int osim_exhaustive(const double* durs, int n, int dma, double sigma, uint64_t rank_lo,
+                    uint64_t rank_hi, int n_dev, osim_summary* out, double* makespans) {
+    int rc = check_common(n, dma, sigma);
+    if (rc) return rc;
+    if (n > 20) return fail(OSIM_EINVAL, "n too large for 64-bit ranks");
+    if ((rc = check_durs(durs, (uint64_t)n))) return rc;
+    if (!out) return fail(OSIM_EINVAL, "out is NULL");
+    const uint64_t total = factorial(n);
+    if (rank_lo > rank_hi || rank_hi > total)
+        return fail(OSIM_EINVAL, "rank range [%llu, %llu) outside [0, %llu)", (unsigned long long)rank_lo,
+                    (unsigned long long)rank_hi, (unsigned long long)total);
+    DevList dl;
+    if ((rc = pick_devs(n_dev, dl))) return rc;
+    const int fast = fast_ok(durs, n, sigma);
+    const int G = (int)dl.v.size();
+    const uint64_t span = rank_hi - rank_lo;
+    std::vector<osim_summary> res(G);
+    std::vector<std::unique_lock<std::mutex>> locks;
+    // enqueue on every device, then collect in device order
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        locks.emplace_back(c->mu);
+        CK(cudaSetDevice(c->dev));
+        const uint64_t lo = rank_lo + span * (uint64_t)gi / (uint64_t)G;
+        const uint64_t hi = rank_lo + span * (uint64_t)(gi + 1) / (uint64_t)G;
+        const int mp = max_parts_for(c);
+        size_t off_parts = align_up(3 * kMaxN * sizeof(double));
+        size_t off_sum = off_parts + align_up(mp * sizeof(Part));
+        size_t off_ms = off_sum + align_up(sizeof(osim_summary));
+        size_t bytes = off_ms + (makespans ? align_up((hi - lo) * sizeof(double)) : 0);
+        void* base;
+        if ((rc = scratch(c, bytes, &base))) return rc;
+        char* b = (char*)base;
+        CK(cudaMemcpyAsync(b, durs, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        double* d_ms = makespans ? (double*)(b + off_ms) : nullptr;
+        rc = enqueue_exhaustive(c, c->stream, (double*)b, n, dma, sigma, lo, hi, fast,
+                                (osim_summary*)(b + off_sum), d_ms, (Part*)(b + off_parts), mp);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(&res[gi], b + off_sum, sizeof(osim_summary), cudaMemcpyDeviceToHost, c->stream));
+        if (makespans)
+            CK(cudaMemcpyAsync(makespans + (lo - rank_lo), d_ms, (hi - lo) * sizeof(double),
+                               cudaMemcpyDeviceToHost, c->stream));
+    }
+    osim_summary acc;
+    memset(&acc, 0, sizeof(acc));
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        CK(cudaSetDevice(c->dev));
+        if ((rc = finish(c, c->stream))) return rc;
+        merge_host(acc, res[gi]);
+    }
+    *out = acc;
+    return 0;
+}
+
+int osim_exhaustive_dev(const double* d_durs, int n, int dma, double sigma, uint64_t rank_lo,
+                        uint64_t rank_hi, int fast, osim_summary* d_out, double* d_makespans,
+                        void* stream) {
+    int rc = check_common(n, dma, sigma);
+    if (rc) return rc;
+    if (rank_lo > rank_hi || rank_hi > factorial(n)) return fail(OSIM_EINVAL, "bad rank range");
+    DevList dl;
+    if ((rc = pick_devs(1, dl))) return rc;
+    DevCtx* c = dl.v[0];
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+    const int mp = max_parts_for(c);
+    void* base;
+    if ((rc = scratch(c, align_up(mp * sizeof(Part)), &base))) return rc;
+    return enqueue_exhaustive(c, st, d_durs, n, dma, sigma, rank_lo, rank_hi, fast, d_out,
+                              d_makespans, (Part*)base, mp);
+}
+
+int osim_eval_perms(const double* durs, int n, int dma, double sigma, const uint8_t* perms,
+                    uint64_t cnt, int n_dev, double* makespans, osim_summary* out) {
+    int rc = check_common(n, dma, sigma);
+    if (rc) return rc;
+    if ((rc = check_durs(durs, (uint64_t)n))) return rc;
+    if (!perms && cnt) return fail(OSIM_EINVAL, "perms is NULL");
+    if (!makespans && cnt) return fail(OSIM_EINVAL, "makespans is NULL");
+    for (uint64_t i = 0; i < cnt; ++i) {  // each row must be a permutation of range(n)
+        unsigned seen = 0;
+        for (int j = 0; j < n; ++j) {
+            const unsigned v = perms[i * n + j];
+            if (v >= (unsigned)n || ((seen >> v) & 1u))
+                return fail(OSIM_EINVAL, "row %llu is not a permutation of range(%d)", (unsigned long long)i, n);
+            seen |= 1u << v;
+        }
+    }
+    DevList dl;
+    if ((rc = pick_devs(n_dev, dl))) return rc;
+    const int fast = fast_ok(durs, n, sigma);
+    const int G = (int)dl.v.size();
+    std::vector<osim_summary> res(G);
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        locks.emplace_back(c->mu);
+        CK(cudaSetDevice(c->dev));
+        const uint64_t lo = cnt * (uint64_t)gi / (uint64_t)G, hi = cnt * (uint64_t)(gi + 1) / (uint64_t)G;
+        const uint64_t m = hi - lo;
+        const int mp = max_parts_for(c);
+        size_t off_parts = align_up(3 * kMaxN * sizeof(double));
+        size_t off_sum = off_parts + align_up(mp * sizeof(Part));
+        size_t off_ms = off_sum + align_up(sizeof(osim_summary));
+        size_t off_p = off_ms + align_up(m * sizeof(double) + 8);
+        size_t bytes = off_p + align_up(m * n + 8);
+        void* base;
+        if ((rc = scratch(c, bytes, &base))) return rc;
+        char* b = (char*)base;
+        CK(cudaMemcpyAsync(b, durs, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        if (m) CK(cudaMemcpyAsync(b + off_p, perms + lo * n, m * n, cudaMemcpyHostToDevice, c->stream));
+        Part* parts = (Part*)(b + off_parts);
+        int g = 0;
+        if (m) {
+            const uint64_t blocks = (m + kBlock - 1) / kBlock;
+#define OSIM_EP(D, F)                                                                            \
+    do {                                                                                         \
+        g = grid_for(k_eval_perms<D, F>, kBlock, 0, c, blocks);                                  \
+        if (g > mp) g = mp;                                                                      \
+        k_eval_perms<D, F><<<g, kBlock, 0, c->stream>>>((double*)b, n, sigma, (uint8_t*)(b + off_p), m, \
+                                                         (double*)(b + off_ms), parts, c->d_err); \
+    } while (0)
+            if (dma == 2) { if (fast) OSIM_EP(2, true); else OSIM_EP(2, false); }
+            else { if (fast) OSIM_EP(1, true); else OSIM_EP(1, false); }
+#undef OSIM_EP
+        }
+        k_final_reduce<<<1, kBlock, 0, c->stream>>>(parts, g, (osim_summary*)(b + off_sum));
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&res[gi], b + off_sum, sizeof(osim_summary), cudaMemcpyDeviceToHost, c->stream));
+        if (m) CK(cudaMemcpyAsync(makespans + lo, b + off_ms, m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    }
+    osim_summary acc;
+    memset(&acc, 0, sizeof(acc));
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        CK(cudaSetDevice(c->dev));
+        if ((rc = finish(c, c->stream))) return rc;
+        // device-local indices -> list indices
+        const uint64_t lo = cnt * (uint64_t)gi / (uint64_t)G;
+        res[gi].best_rank += lo;
+        merge_host(acc, res[gi]);
+    }
+    if (out) *out = acc;
+    return 0;
+}
+
+int osim_exhaustive_batch(const double* durs, uint64_t B, int n, int dma, double sigma, int n_dev,
+                          osim_summary* out) {
+    int rc = check_common(n, dma, sigma);
+    if (rc) return rc;
+    if (n > 12) return fail(OSIM_EINVAL, "batched exhaustive search supports n <= 12");
+    if ((rc = check_durs(durs, B * (uint64_t)n))) return rc;
+    if (!out && B) return fail(OSIM_EINVAL, "out is NULL");
+    DevList dl;
+    if ((rc = pick_devs(n_dev, dl))) return rc;
+    const int fast = fast_ok(durs, B * (uint64_t)n, sigma);
+    const int G = (int)dl.v.size();
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        locks.emplace_back(c->mu);
+        CK(cudaSetDevice(c->dev));
+        const uint64_t lo = B * (uint64_t)gi / (uint64_t)G, hi = B * (uint64_t)(gi + 1) / (uint64_t)G;
+        const uint64_t m = hi - lo;
+        size_t off_out = align_up(m * 3 * n * sizeof(double) + 8);
+        size_t bytes = off_out + align_up(m * sizeof(osim_summary) + 8);
+        void* base;
+        if ((rc = scratch(c, bytes, &base))) return rc;
+        char* b = (char*)base;
+        if (m) {
+            CK(cudaMemcpyAsync(b, durs + lo * 3 * n, m * 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            if ((rc = enqueue_batch(c, c->stream, (double*)b, m, n, dma, sigma, fast, (osim_summary*)(b + off_out))))
+                return rc;
+            CK(cudaMemcpyAsync(out + lo, b + off_out, m * sizeof(osim_summary), cudaMemcpyDeviceToHost, c->stream));
+        }
+    }
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        CK(cudaSetDevice(c->dev));
+        if ((rc = finish(c, c->stream))) return rc;
+    }
+    return 0;
+}
+
+int osim_exhaustive_batch_dev(const double* d_durs, uint64_t B, int n, int dma, double sigma,
+                              int fast, osim_summary* d_out, void* stream) {
+    int rc = check_common(n, dma, sigma);
+    if (rc) return rc;
+    if (n > 12) return fail(OSIM_EINVAL, "batched exhaustive search supports n <= 12");
+    DevList dl;
+    if ((rc = pick_devs(1, dl))) return rc;
+    DevCtx* c = dl.v[0];
+    std::lock_guard<std::mutex> lk(c->mu);
+    return enqueue_batch(c, stream ? (cudaStream_t)stream : c->stream, d_durs, B, n, dma, sigma, fast, d_out);
+}
+
+int osim_heuristic_batch(const double* durs, const uint8_t* id_rank, uint64_t B, int n, int dma,
+                         double sigma, int sum_mode, int n_dev, uint8_t* order, double* makespan,
+                         uint32_t* n_sims) {
+    int rc = check_common(n, dma, sigma);
+    if (rc) return rc;
+    if ((rc = check_durs(durs, B * (uint64_t)n))) return rc;
+    if (B && (!id_rank || !order || !makespan)) return fail(OSIM_EINVAL, "NULL buffer");
+    for (uint64_t b = 0; b < B; ++b) {  // id ranks must be a permutation (unique ids)
+        unsigned seen = 0;
+        for (int j = 0; j < n; ++j) {
+            const unsigned v = id_rank[b * n + j];
+            if (v >= (unsigned)n || ((seen >> v) & 1u))
+                return fail(OSIM_EINVAL, "group %llu: id ranks must be a permutation (duplicate task id?)",
+                            (unsigned long long)b);
+            seen |= 1u << v;
+        }
+    }
+    DevList dl;
+    if ((rc = pick_devs(n_dev, dl))) return rc;
+    const int fast = fast_ok(durs, B * (uint64_t)n, sigma);
+    const int G = (int)dl.v.size();
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        locks.emplace_back(c->mu);
+        CK(cudaSetDevice(c->dev));
+        const uint64_t lo = B * (uint64_t)gi / (uint64_t)G, hi = B * (uint64_t)(gi + 1) / (uint64_t)G;
+        const uint64_t m = hi - lo;
+        if (!m) continue;
+        size_t off_idr = align_up(m * 3 * n * sizeof(double));
+        size_t off_ord = off_idr + align_up(m * n);
+        size_t off_ms = off_ord + align_up(m * n);
+        size_t off_ns = off_ms + align_up(m * sizeof(double));
+        size_t bytes = off_ns + align_up(m * sizeof(uint32_t));
+        void* base;
+        if ((rc = scratch(c, bytes, &base))) return rc;
+        char* b = (char*)base;
+        CK(cudaMemcpyAsync(b, durs + lo * 3 * n, m * 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(b + off_idr, id_rank + lo * n, m * n, cudaMemcpyHostToDevice, c->stream));
+        if ((rc = enqueue_heuristic(c, c->stream, (double*)b, (uint8_t*)(b + off_idr), m, n, dma, sigma,
+                                    sum_mode, fast, (uint8_t*)(b + off_ord), (double*)(b + off_ms),
+                                    (uint32_t*)(b + off_ns))))
+            return rc;
+        CK(cudaMemcpyAsync(order + lo * n, b + off_ord, m * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(makespan + lo, b + off_ms, m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        if (n_sims)
+            CK(cudaMemcpyAsync(n_sims + lo, b + off_ns, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    }
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        CK(cudaSetDevice(c->dev));
+        if ((rc = finish(c, c->stream))) return rc;
+    }
+    return 0;
+}
+
+int osim_heuristic_batch_dev(const double* d_durs, const uint8_t* d_id_rank, uint64_t B, int n,
+                             int dma, double sigma, int sum_mode, int fast, uint8_t* d_order,
+                             double* d_makespan, uint32_t* d_n_sims, void* stream) {
+    int rc = check_common(n, dma, sigma);
+    if (rc) return rc;
+    DevList dl;
+    if ((rc = pick_devs(1, dl))) return rc;
+    DevCtx* c = dl.v[0];
+    std::lock_guard<std::mutex> lk(c->mu);
+    return enqueue_heuristic(c, stream ? (cudaStream_t)stream : c->stream, d_durs, d_id_rank, B, n, dma,
+                             sigma, sum_mode, fast, d_order, d_makespan, d_n_sims);
+}
+
+int osim_timeline(const double* durs, int n, int dma, double sigma, const uint8_t* order,
+                  double* start, double* end, double* makespan, double* idle) {
+    int rc = check_common(n, dma, sigma);
+    if (rc) return rc;
+    if ((rc = check_durs(durs, (uint64_t)n))) return rc;
+    if (!order || !start || !end) return fail(OSIM_EINVAL, "NULL buffer");
+    unsigned seen = 0;
+    for (int j = 0; j < n; ++j) {
+        if (order[j] >= n || ((seen >> order[j]) & 1u)) return fail(OSIM_EINVAL, "order is not a permutation");
+        seen |= 1u << order[j];
+    }
+    DevList dl;
+    if ((rc = pick_devs(1, dl))) return rc;
+    DevCtx* c = dl.v[0];
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->dev));
+    size_t off_o = align_up(3 * kMaxN * sizeof(double));
+    size_t off_s = off_o + 256;
+    size_t off_e = off_s + align_up(3 * kMaxN * sizeof(double));
+    size_t off_r = off_e + align_up(3 * kMaxN * sizeof(double));
+    void* base;
+    if ((rc = scratch(c, off_r + 256, &base))) return rc;
+    char* b = (char*)base;
+    CK(cudaMemcpyAsync(b, durs, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(b + off_o, order, n, cudaMemcpyHostToDevice, c->stream));
+    if (dma == 2)
+        k_timeline<2><<<1, 64, 0, c->stream>>>((double*)b, n, sigma, (uint8_t*)(b + off_o), (double*)(b + off_s),
+                                               (double*)(b + off_e), (double*)(b + off_r), c->d_err);
+    else
+        k_timeline<1><<<1, 64, 0, c->stream>>>((double*)b, n, sigma, (uint8_t*)(b + off_o), (double*)(b + off_s),
+                                               (double*)(b + off_e), (double*)(b + off_r), c->d_err);
+    CK(cudaGetLastError());
+    double res[4];
+    CK(cudaMemcpyAsync(start, b + off_s, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(end, b + off_e, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(res, b + off_r, sizeof(res), cudaMemcpyDeviceToHost, c->stream));
+    if ((rc = finish(c, c->stream))) return rc;
+    if (makespan) *makespan = res[0];
+    if (idle) { idle[0] = res[1]; idle[1] = res[2]; idle[2] = res[3]; }
+    return 0;
+}
+
+int osim_selftest_div(uint64_t samples, uint64_t seed, uint64_t* mismatches) {
+    DevList dl;
+    int rc = pick_devs(1, dl);
+    if (rc) return rc;
+    DevCtx* c = dl.v[0];
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->dev));
+    void* base;
+    if ((rc = scratch(c, 256, &base))) return rc;
+    CK(cudaMemsetAsync(base, 0, 8, c->stream));
+    k_selftest_div<<<c->sms * 8, 256, 0, c->stream>>>(samples, seed, (unsigned long long*)base);
+    CK(cudaGetLastError());
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, base, 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (mismatches) *mismatches = h;
+    return 0;
+}
+
+int osim_fp64_peak(double* tflops) {
+    DevList dl;
+    int rc = pick_devs(1, dl);
+    if (rc) return rc;
+    DevCtx* c = dl.v[0];
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->dev));
+    void* base;
+    if ((rc = scratch(c, 256, &base))) return rc;
+    const int blocks = c->sms * 8, threads = 256, iters = 4096;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    k_fp64_peak<<<blocks, threads, 0, c->stream>>>((double*)base, 64, 1.0000001, 1e-7);  // warm-up
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+        CK(cudaEventRecord(e0, c->stream));
+        k_fp64_peak<<<blocks, threads, 0, c->stream>>>((double*)base, iters, 1.0000001, 1e-7);
+        CK(cudaEventRecord(e1, c->stream));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (ms < best) best = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flops = 2.0 * 8 * 16 * (double)iters * blocks * threads;
+    if (tflops) *tflops = flops / (best * 1e-3) / 1e12;
+    return 0;
+}
+
+}  // extern "C"

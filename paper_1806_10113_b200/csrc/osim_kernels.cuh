@@ -1,0 +1,648 @@
+// osim_kernels.cuh -- sm_100a kernels for the exhaustive oracle, the
+// batched-group launcher and the heuristic (Algorithm 1) candidate loop.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "osim_sim.cuh"
+#include "../../include/offsim_b200.h"
+
+namespace osim {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kBlock = 256;
+
+// ---------------------------------------------------------------------------
+// make_report reduction (oracle.py:41-57) in mergeable form.  The product of
+// makespans is carried as (mantissa in [1,2), binary exponent) instead of a
+// per-ordering log: sum_log = log(lpm) + lpe*ln2 at the end.
+// ---------------------------------------------------------------------------
+struct Part {
+    double best;
+    unsigned long long rank;
+    double worst;
+    double sum;
+    double lpm;
+    long long lpe;
+    unsigned long long count;
+};
+
+__device__ __forceinline__ void part_init(Part& a) {
+    a.best = __longlong_as_double(0x7ff0000000000000ll);
+    a.rank = ~0ull;
+    a.worst = -__longlong_as_double(0x7ff0000000000000ll);
+    a.sum = 0.0;
+    a.lpm = 1.0;
+    a.lpe = 0;
+    a.count = 0;
+}
+
+template <bool EXACT>
+__device__ __forceinline__ void renorm(double& m, long long& e) {
+    if constexpr (EXACT) {
+        int ex;
+        double f = frexp(m, &ex);  // f in [0.5, 1)
+        m = f * 2.0;
+        e += ex - 1;
+    } else {
+        long long bits = __double_as_longlong(m);
+        e += ((bits >> 52) & 0x7ff) - 1023;
+        m = __longlong_as_double((bits & 0x800FFFFFFFFFFFFFll) | (1023ll << 52));
+    }
+}
+
+// per-thread add, ranks visited in increasing order -> strict < keeps the
+// first of equal makespans (np.argmin)
+template <bool EXACT>
+__device__ __forceinline__ void part_add(Part& a, double ms, unsigned long long r) {
+    if (ms < a.best) { a.best = ms; a.rank = r; }
+    a.worst = fmax(a.worst, ms);
+    a.sum = __dadd_rn(a.sum, ms);
+    a.lpm = __dmul_rn(a.lpm, ms);
+    renorm<EXACT>(a.lpm, a.lpe);
+    a.count += 1;
+}
+
+// order-independent for best/rank (lexicographic), fixed tree order for sums
+__device__ __forceinline__ void part_merge(Part& a, const Part& b) {
+    if (b.best < a.best || (b.best == a.best && b.rank < a.rank)) { a.best = b.best; a.rank = b.rank; }
+    a.worst = fmax(a.worst, b.worst);
+    a.sum = __dadd_rn(a.sum, b.sum);
+    a.lpm = __dmul_rn(a.lpm, b.lpm);
+    a.lpe += b.lpe;
+    renorm<false>(a.lpm, a.lpe);
+    a.count += b.count;
+}
+
+__device__ __forceinline__ Part part_shfl(const Part& a, int m) {
+    Part b;
+    b.best = __shfl_xor_sync(kFull, a.best, m);
+    b.rank = __shfl_xor_sync(kFull, a.rank, m);
+    b.worst = __shfl_xor_sync(kFull, a.worst, m);
+    b.sum = __shfl_xor_sync(kFull, a.sum, m);
+    b.lpm = __shfl_xor_sync(kFull, a.lpm, m);
+    b.lpe = __shfl_xor_sync(kFull, a.lpe, m);
+    b.count = __shfl_xor_sync(kFull, a.count, m);
+    return b;
+}
+
+// Block reduce (all threads call; blockDim.x multiple of 32); result valid
+// in thread 0.  Deterministic: xor-tree in the warp, then warps in order.
+__device__ __forceinline__ Part block_reduce(Part a, Part* sh /*[32]*/) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+        Part b = part_shfl(a, m);
+        // keep the tree symmetric: lower lane merges the higher lane's value
+        if ((threadIdx.x & m) == 0) part_merge(a, b);
+        else { Part c = b; part_merge(c, a); a = c; }
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = a;
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        if (l < nw) a = sh[l]; else part_init(a);
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) {
+            Part b = part_shfl(a, m);
+            if ((threadIdx.x & m) == 0) part_merge(a, b);
+            else { Part c = b; part_merge(c, a); a = c; }
+        }
+    }
+    __syncthreads();
+    return a;
+}
+
+__device__ __forceinline__ osim_summary part_to_summary(const Part& a) {
+    osim_summary s;
+    s.best = a.best;
+    s.best_rank = a.rank;
+    s.worst = a.worst;
+    s.sum = a.sum;
+    s.sum_log = a.count ? log(a.lpm) + (double)a.lpe * 0.6931471805599453094 : 0.0;
+    s.count = a.count;
+    return s;
+}
+
+// Stage one group's durations into kind-major shared rows + reciprocals.
+__device__ __forceinline__ void stage_durs(const double* __restrict__ g, int n, double* sd, double* sr) {
+    for (int i = threadIdx.x; i < 3 * kStride; i += blockDim.x) {
+        const int k = i / kStride, t = i % kStride;
+        const double v = t < n ? g[3 * t + k] : 1.0;
+        sd[i] = v;
+        sr[i] = __ddiv_rn(1.0, v);  // RN(1/v): the Markstein reciprocal
+    }
+}
+
+__device__ __forceinline__ void null_masks(const double* sd, int n, unsigned& nH, unsigned& nK,
+                                           unsigned& nD) {
+    nH = nK = nD = 0;
+    for (int t = 0; t < n; ++t) {
+        if (!(sd[0 * kStride + t] > 0.0)) nH |= 1u << t;
+        if (!(sd[1 * kStride + t] > 0.0)) nK |= 1u << t;
+        if (!(sd[2 * kStride + t] > 0.0)) nD |= 1u << t;
+    }
+}
+
+// Warp-uniform run loop: the warp steps until all its lanes drained.
+template <class S>
+__device__ __forceinline__ void run_warp(S& s, int max_steps) {
+#pragma unroll 1
+    for (int st = 0; st < max_steps; ++st) {
+        if (__all_sync(kFull, s.drained())) break;
+        s.step();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Exhaustive search over ranks [lo, hi) of one group (oracle.py:123-135).
+// One thread per ordering, Lehmer-unranked on the fly; per-block partials.
+// ---------------------------------------------------------------------------
+template <int N, int DMA>
+__global__ void __launch_bounds__(kBlock) k_exhaustive_fast(const double* __restrict__ durs,
+                                                            double sigma, uint64_t lo, uint64_t hi,
+                                                            Part* __restrict__ parts,
+                                                            double* __restrict__ ms_out) {
+    __shared__ double sd[3 * kStride], sr[3 * kStride];
+    __shared__ Part sh[32];
+    stage_durs(durs, N, sd, sr);
+    __syncthreads();
+    const double rsig = __ddiv_rn(1.0, sigma);
+    const Durs D{sd, sr};
+    Part acc;
+    part_init(acc);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = lo + (uint64_t)blockIdx.x * blockDim.x; base < hi; base += stride) {
+        const uint64_t r = base + threadIdx.x;
+        const bool valid = r < hi;
+        Sim<DMA, true, true, false> s;
+        s.init(D, unrank<N>(valid ? r : lo), N, sigma, rsig);
+        run_warp(s, 3 * N);
+        if (valid) {
+            part_add<false>(acc, s.now, r);
+            if (ms_out) ms_out[r - lo] = s.now;
+        }
+    }
+    acc = block_reduce(acc, sh);
+    if (threadIdx.x == 0) parts[blockIdx.x] = acc;
+}
+
+template <int DMA>
+__global__ void __launch_bounds__(kBlock) k_exhaustive_gen(const double* __restrict__ durs, int n,
+                                                           double sigma, uint64_t lo, uint64_t hi,
+                                                           Part* __restrict__ parts,
+                                                           double* __restrict__ ms_out,
+                                                           int* __restrict__ err) {
+    __shared__ double sd[3 * kStride], sr[3 * kStride];
+    __shared__ Part sh[32];
+    stage_durs(durs, n, sd, sr);
+    __syncthreads();
+    unsigned nH, nK, nD;
+    null_masks(sd, n, nH, nK, nD);
+    const Durs D{sd, sr};
+    Part acc;
+    part_init(acc);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = lo + (uint64_t)blockIdx.x * blockDim.x; base < hi; base += stride) {
+        const uint64_t r = base + threadIdx.x;
+        const bool valid = r < hi;
+        Sim<DMA, false, false, false> s;
+        s.init(D, unrank_rt(valid ? r : lo, n), n, sigma, 1.0, nH, nK, nD);
+        run_warp(s, 3 * n);
+        if (!s.drained()) atomicExch(err, OSIM_ESTALL);
+        if (valid) {
+            part_add<true>(acc, s.now, r);
+            if (ms_out) ms_out[r - lo] = s.now;
+        }
+    }
+    acc = block_reduce(acc, sh);
+    if (threadIdx.x == 0) parts[blockIdx.x] = acc;
+}
+
+// Deterministic final reduce of per-block partials (fixed order).
+__global__ void __launch_bounds__(kBlock) k_final_reduce(const Part* __restrict__ parts, int P,
+                                                         osim_summary* __restrict__ out) {
+    __shared__ Part sh[32];
+    Part a;
+    part_init(a);
+    for (int i = threadIdx.x; i < P; i += blockDim.x) part_merge(a, parts[i]);
+    a = block_reduce(a, sh);
+    if (threadIdx.x == 0) *out = part_to_summary(a);
+}
+
+// ---------------------------------------------------------------------------
+// Explicit orderings (sampled mode, oracle.py:127-135): thread per ordering.
+// ---------------------------------------------------------------------------
+template <int DMA, bool FAST>
+__global__ void __launch_bounds__(kBlock) k_eval_perms(const double* __restrict__ durs, int n,
+                                                       double sigma,
+                                                       const uint8_t* __restrict__ perms,
+                                                       uint64_t cnt, double* __restrict__ ms_out,
+                                                       Part* __restrict__ parts,
+                                                       int* __restrict__ err) {
+    __shared__ double sd[3 * kStride], sr[3 * kStride];
+    __shared__ Part sh[32];
+    stage_durs(durs, n, sd, sr);
+    __syncthreads();
+    unsigned nH = 0, nK = 0, nD = 0;
+    if constexpr (!FAST) null_masks(sd, n, nH, nK, nD);
+    const double rsig = __ddiv_rn(1.0, sigma);
+    const Durs D{sd, sr};
+    Part acc;
+    part_init(acc);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < cnt; base += stride) {
+        const uint64_t i = base + threadIdx.x;
+        const bool valid = i < cnt;
+        const uint8_t* p = perms + (valid ? i : 0) * (uint64_t)n;
+        uint64_t seq = 0;
+        for (int j = 0; j < n; ++j) seq |= (uint64_t)(p[j] & 0xF) << (4 * j);
+        Sim<DMA, FAST, FAST, false> s;
+        s.init(D, seq, n, sigma, rsig, nH, nK, nD);
+        run_warp(s, 3 * n);
+        if (!s.drained()) atomicExch(err, OSIM_ESTALL);
+        if (valid) {
+            part_add<!FAST>(acc, s.now, i);
+            ms_out[i] = s.now;
+        }
+    }
+    acc = block_reduce(acc, sh);
+    if (threadIdx.x == 0) parts[blockIdx.x] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// Batched groups (config 2): one CTA per group, n! orderings per CTA.
+// ---------------------------------------------------------------------------
+template <int N, int DMA>
+__global__ void __launch_bounds__(kBlock) k_exhaustive_batch_fast(const double* __restrict__ durs,
+                                                                  uint64_t B, double sigma,
+                                                                  osim_summary* __restrict__ out) {
+    __shared__ double sd[3 * kStride], sr[3 * kStride];
+    __shared__ Part sh[32];
+    constexpr uint64_t total = [] {
+        uint64_t f = 1;
+        for (int i = 2; i <= N; ++i) f *= (uint64_t)i;
+        return f;
+    }();
+    const double rsig = __ddiv_rn(1.0, sigma);
+    for (uint64_t b = blockIdx.x; b < B; b += gridDim.x) {
+        stage_durs(durs + b * 3 * N, N, sd, sr);
+        __syncthreads();
+        const Durs D{sd, sr};
+        Part acc;
+        part_init(acc);
+        for (uint64_t base = 0; base < total; base += blockDim.x) {
+            const uint64_t r = base + threadIdx.x;
+            const bool valid = r < total;
+            Sim<DMA, true, true, false> s;
+            s.init(D, unrank<N>(valid ? r : 0), N, sigma, rsig);
+            run_warp(s, 3 * N);
+            if (valid) part_add<false>(acc, s.now, r);
+        }
+        acc = block_reduce(acc, sh);  // ends with __syncthreads: smem reusable
+        if (threadIdx.x == 0) out[b] = part_to_summary(acc);
+    }
+}
+
+template <int DMA>
+__global__ void __launch_bounds__(kBlock) k_exhaustive_batch_gen(const double* __restrict__ durs,
+                                                                 uint64_t B, int n, double sigma,
+                                                                 osim_summary* __restrict__ out,
+                                                                 int* __restrict__ err) {
+    __shared__ double sd[3 * kStride], sr[3 * kStride];
+    __shared__ Part sh[32];
+    uint64_t total = 1;
+    for (int i = 2; i <= n; ++i) total *= (uint64_t)i;
+    for (uint64_t b = blockIdx.x; b < B; b += gridDim.x) {
+        stage_durs(durs + b * 3 * (uint64_t)n, n, sd, sr);
+        __syncthreads();
+        unsigned nH, nK, nD;
+        null_masks(sd, n, nH, nK, nD);
+        const Durs D{sd, sr};
+        Part acc;
+        part_init(acc);
+        for (uint64_t base = 0; base < total; base += blockDim.x) {
+            const uint64_t r = base + threadIdx.x;
+            const bool valid = r < total;
+            Sim<DMA, false, false, false> s;
+            s.init(D, unrank_rt(valid ? r : 0, n), n, sigma, 1.0, nH, nK, nD);
+            run_warp(s, 3 * n);
+            if (!s.drained()) atomicExch(err, OSIM_ESTALL);
+            if (valid) part_add<true>(acc, s.now, r);
+        }
+        acc = block_reduce(acc, sh);
+        if (threadIdx.x == 0) out[b] = part_to_summary(acc);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// One ordering with its full timeline (engine.simulate, engine.py:252-263).
+// ---------------------------------------------------------------------------
+template <int DMA>
+__global__ void k_timeline(const double* __restrict__ durs, int n, double sigma,
+                           const uint8_t* __restrict__ order, double* start, double* end,
+                           double* res /*[4] makespan, idle HtD, K, DtH*/, int* err) {
+    __shared__ double sd[3 * kStride], sr[3 * kStride];
+    stage_durs(durs, n, sd, sr);
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    unsigned nH, nK, nD;
+    null_masks(sd, n, nH, nK, nD);
+    for (int i = 0; i < 3 * n; ++i) { start[i] = -1.0; end[i] = -1.0; }
+    uint64_t seq = 0;
+    for (int j = 0; j < n; ++j) seq |= (uint64_t)(order[j] & 0xF) << (4 * j);
+    Sim<DMA, false, false, false> s;
+    s.init(Durs{sd, sr}, seq, n, sigma, 1.0, nH, nK, nD);
+    TimelineOut tl{start, end};
+    if (!s.run(&tl)) { *err = OSIM_ESTALL; return; }
+    res[0] = s.now;
+    // idle_report (engine.py:68-80): each kind's spans in FIFO order, which
+    // is their (start, end) order
+    for (int k = 0; k < 3; ++k) {
+        double idle = 0.0, prev_end = 0.0;
+        bool any = false;
+        for (int j = 0; j < n; ++j) {
+            const int t = order[j];
+            if (start[3 * t + k] < 0.0) continue;
+            const double st = start[3 * t + k];
+            if (any && st > prev_end) idle = __dadd_rn(idle, __dsub_rn(st, prev_end));
+            prev_end = end[3 * t + k];
+            any = true;
+        }
+        res[1 + k] = idle;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Heuristic (Algorithm 1, heuristic.py:105-125) for many groups.
+// CTA-cooperative: a CTA owns G groups in shared memory; every greedy round
+// all groups have the same prefix length k, so the round's G*(n-k)
+// candidate simulations (select_next_task, heuristic.py:71-77) have equal
+// length and are spread over all threads in lock-step; one thread per
+// group then takes the argmin of (estimate, idle_K, id) and extends the
+// prefix.
+// ---------------------------------------------------------------------------
+constexpr int kHG = 32;     // groups per CTA
+constexpr int kHT = 128;    // threads per CTA
+constexpr int kHS = 97;     // doubles per group: 48 durations + 48 reciprocals + pad
+
+struct HeurShared {
+    double dr[kHG * kHS];
+    double ka[kHG * kMaxN];
+    double kb[kHG * kMaxN];
+    uint64_t ot[kHG];
+    unsigned rmask[kHG];
+    unsigned nH[kHG], nK[kHG], nD[kHG];
+    uint8_t idr[kHG * kMaxN];
+    uint8_t cand[kHG * kMaxN];
+    uint8_t pa[kHG], pb[kHG];
+};
+
+template <int DMA, bool FAST>
+__global__ void __launch_bounds__(kHT) k_heuristic(const double* __restrict__ durs,
+                                                   const uint8_t* __restrict__ id_rank, uint64_t B,
+                                                   int n, double sigma, int sum_mode,
+                                                   uint8_t* __restrict__ order_out,
+                                                   double* __restrict__ ms_out,
+                                                   uint32_t* __restrict__ nsims_out,
+                                                   int* __restrict__ err) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    HeurShared& S = *reinterpret_cast<HeurShared*>(smem_raw);
+    const uint64_t g0 = (uint64_t)blockIdx.x * kHG;
+    const int Gv = (int)((B - g0) < (uint64_t)kHG ? (B - g0) : (uint64_t)kHG);
+    const double rsig = __ddiv_rn(1.0, sigma);
+    const int tid = threadIdx.x;
+
+    // stage durations (kind-major rows) + reciprocals + id ranks
+    for (int i = tid; i < Gv * 3 * kStride; i += blockDim.x) {
+        const int g = i / (3 * kStride), r = i % (3 * kStride);
+        const int k = r / kStride, t = r % kStride;
+        const double v = t < n ? durs[(g0 + g) * 3 * (uint64_t)n + 3 * t + k] : 1.0;
+        S.dr[g * kHS + r] = v;
+        S.dr[g * kHS + 3 * kStride + r] = __ddiv_rn(1.0, v);
+    }
+    for (int i = tid; i < Gv * kMaxN; i += blockDim.x) {
+        const int g = i / kMaxN, t = i % kMaxN;
+        S.idr[i] = t < n ? id_rank[(g0 + g) * (uint64_t)n + t] : 0xFF;
+    }
+    __syncthreads();
+
+    auto durs_of = [&](int g) { return Durs{&S.dr[g * kHS], &S.dr[g * kHS + 3 * kStride]}; };
+    auto DV = [&](int g, int k, int t) { return S.dr[g * kHS + k * kStride + t]; };
+
+    // select_first_task (heuristic.py:22-31): min over rt of
+    // (-(t_k - t_htd), -t_dth, id)
+    if (tid < Gv) {
+        const int g = tid;
+        unsigned nH = 0, nK = 0, nD = 0;
+        for (int t = 0; t < n; ++t) {
+            if (!(DV(g, 0, t) > 0.0)) nH |= 1u << t;
+            if (!(DV(g, 1, t) > 0.0)) nK |= 1u << t;
+            if (!(DV(g, 2, t) > 0.0)) nD |= 1u << t;
+        }
+        S.nH[g] = nH; S.nK[g] = nK; S.nD[g] = nD;
+        unsigned all = (n >= 32) ? ~0u : ((1u << n) - 1u);
+        if (n >= 3) {
+            int best = -1;
+            double b1 = 0, b2 = 0;
+            for (int t = 0; t < n; ++t) {
+                const double k1 = -__dsub_rn(DV(g, 1, t), DV(g, 0, t));
+                const double k2 = -DV(g, 2, t);
+                bool less;
+                if (best < 0) less = true;
+                else if (k1 < b1) less = true;
+                else if (b1 < k1) less = false;
+                else if (k2 < b2) less = true;
+                else if (b2 < k2) less = false;
+                else less = S.idr[g * kMaxN + t] < S.idr[g * kMaxN + best];
+                if (less) { best = t; b1 = k1; b2 = k2; }
+            }
+            S.ot[g] = (uint64_t)best;
+            S.rmask[g] = all & ~(1u << best);
+        } else {
+            S.ot[g] = 0;
+            S.rmask[g] = all;
+        }
+        int c = 0;
+        for (int t = 0; t < n; ++t)
+            if ((S.rmask[g] >> t) & 1u) S.cand[g * kMaxN + c++] = (uint8_t)t;
+    }
+    __syncthreads();
+
+    const int k0 = (n >= 3) ? 1 : 0;  // prefix length after the first pick
+    // greedy rounds: while len(rt) > 2 (heuristic.py:120-123)
+    for (int k = k0; n - k > 2; ++k) {
+        const int m = n - k;
+        const int items = Gv * m;
+        for (int i0 = 0; i0 < items; i0 += blockDim.x) {
+            const int i = i0 + tid;
+            const bool valid = i < items;
+            const int g = valid ? i / m : 0;
+            const int j = valid ? i % m : 0;
+            const int c = S.cand[g * kMaxN + j];
+            const uint64_t seq = S.ot[g] | ((uint64_t)c << (4 * k));
+            Sim<DMA, FAST, FAST, true> s;
+            s.init(durs_of(g), seq, k + 1, sigma, rsig, S.nH[g], S.nK[g], S.nD[g]);
+            run_warp(s, 3 * (k + 1));
+            // _completion_estimate (heuristic.py:34-49); rest in rt order
+            PySum ps;
+            ps.reset();
+            double tail = 0.0;
+            bool any = false;
+            const unsigned rest = S.rmask[g] & ~(1u << c);
+            for (int t = 0; t < n; ++t) {
+                if (!((rest >> t) & 1u)) continue;
+                ps.add(DV(g, 1, t), sum_mode);
+                const double d = DV(g, 2, t);
+                if (!any || d < tail) tail = d;
+                any = true;
+            }
+            const double bound = __dadd_rn(__dadd_rn(s.kEnd, ps.result(sum_mode)), tail);
+            const double est = (bound > s.now) ? bound : s.now;
+            if (valid) {
+                S.ka[g * kMaxN + j] = est;
+                S.kb[g * kMaxN + j] = s.idleK;
+            }
+        }
+        __syncthreads();
+        if (tid < Gv) {
+            const int g = tid;
+            int bj = 0;
+            for (int j = 1; j < m; ++j) {
+                const double e = S.ka[g * kMaxN + j], be = S.ka[g * kMaxN + bj];
+                const double d = S.kb[g * kMaxN + j], bd = S.kb[g * kMaxN + bj];
+                bool less;
+                if (e < be) less = true;
+                else if (be < e) less = false;
+                else if (d < bd) less = true;
+                else if (bd < d) less = false;
+                else less = S.idr[g * kMaxN + S.cand[g * kMaxN + j]] <
+                            S.idr[g * kMaxN + S.cand[g * kMaxN + bj]];
+                if (less) bj = j;
+            }
+            const int c = S.cand[g * kMaxN + bj];
+            S.ot[g] |= (uint64_t)c << (4 * k);
+            S.rmask[g] &= ~(1u << c);
+            int cc = 0;
+            for (int t = 0; t < n; ++t)
+                if ((S.rmask[g] >> t) & 1u) S.cand[g * kMaxN + cc++] = (uint8_t)t;
+        }
+        __syncthreads();
+    }
+
+    const int kl = n - 2;  // select_last_tasks (heuristic.py:81-102)
+    if (n >= 2) {
+        if (tid < Gv) {
+            const int g = tid;
+            int a = S.cand[g * kMaxN + 0], b = S.cand[g * kMaxN + 1];
+            if (S.idr[g * kMaxN + b] < S.idr[g * kMaxN + a]) { int x = a; a = b; b = x; }
+            S.pa[g] = (uint8_t)a;
+            S.pb[g] = (uint8_t)b;
+        }
+        __syncthreads();
+        for (int i0 = 0; i0 < 2 * Gv; i0 += blockDim.x) {
+            const int i = i0 + tid;
+            const bool valid = i < 2 * Gv;
+            const int g = valid ? i >> 1 : 0;
+            const int w = i & 1;
+            const uint64_t x = w ? S.pb[g] : S.pa[g], y = w ? S.pa[g] : S.pb[g];
+            const uint64_t seq = S.ot[g] | (x << (4 * kl)) | (y << (4 * (kl + 1)));
+            Sim<DMA, FAST, FAST, false> s;
+            s.init(durs_of(g), seq, n, sigma, rsig, S.nH[g], S.nK[g], S.nD[g]);
+            run_warp(s, 3 * n);
+            if (valid) S.ka[g * kMaxN + w] = s.now;
+        }
+        __syncthreads();
+        if (tid < Gv) {
+            const int g = tid;
+            const int a = S.pa[g], b = S.pb[g];
+            const double m_ab = S.ka[g * kMaxN + 0], m_ba = S.ka[g * kMaxN + 1];
+            bool ab;
+            if (m_ab < m_ba) ab = true;
+            else if (m_ba < m_ab) ab = false;
+            else ab = !(DV(g, 2, a) <= DV(g, 2, b));  // tie: shorter DtH last
+            S.ot[g] |= ((uint64_t)(ab ? a : b) << (4 * kl)) | ((uint64_t)(ab ? b : a) << (4 * (kl + 1)));
+        }
+        __syncthreads();
+    }
+
+    // final ordering, its makespan and the simulation count
+    for (int i0 = 0; i0 < Gv; i0 += blockDim.x) {
+        const int i = i0 + tid;
+        const bool valid = i < Gv;
+        const int g = valid ? i : 0;
+        Sim<DMA, FAST, FAST, false> s;
+        s.init(durs_of(g), S.ot[g], n, sigma, rsig, S.nH[g], S.nK[g], S.nD[g]);
+        run_warp(s, 3 * n);
+        if (!s.drained()) atomicExch(err, OSIM_ESTALL);
+        if (valid) {
+            ms_out[g0 + g] = s.now;
+            if (nsims_out) nsims_out[g0 + g] = (n >= 3) ? (uint32_t)(n * (n - 1) / 2 - 1) : (n == 2 ? 2u : 0u);
+        }
+    }
+    for (int i = tid; i < Gv * n; i += blockDim.x) {
+        const int g = i / n, p = i % n;
+        order_out[(g0 + g) * (uint64_t)n + p] = (uint8_t)nib(S.ot[g], p);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Diagnostics
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix(uint64_t& x) {
+    uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_selftest_div(uint64_t samples, uint64_t seed, unsigned long long* mism) {
+    uint64_t st = seed ^ ((uint64_t)(blockIdx.x * blockDim.x + threadIdx.x) * 0x2545F4914F6CDD1Dull);
+    unsigned long long bad = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < samples; i += stride) {
+        const uint64_t a = splitmix(st), b = splitmix(st), c = splitmix(st);
+        // y: durations / sigma in [2^-60, 2^60], random mantissa (sometimes all ones)
+        int ey = (int)(a % 121) - 60;
+        uint64_t my = (b & 0xFFFFFFFFFFFFFull);
+        if ((c & 7) == 0) my = 0xFFFFFFFFFFFFFull;
+        if ((c & 7) == 1) my = 0;
+        const double y = __longlong_as_double(((long long)(1023 + ey) << 52) | (long long)my);
+        // x: remaining work: y * fraction, or a raw value of nearby magnitude
+        double x;
+        const uint64_t d = splitmix(st);
+        if ((c >> 3) & 1) {
+            const double frac = (double)(d >> 11) * (1.0 / 9007199254740992.0);
+            x = __dmul_rn(y, frac);
+        } else {
+            int ex = ey + (int)((d >> 52) % 140) - 70;
+            x = __longlong_as_double(((long long)(1023 + ex) << 52) | (long long)(d & 0xFFFFFFFFFFFFFull));
+        }
+        if ((c >> 4 & 63) == 0) x = 0.0;
+        const double ry = __ddiv_rn(1.0, y);
+        if (divq<true>(x, y, ry) != __ddiv_rn(x, y)) ++bad;
+    }
+    for (int m = 16; m >= 1; m >>= 1) bad += __shfl_xor_sync(kFull, bad, m);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(mism, bad);
+}
+
+// DFMA throughput: 8 independent chains per thread.
+__global__ void __launch_bounds__(256) k_fp64_peak(double* sink, int iters, double a, double b) {
+    double x0 = threadIdx.x * 1e-9, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
+    double x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+#pragma unroll 1
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            x0 = __fma_rn(x0, a, b); x1 = __fma_rn(x1, a, b); x2 = __fma_rn(x2, a, b);
+            x3 = __fma_rn(x3, a, b); x4 = __fma_rn(x4, a, b); x5 = __fma_rn(x5, a, b);
+            x6 = __fma_rn(x6, a, b); x7 = __fma_rn(x7, a, b);
+        }
+    }
+    const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 1234.5678) sink[0] = s;
+}
+
+}  // namespace osim

@@ -1,0 +1,380 @@
+// osim_sim.cuh -- register-resident FP64 event loop of the temporal
+// execution model, one simulation per thread.
+//
+// This is the B200 formulation of DeviceSim.step/run/timeline
+// (/root/reference/pkg/src/offsim/engine.py:182-249).  Instead of command
+// objects in per-lane FIFO lists, a thread keeps, per lane, the head
+// position in its ordering (a packed 4-bit-per-position sequence), a
+// running flag and the running command's remaining work `rem` = rw*nd
+// plus its nominal duration `nd` and 1/nd.  Durations live in shared
+// memory as kind-major [3][stride] arrays, so every lookup of a task's
+// stage is conflict-free (<=16 doubles per kind = one 128-byte bank row).
+//
+// Operation order is the reference's (engine.py:207-222), all IEEE double
+// with explicit round-to-nearest intrinsics so nothing is contracted:
+//   cand_c = rem_c / rate_c                       (engine.py:210)
+//   dt     = min_c cand_c ;  now = now + dt        (:210-211)
+//   left_c = rem_c - dt * rate_c                   (:213)
+//   rw_c   = max(left_c, 0.0) / nd_c               (:214)
+//   rem_c  = rw_c * nd_c ;  finalize if rem_c <= 1e-9   (:222)
+// `rem_c` is exactly the product the reference recomputes at the top of
+// the next step, so it is carried instead of rw.
+//
+// Division.  The fast path divides with Markstein's correction from a
+// correctly rounded reciprocal (q0 = x*r, e = fma(-q0, y, x),
+// q = fma(e, r, q0)), which returns the correctly rounded quotient for
+// operands whose quotient and remainder stay clear of the subnormal range;
+// the host only selects it when every duration and sigma lies in
+// [2^-60, 2^60] (see osim_capi.cu), and the GPU self-test compares it with
+// IEEE division.  The general path (null stages, out-of-range inputs)
+// uses IEEE division (__ddiv_rn).
+#pragma once
+
+#include <cstdint>
+
+namespace osim {
+
+constexpr double kEndEps = 1e-9;  // engine.py:26 _END_EPS
+constexpr int kMaxN = 16;         // 4-bit positions in a u64 sequence
+constexpr int kStride = 16;       // doubles per kind row in shared memory
+
+__device__ __forceinline__ int nib(uint64_t seq, int pos) {
+    return (int)((seq >> (4 * pos)) & 0xFull);
+}
+
+template <bool FASTDIV>
+__device__ __forceinline__ double divq(double x, double y, double ry) {
+    if constexpr (FASTDIV) {
+        double q0 = __dmul_rn(x, ry);
+        double e = __fma_rn(-q0, y, x);
+        return __fma_rn(e, ry, q0);
+    } else {
+        return __ddiv_rn(x, y);
+    }
+}
+
+// Python's max(left, 0.0): the first argument unless 0.0 compares greater.
+__device__ __forceinline__ double pymax0(double left) { return (0.0 > left) ? 0.0 : left; }
+
+// Per-thread view of one task group's durations in shared memory.
+struct Durs {
+    const double* d;  // d[k*kStride + t], k = 0 HtD, 1 K, 2 DtH
+    const double* r;  // 1/d, same layout
+    __device__ __forceinline__ double nd(int k, int t) const { return d[k * kStride + t]; }
+    __device__ __forceinline__ double rc(int k, int t) const { return r[k * kStride + t]; }
+};
+
+// Optional full-timeline record (timeline mode only, general path).
+struct TimelineOut {
+    double* start;  // [n][3] by task index
+    double* end;
+};
+
+// ---------------------------------------------------------------------------
+// Simulator state.  DMA: 1 or 2 engines (engine.py:97-104).
+// FAST: every stage of every task is non-null, so the three queues are the
+// ordering itself and readiness reduces to head comparisons
+//   K(p) ready  <=> HtD(p) finalized <=> p < headH        (engine.py:172-173)
+//   DtH(p) ready <=> K(p) finalized  <=> p < headK        (:174-177)
+// Otherwise (general) heads skip null stages (engine.py:129-151) and
+// readiness uses per-kind done bitmasks over task ids.
+// TRACK: also keep k_end and idle["K"] (heuristic.py:46, :74).
+// ---------------------------------------------------------------------------
+template <int DMA, bool FAST, bool FASTDIV, bool TRACK>
+struct Sim {
+    // inputs
+    Durs D;
+    uint64_t seq;
+    int len;
+    double sigma, rsig;
+    // lanes: 2-DMA {0:HtD, 1:DtH, 2:K}; 1-DMA {0:XFER, 2:K}
+    double now;
+    double rem0, rem1, rem2;
+    double nd0, nd1, nd2;
+    double rc0, rc1, rc2;
+    int h0, h1, h2;   // FAST: finalized count; general: head position/slot
+    int kind0;        // 1-DMA: kind of the XFER head command (0 HtD / 2 DtH)
+    bool run0, run1, run2;
+    unsigned doneH, doneK, doneD;  // general path only
+    unsigned nullH, nullK, nullD;
+    int kfin;
+    double kEnd, idleK;
+
+    __device__ __forceinline__ void init(const Durs& d, uint64_t s, int n, double sg, double rsg,
+                                         unsigned nH = 0, unsigned nK = 0, unsigned nD = 0) {
+        D = d;
+        seq = s;
+        len = n;
+        sigma = sg;
+        rsig = rsg;
+        now = 0.0;
+        rem0 = rem1 = rem2 = 1.0;
+        nd0 = nd1 = nd2 = 1.0;
+        rc0 = rc1 = rc2 = 1.0;
+        h0 = h1 = h2 = 0;
+        kind0 = 0;
+        run0 = run1 = run2 = false;
+        kfin = 0;
+        kEnd = 0.0;
+        idleK = 0.0;
+        if constexpr (!FAST) {
+            nullH = nH;
+            nullK = nK;
+            nullD = nD;
+            doneH = nH;
+            doneK = nK;
+            doneD = nD;
+            if constexpr (DMA == 2) {
+                h0 = skip(0, nullH);
+                h1 = skip(0, nullD);
+            } else {
+                h0 = skipx(0);
+            }
+            h2 = skip(0, nullK);
+        }
+    }
+
+    // next position >= p whose stage of the given null-mask is non-null
+    __device__ __forceinline__ int skip(int p, unsigned nullmask) const {
+        while (p < len && ((nullmask >> nib(seq, p)) & 1u)) ++p;
+        return p;
+    }
+    // 1-DMA XFER queue slots: [HtD(p0..), DtH(p0..)] (engine.py:153-154)
+    __device__ __forceinline__ int skipx(int s) const {
+        while (s < 2 * len) {
+            bool isH = s < len;
+            int t = nib(seq, isH ? s : s - len);
+            if (!(((isH ? nullH : nullD) >> t) & 1u)) break;
+            ++s;
+        }
+        return s;
+    }
+
+    __device__ __forceinline__ bool drained() const {
+        if constexpr (FAST) {
+            if constexpr (DMA == 2) return h1 >= len;
+            else return h0 >= 2 * len;
+        } else {
+            if constexpr (DMA == 2) return h0 >= len && h1 >= len && h2 >= len;
+            else return h0 >= 2 * len && h2 >= len;
+        }
+    }
+
+    __device__ __forceinline__ void startK(TimelineOut* tl) {
+        int t = nib(seq, h2);
+        nd2 = D.nd(1, t);
+        rc2 = D.rc(1, t);
+        rem2 = nd2;
+        run2 = true;
+        if constexpr (TRACK) {
+            // idle_report (engine.py:68-80): K spans are FIFO == sorted
+            if (kfin > 0 && now > kEnd) idleK = __dadd_rn(idleK, __dsub_rn(now, kEnd));
+        }
+        if (tl) tl->start[3 * t + 1] = now;
+    }
+
+    // One DeviceSim.step() (engine.py:182-232).  No-op once drained.
+    __device__ __forceinline__ void step(TimelineOut* tl = nullptr) {
+        const double INF = __longlong_as_double(0x7ff0000000000000ll);
+        // ---- start phase (engine.py:188-194)
+        if constexpr (DMA == 2) {
+            if (!run0 && h0 < len) {
+                int t = nib(seq, h0);
+                nd0 = D.nd(0, t); rc0 = D.rc(0, t); rem0 = nd0; run0 = true;
+                if (tl) tl->start[3 * t + 0] = now;
+            }
+            if constexpr (FAST) {
+                if (!run2 && h2 < h0) startK(tl);
+                if (!run1 && h1 < h2) {
+                    int t = nib(seq, h1);
+                    nd1 = D.nd(2, t); rc1 = D.rc(2, t); rem1 = nd1; run1 = true;
+                }
+            } else {
+                if (!run2 && h2 < len && ((doneH >> nib(seq, h2)) & 1u)) startK(tl);
+                if (!run1 && h1 < len) {
+                    int t = nib(seq, h1);
+                    if (((doneK & doneH) >> t) & 1u) {
+                        nd1 = D.nd(2, t); rc1 = D.rc(2, t); rem1 = nd1; run1 = true;
+                        if (tl) tl->start[3 * t + 2] = now;
+                    }
+                }
+            }
+        } else {
+            if (!run0 && h0 < 2 * len) {
+                bool isH = h0 < len;
+                int t = nib(seq, isH ? h0 : h0 - len);
+                bool ready;
+                if constexpr (FAST) ready = isH || (h2 > h0 - len);
+                else ready = isH || (((doneK & doneH) >> t) & 1u);
+                if (ready) {
+                    int k = isH ? 0 : 2;
+                    kind0 = k;
+                    nd0 = D.nd(k, t); rc0 = D.rc(k, t); rem0 = nd0; run0 = true;
+                    if (tl) tl->start[3 * t + k] = now;
+                }
+            }
+            if constexpr (FAST) {
+                if (!run2 && h2 < len && h2 < h0) startK(tl);
+            } else {
+                if (!run2 && h2 < len && ((doneH >> nib(seq, h2)) & 1u)) startK(tl);
+            }
+        }
+        const bool act = run0 | run1 | run2;
+        // ---- rates (engine.py:200-208): both transfer directions slowed by
+        // sigma while an HtD and a DtH execute together on a 2-DMA device
+        bool ov = false;
+        if constexpr (DMA == 2) ov = run0 && run1;
+        // ---- dt (engine.py:210)
+        double c0 = run0 ? (ov ? divq<FASTDIV>(rem0, sigma, rsig) : rem0) : INF;
+        double c1 = INF;
+        if constexpr (DMA == 2) c1 = run1 ? (ov ? divq<FASTDIV>(rem1, sigma, rsig) : rem1) : INF;
+        double c2 = run2 ? rem2 : INF;
+        double dt = fmin(fmin(c0, c1), c2);
+        if (act) now = __dadd_rn(now, dt);  // engine.py:211
+        // ---- remaining work (engine.py:212-214)
+        const double dd = ov ? __dmul_rn(dt, sigma) : dt;
+        rem0 = __dmul_rn(divq<FASTDIV>(pymax0(__dsub_rn(rem0, dd)), nd0, rc0), nd0);
+        if constexpr (DMA == 2)
+            rem1 = __dmul_rn(divq<FASTDIV>(pymax0(__dsub_rn(rem1, dd)), nd1, rc1), nd1);
+        rem2 = __dmul_rn(divq<FASTDIV>(pymax0(__dsub_rn(rem2, dt)), nd2, rc2), nd2);
+        // ---- finalize (engine.py:216-231); the order HtD, DtH, K only
+        // orders the returned list, not the numbers
+        const bool f0 = run0 && rem0 <= kEndEps;
+        const bool f1 = (DMA == 2) && run1 && rem1 <= kEndEps;
+        const bool f2 = run2 && rem2 <= kEndEps;
+        if constexpr (FAST) {
+            if (f0) { run0 = false; ++h0; }
+            if (f1) { run1 = false; ++h1; }
+            if (f2) { run2 = false; ++h2; }
+            if (tl) {
+                // FAST never runs with a timeline record
+            }
+        } else {
+            if (f0) {
+                run0 = false;
+                if constexpr (DMA == 2) {
+                    int t = nib(seq, h0);
+                    doneH |= 1u << t;
+                    if (tl) tl->end[3 * t + 0] = now;
+                    h0 = skip(h0 + 1, nullH);
+                } else {
+                    bool isH = h0 < len;
+                    int t = nib(seq, isH ? h0 : h0 - len);
+                    if (isH) doneH |= 1u << t; else doneD |= 1u << t;
+                    if (tl) tl->end[3 * t + (isH ? 0 : 2)] = now;
+                    h0 = skipx(h0 + 1);
+                }
+            }
+            if (f1) {
+                int t = nib(seq, h1);
+                run1 = false;
+                doneD |= 1u << t;
+                if (tl) tl->end[3 * t + 2] = now;
+                h1 = skip(h1 + 1, nullD);
+            }
+            if (f2) {
+                int t = nib(seq, h2);
+                run2 = false;
+                doneK |= 1u << t;
+                if (tl) tl->end[3 * t + 1] = now;
+                h2 = skip(h2 + 1, nullK);
+            }
+        }
+        if constexpr (TRACK) {
+            if (f2) { kEnd = now; ++kfin; }
+        }
+    }
+
+    // DeviceSim.run (engine.py:237-241).  Every step finalizes at least the
+    // command that set dt, so 3*len steps always suffice; returns false on
+    // a stall (cannot happen without deps, kept as a guard).
+    __device__ __forceinline__ bool run(TimelineOut* tl = nullptr) {
+        const int max_steps = 3 * len;
+        for (int s = 0; s < max_steps; ++s) {
+            if (drained()) break;
+            step(tl);
+        }
+        return drained();
+    }
+};
+
+// Lexicographic unrank of `r` into a packed sequence (itertools.permutations
+// order == Lehmer rank order, oracle.py:125).
+template <int N>
+__device__ __forceinline__ uint64_t unrank(uint64_t r) {
+    uint64_t avail = 0xFEDCBA9876543210ull;
+    uint64_t seq = 0;
+    if constexpr (N <= 12) {
+        uint32_t rr = (uint32_t)r;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            constexpr uint32_t dummy = 0;
+            (void)dummy;
+            uint32_t f = 1;
+#pragma unroll
+            for (int j = 2; j <= N - 1 - i; ++j) f *= (uint32_t)j;
+            uint32_t d = rr / f;
+            rr -= d * f;
+            uint64_t t = (avail >> (4 * d)) & 0xFull;
+            seq |= t << (4 * i);
+            uint64_t low = (1ull << (4 * d)) - 1ull;
+            avail = (avail & low) | ((avail >> 4) & ~low);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            uint64_t f = 1;
+#pragma unroll
+            for (int j = 2; j <= N - 1 - i; ++j) f *= (uint64_t)j;
+            uint64_t d = r / f;
+            r -= d * f;
+            uint64_t t = (avail >> (4 * d)) & 0xFull;
+            seq |= t << (4 * i);
+            uint64_t low = (1ull << (4 * d)) - 1ull;
+            avail = (avail & low) | ((avail >> 4) & ~low);
+        }
+    }
+    return seq;
+}
+
+// Runtime-n unrank (general path).
+__device__ __forceinline__ uint64_t unrank_rt(uint64_t r, int n) {
+    uint64_t avail = 0xFEDCBA9876543210ull;
+    uint64_t seq = 0;
+    for (int i = 0; i < n; ++i) {
+        uint64_t f = 1;
+        for (int j = 2; j <= n - 1 - i; ++j) f *= (uint64_t)j;
+        uint64_t d = r / f;
+        r -= d * f;
+        uint64_t t = (avail >> (4 * d)) & 0xFull;
+        seq |= t << (4 * i);
+        uint64_t low = (1ull << (4 * d)) - 1ull;
+        avail = (avail & low) | ((avail >> 4) & ~low);
+    }
+    return seq;
+}
+
+// CPython builtin sum() over doubles (bltinmodule.c builtin_sum_impl):
+// 3.12+ Neumaier compensation, <=3.11 naive; the int start 0 is added first.
+struct PySum {
+    double f, c;
+    bool any;
+    __device__ __forceinline__ void reset() { f = 0.0; c = 0.0; any = false; }
+    __device__ __forceinline__ void add(double x, int mode) {
+        if (!any) { f = __dadd_rn(0.0, x); any = true; return; }
+        if (mode) {
+            double t = __dadd_rn(f, x);
+            if (fabs(f) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
+            else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));
+            f = t;
+        } else {
+            f = __dadd_rn(f, x);
+        }
+    }
+    __device__ __forceinline__ double result(int mode) const {
+        if (mode && c != 0.0 && isfinite(c)) return __dadd_rn(f, c);
+        return f;
+    }
+};
+
+}  // namespace osim

@@ -1,0 +1,408 @@
+"""Generate golden fixtures by running the UNMODIFIED reference (offsim).
+
+Run in the build container only (the reference is not on the GPU box):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [--c3]
+
+The reference is imported read-only from /root/reference/pkg/src.  Every
+float is stored as ``float.hex`` so the fixtures are bit-exact.  The Python
+version is recorded because builtin ``sum()`` (heuristic.py:47) changed to
+Neumaier summation in CPython 3.12.
+
+Fixtures (all under tests/golden/):
+  c1_bk.json          BK0..BK100 x {1dma, 2dma}: exhaustive report + heuristic (config 1)
+  sim_random.json     random ordered groups: full timelines, k_end, idle, steps
+  heuristic_random.json  random groups through reorder_batch (sum-sensitive)
+  c2_tg.json          config-2 TGs 0..3 (8 tasks, 8! orderings each)
+  c4_sample.json      config-4 input (AMD, 12 tasks): strided-rank makespans, sigma 0.5 / 0.375
+  c5_sample.json      config-5 inputs (16 tasks) x 3 profiles through reorder_batch
+  sampled.json        exhaustive_search in sampled (cap) mode
+  c3_full.json        (--c3, ~3 min on 8 cores) config-3 full 10! sweep
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import math
+import multiprocessing as mp
+import os
+import sys
+from itertools import islice, permutations
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+sys.path.insert(0, REF_SRC)
+
+import offsim  # noqa: E402
+from offsim import engine, heuristic  # noqa: E402
+from offsim.model import DeviceProfile, TaskSpec  # noqa: E402
+from offsim.oracle import exhaustive_search  # noqa: E402
+from offsim.workload import BK_NAMES, load_bk_benchmark, sample_real_tasks  # noqa: E402
+from offsim.cli import load_profile_arg  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+H = float.hex
+
+
+def meta():
+    return {
+        "python": sys.version.split()[0],
+        "sum_mode": 1 if sys.version_info >= (3, 12) else 0,
+        "numpy": np.__version__,
+        "generator": "tests/golden/make_golden.py",
+        "reference": REF_SRC,
+    }
+
+
+def dump(name, doc):
+    doc = {"meta": meta(), **doc}
+    with open(os.path.join(HERE, name), "w") as fh:
+        json.dump(doc, fh, indent=None, separators=(",", ":"))
+        fh.write("\n")
+    print("wrote", name, os.path.getsize(os.path.join(HERE, name)), "bytes")
+
+
+def prof(dma, sigma):
+    return DeviceProfile("g", dma, 0.0, 1.0, 0.0, 1.0, overlap_sigma=sigma)
+
+
+def counting_reorder(tasks, profile):
+    """reorder_batch with the number of simulate() calls it made."""
+    calls = [0]
+    real = heuristic.simulate
+
+    def counted(*a, **k):
+        calls[0] += 1
+        return real(*a, **k)
+
+    heuristic.simulate = counted
+    try:
+        out = heuristic.reorder_batch(tasks, profile)
+    finally:
+        heuristic.simulate = real
+    return out, calls[0]
+
+
+def run_steps(tasks, profile):
+    sim = engine.DeviceSim(profile)
+    sim.submit(tasks)
+    steps = 0
+    while not sim.drained():
+        assert sim.step() is not None
+        steps += 1
+    return sim.timeline(), steps
+
+
+def timeline_doc(tasks, order_idx, profile):
+    ordered = [tasks[i] for i in order_idx]
+    tl, steps = run_steps(ordered, profile)
+    ref = engine.simulate(ordered, profile)
+    assert ref.makespan == tl.makespan
+    idx = {t.id: i for i, t in enumerate(tasks)}
+    kinds = {engine.KIND_HTD: 0, engine.KIND_K: 1, engine.KIND_DTH: 2}
+    start = [[None] * 3 for _ in tasks]
+    end = [[None] * 3 for _ in tasks]
+    for c in tl.commands:
+        start[idx[c.task_id]][kinds[c.kind]] = H(c.start)
+        end[idx[c.task_id]][kinds[c.kind]] = H(c.end)
+    k_end = max((c.end for c in tl.commands if c.kind == engine.KIND_K), default=0.0)
+    return {
+        "makespan": H(tl.makespan),
+        "k_end": H(k_end),
+        "idle": [H(tl.idle[k]) for k in engine.KINDS],
+        "start": start,
+        "end": end,
+        "steps": steps,
+        "sorted_kinds": [kinds[c.kind] for c in tl.commands],
+        "sorted_tasks": [idx[c.task_id] for c in tl.commands],
+    }
+
+
+def durs_of(tasks, profile=None):
+    return [[H(float(x)) for x in offsim.stage_times(t, profile)] for t in tasks]
+
+
+def id_rank(tasks):
+    order = sorted(range(len(tasks)), key=lambda i: tasks[i].id)
+    rank = [0] * len(tasks)
+    for r, i in enumerate(order):
+        rank[i] = r
+    return rank
+
+
+def report_doc(tasks, profile, cap=10_000, seed=0, full=True):
+    rep = exhaustive_search(tasks, profile, cap=cap, seed=seed)
+    ms = np.asarray(rep.makespans)
+    idx = {t.id: i for i, t in enumerate(tasks)}
+    orderings = [[idx[i] for i in o] for o in rep.orderings]
+    head = len(ms) if full else 64
+    return {
+        "count": len(ms),
+        "makespans": [H(m) for m in rep.makespans[:head]],
+        "orderings": orderings[:head],
+        "makespans_sha256": hashlib.sha256(ms.astype("<f8").tobytes()).hexdigest(),
+        "orderings_sha256": hashlib.sha256(np.asarray(orderings, dtype=np.uint8).tobytes()).hexdigest(),
+        "best": H(rep.best),
+        "argmin": int(np.argmin(ms)),
+        "best_ordering": [idx[i] for i in rep.best_ordering],
+        "worst": H(rep.worst),
+        "median": H(rep.median),
+        "geomean": H(rep.geomean),
+        "mean": H(float(ms.mean())),
+        "exhaustive": rep.exhaustive,
+    }
+
+
+def heuristic_doc(tasks, profile):
+    out, calls = counting_reorder(tasks, profile)
+    idx = {t.id: i for i, t in enumerate(tasks)}
+    return {
+        "order": [idx[t.id] for t in out],
+        "makespan": H(engine.simulate(out, profile).makespan),
+        "n_sims": calls,
+    }
+
+
+# ---------------------------------------------------------------- C1
+def gen_c1():
+    cases = []
+    for name in BK_NAMES:
+        tasks = list(load_bk_benchmark(name).tasks)
+        for pname in ("1dma", "2dma"):
+            p = load_profile_arg(pname)
+            cases.append(
+                {
+                    "bk": name,
+                    "profile": pname,
+                    "dma": p.dma_engines,
+                    "sigma": H(p.overlap_sigma),
+                    "ids": [t.id for t in tasks],
+                    "durs": durs_of(tasks, p),
+                    "id_rank": id_rank(tasks),
+                    "report": report_doc(tasks, p),
+                    "heuristic": heuristic_doc(tasks, p),
+                    "timeline_identity": timeline_doc(tasks, list(range(len(tasks))), p),
+                }
+            )
+    dump("c1_bk.json", {"cases": cases})
+
+
+# ---------------------------------------------------------- random sims
+def rand_task_durs(rng, n, mode):
+    out = []
+    for _ in range(n):
+        while True:
+            if mode == "int":
+                d = [float(rng.integers(0, 6)) for _ in range(3)]
+            elif mode == "mixed":
+                d = [float(rng.integers(1, 4)) if rng.random() < 0.5 else float(rng.uniform(0.1, 5.0)) for _ in range(3)]
+            else:
+                d = [float(rng.uniform(0.01, 10.0)) for _ in range(3)]
+            for k in range(3):
+                if mode != "int" and rng.random() < 0.12:
+                    d[k] = 0.0
+            if d[0] + d[2] > 0 or d[1] > 0:
+                if max(d) > 0:
+                    break
+        out.append(d)
+    return out
+
+
+def gen_sim_random(count=800):
+    rng = np.random.default_rng(1806_10113)
+    sigmas = [0.375, 0.5, 0.8, 1.0]
+    cases = []
+    for c in range(count):
+        n = int(rng.integers(1, 9))
+        mode = ["int", "mixed", "real"][c % 3]
+        dma = 1 + (c // 3) % 2
+        sigma = sigmas[(c // 6) % 4]
+        d = rand_task_durs(rng, n, mode)
+        tasks = [TaskSpec(id=f"t{i}", fixed_durations=tuple(d[i])) for i in range(n)]
+        order = [int(x) for x in rng.permutation(n)]
+        p = prof(dma, sigma)
+        doc = timeline_doc(tasks, order, p)
+        doc.update({"n": n, "dma": dma, "sigma": H(sigma), "durs": [[H(x) for x in r] for r in d], "order": order})
+        cases.append(doc)
+    dump("sim_random.json", {"cases": cases})
+
+
+# ------------------------------------------------------ random heuristic
+DEVICE_PROFILES = {
+    # config 5: NVIDIA-style, AMD-style, Xeon-Phi-style
+    "nvidia": ("K20", 2, 0.5),
+    "amd": ("AMD", 2, 0.375),
+    "phi": ("PHI", 1, 1.0),
+}
+
+
+def gen_heuristic_random():
+    rng = np.random.default_rng(7)
+    cases = []
+    for pname, (dev, dma, sigma) in DEVICE_PROFILES.items():
+        p = prof(dma, sigma)
+        for n in range(1, 17):
+            for rep in range(3 if n < 16 else 10):
+                seed = 1000 * n + rep
+                tasks = sample_real_tasks(dev, n, seed=seed)
+                doc = heuristic_doc(tasks, p)
+                doc.update({"profile": pname, "dma": dma, "sigma": H(sigma), "n": n, "seed": seed,
+                            "ids": [t.id for t in tasks], "durs": durs_of(tasks), "id_rank": id_rank(tasks)})
+                cases.append(doc)
+    # small integer-valued groups (ties everywhere), like tests/test_heuristic.py:113-128
+    for c in range(120):
+        n = int(rng.integers(1, 8))
+        dma = 1 + c % 2
+        sigma = [0.5, 0.375, 1.0, 0.8][c % 4]
+        d = rand_task_durs(rng, n, "int" if c % 2 else "mixed")
+        ids = [f"x{int(v)}" for v in rng.permutation(100)[:n]]
+        tasks = [TaskSpec(id=ids[i], fixed_durations=tuple(d[i])) for i in range(n)]
+        p = prof(dma, sigma)
+        doc = heuristic_doc(tasks, p)
+        doc.update({"profile": "rand", "dma": dma, "sigma": H(sigma), "n": n, "seed": c,
+                    "ids": ids, "durs": durs_of(tasks), "id_rank": id_rank(tasks)})
+        cases.append(doc)
+    dump("heuristic_random.json", {"cases": cases})
+
+
+# ---------------------------------------------------------------- C2
+C2_SEED = 18061011302
+C2_TABLE2 = [(0.1, 0.8, 0.1), (0.2, 0.7, 0.1), (0.3, 0.6, 0.1), (0.1, 0.7, 0.2),
+             (0.6, 0.2, 0.2), (0.2, 0.2, 0.6), (0.4, 0.2, 0.4), (0.8, 0.1, 0.1)]
+
+
+def c2_durations(n_tg):
+    """Config-2 inputs: Table-2 x 10 ms x U(0.5, 1.5)."""
+    base = np.array([[f * 10.0 for f in row] for row in C2_TABLE2])
+    rng = np.random.default_rng(C2_SEED)
+    return base[None] * rng.uniform(0.5, 1.5, (100000, 8, 3))[:n_tg]
+
+
+def gen_c2(n_tg=4):
+    d = c2_durations(n_tg)
+    p = load_profile_arg("2dma")
+    tgs = []
+    for b in range(n_tg):
+        tasks = [TaskSpec(id=f"t{i:02d}", fixed_durations=tuple(float(x) for x in d[b, i])) for i in range(8)]
+        rep = exhaustive_search(tasks, p, cap=40320)
+        ms = np.asarray(rep.makespans)
+        tgs.append({
+            "tg": b,
+            "durs": [[H(float(x)) for x in r] for r in d[b]],
+            "best": H(rep.best), "argmin": int(np.argmin(ms)), "worst": H(rep.worst),
+            "median": H(rep.median), "geomean": H(rep.geomean), "mean": H(float(ms.mean())),
+            "sum": H(float(ms.sum())),
+            "makespans_sha256": hashlib.sha256(ms.astype("<f8").tobytes()).hexdigest(),
+            "makespans_head": [H(float(m)) for m in ms[:512]],
+        })
+        print("c2 tg", b, rep.best)
+    dump("c2_tg.json", {"seed": C2_SEED, "dma": 2, "sigma": H(0.5), "tgs": tgs})
+
+
+# ---------------------------------------------------------------- C4
+def gen_c4(samples=2000):
+    tasks = sample_real_tasks("AMD", 12, seed=12)
+    total = math.factorial(12)
+    stride = total // samples
+    ranks = [k * stride for k in range(samples)] + [total - 1]
+    out = {}
+    for sigma in (0.5, 0.375):
+        p = prof(2, sigma)
+        ms = []
+        for r in ranks:
+            perm = unrank(r, 12)
+            ms.append(H(engine.simulate([tasks[i] for i in perm], p).makespan))
+        out[str(sigma)] = ms
+    dump("c4_sample.json", {"durs": durs_of(tasks), "ids": [t.id for t in tasks], "dma": 2,
+                            "ranks": ranks, "makespans": out})
+
+
+def unrank(r, n):
+    avail = list(range(n))
+    perm = []
+    for i in range(n):
+        f = math.factorial(n - 1 - i)
+        d, r = divmod(r, f)
+        perm.append(avail.pop(d))
+    return perm
+
+
+# ---------------------------------------------------------------- C5
+def gen_c5(per_profile=200):
+    out = []
+    for pname, (dev, dma, sigma) in DEVICE_PROFILES.items():
+        p = prof(dma, sigma)
+        rows = []
+        for b in range(per_profile):
+            tasks = sample_real_tasks(dev, 16, seed=b)
+            doc = heuristic_doc(tasks, p)
+            rows.append({"b": b, "ids": [t.id for t in tasks], "durs": durs_of(tasks),
+                         "id_rank": id_rank(tasks), **doc})
+        out.append({"profile": pname, "device": dev, "dma": dma, "sigma": H(sigma), "rows": rows})
+        print("c5", pname)
+    dump("c5_sample.json", {"profiles": out})
+
+
+# ------------------------------------------------------------ sampled
+def gen_sampled():
+    p = load_profile_arg("2dma")
+    cases = []
+    t6 = [TaskSpec(id=f"t{i}", fixed_durations=(0.5 + 0.1 * i, 2.0, 0.5)) for i in range(6)]
+    cases.append({"name": "six_cap50_seed9", "cap": 50, "seed": 9, "durs": durs_of(t6),
+                  **report_doc(t6, p, cap=50, seed=9)})
+    t8 = sample_real_tasks("K20", 8, seed=3)
+    cases.append({"name": "k20_8_default_cap", "cap": 10_000, "seed": 0, "durs": durs_of(t8),
+                  **report_doc(t8, p, full=False)})
+    dump("sampled.json", {"dma": 2, "sigma": H(0.5), "cases": cases})
+
+
+# ---------------------------------------------------------------- C3
+def _c3_chunk(args):
+    lo, hi = args
+    tasks = sample_real_tasks("K20", 10, seed=10)
+    p = load_profile_arg("2dma")
+    out = np.empty(hi - lo)
+    for j, perm in enumerate(islice(permutations(range(10)), lo, hi)):
+        out[j] = engine.simulate([tasks[i] for i in perm], p).makespan
+    return lo, out
+
+
+def gen_c3(procs=8):
+    total = math.factorial(10)
+    chunks = [(total * k // 64, total * (k + 1) // 64) for k in range(64)]
+    ms = np.empty(total)
+    with mp.Pool(procs) as pool:
+        for lo, out in pool.imap_unordered(_c3_chunk, chunks):
+            ms[lo:lo + len(out)] = out
+    tasks = sample_real_tasks("K20", 10, seed=10)
+    relabeled = [TaskSpec(id=f"t{i:02d}", fixed_durations=t.fixed_durations) for i, t in enumerate(tasks)]
+    p = load_profile_arg("2dma")
+    heur = heuristic_doc(relabeled, p)
+    hms = float.fromhex(heur["makespan"])
+    dump("c3_full.json", {
+        "durs": durs_of(tasks), "dma": 2, "sigma": H(0.5),
+        "best": H(float(ms.min())), "argmin": int(np.argmin(ms)), "worst": H(float(ms.max())),
+        "median": H(float(np.median(ms))), "geomean": H(float(np.exp(np.log(ms).mean()))),
+        "mean": H(float(ms.mean())), "count": total,
+        "makespans_sha256": hashlib.sha256(ms.astype("<f8").tobytes()).hexdigest(),
+        "heuristic_relabeled_t00": heur,
+        "below_heuristic": int((ms < hms).sum()),
+    })
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--c3", action="store_true")
+    ap.add_argument("--only", default="")
+    a = ap.parse_args()
+    if a.c3:
+        gen_c3()
+        sys.exit(0)
+    gens = {"c1": gen_c1, "sim": gen_sim_random, "heur": gen_heuristic_random, "c2": gen_c2,
+            "c4": gen_c4, "c5": gen_c5, "sampled": gen_sampled}
+    for k, g in gens.items():
+        if not a.only or k in a.only.split(","):
+            g()

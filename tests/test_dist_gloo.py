@@ -1,0 +1,65 @@
+"""N>1 path on CPU: world_size-2 gloo process group, rank-range sharding and
+the all_gather combine of dist.exhaustive_summary_distributed.  The local
+shard reduction is the CPU oracle here (no GPU in this container); the
+combine must reproduce the single-process whole-space summary."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as tdist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+from tests._golden import F, close, durs, load
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _oracle_local(d, dma, sigma, lo, hi):
+    s, _ = O.exhaustive(d, dma, sigma, lo, hi, threads=2)
+    return s
+
+
+def _worker(rank, world, port, d, dma, sigma, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1806_10113_b200.dist import exhaustive_summary_distributed
+
+        s = exhaustive_summary_distributed(d, dma, sigma, local_fn=_oracle_local)
+        q.put((rank, s.best, s.best_rank, s.worst, s.count, s.sum, s.sum_log))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_sharded_exhaustive_matches_whole_space(world):
+    c = load("c1_bk.json")["cases"][3]  # BK25 2-DMA: a unique best at rank 19
+    d = np.concatenate([durs(c["durs"]), durs(c["durs"])[:3] * 1.25])  # 7 tasks, 5040 orderings
+    dma, sigma = c["dma"], F(c["sigma"])
+    whole, _ = O.exhaustive(d, dma, sigma, threads=4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, d, dma, sigma, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, best, rank, worst, count, sm, sl in results:
+        assert best == whole["best"] and rank == whole["best_rank"] and worst == whole["worst"]
+        assert count == whole["count"] == 5040
+        assert close(sm, whole["sum"]) and close(sl, whole["sum_log"])
+    # every rank holds the identical combined summary
+    assert len({r[1:] for r in results}) == 1

@@ -1,0 +1,252 @@
+"""Parity of the CUDA path (through the C-ABI) with the reference goldens and
+the pinned CPU oracle.  Bit-exact for makespans, argmin ranks, heuristic
+orderings and simulation counts; 1e-12 relative for mean and geomean
+(north_star tolerance)."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_1806_10113_b200 as osim
+from oracle import oracle as O
+from paper_1806_10113_b200 import _capi, synth
+from tests._golden import F, close, durs, fl, load, sha
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-12
+
+
+def assert_summary_vs_oracle(s, o):
+    assert s["count"] == o["count"]
+    assert s["best"] == o["best"] and s["best_rank"] == o["best_rank"]
+    assert s["worst"] == o["worst"]
+    assert close(s["sum"], o["sum"], REL)
+    assert close(s["sum_log"], o["sum_log"], REL)
+
+
+def test_device_present_and_library_loaded():
+    assert _capi.init() >= 1
+    assert b"sm_100a" in _capi.load().osim_version()
+
+
+def test_fast_division_matches_ieee():
+    assert _capi.selftest_div(200_000_000, seed=7) == 0
+    assert _capi.selftest_div(50_000_000, seed=12345) == 0
+
+
+def test_timelines_bit_exact():
+    g = load("sim_random.json")
+    for c in g["cases"]:
+        d = durs(c["durs"])
+        st, en, ms, idle = _capi.timeline(d, c["dma"], F(c["sigma"]), c["order"])
+        assert ms == F(c["makespan"])
+        assert idle.tolist() == fl(c["idle"])
+        for t in range(c["n"]):
+            for k in range(3):
+                if c["start"][t][k] is None:
+                    assert st[t, k] == -1.0
+                else:
+                    assert st[t, k] == F(c["start"][t][k]) and en[t, k] == F(c["end"][t][k])
+
+
+def test_simulate_dropin_timeline_order():
+    c = load("c1_bk.json")["cases"][5]
+    p = osim.DeviceProfile("2dma", 2, 0.01, 6e6, 0.01, 6e6, overlap_sigma=0.5)
+    ids, d = synth.bk_group(c["bk"])
+    tasks = [osim.TaskSpec(i, fixed_durations=tuple(r)) for i, r in zip(ids, d.tolist())]
+    tl = osim.simulate(tasks, p)
+    want = c["timeline_identity"]
+    assert tl.makespan == F(want["makespan"])
+    kinds = {"HtD": 0, "K": 1, "DtH": 2}
+    assert [kinds[x.kind] for x in tl.commands] == want["sorted_kinds"]
+    assert [ids.index(x.task_id) for x in tl.commands] == want["sorted_tasks"]
+    assert [tl.idle[k] for k in osim.KINDS] == fl(want["idle"])
+
+
+@pytest.mark.parametrize("idx", range(10))
+def test_c1_dropin_report_and_heuristic(idx):
+    c = load("c1_bk.json")["cases"][idx]
+    p = osim.DeviceProfile(c["profile"], c["dma"], 0.0, 1.0, 0.0, 1.0, overlap_sigma=F(c["sigma"]))
+    ids = c["ids"]
+    tasks = [osim.TaskSpec(i, fixed_durations=tuple(r)) for i, r in zip(ids, durs(c["durs"]).tolist())]
+    rep = osim.exhaustive_search(tasks, p)
+    want = c["report"]
+    assert rep.exhaustive is True
+    assert rep.makespans == fl(want["makespans"])
+    assert [[ids.index(x) for x in o] for o in rep.orderings] == want["orderings"]
+    assert rep.best == F(want["best"]) and rep.worst == F(want["worst"])
+    assert [ids.index(x) for x in rep.best_ordering] == want["best_ordering"]
+    assert rep.median == F(want["median"]) and rep.geomean == F(want["geomean"])
+    out = osim.reorder_batch(tasks, p)
+    assert [ids.index(t.id) for t in out] == c["heuristic"]["order"]
+    assert osim.simulate(out, p).makespan == F(c["heuristic"]["makespan"])
+
+
+def test_c2_tgs_full_space():
+    g = load("c2_tg.json")
+    for tg in g["tgs"]:
+        s, ms = _capi.exhaustive(durs(tg["durs"]), g["dma"], F(g["sigma"]), 0, 40320, want_makespans=True)
+        assert sha(ms) == tg["makespans_sha256"]
+        assert s["best"] == F(tg["best"]) and s["best_rank"] == tg["argmin"] and s["worst"] == F(tg["worst"])
+        assert float(np.median(ms)) == F(tg["median"])
+        assert close(s["sum"] / s["count"], F(tg["mean"]), REL)
+        assert close(math.exp(s["sum_log"] / s["count"]), F(tg["geomean"]), REL)
+
+
+def test_c2_batch_vs_oracle():
+    d = synth.c2_batch(512)
+    out = _capi.exhaustive_batch(d, 2, 0.5)
+    g = load("c2_tg.json")
+    for tg in g["tgs"]:
+        o = out[tg["tg"]]
+        assert o["best"] == F(tg["best"]) and o["best_rank"] == tg["argmin"] and o["worst"] == F(tg["worst"])
+        assert close(o["sum"] / o["count"], F(tg["mean"]), REL)
+    rng = np.random.default_rng(3)
+    for b in rng.choice(512, 24, replace=False):
+        o, _ = O.exhaustive(d[b], 2, 0.5, threads=8)
+        assert_summary_vs_oracle({k: out[b][k].item() for k in out.dtype.names}, o)
+    # 1-DMA on the same groups
+    out1 = _capi.exhaustive_batch(d[:16], 1, 1.0)
+    for b in range(0, 16, 5):
+        o, _ = O.exhaustive(d[b], 1, 1.0, threads=8)
+        assert_summary_vs_oracle({k: out1[b][k].item() for k in out1.dtype.names}, o)
+
+
+def test_c3_full_space_bit_exact():
+    g = load("c3_full.json")
+    s, ms = _capi.exhaustive(durs(g["durs"]), g["dma"], F(g["sigma"]), 0, 3628800, want_makespans=True)
+    assert s["count"] == 3628800
+    assert sha(ms) == g["makespans_sha256"]
+    assert s["best"] == F(g["best"]) and s["best_rank"] == g["argmin"] and s["worst"] == F(g["worst"])
+    assert float(np.median(ms)) == F(g["median"])
+    assert close(s["sum"] / s["count"], F(g["mean"]), REL)
+    assert close(math.exp(s["sum_log"] / s["count"]), F(g["geomean"]), REL)
+
+
+def test_c3_heuristic_and_percentile():
+    g = load("c3_full.json")
+    h = g["heuristic_relabeled_t00"]
+    order, ms, sims = _capi.heuristic_batch(durs(g["durs"])[None], np.arange(10, dtype=np.uint8)[None], 2,
+                                            0.5, osim.SUM_MODE)
+    assert order[0].tolist() == h["order"] and ms[0] == F(h["makespan"]) and sims[0] == h["n_sims"]
+
+
+def test_c4_sampled_ranks_and_subrange():
+    g = load("c4_sample.json")
+    d = durs(g["durs"])
+    perms = np.array([O.unrank(r, 12) for r in g["ranks"]], dtype=np.uint8)
+    for sig, want in g["makespans"].items():
+        s, ms = _capi.eval_perms(d, 2, float(sig), perms)
+        assert ms.tolist() == fl(want)
+        # a 1M-rank window of the 12! space against the oracle
+        lo = 123_456_789
+        s, _ = _capi.exhaustive(d, 2, float(sig), lo, lo + 1_000_000)
+        o, _ = O.exhaustive(d, 2, float(sig), lo, lo + 1_000_000, threads=8)
+        assert_summary_vs_oracle(s, o)
+
+
+def test_c4_full_space_consistency():
+    d = synth.c4_group()
+    total = math.factorial(12)
+    whole, _ = _capi.exhaustive(d, 2, 0.5, 0, total)
+    assert whole["count"] == total
+    parts = [_capi.exhaustive(d, 2, 0.5, total * i // 4, total * (i + 1) // 4)[0] for i in range(4)]
+    best = min(parts, key=lambda p: (p["best"], p["best_rank"]))
+    assert whole["best"] == best["best"] and whole["best_rank"] == best["best_rank"]
+    assert whole["worst"] == max(p["worst"] for p in parts)
+    assert close(whole["sum"], sum(p["sum"] for p in parts), REL)
+    # the argmin ordering re-simulates to the best makespan
+    perm = np.array([osim.search.unrank(whole["best_rank"], 12)], dtype=np.uint8)
+    _, ms = _capi.eval_perms(d, 2, 0.5, perm)
+    assert ms[0] == whole["best"]
+    r = O.simulate(d, perm[0].tolist(), 2, 0.5)
+    assert r.makespan == whole["best"]
+
+
+def test_c5_heuristic_rows_bit_exact():
+    g = load("c5_sample.json")
+    for p in g["profiles"]:
+        rows = p["rows"]
+        d = np.stack([durs(r["durs"]) for r in rows])
+        ranks = np.array([r["id_rank"] for r in rows], dtype=np.uint8)
+        order, ms, sims = _capi.heuristic_batch(d, ranks, p["dma"], F(p["sigma"]), g["meta"]["sum_mode"])
+        for i, r in enumerate(rows):
+            assert order[i].tolist() == r["order"], (p["profile"], r["b"])
+            assert ms[i] == F(r["makespan"]) and sims[i] == r["n_sims"]
+
+
+@pytest.mark.parametrize("profile", ["nvidia", "amd", "phi"])
+def test_c5_heuristic_vs_oracle_many(profile):
+    d, r = synth.c5_batch(profile, 3000, start=500_000)
+    _, dma, sigma = synth.PROFILES[profile]
+    order, ms, sims = _capi.heuristic_batch(d, r, dma, sigma, osim.SUM_MODE)
+    o_order, o_ms, o_sims = O.reorder_batch(d, r, dma, sigma, osim.SUM_MODE, threads=8)
+    assert np.array_equal(order, o_order)
+    assert np.array_equal(ms, o_ms)
+    assert np.array_equal(sims, o_sims)
+
+
+def test_heuristic_random_goldens():
+    g = load("heuristic_random.json")
+    for c in g["cases"]:
+        order, ms, sims = _capi.heuristic_batch(durs(c["durs"])[None], np.array([c["id_rank"]], np.uint8),
+                                                c["dma"], F(c["sigma"]), g["meta"]["sum_mode"])
+        assert order[0].tolist() == c["order"], (c["profile"], c["n"], c["seed"])
+        assert ms[0] == F(c["makespan"]) and sims[0] == c["n_sims"]
+
+
+def test_null_stages_general_path_vs_oracle():
+    rng = np.random.default_rng(11)
+    for trial in range(40):
+        n = int(rng.integers(2, 8))
+        d = rng.integers(0, 5, (n, 3)).astype(np.float64)
+        d[d.sum(1) == 0, 1] = 1.0
+        dma = 1 + trial % 2
+        sigma = [0.5, 0.375, 0.8, 1.0][trial % 4]
+        s, ms = _capi.exhaustive(d, dma, sigma, 0, math.factorial(n), want_makespans=True)
+        o, oms = O.exhaustive(d, dma, sigma, makespans=True)
+        assert np.array_equal(ms, oms)
+        assert_summary_vs_oracle(s, o)
+        ids = [f"t{i}" for i in rng.permutation(n)]
+        rk = np.array(sorted(range(n), key=lambda i: ids[i]), dtype=np.uint8).argsort().astype(np.uint8)
+        order, hm, hs = _capi.heuristic_batch(d[None], rk[None], dma, sigma, osim.SUM_MODE)
+        oo, om, osims = O.reorder(d, rk, dma, sigma, osim.SUM_MODE)
+        assert order[0].tolist() == oo and hm[0] == om and hs[0] == osims
+
+
+def test_sampled_mode_dropin():
+    g = load("sampled.json")
+    p = osim.DeviceProfile("2dma", 2, 0.0, 1.0, 0.0, 1.0, overlap_sigma=F(g["sigma"]))
+    for c in g["cases"]:
+        tasks = [osim.TaskSpec(f"t{i}", fixed_durations=tuple(r)) for i, r in enumerate(durs(c["durs"]).tolist())]
+        rep = osim.exhaustive_search(tasks, p, cap=c["cap"], seed=c["seed"])
+        assert rep.exhaustive is False
+        assert sha(np.array(rep.makespans)) == c["makespans_sha256"]
+        assert rep.best == F(c["best"]) and rep.worst == F(c["worst"])
+        assert rep.median == F(c["median"]) and rep.geomean == F(c["geomean"])
+        assert [int(x[1:]) for x in rep.best_ordering] == c["best_ordering"]
+
+
+def test_errors_map_to_reference_exceptions():
+    d = np.ones((3, 3))
+    with pytest.raises(ValueError):
+        _capi.exhaustive(d, 3, 0.5, 0, 6)
+    with pytest.raises(ValueError):
+        _capi.exhaustive(d, 2, 1.5, 0, 6)
+    with pytest.raises(ValueError):
+        _capi.exhaustive(d, 2, 0.5, 0, 7)
+    with pytest.raises(ValueError):
+        _capi.exhaustive(np.ones((17, 3)), 2, 0.5, 0, 1)
+    with pytest.raises(osim.UnresolvableDuration):
+        _capi.exhaustive(np.zeros((2, 3)), 2, 0.5, 0, 2)
+    with pytest.raises(Exception):
+        _capi.exhaustive(d, 2, 0.5, 0, 6, n_dev=64)
+
+
+def test_determinism_run_to_run():
+    d = synth.c4_group()
+    a, _ = _capi.exhaustive(d, 2, 0.375, 0, 50_000_000)
+    b, _ = _capi.exhaustive(d, 2, 0.375, 0, 50_000_000)
+    assert a == b
