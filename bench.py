@@ -193,8 +193,12 @@ def run_ours(a):
     _capi.set_device(D.local)
     L = _capi.load()
     dev = torch.device("cuda", D.local)
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the library maps a NULL stream to its
+    # own stream, and torch's legacy default stream has handle 0
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     sp = C.c_void_p(stream.cuda_stream)
+    assert stream.cuda_stream != 0
     flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     def flush():
