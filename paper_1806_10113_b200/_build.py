@@ -17,15 +17,19 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liboffsim_b200.so")
-SOURCES = [os.path.join(CSRC, "osim_capi.cu")]
-HEADERS = [os.path.join(CSRC, f) for f in ("osim_sim.cuh", "osim_kernels.cuh")] + [
+SOURCES = [os.path.join(CSRC, f) for f in (
+    "osim_capi.cu", "osim_exh_d2s1.cu", "osim_exh_d2s0.cu", "osim_exh_d1.cu",
+    "osim_batch_d2.cu", "osim_batch_d1.cu", "osim_heur.cu")]
+HEADERS = [os.path.join(CSRC, f) for f in (
+    "osim_sim.cuh", "osim_kernels.cuh", "osim_launch.cuh", "osim_exh_impl.cuh", "osim_batch_impl.cuh")] + [
     os.path.join(ROOT, "include", "offsim_b200.h")
 ]
+OBJDIR = os.path.join(PKG, "build")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-I", os.path.join(ROOT, "include"),
 ]
 
@@ -44,12 +48,26 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
-        return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", *SOURCES]
+def _compile(src: str, verbose: bool) -> str:
+    obj = os.path.join(OBJDIR, os.path.basename(src).replace(".cu", ".o"))
+    cmd = [nvcc(), *NVCC_FLAGS, "-c", "-o", obj, src]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    return obj
+
+
+def build(force: bool = False, verbose: bool = False, jobs: int = 0) -> str:
+    """Compile the translation units in parallel, link the shared library."""
+    if not force and not stale():
+        return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
+    os.makedirs(OBJDIR, exist_ok=True)
+    jobs = jobs or min(len(SOURCES), os.cpu_count() or 1)
+    with ThreadPoolExecutor(jobs) as ex:
+        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp", *objs]
     subprocess.run(cmd, check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB

@@ -6,12 +6,13 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
 
-#include "osim_kernels.cuh"
+#include "osim_launch.cuh"
 
 using namespace osim;
 
@@ -123,62 +124,37 @@ uint64_t factorial(int n) {
 
 template <class K>
 int grid_for(K kernel, int threads, size_t smem, const DevCtx* c, uint64_t work_blocks) {
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
-    if (per_sm < 1) per_sm = 1;
-    uint64_t g = (uint64_t)per_sm * c->sms;
-    if (work_blocks < g) g = work_blocks;
-    if (g < 1) g = 1;
-    return (int)g;
+    return osim::grid_for_sms(kernel, threads, smem, c->sms, work_blocks);
 }
 
-// ---- launchers (stream-ordered, no sync) -------------------------------
-template <int N, int DMA>
-int launch_exh_fast_t(DevCtx* c, cudaStream_t st, const double* d_durs, double sigma, uint64_t lo,
-                      uint64_t hi, Part* parts, int max_parts, double* d_ms, int* grid_out) {
-    auto k = k_exhaustive_fast<N, DMA>;
-    uint64_t blocks = (hi - lo + kBlock - 1) / kBlock;
-    int g = grid_for(k, kBlock, 0, c, blocks);
-    if (g > max_parts) g = max_parts;
-    k<<<g, kBlock, 0, st>>>(d_durs, sigma, lo, hi, parts, d_ms);
-    *grid_out = g;
+bool sigma_pow2(double sigma) {
+    int e;
+    double m = std::frexp(sigma, &e);
+    return m == 0.5 && e > -900;
+}
+
+int launch_exh_fast_dispatch(int dma, int n, DevCtx* c, cudaStream_t st, const double* d_durs, double sigma,
+                             uint64_t lo, uint64_t hi, Part* parts, int max_parts, double* d_ms, int* g) {
+    const LaunchCfg cfg{c->sms, st};
+    const int L = pfx_l_for(n);
+    int rc;
+    if (dma == 2)
+        rc = sigma_pow2(sigma) ? exh_fast_launch_d2s1(n, L, cfg, d_durs, sigma, lo, hi, parts, max_parts, d_ms, g)
+                               : exh_fast_launch_d2s0(n, L, cfg, d_durs, sigma, lo, hi, parts, max_parts, d_ms, g);
+    else
+        rc = exh_fast_launch_d1(n, L, cfg, d_durs, sigma, lo, hi, parts, max_parts, d_ms, g);
+    if (rc) return fail(OSIM_EINVAL, "unsupported n=%d", n);
     return 0;
 }
 
-template <int DMA>
-int launch_exh_fast(int n, DevCtx* c, cudaStream_t st, const double* d_durs, double sigma,
-                    uint64_t lo, uint64_t hi, Part* parts, int max_parts, double* d_ms, int* g) {
-    switch (n) {
-#define OSIM_CASE(NN) \
-    case NN: return launch_exh_fast_t<NN, DMA>(c, st, d_durs, sigma, lo, hi, parts, max_parts, d_ms, g);
-        OSIM_CASE(1) OSIM_CASE(2) OSIM_CASE(3) OSIM_CASE(4) OSIM_CASE(5) OSIM_CASE(6)
-        OSIM_CASE(7) OSIM_CASE(8) OSIM_CASE(9) OSIM_CASE(10) OSIM_CASE(11) OSIM_CASE(12)
-        OSIM_CASE(13) OSIM_CASE(14) OSIM_CASE(15) OSIM_CASE(16)
-#undef OSIM_CASE
-    }
-    return fail(OSIM_EINVAL, "unsupported n=%d", n);
-}
-
-template <int N, int DMA>
-int launch_batch_fast_t(DevCtx* c, cudaStream_t st, const double* d_durs, uint64_t B, double sigma,
-                        osim_summary* d_out) {
-    auto k = k_exhaustive_batch_fast<N, DMA>;
-    int g = grid_for(k, kBlock, 0, c, B);
-    k<<<g, kBlock, 0, st>>>(d_durs, B, sigma, d_out);
+int launch_batch_fast_dispatch(int dma, int n, DevCtx* c, cudaStream_t st, const double* d_durs, uint64_t B,
+                               double sigma, osim_summary* d_out) {
+    const LaunchCfg cfg{c->sms, st};
+    const int L = pfx_l_for(n);
+    int rc = dma == 2 ? batch_fast_launch_d2(n, L, sigma_pow2(sigma), cfg, d_durs, B, sigma, d_out)
+                      : batch_fast_launch_d1(n, L, cfg, d_durs, B, sigma, d_out);
+    if (rc) return fail(OSIM_EINVAL, "unsupported n=%d", n);
     return 0;
-}
-
-template <int DMA>
-int launch_batch_fast(int n, DevCtx* c, cudaStream_t st, const double* d_durs, uint64_t B,
-                      double sigma, osim_summary* d_out) {
-    switch (n) {
-#define OSIM_CASE(NN) case NN: return launch_batch_fast_t<NN, DMA>(c, st, d_durs, B, sigma, d_out);
-        OSIM_CASE(1) OSIM_CASE(2) OSIM_CASE(3) OSIM_CASE(4) OSIM_CASE(5) OSIM_CASE(6)
-        OSIM_CASE(7) OSIM_CASE(8) OSIM_CASE(9) OSIM_CASE(10) OSIM_CASE(11) OSIM_CASE(12)
-        OSIM_CASE(13) OSIM_CASE(14) OSIM_CASE(15) OSIM_CASE(16)
-#undef OSIM_CASE
-    }
-    return fail(OSIM_EINVAL, "unsupported n=%d", n);
 }
 
 // Enqueue exhaustive over [lo, hi) and its final reduce into d_out.
@@ -189,8 +165,7 @@ int enqueue_exhaustive(DevCtx* c, cudaStream_t st, const double* d_durs, int n, 
     int rc = 0;
     if (hi > lo) {
         if (fast) {
-            rc = dma == 2 ? launch_exh_fast<2>(n, c, st, d_durs, sigma, lo, hi, parts, max_parts, d_ms, &g)
-                          : launch_exh_fast<1>(n, c, st, d_durs, sigma, lo, hi, parts, max_parts, d_ms, &g);
+            rc = launch_exh_fast_dispatch(dma, n, c, st, d_durs, sigma, lo, hi, parts, max_parts, d_ms, &g);
         } else {
             uint64_t blocks = (hi - lo + kBlock - 1) / kBlock;
             if (dma == 2) {
@@ -219,8 +194,7 @@ int enqueue_batch(DevCtx* c, cudaStream_t st, const double* d_durs, uint64_t B, 
     if (B == 0) return 0;
     int rc = 0;
     if (fast) {
-        rc = dma == 2 ? launch_batch_fast<2>(n, c, st, d_durs, B, sigma, d_out)
-                      : launch_batch_fast<1>(n, c, st, d_durs, B, sigma, d_out);
+        rc = launch_batch_fast_dispatch(dma, n, c, st, d_durs, B, sigma, d_out);
     } else if (dma == 2) {
         int g = grid_for(k_exhaustive_batch_gen<2>, kBlock, 0, c, B);
         k_exhaustive_batch_gen<2><<<g, kBlock, 0, st>>>(d_durs, B, n, sigma, d_out, c->d_err);
@@ -237,14 +211,9 @@ int enqueue_heuristic(DevCtx* c, cudaStream_t st, const double* d_durs, const ui
                       uint64_t B, int n, int dma, double sigma, int sum_mode, int fast,
                       uint8_t* d_order, double* d_ms, uint32_t* d_ns) {
     if (B == 0) return 0;
-    const uint64_t grid = (B + kHG - 1) / kHG;
-    if (grid > 0x7fffffffull) return fail(OSIM_EINVAL, "batch too large");
-    const size_t sm = sizeof(HeurShared);
-#define OSIM_HL(D, F) \
-    k_heuristic<D, F><<<(unsigned)grid, kHT, sm, st>>>(d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms, d_ns, c->d_err)
-    if (dma == 2) { if (fast) OSIM_HL(2, true); else OSIM_HL(2, false); }
-    else { if (fast) OSIM_HL(1, true); else OSIM_HL(1, false); }
-#undef OSIM_HL
+    if ((B + kHG - 1) / kHG > 0x7fffffffull) return fail(OSIM_EINVAL, "batch too large");
+    heuristic_launch(dma, fast != 0, LaunchCfg{c->sms, st}, d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms,
+                     d_ns, c->d_err);
     CK(cudaGetLastError());
     return 0;
 }

@@ -157,38 +157,9 @@ __device__ __forceinline__ void run_warp(S& s, int max_steps) {
 }
 
 // ---------------------------------------------------------------------------
-// Exhaustive search over ranks [lo, hi) of one group (oracle.py:123-135).
-// One thread per ordering, Lehmer-unranked on the fly; per-block partials.
+// Exhaustive search, general path (null stages or out-of-range durations):
+// one thread per ordering, Lehmer-unranked, IEEE division.
 // ---------------------------------------------------------------------------
-template <int N, int DMA>
-__global__ void __launch_bounds__(kBlock) k_exhaustive_fast(const double* __restrict__ durs,
-                                                            double sigma, uint64_t lo, uint64_t hi,
-                                                            Part* __restrict__ parts,
-                                                            double* __restrict__ ms_out) {
-    __shared__ double sd[3 * kStride], sr[3 * kStride];
-    __shared__ Part sh[32];
-    stage_durs(durs, N, sd, sr);
-    __syncthreads();
-    const double rsig = __ddiv_rn(1.0, sigma);
-    const Durs D{sd, sr};
-    Part acc;
-    part_init(acc);
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t base = lo + (uint64_t)blockIdx.x * blockDim.x; base < hi; base += stride) {
-        const uint64_t r = base + threadIdx.x;
-        const bool valid = r < hi;
-        Sim<DMA, true, true, false> s;
-        s.init(D, unrank<N>(valid ? r : lo), N, sigma, rsig);
-        run_warp(s, 3 * N);
-        if (valid) {
-            part_add<false>(acc, s.now, r);
-            if (ms_out) ms_out[r - lo] = s.now;
-        }
-    }
-    acc = block_reduce(acc, sh);
-    if (threadIdx.x == 0) parts[blockIdx.x] = acc;
-}
-
 template <int DMA>
 __global__ void __launch_bounds__(kBlock) k_exhaustive_gen(const double* __restrict__ durs, int n,
                                                            double sigma, uint64_t lo, uint64_t hi,
@@ -222,7 +193,7 @@ __global__ void __launch_bounds__(kBlock) k_exhaustive_gen(const double* __restr
 }
 
 // Deterministic final reduce of per-block partials (fixed order).
-__global__ void __launch_bounds__(kBlock) k_final_reduce(const Part* __restrict__ parts, int P,
+static __global__ void __launch_bounds__(kBlock) k_final_reduce(const Part* __restrict__ parts, int P,
                                                          osim_summary* __restrict__ out) {
     __shared__ Part sh[32];
     Part a;
@@ -230,6 +201,136 @@ __global__ void __launch_bounds__(kBlock) k_final_reduce(const Part* __restrict_
     for (int i = threadIdx.x; i < P; i += blockDim.x) part_merge(a, parts[i]);
     a = block_reduce(a, sh);
     if (threadIdx.x == 0) *out = part_to_summary(a);
+}
+
+// ---------------------------------------------------------------------------
+// Prefix-sharing exhaustive search (fast path).
+// Lexicographic rank order groups orderings by prefix: ranks
+// [P*L!, (P+1)*L!) share positions 0..M-1 (M = N-L) and permute the L
+// remaining tasks.  Everything the simulator does before the HtD (XFER) lane
+// is free to start position M depends only on positions 0..M-1: a command
+// of position >= M can only start after HtD(M) started, and HtD(M) starts
+// the step after HtD(M-1) finalized (both FIFOs hold the ordering in
+// position order; on a 1-DMA device every DtH queues behind every HtD).  So
+// a thread simulates its prefix once up to that checkpoint (phase A), keeps
+// the register state, and replays only the L! suffixes from it (phase B).
+// The per-ordering operation sequence is unchanged, so results are
+// bit-identical to simulating each ordering from time 0.
+// ---------------------------------------------------------------------------
+template <int L>
+struct Fact {
+    static constexpr uint64_t v = (uint64_t)L * Fact<L - 1>::v;
+};
+template <>
+struct Fact<0> {
+    static constexpr uint64_t v = 1;
+};
+
+__device__ __forceinline__ void stage_dr(const double* __restrict__ g, int n, double2* sdr) {
+    for (int i = threadIdx.x; i < 3 * kStride; i += blockDim.x) {
+        const int k = i / kStride, t = i % kStride;
+        const double v = t < n ? g[3 * t + k] : 1.0;
+        sdr[i] = make_double2(v, __ddiv_rn(1.0, v));
+    }
+}
+
+// Simulate prefix P of length M and every suffix; accumulate leaves that
+// fall inside [lo, hi).  All threads of the warp must call together.
+template <int N, int DMA, bool SIGP2, int L, bool WRITE_MS>
+__device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double rsig, uint64_t P,
+                                           bool validP, uint64_t lo, uint64_t hi, Part& acc,
+                                           double* __restrict__ ms_out, uint64_t ms_base) {
+    constexpr int M = N - L;
+    constexpr uint64_t LF = Fact<L>::v;
+    const uint64_t seq0 = unrank<N>(P * LF);  // prefix + ascending remainder
+    using FS = FastSim<DMA, SIGP2, false, (N <= 15)>;
+    FS s;
+    s.init(base, seq0, N);
+    int sa = 0;
+    if constexpr (M > 0) {
+#pragma unroll 1
+        while (__any_sync(kFull, s.htd_done() < M)) {
+            if (s.htd_done() < M) {
+                s.step(sigma, rsig);
+                ++sa;
+            }
+        }
+    }
+    const int rest = 3 * N - __reduce_min_sync(kFull, sa);
+    const FS ck = s;
+    const uint64_t pre = (M > 0) ? (seq0 & ((1ull << (4 * M)) - 1ull)) : 0ull;
+    const uint64_t rem = seq0 >> (4 * M);  // L ascending task ids
+#pragma unroll 1
+    for (int j = 0; j < (int)LF; ++j) {
+        const uint64_t idx = unrank<L>((uint64_t)j);
+        uint64_t suf = 0;
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+            const uint32_t id = (uint32_t)(idx >> (4 * i)) & 0xFu;
+            suf |= ((rem >> (4 * id)) & 0xFull) << (4 * (M + i));
+        }
+        s = ck;
+        s.set_seq(pre | suf);
+#pragma unroll 2
+        for (int st = 0; st < rest; ++st) s.step(sigma, rsig);
+        const uint64_t r = P * LF + (uint64_t)j;
+        if (validP && r >= lo && r < hi) {
+            part_add<false>(acc, s.now, r);
+            if constexpr (WRITE_MS) {
+                if (ms_out) ms_out[r - ms_base] = s.now;
+            }
+        }
+    }
+}
+
+template <int N, int DMA, bool SIGP2, int L>
+__global__ void __launch_bounds__(kBlock) k_exhaustive_pfx(const double* __restrict__ durs, double sigma,
+                                                           uint64_t lo, uint64_t hi, Part* __restrict__ parts,
+                                                           double* __restrict__ ms_out) {
+    __shared__ double2 sdr[3 * kStride];
+    __shared__ Part sh[32];
+    stage_dr(durs, N, sdr);
+    __syncthreads();
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
+    const double rsig = __ddiv_rn(1.0, sigma);
+    constexpr uint64_t LF = Fact<L>::v;
+    const uint64_t p_lo = lo / LF, p_hi = (hi + LF - 1) / LF;
+    Part acc;
+    part_init(acc);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t pb = p_lo + (uint64_t)blockIdx.x * blockDim.x; pb < p_hi; pb += stride) {
+        const uint64_t P = pb + threadIdx.x;
+        const bool validP = P < p_hi;
+        pfx_leaves<N, DMA, SIGP2, L, true>(base, sigma, rsig, validP ? P : p_lo, validP, lo, hi, acc, ms_out, lo);
+    }
+    acc = block_reduce(acc, sh);
+    if (threadIdx.x == 0) parts[blockIdx.x] = acc;
+}
+
+// Batched groups with prefix sharing: one CTA per group.
+template <int N, int DMA, bool SIGP2, int L>
+__global__ void __launch_bounds__(kBlock) k_exhaustive_batch_pfx(const double* __restrict__ durs, uint64_t B,
+                                                                 double sigma, osim_summary* __restrict__ out) {
+    __shared__ double2 sdr[3 * kStride];
+    __shared__ Part sh[32];
+    constexpr uint64_t total = Fact<N>::v;
+    constexpr uint64_t NP = total / Fact<L>::v;
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
+    const double rsig = __ddiv_rn(1.0, sigma);
+    for (uint64_t b = blockIdx.x; b < B; b += gridDim.x) {
+        stage_dr(durs + b * 3 * N, N, sdr);
+        __syncthreads();
+        Part acc;
+        part_init(acc);
+        for (uint64_t pb = 0; pb < NP; pb += blockDim.x) {
+            const uint64_t P = pb + threadIdx.x;
+            const bool validP = P < NP;
+            pfx_leaves<N, DMA, SIGP2, L, false>(base, sigma, rsig, validP ? P : 0, validP, 0, total, acc,
+                                                nullptr, 0);
+        }
+        acc = block_reduce(acc, sh);  // ends with __syncthreads: smem reusable
+        if (threadIdx.x == 0) out[b] = part_to_summary(acc);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -272,40 +373,7 @@ __global__ void __launch_bounds__(kBlock) k_eval_perms(const double* __restrict_
     if (threadIdx.x == 0) parts[blockIdx.x] = acc;
 }
 
-// ---------------------------------------------------------------------------
-// Batched groups (config 2): one CTA per group, n! orderings per CTA.
-// ---------------------------------------------------------------------------
-template <int N, int DMA>
-__global__ void __launch_bounds__(kBlock) k_exhaustive_batch_fast(const double* __restrict__ durs,
-                                                                  uint64_t B, double sigma,
-                                                                  osim_summary* __restrict__ out) {
-    __shared__ double sd[3 * kStride], sr[3 * kStride];
-    __shared__ Part sh[32];
-    constexpr uint64_t total = [] {
-        uint64_t f = 1;
-        for (int i = 2; i <= N; ++i) f *= (uint64_t)i;
-        return f;
-    }();
-    const double rsig = __ddiv_rn(1.0, sigma);
-    for (uint64_t b = blockIdx.x; b < B; b += gridDim.x) {
-        stage_durs(durs + b * 3 * N, N, sd, sr);
-        __syncthreads();
-        const Durs D{sd, sr};
-        Part acc;
-        part_init(acc);
-        for (uint64_t base = 0; base < total; base += blockDim.x) {
-            const uint64_t r = base + threadIdx.x;
-            const bool valid = r < total;
-            Sim<DMA, true, true, false> s;
-            s.init(D, unrank<N>(valid ? r : 0), N, sigma, rsig);
-            run_warp(s, 3 * N);
-            if (valid) part_add<false>(acc, s.now, r);
-        }
-        acc = block_reduce(acc, sh);  // ends with __syncthreads: smem reusable
-        if (threadIdx.x == 0) out[b] = part_to_summary(acc);
-    }
-}
-
+// Batched groups, general path: one CTA per group, n! orderings per CTA.
 template <int DMA>
 __global__ void __launch_bounds__(kBlock) k_exhaustive_batch_gen(const double* __restrict__ durs,
                                                                  uint64_t B, int n, double sigma,
@@ -386,10 +454,10 @@ __global__ void k_timeline(const double* __restrict__ durs, int n, double sigma,
 // ---------------------------------------------------------------------------
 constexpr int kHG = 32;     // groups per CTA
 constexpr int kHT = 128;    // threads per CTA
-constexpr int kHS = 97;     // doubles per group: 48 durations + 48 reciprocals + pad
+constexpr int kHS = 49;     // double2 per group: [3][16] {nd, 1/nd} + 1 pad (bank spread)
 
 struct HeurShared {
-    double dr[kHG * kHS];
+    double2 dr[kHG * kHS];
     double ka[kHG * kMaxN];
     double kb[kHG * kMaxN];
     uint64_t ot[kHG];
@@ -398,6 +466,38 @@ struct HeurShared {
     uint8_t idr[kHG * kMaxN];
     uint8_t cand[kHG * kMaxN];
     uint8_t pa[kHG], pb[kHG];
+};
+
+// One simulation of `seq` (len positions) of group g; FAST uses FastSim.
+template <int DMA, bool FAST, bool TRACK>
+struct HeurRun {
+    double ms, kEnd, idleK;
+    bool ok;
+    __device__ __forceinline__ void run(HeurShared& S, uint32_t sbase, int g, uint64_t seq, int len, double sigma,
+                                        double rsig, bool sp2) {
+        if constexpr (FAST) {
+            const uint32_t base = sbase + (uint32_t)(g * kHS * sizeof(double2));
+            if (sp2 && DMA == 2) {
+                FastSim<DMA, true, TRACK, false> s;
+                s.init(base, seq, len);
+#pragma unroll 1
+                for (int st = 0; st < 3 * len; ++st) s.step(sigma, rsig);
+                ms = s.now; kEnd = s.kEnd; idleK = s.idleK; ok = s.drained();
+            } else {
+                FastSim<DMA, false, TRACK, false> s;
+                s.init(base, seq, len);
+#pragma unroll 1
+                for (int st = 0; st < 3 * len; ++st) s.step(sigma, rsig);
+                ms = s.now; kEnd = s.kEnd; idleK = s.idleK; ok = s.drained();
+            }
+        } else {
+            const double* p = reinterpret_cast<const double*>(&S.dr[g * kHS]);
+            Sim<DMA, false, false, TRACK> s;
+            s.init(Durs{p, p + 1, 2}, seq, len, sigma, rsig, S.nH[g], S.nK[g], S.nD[g]);
+            run_warp(s, 3 * len);
+            ms = s.now; kEnd = s.kEnd; idleK = s.idleK; ok = s.drained();
+        }
+    }
 };
 
 template <int DMA, bool FAST>
@@ -410,18 +510,20 @@ __global__ void __launch_bounds__(kHT) k_heuristic(const double* __restrict__ du
                                                    int* __restrict__ err) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     HeurShared& S = *reinterpret_cast<HeurShared*>(smem_raw);
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(S.dr);
     const uint64_t g0 = (uint64_t)blockIdx.x * kHG;
     const int Gv = (int)((B - g0) < (uint64_t)kHG ? (B - g0) : (uint64_t)kHG);
     const double rsig = __ddiv_rn(1.0, sigma);
+    int se;
+    const bool sp2 = frexp(sigma, &se) == 0.5;
     const int tid = threadIdx.x;
 
-    // stage durations (kind-major rows) + reciprocals + id ranks
+    // stage durations ({nd, 1/nd}, kind-major rows) + id ranks
     for (int i = tid; i < Gv * 3 * kStride; i += blockDim.x) {
         const int g = i / (3 * kStride), r = i % (3 * kStride);
         const int k = r / kStride, t = r % kStride;
         const double v = t < n ? durs[(g0 + g) * 3 * (uint64_t)n + 3 * t + k] : 1.0;
-        S.dr[g * kHS + r] = v;
-        S.dr[g * kHS + 3 * kStride + r] = __ddiv_rn(1.0, v);
+        S.dr[g * kHS + r] = make_double2(v, __ddiv_rn(1.0, v));
     }
     for (int i = tid; i < Gv * kMaxN; i += blockDim.x) {
         const int g = i / kMaxN, t = i % kMaxN;
@@ -429,8 +531,7 @@ __global__ void __launch_bounds__(kHT) k_heuristic(const double* __restrict__ du
     }
     __syncthreads();
 
-    auto durs_of = [&](int g) { return Durs{&S.dr[g * kHS], &S.dr[g * kHS + 3 * kStride]}; };
-    auto DV = [&](int g, int k, int t) { return S.dr[g * kHS + k * kStride + t]; };
+    auto DV = [&](int g, int k, int t) { return S.dr[g * kHS + k * kStride + t].x; };
 
     // select_first_task (heuristic.py:22-31): min over rt of
     // (-(t_k - t_htd), -t_dth, id)
@@ -483,9 +584,8 @@ __global__ void __launch_bounds__(kHT) k_heuristic(const double* __restrict__ du
             const int j = valid ? i % m : 0;
             const int c = S.cand[g * kMaxN + j];
             const uint64_t seq = S.ot[g] | ((uint64_t)c << (4 * k));
-            Sim<DMA, FAST, FAST, true> s;
-            s.init(durs_of(g), seq, k + 1, sigma, rsig, S.nH[g], S.nK[g], S.nD[g]);
-            run_warp(s, 3 * (k + 1));
+            HeurRun<DMA, FAST, true> hr;
+            hr.run(S, sbase, g, seq, k + 1, sigma, rsig, sp2);
             // _completion_estimate (heuristic.py:34-49); rest in rt order
             PySum ps;
             ps.reset();
@@ -499,11 +599,11 @@ __global__ void __launch_bounds__(kHT) k_heuristic(const double* __restrict__ du
                 if (!any || d < tail) tail = d;
                 any = true;
             }
-            const double bound = __dadd_rn(__dadd_rn(s.kEnd, ps.result(sum_mode)), tail);
-            const double est = (bound > s.now) ? bound : s.now;
+            const double bound = __dadd_rn(__dadd_rn(hr.kEnd, ps.result(sum_mode)), tail);
+            const double est = (bound > hr.ms) ? bound : hr.ms;
             if (valid) {
                 S.ka[g * kMaxN + j] = est;
-                S.kb[g * kMaxN + j] = s.idleK;
+                S.kb[g * kMaxN + j] = hr.idleK;
             }
         }
         __syncthreads();
@@ -549,10 +649,9 @@ __global__ void __launch_bounds__(kHT) k_heuristic(const double* __restrict__ du
             const int w = i & 1;
             const uint64_t x = w ? S.pb[g] : S.pa[g], y = w ? S.pa[g] : S.pb[g];
             const uint64_t seq = S.ot[g] | (x << (4 * kl)) | (y << (4 * (kl + 1)));
-            Sim<DMA, FAST, FAST, false> s;
-            s.init(durs_of(g), seq, n, sigma, rsig, S.nH[g], S.nK[g], S.nD[g]);
-            run_warp(s, 3 * n);
-            if (valid) S.ka[g * kMaxN + w] = s.now;
+            HeurRun<DMA, FAST, false> hr;
+            hr.run(S, sbase, g, seq, n, sigma, rsig, sp2);
+            if (valid) S.ka[g * kMaxN + w] = hr.ms;
         }
         __syncthreads();
         if (tid < Gv) {
@@ -573,12 +672,11 @@ __global__ void __launch_bounds__(kHT) k_heuristic(const double* __restrict__ du
         const int i = i0 + tid;
         const bool valid = i < Gv;
         const int g = valid ? i : 0;
-        Sim<DMA, FAST, FAST, false> s;
-        s.init(durs_of(g), S.ot[g], n, sigma, rsig, S.nH[g], S.nK[g], S.nD[g]);
-        run_warp(s, 3 * n);
-        if (!s.drained()) atomicExch(err, OSIM_ESTALL);
+        HeurRun<DMA, FAST, false> hr;
+        hr.run(S, sbase, g, S.ot[g], n, sigma, rsig, sp2);
+        if (!hr.ok) atomicExch(err, OSIM_ESTALL);
         if (valid) {
-            ms_out[g0 + g] = s.now;
+            ms_out[g0 + g] = hr.ms;
             if (nsims_out) nsims_out[g0 + g] = (n >= 3) ? (uint32_t)(n * (n - 1) / 2 - 1) : (n == 2 ? 2u : 0u);
         }
     }
@@ -598,7 +696,7 @@ __device__ __forceinline__ uint64_t splitmix(uint64_t& x) {
     return z ^ (z >> 31);
 }
 
-__global__ void k_selftest_div(uint64_t samples, uint64_t seed, unsigned long long* mism) {
+static __global__ void k_selftest_div(uint64_t samples, uint64_t seed, unsigned long long* mism) {
     uint64_t st = seed ^ ((uint64_t)(blockIdx.x * blockDim.x + threadIdx.x) * 0x2545F4914F6CDD1Dull);
     unsigned long long bad = 0;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -629,7 +727,7 @@ __global__ void k_selftest_div(uint64_t samples, uint64_t seed, unsigned long lo
 }
 
 // DFMA throughput: 8 independent chains per thread.
-__global__ void __launch_bounds__(256) k_fp64_peak(double* sink, int iters, double a, double b) {
+static __global__ void __launch_bounds__(256) k_fp64_peak(double* sink, int iters, double a, double b) {
     double x0 = threadIdx.x * 1e-9, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
     double x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
 #pragma unroll 1

@@ -1,0 +1,63 @@
+// osim_launch.cuh -- internal launcher interface between the C-ABI host code
+// (osim_capi.cu) and the kernel translation units, which are compiled in
+// parallel (osim_exh_*.cu, osim_batch_*.cu, osim_heur.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "osim_kernels.cuh"
+
+namespace osim {
+
+struct LaunchCfg {
+    int sms;
+    cudaStream_t st;
+};
+
+template <class K>
+int grid_for_sms(K kernel, int threads, size_t smem, int sms, uint64_t work_blocks) {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    uint64_t g = (uint64_t)per_sm * sms;
+    if (work_blocks < g) g = work_blocks;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+// Suffix length L of the prefix-sharing kernels per n.
+// OSIM_PFX_L=<3|4|5> overrides it for n in {8, 10, 12} (tuning only).
+constexpr int default_pfx_l(int n) { return n <= 3 ? 1 : (n <= 5 ? 2 : (n <= 10 ? 3 : 4)); }
+constexpr bool tunable_n(int n) { return n == 8 || n == 10 || n == 12; }
+
+inline int pfx_l_for(int n) {
+    static const int env = [] {
+        const char* e = getenv("OSIM_PFX_L");
+        return e ? atoi(e) : 0;
+    }();
+    if (env >= 3 && env <= 5 && tunable_n(n)) return env;
+    return default_pfx_l(n);
+}
+
+// exhaustive, all stages non-null, prefix-sharing (returns -1: unsupported n)
+#define OSIM_EXH_DECL(NAME)                                                                          \
+    int NAME(int n, int L, const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo,   \
+             uint64_t hi, Part* parts, int max_parts, double* d_ms, int* grid_out);
+OSIM_EXH_DECL(exh_fast_launch_d2s1)
+OSIM_EXH_DECL(exh_fast_launch_d2s0)
+OSIM_EXH_DECL(exh_fast_launch_d1)
+#undef OSIM_EXH_DECL
+
+int batch_fast_launch_d2(int n, int L, bool sp2, const LaunchCfg& cfg, const double* d_durs, uint64_t B,
+                         double sigma, osim_summary* d_out);
+int batch_fast_launch_d1(int n, int L, const LaunchCfg& cfg, const double* d_durs, uint64_t B, double sigma,
+                         osim_summary* d_out);
+
+void heuristic_launch(int dma, bool fast, const LaunchCfg& cfg, const double* d_durs, const uint8_t* d_idr,
+                      uint64_t B, int n, double sigma, int sum_mode, uint8_t* d_order, double* d_ms,
+                      uint32_t* d_ns, int* d_err);
+
+}  // namespace osim

@@ -58,10 +58,11 @@ __device__ __forceinline__ double pymax0(double left) { return (0.0 > left) ? 0.
 
 // Per-thread view of one task group's durations in shared memory.
 struct Durs {
-    const double* d;  // d[k*kStride + t], k = 0 HtD, 1 K, 2 DtH
+    const double* d;  // d[s*(k*kStride + t)], k = 0 HtD, 1 K, 2 DtH
     const double* r;  // 1/d, same layout
-    __device__ __forceinline__ double nd(int k, int t) const { return d[k * kStride + t]; }
-    __device__ __forceinline__ double rc(int k, int t) const { return r[k * kStride + t]; }
+    int s = 1;        // 1: separate arrays; 2: interleaved {nd, 1/nd} pairs
+    __device__ __forceinline__ double nd(int k, int t) const { return d[s * (k * kStride + t)]; }
+    __device__ __forceinline__ double rc(int k, int t) const { return r[s * (k * kStride + t)]; }
 };
 
 // Optional full-timeline record (timeline mode only, general path).
@@ -295,6 +296,155 @@ struct Sim {
             step(tl);
         }
         return drained();
+    }
+};
+
+// ---------------------------------------------------------------------------
+// FastSim: the all-stages-non-null path with the instruction count cut to
+// the bone (the kernels are issue-bound, not FP64-bound).  Exactly the same
+// arithmetic as Sim<FAST=true>; the differences are representational:
+//  * idle lanes hold rem = 2^900 instead of a running flag in the dt min and
+//    the update (no selects; 2^900 * (1/nd) cannot overflow for durations in
+//    [2^-60, 2^60], and 2^900 - dt == 2^900);
+//  * max(left, 0.0) (engine.py:214) is dropped: when left <= 0 the command
+//    finalizes in this step with or without it (rw*nd <= 0 <= 1e-9), and a
+//    finalized command's rw is never read again (engine.py:223);
+//  * dt = min(rem_H/s, rem_D/s, rem_K) = min(RN(min(rem_H, rem_D)/s), rem_K):
+//    RN(x/s) is monotone in x, so one division per step instead of two;
+//  * {nd, 1/nd} of a (kind, task) is one predicated 16-byte shared load.
+// Durations live in shared memory as double2 [3][16] at `base` (32-bit
+// shared address): kind k, task t at base + k*256 + t*16.
+// ---------------------------------------------------------------------------
+constexpr double kBig = 0x1p900;
+// a lane is idle iff its rem is the sentinel (>= 2^899): one integer compare
+// on the high word instead of a running flag
+constexpr int kIdleHi = 0x78200000;  // high word of 2^899
+
+__device__ __forceinline__ bool idle(double r) { return __double2hiint(r) >= kIdleHi; }
+
+// predicated {nd, 1/nd} load; on success rem = nd (a new command starts)
+__device__ __forceinline__ void start_if(bool p, uint32_t addr, double& nd, double& rc, double& rem) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+        "@q ld.shared.v2.f64 {%0, %1}, [%3];\n\t@q mov.f64 %2, %0;\n\t}"
+        : "+d"(nd), "+d"(rc), "+d"(rem)
+        : "r"(addr), "r"((int)p));
+}
+__device__ __forceinline__ void mul_if(bool p, double& x, double y) {
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q mul.rn.f64 %0, %0, %1;\n\t}"
+        : "+d"(x) : "d"(y), "r"((int)p));
+}
+__device__ __forceinline__ void add_if(bool p, double& x, double y) {
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q add.rn.f64 %0, %0, %1;\n\t}"
+        : "+d"(x) : "d"(y), "r"((int)p));
+}
+
+__device__ __forceinline__ double dmin(double a, double b) { return (b < a) ? b : a; }
+
+// byte offset (task*16) of the task at shift `sh` (= 4*position).  PRE: the
+// sequence is stored pre-shifted left by 4 (positions 0..14 only).
+template <bool PRE>
+__device__ __forceinline__ uint32_t task_off(uint64_t seq, int sh) {
+    if constexpr (PRE) return (uint32_t)(seq >> sh) & 0xF0u;
+    else return ((uint32_t)(seq >> sh) & 0xFu) << 4;
+}
+
+template <int DMA, bool SIGP2, bool TRACK, bool PRE>
+struct FastSim {
+    uint32_t base;
+    uint64_t seq;   // packed ordering (pre-shifted by 4 when PRE)
+    int n4;         // 4*n
+    double now;
+    double r0, r1, r2;  // 2-DMA: HtD, DtH, K;  1-DMA: XFER, -, K.  kBig = idle
+    double d0, d1, d2;
+    double c0, c1, c2;
+    int s0, s1, s2;     // 4 * finalized count per lane
+    double kEnd, idleK;
+
+    __device__ __forceinline__ void init(uint32_t b, uint64_t sq, int n) {
+        base = b;
+        seq = PRE ? (sq << 4) : sq;
+        n4 = 4 * n;
+        now = 0.0;
+        r0 = r1 = r2 = kBig;
+        d0 = d1 = d2 = 1.0;
+        c0 = c1 = c2 = 1.0;
+        s0 = s1 = s2 = 0;
+        kEnd = 0.0;
+        idleK = 0.0;
+    }
+    __device__ __forceinline__ void set_seq(uint64_t sq) { seq = PRE ? (sq << 4) : sq; }
+    // finalized HtD commands (the prefix-checkpoint test) for both modes
+    __device__ __forceinline__ int htd_done() const { return s0 >> 2; }
+
+    __device__ __forceinline__ bool drained() const {
+        if constexpr (DMA == 2) return s1 >= n4;
+        else return s0 >= 2 * n4;
+    }
+
+    __device__ __forceinline__ double upd(double rem, double dd, double nd, double rc) const {
+        return __dmul_rn(divq<true>(__dsub_rn(rem, dd), nd, rc), nd);
+    }
+
+    __device__ __forceinline__ void k_idle_gap(bool st2) {
+        if constexpr (TRACK) {
+            // idle_report (engine.py:68-80) over K spans in FIFO (= sorted) order
+            const double gap = __dsub_rn(now, kEnd);
+            add_if(st2 && s2 > 0 && now > kEnd, idleK, gap);
+        }
+    }
+
+    __device__ __forceinline__ void step(double sigma, double rsig) {
+        // ---- start phase (engine.py:188-194); readiness in the all-non-null
+        // case: K(p) needs HtD(p) finalized, DtH(p) needs K(p) finalized
+        if constexpr (DMA == 2) {
+            const bool st0 = idle(r0) && s0 < n4;
+            const bool st2 = idle(r2) && s2 < s0;
+            const bool st1 = idle(r1) && s1 < s2;
+            k_idle_gap(st2);
+            start_if(st0, base + task_off<PRE>(seq, s0), d0, c0, r0);
+            start_if(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
+            start_if(st1, base + 512 + task_off<PRE>(seq, s1), d1, c1, r1);
+        } else {
+            const bool isH = s0 < n4;
+            const int ps = isH ? s0 : s0 - n4;
+            const bool st0 = idle(r0) && s0 < 2 * n4 && (isH || s2 > ps);
+            const bool st2 = idle(r2) && s2 < n4 && s2 < s0;
+            k_idle_gap(st2);
+            start_if(st0, base + (isH ? 0u : 512u) + task_off<PRE>(seq, ps), d0, c0, r0);
+            start_if(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
+        }
+        // ---- dt (engine.py:200-210)
+        double dt, dd;
+        if constexpr (DMA == 2) {
+            const bool ov = !idle(r0) && !idle(r1);
+            double m = dmin(r0, r1);
+            if constexpr (SIGP2) mul_if(ov, m, rsig);
+            else if (ov) m = divq<true>(m, sigma, rsig);
+            dt = dmin(m, r2);
+            dd = dt;
+            mul_if(ov, dd, sigma);
+        } else {
+            dt = dmin(r0, r2);
+            dd = dt;
+        }
+        // nothing runs (drained) iff dt is the sentinel: then the step must be
+        // a no-op, so dt = 0 keeps `now` and every rem unchanged
+        if (idle(dt)) { dt = 0.0; dd = 0.0; }
+        now = __dadd_rn(now, dt);  // engine.py:211
+        // ---- update + finalize (engine.py:212-231)
+        r0 = upd(r0, dd, d0, c0);
+        r2 = upd(r2, dt, d2, c2);
+        if constexpr (DMA == 2) r1 = upd(r1, dd, d1, c1);
+        if (r0 <= kEndEps) { r0 = kBig; s0 += 4; }
+        if constexpr (DMA == 2) {
+            if (r1 <= kEndEps) { r1 = kBig; s1 += 4; }
+        }
+        if (r2 <= kEndEps) {
+            r2 = kBig;
+            s2 += 4;
+            if constexpr (TRACK) kEnd = now;
+        }
     }
 };
 
