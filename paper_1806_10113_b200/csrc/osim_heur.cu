@@ -1,4 +1,6 @@
 // osim_heur.cu -- instantiations and launch of the heuristic kernel.
+#include <cmath>
+
 #include "osim_launch.cuh"
 
 namespace osim {
@@ -8,10 +10,20 @@ void heuristic_launch(int dma, bool fast, const LaunchCfg& cfg, const double* d_
                       uint32_t* d_ns, int* d_err) {
     const unsigned grid = (unsigned)((B + kHG - 1) / kHG);
     const size_t sm = sizeof(HeurShared);
-#define OSIM_HL(D, F) \
-    k_heuristic<D, F><<<grid, kHT, sm, cfg.st>>>(d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms, d_ns, d_err)
-    if (dma == 2) { if (fast) OSIM_HL(2, true); else OSIM_HL(2, false); }
-    else { if (fast) OSIM_HL(1, true); else OSIM_HL(1, false); }
+    if (fast) {
+        int e;
+        const bool sp2 = std::frexp(sigma, &e) == 0.5;
+#define OSIM_HF(D, P)                                                                                       \
+    k_heuristic_fast<D, P><<<grid, kHT, kWPB * sizeof(HeurWarpShared<D, P>), cfg.st>>>(d_durs, d_idr, B, n, sigma, \
+                                                                                 sum_mode, d_order, d_ms, d_ns)
+        if (dma == 2) { if (sp2) OSIM_HF(2, true); else OSIM_HF(2, false); }
+        else OSIM_HF(1, false);
+#undef OSIM_HF
+        return;
+    }
+#define OSIM_HL(D) \
+    k_heuristic<D, false><<<grid, kHT, sm, cfg.st>>>(d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms, d_ns, d_err)
+    if (dma == 2) OSIM_HL(2); else OSIM_HL(1);
 #undef OSIM_HL
 }
 

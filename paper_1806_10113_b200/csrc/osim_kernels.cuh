@@ -687,6 +687,237 @@ __global__ void __launch_bounds__(kHT) k_heuristic(const double* __restrict__ du
 }
 
 // ---------------------------------------------------------------------------
+// Heuristic, all-stages-non-null path with prefix checkpoints.
+// Same CTA-cooperative schedule as k_heuristic, plus: every candidate
+// simulation of a greedy round is `simulate(ot + [cand])`, and the state of
+// that simulation up to the step in which the HtD lane frees up after
+// position len(ot)-1 depends on `ot` only (the argument of
+// k_exhaustive_pfx).  Each group keeps that state in shared memory; the
+// round's candidates start from it, and after the argmin one thread per
+// group advances it by the chosen task.  The final pair's two simulations
+// start from the last checkpoint and their makespans are the reported
+// makespan of the chosen ordering.  Per-simulation operation sequences are
+// unchanged, so every estimate, idle time and makespan is bit-identical.
+// ---------------------------------------------------------------------------
+constexpr int kWG = 8;                 // groups per warp
+constexpr int kWPB = 4;                // warps per CTA (kHT threads)
+static_assert(kWG * kWPB == kHG, "groups per CTA");
+
+template <int DMA, bool SP2>
+struct HeurWarpShared {
+    using FS = FastSim<DMA, SP2, true, false>;
+    double2 dr[kWG * kHS];
+    typename FS::Ck ck[kWG];
+    double ka[kWG * kMaxN];
+    double kb[kWG * kMaxN];
+    uint64_t ot[kWG];
+    unsigned rmask[kWG];
+    uint8_t idr[kWG * kMaxN];
+    uint8_t cand[kWG * kMaxN];
+    uint8_t pa[kWG], pb[kWG];
+};
+
+template <int DMA, bool SP2>
+__global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict__ durs,
+                                                        const uint8_t* __restrict__ id_rank, uint64_t B, int n,
+                                                        double sigma, int sum_mode,
+                                                        uint8_t* __restrict__ order_out,
+                                                        double* __restrict__ ms_out,
+                                                        uint32_t* __restrict__ nsims_out) {
+    using SH = HeurWarpShared<DMA, SP2>;
+    using FS = typename SH::FS;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    SH& S = reinterpret_cast<SH*>(smem_raw)[warp];
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(S.dr);
+    const uint64_t g0 = ((uint64_t)blockIdx.x * kWPB + warp) * kWG;
+    if (g0 >= B) return;  // whole warp leaves together; no block barriers below
+    const int Gv = (int)((B - g0) < (uint64_t)kWG ? (B - g0) : (uint64_t)kWG);
+    const double rsig = __ddiv_rn(1.0, sigma);
+    auto gbase = [&](int g) { return sbase + (uint32_t)(g * kHS * sizeof(double2)); };
+
+    for (int i = lane; i < Gv * 3 * kStride; i += 32) {
+        const int g = i / (3 * kStride), r = i % (3 * kStride);
+        const int k = r / kStride, t = r % kStride;
+        const double v = t < n ? durs[(g0 + g) * 3 * (uint64_t)n + 3 * t + k] : 1.0;
+        S.dr[g * kHS + r] = make_double2(v, __ddiv_rn(1.0, v));
+    }
+    for (int i = lane; i < Gv * kMaxN; i += 32) {
+        const int g = i / kMaxN, t = i % kMaxN;
+        S.idr[i] = t < n ? id_rank[(g0 + g) * (uint64_t)n + t] : 0xFF;
+    }
+    __syncwarp();
+    auto DV = [&](int g, int k, int t) { return S.dr[g * kHS + k * kStride + t].x; };
+
+    // select_first_task (heuristic.py:22-31) and the first checkpoint
+    if (lane < Gv) {
+        const int g = lane;
+        const unsigned all = (1u << n) - 1u;
+        FS s;
+        if (n >= 3) {
+            int best = -1;
+            double b1 = 0, b2 = 0;
+            for (int t = 0; t < n; ++t) {
+                const double k1 = -__dsub_rn(DV(g, 1, t), DV(g, 0, t));
+                const double k2 = -DV(g, 2, t);
+                bool less;
+                if (best < 0) less = true;
+                else if (k1 < b1) less = true;
+                else if (b1 < k1) less = false;
+                else if (k2 < b2) less = true;
+                else if (b2 < k2) less = false;
+                else less = S.idr[g * kMaxN + t] < S.idr[g * kMaxN + best];
+                if (less) { best = t; b1 = k1; b2 = k2; }
+            }
+            S.ot[g] = (uint64_t)best;
+            S.rmask[g] = all & ~(1u << best);
+            s.init(gbase(g), S.ot[g], 1);
+            while (s.htd_done() < 1) s.step(sigma, rsig);
+        } else {
+            S.ot[g] = 0;
+            S.rmask[g] = all;
+            s.init(gbase(g), 0, 1);  // empty prefix: the initial state
+        }
+        s.save(S.ck[g]);
+        int c = 0;
+        for (int t = 0; t < n; ++t)
+            if ((S.rmask[g] >> t) & 1u) S.cand[g * kMaxN + c++] = (uint8_t)t;
+    }
+    __syncwarp();
+
+    const int k0 = (n >= 3) ? 1 : 0;
+    for (int k = k0; n - k > 2; ++k) {  // heuristic.py:120-123
+        const int m = n - k;
+        const int items = Gv * m;
+        for (int i0 = 0; i0 < items; i0 += 32) {
+            const int i = i0 + lane;
+            const bool valid = i < items;
+            const int g = valid ? i / m : 0;
+            const int j = valid ? i % m : 0;
+            const int c = S.cand[g * kMaxN + j];
+            FS s;
+            s.init(gbase(g), S.ot[g] | ((uint64_t)c << (4 * k)), k + 1);
+            s.load(S.ck[g]);
+            const int rest = __reduce_max_sync(kFull, 3 * (k + 1) - s.finalized());
+#pragma unroll 1
+            for (int st = 0; st < rest; ++st) s.step(sigma, rsig);
+            // _completion_estimate (heuristic.py:34-49): builtin sum of the
+            // rest's t_k in rt order (cand[] is rt in input order), min t_dth.
+            // Warp-uniform loop over the m candidates, skipping j.
+            double f = 0.0, cmp = 0.0, tail = kBig;
+#pragma unroll 1
+            for (int i = 0; i < m; ++i) {
+                const int t = S.cand[g * kMaxN + i];
+                const double x = DV(g, 1, t), d = DV(g, 2, t);
+                const bool use = i != j;
+                const double tt = __dadd_rn(f, x);
+                double e;
+                if (sum_mode) {  // Neumaier (CPython >= 3.12); f = 0 first is 0 + x0
+                    e = (fabs(f) >= fabs(x)) ? __dadd_rn(__dsub_rn(f, tt), x) : __dadd_rn(__dsub_rn(x, tt), f);
+                } else {
+                    e = 0.0;
+                }
+                if (use) {
+                    cmp = __dadd_rn(cmp, e);
+                    f = tt;
+                    tail = dmin(d, tail);
+                }
+            }
+            if (sum_mode && cmp != 0.0 && isfinite(cmp)) f = __dadd_rn(f, cmp);
+            const double bound = __dadd_rn(__dadd_rn(s.kEnd, f), tail);
+            const double est = (bound > s.now) ? bound : s.now;
+            if (valid) {
+                S.ka[g * kMaxN + j] = est;
+                S.kb[g * kMaxN + j] = s.idleK;
+            }
+        }
+        __syncwarp();
+        if (lane < Gv) {
+            const int g = lane;
+            int bj = 0;
+            for (int j = 1; j < m; ++j) {
+                const double e = S.ka[g * kMaxN + j], be = S.ka[g * kMaxN + bj];
+                const double d = S.kb[g * kMaxN + j], bd = S.kb[g * kMaxN + bj];
+                bool less;
+                if (e < be) less = true;
+                else if (be < e) less = false;
+                else if (d < bd) less = true;
+                else if (bd < d) less = false;
+                else less = S.idr[g * kMaxN + S.cand[g * kMaxN + j]] <
+                            S.idr[g * kMaxN + S.cand[g * kMaxN + bj]];
+                if (less) bj = j;
+            }
+            const int c = S.cand[g * kMaxN + bj];
+            S.ot[g] |= (uint64_t)c << (4 * k);
+            S.rmask[g] &= ~(1u << c);
+            int cc = 0;
+            for (int t = 0; t < n; ++t)
+                if ((S.rmask[g] >> t) & 1u) S.cand[g * kMaxN + cc++] = (uint8_t)t;
+            // advance the checkpoint by the chosen task (prefix length k+1)
+            FS s;
+            s.init(gbase(g), S.ot[g], k + 1);
+            s.load(S.ck[g]);
+            while (s.htd_done() < k + 1) s.step(sigma, rsig);
+            s.save(S.ck[g]);
+        }
+        __syncwarp();
+    }
+
+    const int kl = n - 2;  // select_last_tasks (heuristic.py:81-102)
+    if (n >= 2) {
+        if (lane < Gv) {
+            const int g = lane;
+            int a = S.cand[g * kMaxN + 0], b = S.cand[g * kMaxN + 1];
+            if (S.idr[g * kMaxN + b] < S.idr[g * kMaxN + a]) { int x = a; a = b; b = x; }
+            S.pa[g] = (uint8_t)a;
+            S.pb[g] = (uint8_t)b;
+        }
+        __syncwarp();
+        {
+            const int i = lane;  // 2 * kWG <= 32 items
+            const bool valid = i < 2 * Gv;
+            const int g = valid ? i >> 1 : 0;
+            const int w = i & 1;
+            const uint64_t x = w ? S.pb[g] : S.pa[g], y = w ? S.pa[g] : S.pb[g];
+            FS s;
+            s.init(gbase(g), S.ot[g] | (x << (4 * kl)) | (y << (4 * (kl + 1))), n);
+            s.load(S.ck[g]);
+            const int rest = __reduce_max_sync(kFull, 3 * n - s.finalized());
+#pragma unroll 1
+            for (int st = 0; st < rest; ++st) s.step(sigma, rsig);
+            if (valid) S.ka[g * kMaxN + w] = s.now;
+        }
+        __syncwarp();
+    }
+    if (lane < Gv) {
+        const int g = lane;
+        double ms;
+        if (n >= 2) {
+            const int a = S.pa[g], b = S.pb[g];
+            const double m_ab = S.ka[g * kMaxN + 0], m_ba = S.ka[g * kMaxN + 1];
+            bool ab;
+            if (m_ab < m_ba) ab = true;
+            else if (m_ba < m_ab) ab = false;
+            else ab = !(DV(g, 2, a) <= DV(g, 2, b));  // tie: shorter DtH last
+            S.ot[g] |= ((uint64_t)(ab ? a : b) << (4 * kl)) | ((uint64_t)(ab ? b : a) << (4 * (kl + 1)));
+            ms = ab ? m_ab : m_ba;  // simulate(ot + chosen pair)
+        } else {
+            FS s;  // n == 1: reorder_batch returns [tg[0]] without simulating
+            s.init(gbase(g), 0, 1);
+            for (int st = 0; st < 3; ++st) s.step(sigma, rsig);
+            ms = s.now;
+        }
+        ms_out[g0 + g] = ms;
+        if (nsims_out) nsims_out[g0 + g] = (n >= 3) ? (uint32_t)(n * (n - 1) / 2 - 1) : (n == 2 ? 2u : 0u);
+    }
+    __syncwarp();
+    for (int i = lane; i < Gv * n; i += 32) {
+        const int g = i / n, p = i % n;
+        order_out[(g0 + g) * (uint64_t)n + p] = (uint8_t)nib(S.ot[g], p);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Diagnostics
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t splitmix(uint64_t& x) {

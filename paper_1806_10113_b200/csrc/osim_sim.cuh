@@ -325,10 +325,11 @@ __device__ __forceinline__ bool idle(double r) { return __double2hiint(r) >= kId
 // predicated {nd, 1/nd} load; on success rem = nd (a new command starts)
 __device__ __forceinline__ void start_if(bool p, uint32_t addr, double& nd, double& rc, double& rem) {
     asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
-        "@q ld.shared.v2.f64 {%0, %1}, [%3];\n\t@q mov.f64 %2, %0;\n\t}"
-        : "+d"(nd), "+d"(rc), "+d"(rem)
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t"
+        "@q ld.shared.v2.f64 {%0, %1}, [%2];\n\t}"
+        : "+d"(nd), "+d"(rc)
         : "r"(addr), "r"((int)p));
+    rem = p ? nd : rem;
 }
 __device__ __forceinline__ void mul_if(bool p, double& x, double y) {
     asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q mul.rn.f64 %0, %0, %1;\n\t}"
@@ -374,6 +375,23 @@ struct FastSim {
         idleK = 0.0;
     }
     __device__ __forceinline__ void set_seq(uint64_t sq) { seq = PRE ? (sq << 4) : sq; }
+    __device__ __forceinline__ int finalized() const { return (s0 + s1 + s2) >> 2; }
+
+    // checkpoint image (prefix sharing across calls, e.g. in shared memory)
+    struct Ck {
+        double now, r0, r1, r2, d0, d1, d2, c0, c1, c2, kEnd, idleK;
+        int s0, s1, s2, pad;
+    };
+    __device__ __forceinline__ void save(Ck& k) const {
+        k.now = now; k.r0 = r0; k.r1 = r1; k.r2 = r2; k.d0 = d0; k.d1 = d1; k.d2 = d2;
+        k.c0 = c0; k.c1 = c1; k.c2 = c2; k.kEnd = kEnd; k.idleK = idleK;
+        k.s0 = s0; k.s1 = s1; k.s2 = s2;
+    }
+    __device__ __forceinline__ void load(const Ck& k) {
+        now = k.now; r0 = k.r0; r1 = k.r1; r2 = k.r2; d0 = k.d0; d1 = k.d1; d2 = k.d2;
+        c0 = k.c0; c1 = k.c1; c2 = k.c2; kEnd = k.kEnd; idleK = k.idleK;
+        s0 = k.s0; s1 = k.s1; s2 = k.s2;
+    }
     // finalized HtD commands (the prefix-checkpoint test) for both modes
     __device__ __forceinline__ int htd_done() const { return s0 >> 2; }
 
