@@ -50,7 +50,8 @@ def stale() -> bool:
 
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(OBJDIR, os.path.basename(src).replace(".cu", ".o"))
-    cmd = [nvcc(), *NVCC_FLAGS, "-c", "-o", obj, src]
+    extra = os.environ.get("OSIM_NVCC_EXTRA", "").split()  # tuning only, e.g. -DOSIM_PFX_MINB=3
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", "-o", obj, src]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

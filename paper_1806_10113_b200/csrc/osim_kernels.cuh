@@ -13,6 +13,9 @@ namespace osim {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kBlock = 256;
+#ifndef OSIM_PFX_MINB
+#define OSIM_PFX_MINB 5  // min resident CTAs per SM for the prefix kernels (48 registers)
+#endif
 
 // ---------------------------------------------------------------------------
 // make_report reduction (oracle.py:41-57) in mergeable form.  The product of
@@ -234,12 +237,35 @@ __device__ __forceinline__ void stage_dr(const double* __restrict__ g, int n, do
     }
 }
 
+// Per-thread checkpoint slot in shared memory, structure-of-arrays so that
+// the 32 lanes of a warp touch 32 consecutive 8-byte words (conflict-free);
+// keeping it out of registers lifts occupancy (the register state is halved).
+struct CkSlots {
+    double v[12][kBlock];  // now, r0..r2, d0..d2, c0..c2, kEnd, idleK
+    int h[3][kBlock];      // s0..s2
+};
+
+template <class FS>
+__device__ __forceinline__ void ck_store(CkSlots& K, int i, const FS& s) {
+    K.v[0][i] = s.now; K.v[1][i] = s.r0; K.v[2][i] = s.r1; K.v[3][i] = s.r2;
+    K.v[4][i] = s.d0; K.v[5][i] = s.d1; K.v[6][i] = s.d2;
+    K.v[7][i] = s.c0; K.v[8][i] = s.c1; K.v[9][i] = s.c2;
+    K.h[0][i] = s.s0; K.h[1][i] = s.s1; K.h[2][i] = s.s2;
+}
+template <class FS>
+__device__ __forceinline__ void ck_load(const CkSlots& K, int i, FS& s) {
+    s.now = K.v[0][i]; s.r0 = K.v[1][i]; s.r1 = K.v[2][i]; s.r2 = K.v[3][i];
+    s.d0 = K.v[4][i]; s.d1 = K.v[5][i]; s.d2 = K.v[6][i];
+    s.c0 = K.v[7][i]; s.c1 = K.v[8][i]; s.c2 = K.v[9][i];
+    s.s0 = K.h[0][i]; s.s1 = K.h[1][i]; s.s2 = K.h[2][i];
+}
+
 // Simulate prefix P of length M and every suffix; accumulate leaves that
 // fall inside [lo, hi).  All threads of the warp must call together.
 template <int N, int DMA, bool SIGP2, int L, bool WRITE_MS>
 __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double rsig, uint64_t P,
                                            bool validP, uint64_t lo, uint64_t hi, Part& acc,
-                                           double* __restrict__ ms_out, uint64_t ms_base) {
+                                           double* __restrict__ ms_out, uint64_t ms_base, CkSlots& K) {
     constexpr int M = N - L;
     constexpr uint64_t LF = Fact<L>::v;
     const uint64_t seq0 = unrank<N>(P * LF);  // prefix + ascending remainder
@@ -257,7 +283,7 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
         }
     }
     const int rest = 3 * N - __reduce_min_sync(kFull, sa);
-    const FS ck = s;
+    ck_store(K, threadIdx.x, s);
     const uint64_t pre = (M > 0) ? (seq0 & ((1ull << (4 * M)) - 1ull)) : 0ull;
     const uint64_t rem = seq0 >> (4 * M);  // L ascending task ids
 #pragma unroll 1
@@ -269,7 +295,7 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
             const uint32_t id = (uint32_t)(idx >> (4 * i)) & 0xFu;
             suf |= ((rem >> (4 * id)) & 0xFull) << (4 * (M + i));
         }
-        s = ck;
+        ck_load(K, threadIdx.x, s);
         s.set_seq(pre | suf);
 #pragma unroll 2
         for (int st = 0; st < rest; ++st) s.step(sigma, rsig);
@@ -284,11 +310,12 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
 }
 
 template <int N, int DMA, bool SIGP2, int L>
-__global__ void __launch_bounds__(kBlock) k_exhaustive_pfx(const double* __restrict__ durs, double sigma,
+__global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const double* __restrict__ durs, double sigma,
                                                            uint64_t lo, uint64_t hi, Part* __restrict__ parts,
                                                            double* __restrict__ ms_out) {
     __shared__ double2 sdr[3 * kStride];
     __shared__ Part sh[32];
+    __shared__ CkSlots K;
     stage_dr(durs, N, sdr);
     __syncthreads();
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
@@ -301,7 +328,7 @@ __global__ void __launch_bounds__(kBlock) k_exhaustive_pfx(const double* __restr
     for (uint64_t pb = p_lo + (uint64_t)blockIdx.x * blockDim.x; pb < p_hi; pb += stride) {
         const uint64_t P = pb + threadIdx.x;
         const bool validP = P < p_hi;
-        pfx_leaves<N, DMA, SIGP2, L, true>(base, sigma, rsig, validP ? P : p_lo, validP, lo, hi, acc, ms_out, lo);
+        pfx_leaves<N, DMA, SIGP2, L, true>(base, sigma, rsig, validP ? P : p_lo, validP, lo, hi, acc, ms_out, lo, K);
     }
     acc = block_reduce(acc, sh);
     if (threadIdx.x == 0) parts[blockIdx.x] = acc;
@@ -309,10 +336,11 @@ __global__ void __launch_bounds__(kBlock) k_exhaustive_pfx(const double* __restr
 
 // Batched groups with prefix sharing: one CTA per group.
 template <int N, int DMA, bool SIGP2, int L>
-__global__ void __launch_bounds__(kBlock) k_exhaustive_batch_pfx(const double* __restrict__ durs, uint64_t B,
+__global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_batch_pfx(const double* __restrict__ durs, uint64_t B,
                                                                  double sigma, osim_summary* __restrict__ out) {
     __shared__ double2 sdr[3 * kStride];
     __shared__ Part sh[32];
+    __shared__ CkSlots K;
     constexpr uint64_t total = Fact<N>::v;
     constexpr uint64_t NP = total / Fact<L>::v;
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
@@ -326,7 +354,7 @@ __global__ void __launch_bounds__(kBlock) k_exhaustive_batch_pfx(const double* _
             const uint64_t P = pb + threadIdx.x;
             const bool validP = P < NP;
             pfx_leaves<N, DMA, SIGP2, L, false>(base, sigma, rsig, validP ? P : 0, validP, 0, total, acc,
-                                                nullptr, 0);
+                                                nullptr, 0, K);
         }
         acc = block_reduce(acc, sh);  // ends with __syncthreads: smem reusable
         if (threadIdx.x == 0) out[b] = part_to_summary(acc);

@@ -325,11 +325,10 @@ __device__ __forceinline__ bool idle(double r) { return __double2hiint(r) >= kId
 // predicated {nd, 1/nd} load; on success rem = nd (a new command starts)
 __device__ __forceinline__ void start_if(bool p, uint32_t addr, double& nd, double& rc, double& rem) {
     asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t"
-        "@q ld.shared.v2.f64 {%0, %1}, [%2];\n\t}"
-        : "+d"(nd), "+d"(rc)
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+        "@q ld.shared.v2.f64 {%0, %1}, [%3];\n\t@q ld.shared.f64 %2, [%3];\n\t}"
+        : "+d"(nd), "+d"(rc), "+d"(rem)
         : "r"(addr), "r"((int)p));
-    rem = p ? nd : rem;
 }
 __device__ __forceinline__ void mul_if(bool p, double& x, double y) {
     asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q mul.rn.f64 %0, %0, %1;\n\t}"
@@ -341,6 +340,17 @@ __device__ __forceinline__ void add_if(bool p, double& x, double y) {
 }
 
 __device__ __forceinline__ double dmin(double a, double b) { return (b < a) ? b : a; }
+
+// idle sentinel by high word only (the low word is irrelevant: any value with
+// that high word is ~2^900)
+__device__ __forceinline__ double retire(double r) { return __hiloint2double(0x78300000, __double2loint(r)); }
+// finalize of the lane that holds the group's last command: instead of the
+// sentinel, the high word becomes 0 (rem ~ a subnormal), so later steps have
+// dt ~ 0 and now + dt == now exactly -- a drained thread's steps are no-ops.
+__device__ __forceinline__ double retire_or_drain(bool fin, double r, bool last) {
+    const int hi = last ? 0 : 0x78300000;
+    return __hiloint2double(fin ? hi : __double2hiint(r), __double2loint(r));
+}
 
 // byte offset (task*16) of the task at shift `sh` (= 4*position).  PRE: the
 // sequence is stored pre-shifted left by 4 (positions 0..14 only).
@@ -446,20 +456,27 @@ struct FastSim {
             dt = dmin(r0, r2);
             dd = dt;
         }
-        // nothing runs (drained) iff dt is the sentinel: then the step must be
-        // a no-op, so dt = 0 keeps `now` and every rem unchanged
-        if (idle(dt)) { dt = 0.0; dd = 0.0; }
         now = __dadd_rn(now, dt);  // engine.py:211
-        // ---- update + finalize (engine.py:212-231)
+        // ---- update + finalize (engine.py:212-231).  A finalized lane goes
+        // idle by setting only the high word of rem to the sentinel's.  The
+        // command that drains the group (the last DtH: 2-DMA lane 1, 1-DMA
+        // lane 0) instead leaves rem = 0, so every later step has dt = 0 and
+        // is a no-op (drained threads keep stepping in warp lock-step).
         r0 = upd(r0, dd, d0, c0);
         r2 = upd(r2, dt, d2, c2);
         if constexpr (DMA == 2) r1 = upd(r1, dd, d1, c1);
-        if (r0 <= kEndEps) { r0 = kBig; s0 += 4; }
         if constexpr (DMA == 2) {
-            if (r1 <= kEndEps) { r1 = kBig; s1 += 4; }
+            if (r0 <= kEndEps) { r0 = retire(r0); s0 += 4; }
+            const bool f1 = r1 <= kEndEps;
+            r1 = retire_or_drain(f1, r1, s1 + 4 >= n4);
+            s1 += f1 ? 4 : 0;
+        } else {
+            const bool f0 = r0 <= kEndEps;
+            r0 = retire_or_drain(f0, r0, s0 + 4 >= 2 * n4);
+            s0 += f0 ? 4 : 0;
         }
         if (r2 <= kEndEps) {
-            r2 = kBig;
+            r2 = retire(r2);
             s2 += 4;
             if constexpr (TRACK) kEnd = now;
         }
