@@ -246,7 +246,9 @@ def run_ours(a):
                            "DDIV counted as one op) x orderings per launch / CUDA-event launch time; peak = "
                            "measured DFMA instructions/s of this GPU (osim_fp64_peak, %.2f TFLOP/s at 2 "
                            "flops/DFMA), i.e. FP64-pipe issue capacity in ops/s" % (ops_per, peak_tflops)),
-            "kernel": "k_exhaustive_fast<12,2>", "launch_ms": kern_avg * 1e3}
+            "kernel": "k_exhaustive_pfx<12,2,sigma-pow2,L=4>", "launch_ms": kern_avg * 1e3,
+            "ncu_executed": {k: v for k, v in profile_headline().items()
+                             if k in ("issue_active_pct", "fp64_pipe_active_pct", "warp_exec_efficiency", "source")}}
 
     # ---- e2e through the public API (host buffers) ---------------------------
     e2e_steps = max(3, a.steps // 2)
@@ -300,15 +302,19 @@ def run_ours(a):
         D.pg.destroy_process_group()
 
 
-def profile_traffic():
-    """dram read+write bytes per launch of the headline kernel from the
-    committed ncu capture summary, if present."""
+def profile_headline():
+    """The committed ncu capture summary of the headline kernel (DRAM bytes
+    per launch, issue / FP64-pipe utilization), if present."""
     p = os.path.join(ROOT, "profiles", "ncu_headline.json")
     try:
         with open(p) as fh:
-            return json.load(fh).get("dram_bytes_per_launch")
+            return json.load(fh)
     except (OSError, ValueError):
-        return None
+        return {}
+
+
+def profile_traffic():
+    return profile_headline().get("dram_bytes_per_launch")
 
 
 def run_secondary(a, D, torch, dev, sp, flush, ops, peak_ops, L):
