@@ -99,6 +99,16 @@ int osim_heuristic_batch(const double* durs, const uint8_t* id_rank, uint64_t B,
                          double sigma, int sum_mode, int n_dev, uint8_t* order, double* makespan,
                          uint32_t* n_sims);
 
+/* Order statistics of exhaustive_search without host lists (SURVEY.md 8(f)
+ * row f2): the summary, *below = number of makespans strictly below
+ * `threshold` (the `offsim permute` percentile numerator, cli.py:100-103;
+ * -INFINITY counts none) and *median = np.median of the makespans of ranks
+ * [rank_lo, rank_hi) (oracle.py:54; nullable).  The makespans stay in HBM
+ * (8 bytes per ordering) and the median is an exact radix selection. */
+int osim_exhaustive_stats(const double* durs, int n, int dma, double sigma, uint64_t rank_lo,
+                          uint64_t rank_hi, double threshold, int n_dev, osim_summary* out,
+                          uint64_t* below, double* median);
+
 /* engine.simulate for one ordering: start/end[n][3] by task index
  * (-1 = null stage), makespan, idle[3] = idle_report (HtD, K, DtH). */
 int osim_timeline(const double* durs, int n, int dma, double sigma, const uint8_t* order,
@@ -112,6 +122,17 @@ int osim_fast_eligible(const double* durs, uint64_t count /* tasks */, double si
 int osim_exhaustive_dev(const double* d_durs, int n, int dma, double sigma, uint64_t rank_lo,
                         uint64_t rank_hi, int fast, osim_summary* d_out, double* d_makespans,
                         void* stream);
+/* As osim_exhaustive_dev plus the below-threshold count (d_below: one uint64). */
+int osim_exhaustive_ex_dev(const double* d_durs, int n, int dma, double sigma, uint64_t rank_lo,
+                           uint64_t rank_hi, int fast, double threshold, osim_summary* d_out,
+                           uint64_t* d_below, double* d_makespans, void* stream);
+/* One radix-selection pass over positive doubles in HBM: d_hist[2^digit_bits]
+ * = histogram of the next digit_bits bits (MSB first) of the values whose top
+ * prefix_bits bits equal `prefix` (digit_bits <= 11).  Ranks sum these
+ * histograms (e.g. NCCL all_reduce) to select an order statistic of a
+ * sharded makespan set. */
+int osim_radix_hist_dev(const double* d_vals, uint64_t count, uint64_t prefix, int prefix_bits,
+                        int digit_bits, uint32_t* d_hist, void* stream);
 int osim_exhaustive_batch_dev(const double* d_durs, uint64_t B, int n, int dma, double sigma,
                               int fast, osim_summary* d_out, void* stream);
 int osim_heuristic_batch_dev(const double* d_durs, const uint8_t* d_id_rank, uint64_t B, int n,

@@ -43,12 +43,16 @@ from .model import (
 )
 from .search import (
     DEFAULT_CAP,
+    OrderingStats,
     OrderingSummary,
     PermutationReport,
     exhaustive_search,
+    exhaustive_stats,
+    exhaustive_stats_durs,
     exhaustive_summary,
     exhaustive_summary_batch,
     exhaustive_summary_durs,
+    heuristic_percentile,
     make_report,
     sample_permutations,
 )
@@ -57,10 +61,11 @@ __version__ = "0.1.0"
 
 __all__ = [
     "Command", "DeviceProfile", "Direction", "InsufficientSamples", "KINDS", "NegativeFitWarning",
-    "OffsimError", "OrderingSummary", "PermutationReport", "SUM_MODE", "TaskDominance", "TaskSpec",
+    "OffsimError", "OrderingStats", "OrderingSummary", "PermutationReport", "SUM_MODE", "TaskDominance", "TaskSpec",
     "Timeline", "UnresolvableDuration", "classify_task", "DEFAULT_CAP", "estimate_kernel",
     "estimate_transfer", "exhaustive_search", "exhaustive_summary", "exhaustive_summary_batch",
-    "exhaustive_summary_durs", "fit_kernel_model", "idle_report", "make_report", "recompute_overlap",
+    "exhaustive_summary_durs", "exhaustive_stats", "exhaustive_stats_durs", "fit_kernel_model",
+    "heuristic_percentile", "idle_report", "make_report", "recompute_overlap",
     "reorder_batch", "reorder_batch_many", "reorder_durs", "sample_permutations", "select_first_task",
     "select_last_tasks", "select_next_task", "simulate", "stage_times",
 ]

@@ -25,7 +25,8 @@ EXPORTS = (
     "osim_version", "osim_last_error", "osim_init", "osim_shutdown", "osim_set_device",
     "osim_exhaustive", "osim_eval_perms", "osim_exhaustive_batch", "osim_heuristic_batch",
     "osim_timeline", "osim_fast_eligible", "osim_exhaustive_dev", "osim_exhaustive_batch_dev",
-    "osim_heuristic_batch_dev", "osim_selftest_div", "osim_fp64_peak",
+    "osim_heuristic_batch_dev", "osim_selftest_div", "osim_fp64_peak", "osim_exhaustive_stats",
+    "osim_exhaustive_ex_dev", "osim_radix_hist_dev",
 )
 
 
@@ -92,6 +93,9 @@ def load(path: str = LIB_PATH):
             "osim_exhaustive_batch_dev": ([vp, u64, i, i, d, i, vp, vp], i),
             "osim_heuristic_batch_dev": ([vp, vp, u64, i, i, d, i, i, vp, vp, vp, vp], i),
             "osim_selftest_div": ([u64, u64, C.POINTER(u64)], i),
+            "osim_exhaustive_stats": ([dp, i, i, d, u64, u64, d, i, sp, C.POINTER(u64), dp], i),
+            "osim_exhaustive_ex_dev": ([vp, i, i, d, u64, u64, i, d, vp, vp, vp, vp], i),
+            "osim_radix_hist_dev": ([vp, u64, u64, i, i, vp, vp], i),
             "osim_fp64_peak": ([dp], i),
         }
         for name, (args, res) in sig.items():
@@ -149,6 +153,19 @@ def exhaustive(durs, dma, sigma, lo, hi, n_dev=1, want_makespans=False):
     check(load().osim_exhaustive(ptr(d, C.c_double), n, int(dma), float(sigma), int(lo), int(hi), int(n_dev),
                                  C.byref(out), ptr(ms, C.c_double) if ms is not None else None))
     return out.as_dict(), ms
+
+
+def exhaustive_stats(durs, dma, sigma, lo, hi, threshold=float("-inf"), n_dev=1, median=True):
+    """(summary dict, count strictly below threshold, exact median or None)."""
+    d = f64(durs, (-1, 3))
+    n = d.shape[0]
+    out = OsimSummary()
+    below = C.c_uint64()
+    med = C.c_double()
+    check(load().osim_exhaustive_stats(ptr(d, C.c_double), n, int(dma), float(sigma), int(lo), int(hi),
+                                       float(threshold), int(n_dev), C.byref(out), C.byref(below),
+                                       C.byref(med) if median else None))
+    return out.as_dict(), below.value, (med.value if median else None)
 
 
 def eval_perms(durs, dma, sigma, perms, n_dev=1):

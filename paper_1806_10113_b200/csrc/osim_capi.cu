@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -134,15 +135,17 @@ bool sigma_pow2(double sigma) {
 }
 
 int launch_exh_fast_dispatch(int dma, int n, DevCtx* c, cudaStream_t st, const double* d_durs, double sigma,
-                             uint64_t lo, uint64_t hi, Part* parts, int max_parts, double* d_ms, int* g) {
+                             uint64_t lo, uint64_t hi, double thr, Part* parts, int max_parts, double* d_ms,
+                             int* g) {
     const LaunchCfg cfg{c->sms, st};
     const int L = pfx_l_for(n);
     int rc;
     if (dma == 2)
-        rc = sigma_pow2(sigma) ? exh_fast_launch_d2s1(n, L, cfg, d_durs, sigma, lo, hi, parts, max_parts, d_ms, g)
-                               : exh_fast_launch_d2s0(n, L, cfg, d_durs, sigma, lo, hi, parts, max_parts, d_ms, g);
+        rc = sigma_pow2(sigma)
+                 ? exh_fast_launch_d2s1(n, L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g)
+                 : exh_fast_launch_d2s0(n, L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g);
     else
-        rc = exh_fast_launch_d1(n, L, cfg, d_durs, sigma, lo, hi, parts, max_parts, d_ms, g);
+        rc = exh_fast_launch_d1(n, L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g);
     if (rc) return fail(OSIM_EINVAL, "unsupported n=%d", n);
     return 0;
 }
@@ -160,29 +163,30 @@ int launch_batch_fast_dispatch(int dma, int n, DevCtx* c, cudaStream_t st, const
 // Enqueue exhaustive over [lo, hi) and its final reduce into d_out.
 int enqueue_exhaustive(DevCtx* c, cudaStream_t st, const double* d_durs, int n, int dma,
                        double sigma, uint64_t lo, uint64_t hi, int fast, osim_summary* d_out,
-                       double* d_ms, Part* parts, int max_parts) {
+                       double* d_ms, Part* parts, int max_parts, double thr = -HUGE_VAL,
+                       unsigned long long* d_below = nullptr) {
     int g = 1;
     int rc = 0;
     if (hi > lo) {
         if (fast) {
-            rc = launch_exh_fast_dispatch(dma, n, c, st, d_durs, sigma, lo, hi, parts, max_parts, d_ms, &g);
+            rc = launch_exh_fast_dispatch(dma, n, c, st, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, &g);
         } else {
             uint64_t blocks = (hi - lo + kBlock - 1) / kBlock;
             if (dma == 2) {
                 g = grid_for(k_exhaustive_gen<2>, kBlock, 0, c, blocks);
                 if (g > max_parts) g = max_parts;
-                k_exhaustive_gen<2><<<g, kBlock, 0, st>>>(d_durs, n, sigma, lo, hi, parts, d_ms, c->d_err);
+                k_exhaustive_gen<2><<<g, kBlock, 0, st>>>(d_durs, n, sigma, lo, hi, thr, parts, d_ms, c->d_err);
             } else {
                 g = grid_for(k_exhaustive_gen<1>, kBlock, 0, c, blocks);
                 if (g > max_parts) g = max_parts;
-                k_exhaustive_gen<1><<<g, kBlock, 0, st>>>(d_durs, n, sigma, lo, hi, parts, d_ms, c->d_err);
+                k_exhaustive_gen<1><<<g, kBlock, 0, st>>>(d_durs, n, sigma, lo, hi, thr, parts, d_ms, c->d_err);
             }
         }
         if (rc) return rc;
     } else {
         g = 0;
     }
-    k_final_reduce<<<1, kBlock, 0, st>>>(parts, g, d_out);
+    k_final_reduce<<<1, kBlock, 0, st>>>(parts, g, d_out, d_below);
     CK(cudaGetLastError());
     return 0;
 }
@@ -270,6 +274,50 @@ int pick_devs(int n_dev, DevList& out) {
     return 0;
 }
 
+
+// k-th smallest (0-based) of the positive doubles held by several devices
+// (each device: d_vals[i] with counts[i] values); histograms of every pass
+// are summed over devices on the host.  Exact: the result is a bit pattern.
+int select_kth(std::vector<DevCtx*>& devs, std::vector<const double*>& vals, std::vector<uint64_t>& counts,
+               std::vector<unsigned*>& d_hist, uint64_t k, double* out) {
+    unsigned long long prefix = 0;
+    int pbits = 0;
+    std::vector<unsigned> h(1 << kRadixBits), tot(1 << kRadixBits);
+    while (pbits < 64) {
+        const int d = (64 - pbits) < kRadixBits ? (64 - pbits) : kRadixBits;
+        const int nb = 1 << d;
+        std::fill(tot.begin(), tot.begin() + nb, 0u);
+        for (size_t i = 0; i < devs.size(); ++i) {
+            DevCtx* c = devs[i];
+            CK(cudaSetDevice(c->dev));
+            CK(cudaMemsetAsync(d_hist[i], 0, nb * sizeof(unsigned), c->stream));
+            if (counts[i]) {
+                const uint64_t blocks = (counts[i] + 255) / 256;
+                const int g = (int)(blocks < (uint64_t)c->sms * 8 ? blocks : (uint64_t)c->sms * 8);
+                k_radix_hist<<<g, 256, 0, c->stream>>>((const unsigned long long*)vals[i], counts[i], prefix, pbits,
+                                                       d, d_hist[i]);
+                CK(cudaGetLastError());
+            }
+            CK(cudaMemcpyAsync(h.data(), d_hist[i], nb * sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            for (int b = 0; b < nb; ++b) tot[b] += h[b];
+        }
+        uint64_t cum = 0;
+        int bin = 0;
+        for (; bin < nb; ++bin) {
+            if (cum + tot[bin] > k) break;
+            cum += tot[bin];
+        }
+        if (bin == nb) return fail(OSIM_EINVAL, "rank %llu outside the value set", (unsigned long long)k);
+        k -= cum;
+        prefix = (prefix << d) | (unsigned long long)bin;
+        pbits += d;
+    }
+    double v;
+    memcpy(&v, &prefix, sizeof(v));
+    *out = v;
+    return 0;
+}
 }  // namespace
 
 extern "C" {
@@ -387,6 +435,121 @@ int osim_exhaustive_dev(const double* d_durs, int n, int dma, double sigma, uint
                               d_makespans, (Part*)base, mp);
 }
 
+int osim_exhaustive_stats(const double* durs, int n, int dma, double sigma, uint64_t rank_lo, uint64_t rank_hi,
+                          double threshold, int n_dev, osim_summary* out, uint64_t* below, double* median) {
+    int rc = check_common(n, dma, sigma);
+    if (rc) return rc;
+    if ((rc = check_durs(durs, (uint64_t)n))) return rc;
+    if (!out) return fail(OSIM_EINVAL, "out is NULL");
+    const uint64_t total = factorial(n);
+    if (rank_lo > rank_hi || rank_hi > total) return fail(OSIM_EINVAL, "bad rank range");
+    DevList dl;
+    if ((rc = pick_devs(n_dev, dl))) return rc;
+    const int fast = fast_ok(durs, n, sigma);
+    const int G = (int)dl.v.size();
+    const uint64_t span = rank_hi - rank_lo;
+    std::vector<osim_summary> res(G);
+    std::vector<unsigned long long> bel(G, 0);
+    std::vector<const double*> vals(G);
+    std::vector<uint64_t> counts(G);
+    std::vector<unsigned*> hists(G);
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        locks.emplace_back(c->mu);
+        CK(cudaSetDevice(c->dev));
+        const uint64_t lo = rank_lo + span * (uint64_t)gi / (uint64_t)G;
+        const uint64_t hi = rank_lo + span * (uint64_t)(gi + 1) / (uint64_t)G;
+        const int mp = max_parts_for(c);
+        size_t off_parts = align_up(3 * kMaxN * sizeof(double));
+        size_t off_sum = off_parts + align_up(mp * sizeof(Part));
+        size_t off_bel = off_sum + align_up(sizeof(osim_summary));
+        size_t off_hist = off_bel + 256;
+        size_t off_ms = off_hist + align_up((1u << kRadixBits) * sizeof(unsigned));
+        size_t bytes = off_ms + align_up((hi - lo) * sizeof(double) + 8);
+        void* base;
+        if ((rc = scratch(c, bytes, &base))) return rc;
+        char* b = (char*)base;
+        CK(cudaMemcpyAsync(b, durs, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        rc = enqueue_exhaustive(c, c->stream, (double*)b, n, dma, sigma, lo, hi, fast, (osim_summary*)(b + off_sum),
+                                (double*)(b + off_ms), (Part*)(b + off_parts), mp, threshold,
+                                (unsigned long long*)(b + off_bel));
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(&res[gi], b + off_sum, sizeof(osim_summary), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(&bel[gi], b + off_bel, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+        vals[gi] = (const double*)(b + off_ms);
+        counts[gi] = hi - lo;
+        hists[gi] = (unsigned*)(b + off_hist);
+    }
+    osim_summary acc;
+    memset(&acc, 0, sizeof(acc));
+    uint64_t nbelow = 0;
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        CK(cudaSetDevice(c->dev));
+        if ((rc = finish(c, c->stream))) return rc;
+        merge_host(acc, res[gi]);
+        nbelow += bel[gi];
+    }
+    *out = acc;
+    if (below) *below = nbelow;
+    if (median) {
+        // np.median (numpy/lib/function_base.py): the middle value, or for an
+        // even count the mean of the two middle values, (a + b) / 2
+        const uint64_t cnt = acc.count;
+        if (cnt == 0) {
+            *median = NAN;
+        } else if (cnt & 1) {
+            if ((rc = select_kth(dl.v, vals, counts, hists, cnt / 2, median))) return rc;
+        } else {
+            double a, bb;
+            if ((rc = select_kth(dl.v, vals, counts, hists, cnt / 2 - 1, &a))) return rc;
+            if ((rc = select_kth(dl.v, vals, counts, hists, cnt / 2, &bb))) return rc;
+            volatile double s = a + bb;  // two IEEE roundings, as numpy's mean
+            *median = s / 2.0;
+        }
+    }
+    return 0;
+}
+
+int osim_radix_hist_dev(const double* d_vals, uint64_t count, uint64_t prefix, int prefix_bits, int digit_bits,
+                        uint32_t* d_hist, void* stream) {
+    if (prefix_bits < 0 || digit_bits < 1 || digit_bits > kRadixBits || prefix_bits + digit_bits > 64)
+        return fail(OSIM_EINVAL, "bad radix digit (prefix %d bits, digit %d bits)", prefix_bits, digit_bits);
+    DevList dl;
+    int rc = pick_devs(1, dl);
+    if (rc) return rc;
+    DevCtx* c = dl.v[0];
+    cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+    CK(cudaMemsetAsync(d_hist, 0, (1u << digit_bits) * sizeof(unsigned), st));
+    if (count) {
+        const uint64_t blocks = (count + 255) / 256;
+        const int g = (int)(blocks < (uint64_t)c->sms * 8 ? blocks : (uint64_t)c->sms * 8);
+        k_radix_hist<<<g, 256, 0, st>>>((const unsigned long long*)d_vals, count, prefix, prefix_bits, digit_bits,
+                                        d_hist);
+    }
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int osim_exhaustive_ex_dev(const double* d_durs, int n, int dma, double sigma, uint64_t rank_lo, uint64_t rank_hi,
+                           int fast, double threshold, osim_summary* d_out, uint64_t* d_below, double* d_makespans,
+                           void* stream) {
+    int rc = check_common(n, dma, sigma);
+    if (rc) return rc;
+    if (rank_lo > rank_hi || rank_hi > factorial(n)) return fail(OSIM_EINVAL, "bad rank range");
+    DevList dl;
+    if ((rc = pick_devs(1, dl))) return rc;
+    DevCtx* c = dl.v[0];
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+    const int mp = max_parts_for(c);
+    void* base;
+    if ((rc = scratch(c, align_up(mp * sizeof(Part)), &base))) return rc;
+    return enqueue_exhaustive(c, st, d_durs, n, dma, sigma, rank_lo, rank_hi, fast, d_out, d_makespans, (Part*)base,
+                              mp, threshold, (unsigned long long*)d_below);
+}
+
 int osim_eval_perms(const double* durs, int n, int dma, double sigma, const uint8_t* perms,
                     uint64_t cnt, int n_dev, double* makespans, osim_summary* out) {
     int rc = check_common(n, dma, sigma);
@@ -434,14 +597,14 @@ int osim_eval_perms(const double* durs, int n, int dma, double sigma, const uint
     do {                                                                                         \
         g = grid_for(k_eval_perms<D, F>, kBlock, 0, c, blocks);                                  \
         if (g > mp) g = mp;                                                                      \
-        k_eval_perms<D, F><<<g, kBlock, 0, c->stream>>>((double*)b, n, sigma, (uint8_t*)(b + off_p), m, \
+        k_eval_perms<D, F><<<g, kBlock, 0, c->stream>>>((double*)b, n, sigma, (uint8_t*)(b + off_p), m, -HUGE_VAL, \
                                                          (double*)(b + off_ms), parts, c->d_err); \
     } while (0)
             if (dma == 2) { if (fast) OSIM_EP(2, true); else OSIM_EP(2, false); }
             else { if (fast) OSIM_EP(1, true); else OSIM_EP(1, false); }
 #undef OSIM_EP
         }
-        k_final_reduce<<<1, kBlock, 0, c->stream>>>(parts, g, (osim_summary*)(b + off_sum));
+        k_final_reduce<<<1, kBlock, 0, c->stream>>>(parts, g, (osim_summary*)(b + off_sum), nullptr);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(&res[gi], b + off_sum, sizeof(osim_summary), cudaMemcpyDeviceToHost, c->stream));
         if (m) CK(cudaMemcpyAsync(makespans + lo, b + off_ms, m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));

@@ -8,36 +8,36 @@ namespace osim {
 namespace {
 
 template <int N, int L>
-int exh_t(const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo, uint64_t hi, Part* parts,
-          int max_parts, double* d_ms, int* grid_out) {
+int exh_t(const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo, uint64_t hi, double thr,
+          Part* parts, int max_parts, double* d_ms, int* grid_out) {
     auto k = k_exhaustive_pfx<N, OSIM_DMA, OSIM_SP2, L>;
     constexpr uint64_t LF = Fact<L>::v;
     const uint64_t prefixes = (hi + LF - 1) / LF - lo / LF;
     int g = grid_for_sms(k, kBlock, 0, cfg.sms, (prefixes + kBlock - 1) / kBlock);
     if (g > max_parts) g = max_parts;
-    k<<<g, kBlock, 0, cfg.st>>>(d_durs, sigma, lo, hi, parts, d_ms);
+    k<<<g, kBlock, 0, cfg.st>>>(d_durs, sigma, lo, hi, thr, parts, d_ms);
     *grid_out = g;
     return 0;
 }
 
 template <int N>
 int exh_n(int L, const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo, uint64_t hi,
-          Part* parts, int max_parts, double* d_ms, int* g) {
+          double thr, Part* parts, int max_parts, double* d_ms, int* g) {
     if constexpr (tunable_n(N)) {
-        if (L == 3) return exh_t<N, 3>(cfg, d_durs, sigma, lo, hi, parts, max_parts, d_ms, g);
-        if (L == 5) return exh_t<N, 5>(cfg, d_durs, sigma, lo, hi, parts, max_parts, d_ms, g);
-        if (L == 4) return exh_t<N, 4>(cfg, d_durs, sigma, lo, hi, parts, max_parts, d_ms, g);
+        if (L == 3) return exh_t<N, 3>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g);
+        if (L == 5) return exh_t<N, 5>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g);
+        if (L == 4) return exh_t<N, 4>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g);
     }
-    return exh_t<N, default_pfx_l(N)>(cfg, d_durs, sigma, lo, hi, parts, max_parts, d_ms, g);
+    return exh_t<N, default_pfx_l(N)>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g);
 }
 
 }  // namespace
 
 int OSIM_EXH_NAME(int n, int L, const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo,
-                  uint64_t hi, Part* parts, int max_parts, double* d_ms, int* g) {
+                  uint64_t hi, double thr, Part* parts, int max_parts, double* d_ms, int* g) {
     switch (n) {
 #define OSIM_CASE(NN) \
-    case NN: return exh_n<NN>(L, cfg, d_durs, sigma, lo, hi, parts, max_parts, d_ms, g);
+    case NN: return exh_n<NN>(L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g);
         OSIM_CASE(1) OSIM_CASE(2) OSIM_CASE(3) OSIM_CASE(4) OSIM_CASE(5) OSIM_CASE(6)
         OSIM_CASE(7) OSIM_CASE(8) OSIM_CASE(9) OSIM_CASE(10) OSIM_CASE(11) OSIM_CASE(12)
         OSIM_CASE(13) OSIM_CASE(14) OSIM_CASE(15) OSIM_CASE(16)

@@ -30,6 +30,7 @@ struct Part {
     double lpm;
     long long lpe;
     unsigned long long count;
+    unsigned long long below;  // makespans strictly below the threshold (cli.py:102)
 };
 
 __device__ __forceinline__ void part_init(Part& a) {
@@ -40,6 +41,7 @@ __device__ __forceinline__ void part_init(Part& a) {
     a.lpm = 1.0;
     a.lpe = 0;
     a.count = 0;
+    a.below = 0;
 }
 
 template <bool EXACT>
@@ -59,8 +61,9 @@ __device__ __forceinline__ void renorm(double& m, long long& e) {
 // per-thread add, ranks visited in increasing order -> strict < keeps the
 // first of equal makespans (np.argmin)
 template <bool EXACT>
-__device__ __forceinline__ void part_add(Part& a, double ms, unsigned long long r) {
+__device__ __forceinline__ void part_add(Part& a, double ms, unsigned long long r, double thr) {
     if (ms < a.best) { a.best = ms; a.rank = r; }
+    a.below += (ms < thr) ? 1ull : 0ull;
     a.worst = fmax(a.worst, ms);
     a.sum = __dadd_rn(a.sum, ms);
     a.lpm = __dmul_rn(a.lpm, ms);
@@ -77,6 +80,7 @@ __device__ __forceinline__ void part_merge(Part& a, const Part& b) {
     a.lpe += b.lpe;
     renorm<false>(a.lpm, a.lpe);
     a.count += b.count;
+    a.below += b.below;
 }
 
 __device__ __forceinline__ Part part_shfl(const Part& a, int m) {
@@ -88,6 +92,7 @@ __device__ __forceinline__ Part part_shfl(const Part& a, int m) {
     b.lpm = __shfl_xor_sync(kFull, a.lpm, m);
     b.lpe = __shfl_xor_sync(kFull, a.lpe, m);
     b.count = __shfl_xor_sync(kFull, a.count, m);
+    b.below = __shfl_xor_sync(kFull, a.below, m);
     return b;
 }
 
@@ -165,7 +170,7 @@ __device__ __forceinline__ void run_warp(S& s, int max_steps) {
 // ---------------------------------------------------------------------------
 template <int DMA>
 __global__ void __launch_bounds__(kBlock) k_exhaustive_gen(const double* __restrict__ durs, int n,
-                                                           double sigma, uint64_t lo, uint64_t hi,
+                                                           double sigma, uint64_t lo, uint64_t hi, double thr,
                                                            Part* __restrict__ parts,
                                                            double* __restrict__ ms_out,
                                                            int* __restrict__ err) {
@@ -187,7 +192,7 @@ __global__ void __launch_bounds__(kBlock) k_exhaustive_gen(const double* __restr
         run_warp(s, 3 * n);
         if (!s.drained()) atomicExch(err, OSIM_ESTALL);
         if (valid) {
-            part_add<true>(acc, s.now, r);
+            part_add<true>(acc, s.now, r, thr);
             if (ms_out) ms_out[r - lo] = s.now;
         }
     }
@@ -197,13 +202,17 @@ __global__ void __launch_bounds__(kBlock) k_exhaustive_gen(const double* __restr
 
 // Deterministic final reduce of per-block partials (fixed order).
 static __global__ void __launch_bounds__(kBlock) k_final_reduce(const Part* __restrict__ parts, int P,
-                                                         osim_summary* __restrict__ out) {
+                                                         osim_summary* __restrict__ out,
+                                                         unsigned long long* __restrict__ below) {
     __shared__ Part sh[32];
     Part a;
     part_init(a);
     for (int i = threadIdx.x; i < P; i += blockDim.x) part_merge(a, parts[i]);
     a = block_reduce(a, sh);
-    if (threadIdx.x == 0) *out = part_to_summary(a);
+    if (threadIdx.x == 0) {
+        *out = part_to_summary(a);
+        if (below) *below = a.below;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -264,7 +273,7 @@ __device__ __forceinline__ void ck_load(const CkSlots& K, int i, FS& s) {
 // fall inside [lo, hi).  All threads of the warp must call together.
 template <int N, int DMA, bool SIGP2, int L, bool WRITE_MS>
 __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double rsig, uint64_t P,
-                                           bool validP, uint64_t lo, uint64_t hi, Part& acc,
+                                           bool validP, uint64_t lo, uint64_t hi, double thr, Part& acc,
                                            double* __restrict__ ms_out, uint64_t ms_base, CkSlots& K) {
     constexpr int M = N - L;
     constexpr uint64_t LF = Fact<L>::v;
@@ -301,7 +310,7 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
         for (int st = 0; st < rest; ++st) s.step(sigma, rsig);
         const uint64_t r = P * LF + (uint64_t)j;
         if (validP && r >= lo && r < hi) {
-            part_add<false>(acc, s.now, r);
+            part_add<false>(acc, s.now, r, thr);
             if constexpr (WRITE_MS) {
                 if (ms_out) ms_out[r - ms_base] = s.now;
             }
@@ -311,7 +320,7 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
 
 template <int N, int DMA, bool SIGP2, int L>
 __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const double* __restrict__ durs, double sigma,
-                                                           uint64_t lo, uint64_t hi, Part* __restrict__ parts,
+                                                           uint64_t lo, uint64_t hi, double thr, Part* __restrict__ parts,
                                                            double* __restrict__ ms_out) {
     __shared__ double2 sdr[3 * kStride];
     __shared__ Part sh[32];
@@ -328,7 +337,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
     for (uint64_t pb = p_lo + (uint64_t)blockIdx.x * blockDim.x; pb < p_hi; pb += stride) {
         const uint64_t P = pb + threadIdx.x;
         const bool validP = P < p_hi;
-        pfx_leaves<N, DMA, SIGP2, L, true>(base, sigma, rsig, validP ? P : p_lo, validP, lo, hi, acc, ms_out, lo, K);
+        pfx_leaves<N, DMA, SIGP2, L, true>(base, sigma, rsig, validP ? P : p_lo, validP, lo, hi, thr, acc, ms_out, lo, K);
     }
     acc = block_reduce(acc, sh);
     if (threadIdx.x == 0) parts[blockIdx.x] = acc;
@@ -353,7 +362,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_batch_pfx(
         for (uint64_t pb = 0; pb < NP; pb += blockDim.x) {
             const uint64_t P = pb + threadIdx.x;
             const bool validP = P < NP;
-            pfx_leaves<N, DMA, SIGP2, L, false>(base, sigma, rsig, validP ? P : 0, validP, 0, total, acc,
+            pfx_leaves<N, DMA, SIGP2, L, false>(base, sigma, rsig, validP ? P : 0, validP, 0, total, -kBig, acc,
                                                 nullptr, 0, K);
         }
         acc = block_reduce(acc, sh);  // ends with __syncthreads: smem reusable
@@ -368,7 +377,7 @@ template <int DMA, bool FAST>
 __global__ void __launch_bounds__(kBlock) k_eval_perms(const double* __restrict__ durs, int n,
                                                        double sigma,
                                                        const uint8_t* __restrict__ perms,
-                                                       uint64_t cnt, double* __restrict__ ms_out,
+                                                       uint64_t cnt, double thr, double* __restrict__ ms_out,
                                                        Part* __restrict__ parts,
                                                        int* __restrict__ err) {
     __shared__ double sd[3 * kStride], sr[3 * kStride];
@@ -393,7 +402,7 @@ __global__ void __launch_bounds__(kBlock) k_eval_perms(const double* __restrict_
         run_warp(s, 3 * n);
         if (!s.drained()) atomicExch(err, OSIM_ESTALL);
         if (valid) {
-            part_add<!FAST>(acc, s.now, i);
+            part_add<!FAST>(acc, s.now, i, thr);
             ms_out[i] = s.now;
         }
     }
@@ -426,7 +435,7 @@ __global__ void __launch_bounds__(kBlock) k_exhaustive_batch_gen(const double* _
             s.init(D, unrank_rt(valid ? r : 0, n), n, sigma, 1.0, nH, nK, nD);
             run_warp(s, 3 * n);
             if (!s.drained()) atomicExch(err, OSIM_ESTALL);
-            if (valid) part_add<true>(acc, s.now, r);
+            if (valid) part_add<true>(acc, s.now, r, -kBig);
         }
         acc = block_reduce(acc, sh);
         if (threadIdx.x == 0) out[b] = part_to_summary(acc);
@@ -943,6 +952,42 @@ __global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict
         const int g = i / n, p = i % n;
         order_out[(g0 + g) * (uint64_t)n + p] = (uint8_t)nib(S.ot[g], p);
     }
+}
+
+// ---------------------------------------------------------------------------
+// Exact order statistics over makespans kept in HBM (np.median for spaces too
+// large for the host).  Positive doubles order like
+// their uint64 bit patterns, so the k-th smallest is found digit by digit
+// (MSB first): each pass histograms the next kRadixBits bits of the values
+// that match the already-fixed prefix.  Lanes of a warp that hit the same bin
+// are aggregated with __match_any_sync (makespans share their top bits).
+// ---------------------------------------------------------------------------
+constexpr int kRadixBits = 11;
+
+static __global__ void __launch_bounds__(256) k_radix_hist(const unsigned long long* __restrict__ vals,
+                                                           uint64_t count, unsigned long long prefix, int pbits,
+                                                           int dbits, unsigned* __restrict__ hist) {
+    __shared__ unsigned sh[1 << kRadixBits];
+    const int nb = 1 << dbits;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const int shift = 64 - pbits - dbits;
+    const unsigned mask = (unsigned)nb - 1u;
+    const int lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x; b < count; b += stride) {
+        const uint64_t i = b + threadIdx.x;
+        const bool valid = i < count;
+        const unsigned long long u = valid ? vals[i] : 0ull;
+        const bool match = valid && (pbits == 0 || (u >> (64 - pbits)) == prefix);
+        const unsigned digit = (unsigned)(u >> shift) & mask;
+        const unsigned key = match ? digit : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(kFull, key);
+        if (match && lane == __ffs(peers) - 1) atomicAdd(&sh[digit], (unsigned)__popc(peers));
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nb; i += blockDim.x)
+        if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
 // ---------------------------------------------------------------------------

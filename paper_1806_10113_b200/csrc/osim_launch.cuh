@@ -45,7 +45,7 @@ inline int pfx_l_for(int n) {
 // exhaustive, all stages non-null, prefix-sharing (returns -1: unsupported n)
 #define OSIM_EXH_DECL(NAME)                                                                          \
     int NAME(int n, int L, const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo,   \
-             uint64_t hi, Part* parts, int max_parts, double* d_ms, int* grid_out);
+             uint64_t hi, double thr, Part* parts, int max_parts, double* d_ms, int* grid_out);
 OSIM_EXH_DECL(exh_fast_launch_d2s1)
 OSIM_EXH_DECL(exh_fast_launch_d2s0)
 OSIM_EXH_DECL(exh_fast_launch_d1)

@@ -180,3 +180,51 @@ def exhaustive_summary_batch(groups, profile: DeviceProfile, n_dev: int = 1) -> 
     else:
         d = np.stack([resolve_group(g, profile) for g in groups])
     return _capi.exhaustive_batch(d, profile.dma_engines, profile.overlap_sigma, n_dev=n_dev)
+
+
+# ---- full-distribution statistics ----------------
+
+@dataclass
+class OrderingStats:
+    """OrderingSummary plus the exact median and the below-threshold count."""
+
+    summary: OrderingSummary
+    median: float
+    below: int
+    threshold: float
+
+    @property
+    def percentile(self) -> float:
+        """100 * below / count, as `offsim permute` reports it (cli.py:102-103)."""
+        return 100.0 * self.below / self.summary.count if self.summary.count else float("nan")
+
+
+def exhaustive_stats_durs(durs, dma: int, sigma: float, threshold: float = float("-inf"), rank_lo: int = 0,
+                          rank_hi: Optional[int] = None, n_dev: int = 1) -> OrderingStats:
+    d = np.asarray(durs, dtype=np.float64).reshape(-1, 3)
+    n = d.shape[0]
+    if rank_hi is None:
+        rank_hi = math.factorial(n)
+    s, below, med = _capi.exhaustive_stats(d, dma, sigma, rank_lo, rank_hi, threshold, n_dev=n_dev)
+    return OrderingStats(summary_from_dict(s, n), med, below, threshold)
+
+
+def exhaustive_stats(tasks: Sequence[TaskSpec], profile: DeviceProfile, threshold: Optional[float] = None,
+                     rank_lo: int = 0, rank_hi: Optional[int] = None, n_dev: int = 1) -> OrderingStats:
+    """Median / percentile of the makespan distribution over every ordering
+    without materializing it on the host (12! works)."""
+    if not tasks:
+        raise ValueError("task set must be non-empty")
+    thr = float("-inf") if threshold is None else float(threshold)
+    return exhaustive_stats_durs(resolve_group(tasks, profile), profile.dma_engines, profile.overlap_sigma, thr,
+                                 rank_lo, rank_hi, n_dev)
+
+
+def heuristic_percentile(tasks: Sequence[TaskSpec], profile: DeviceProfile, n_dev: int = 1):
+    """The `offsim permute` figure (cli.py:96-103) over the full ordering
+    space: (heuristic makespan, percentile of orderings strictly faster)."""
+    from .heuristic import reorder_batch_many
+
+    _, ms = reorder_batch_many([list(tasks)], profile, return_makespans=True)
+    st = exhaustive_stats(tasks, profile, threshold=float(ms[0]), n_dev=n_dev)
+    return float(ms[0]), st.percentile, st

@@ -250,3 +250,61 @@ def test_determinism_run_to_run():
     a, _ = _capi.exhaustive(d, 2, 0.375, 0, 50_000_000)
     b, _ = _capi.exhaustive(d, 2, 0.375, 0, 50_000_000)
     assert a == b
+
+
+# ---- row f2: percentile count and exact median on the device ---------------
+
+def test_c3_median_and_heuristic_percentile_on_device():
+    g = load("c3_full.json")
+    h = g["heuristic_relabeled_t00"]
+    s, below, med = _capi.exhaustive_stats(durs(g["durs"]), 2, 0.5, 0, 3628800, threshold=F(h["makespan"]))
+    assert med == F(g["median"])
+    assert below == g["below_heuristic"]
+    assert s["best_rank"] == g["argmin"] and s["best"] == F(g["best"])
+
+
+def test_medians_match_numpy_goldens():
+    for c in load("c1_bk.json")["cases"]:
+        _, below, med = _capi.exhaustive_stats(durs(c["durs"]), c["dma"], F(c["sigma"]), 0, 24)
+        assert med == F(c["report"]["median"]) and below == 0
+    g = load("c2_tg.json")
+    for tg in g["tgs"]:
+        _, _, med = _capi.exhaustive_stats(durs(tg["durs"]), 2, 0.5, 0, 40320)
+        assert med == F(tg["median"])
+
+
+def test_c4_window_median_odd_and_even_vs_numpy():
+    d = synth.c4_group()
+    for lo, cnt in ((77_777_777, 1_000_001), (300_000_000, 999_998)):
+        _, oms = O.exhaustive(d, 2, 0.375, lo, lo + cnt, threads=8, makespans=True)
+        thr = float(np.quantile(oms, 0.3))
+        s, below, med = _capi.exhaustive_stats(d, 2, 0.375, lo, lo + cnt, threshold=thr)
+        assert med == float(np.median(oms))
+        assert below == int((oms < thr).sum())
+        assert s["count"] == cnt
+
+
+def test_c4_full_space_median_is_an_order_statistic():
+    d = synth.c4_group()
+    total = math.factorial(12)
+    s, below, med = _capi.exhaustive_stats(d, 2, 0.5, 0, total, threshold=float("inf"))
+    assert below == total == s["count"]
+    # even count: med = (v[k-1] + v[k]) / 2 with k = total/2 -> at most k values
+    # lie strictly below it and at least k at or below it
+    _, lt, _ = _capi.exhaustive_stats(d, 2, 0.5, 0, total, threshold=med, median=False)
+    _, le, _ = _capi.exhaustive_stats(d, 2, 0.5, 0, total, threshold=float(np.nextafter(med, np.inf)),
+                                      median=False)
+    assert lt <= total // 2 <= le
+    assert s["best"] <= med <= s["worst"]
+
+
+def test_heuristic_percentile_dropin():
+    g = load("c3_full.json")
+    p = osim.DeviceProfile("2dma", 2, 0.01, 6e6, 0.01, 6e6, overlap_sigma=0.5)
+    tasks = [osim.TaskSpec(f"t{i:02d}", fixed_durations=tuple(r)) for i, r in enumerate(durs(g["durs"]).tolist())]
+    hms, pct, st = osim.heuristic_percentile(tasks, p)
+    h = g["heuristic_relabeled_t00"]
+    assert hms == F(h["makespan"])
+    assert st.below == g["below_heuristic"]
+    assert pct == 100.0 * g["below_heuristic"] / 3628800
+    assert st.median == F(g["median"])
