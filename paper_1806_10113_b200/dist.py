@@ -92,3 +92,119 @@ def exhaustive_summary_distributed(durs, dma: int, sigma: float, group=None,
     tdist.all_gather(bufs, mine, group=group)
     parts = [unpack(b.cpu().numpy()) for b in bufs]
     return summary_from_dict(combine(parts), n)
+
+
+# ---- order statistics of a sharded makespan set (row f2) -------------------
+
+RADIX_BITS = 11
+
+
+def _bits_to_double(b: int) -> float:
+    return float(np.array([b], dtype=np.uint64).view(np.float64)[0])
+
+
+def select_kth_distributed(local_hist: Callable, k: int, group=None, device=None) -> float:
+    """k-th smallest (0-based) positive double of a set sharded over ranks.
+
+    local_hist(prefix, prefix_bits, digit_bits) -> int64 histogram of this
+    rank's values (2**digit_bits bins, MSB-first digits of the bit pattern,
+    values whose top prefix_bits bits equal prefix).  One all_reduce(SUM)
+    per pass combines the ranks (NCCL on GPUs); every rank gets the answer.
+    """
+    import torch
+    import torch.distributed as tdist
+
+    backend = tdist.get_backend(group)
+    dev = device if device is not None else (torch.device("cuda", torch.cuda.current_device())
+                                             if backend == "nccl" else torch.device("cpu"))
+    prefix, pbits = 0, 0
+    while pbits < 64:
+        d = min(RADIX_BITS, 64 - pbits)
+        h = torch.from_numpy(np.ascontiguousarray(local_hist(prefix, pbits, d), dtype=np.int64)).to(dev)
+        tdist.all_reduce(h, group=group)
+        tot = h.cpu().numpy()
+        cum = np.cumsum(tot)
+        b = int(np.searchsorted(cum, k, side="right"))
+        if b >= len(tot):
+            raise ValueError(f"rank {k} outside the value set")
+        k -= int(cum[b - 1]) if b > 0 else 0
+        prefix = (prefix << d) | b
+        pbits += d
+    return _bits_to_double(prefix)
+
+
+def numpy_hist(vals: np.ndarray):
+    """Host histogram of positive doubles (test double of osim_radix_hist_dev)."""
+    u = np.ascontiguousarray(vals, dtype=np.float64).view(np.uint64)
+
+    def hist(prefix, pbits, dbits):
+        sel = u if pbits == 0 else u[(u >> np.uint64(64 - pbits)) == np.uint64(prefix)]
+        dig = (sel >> np.uint64(64 - pbits - dbits)) & np.uint64((1 << dbits) - 1)
+        return np.bincount(dig.astype(np.int64), minlength=1 << dbits)
+
+    return hist
+
+
+def median_distributed(local_hist: Callable, count: int, group=None, device=None) -> float:
+    """np.median of the sharded set: the middle value, or (a + b) / 2."""
+    if count % 2:
+        return select_kth_distributed(local_hist, count // 2, group, device)
+    a = select_kth_distributed(local_hist, count // 2 - 1, group, device)
+    b = select_kth_distributed(local_hist, count // 2, group, device)
+    return float(np.float64(a) + np.float64(b)) / 2.0
+
+
+def exhaustive_stats_distributed(durs, dma: int, sigma: float, threshold: float = float("-inf"), group=None):
+    """Summary, below-threshold count and exact median of one group's whole
+    ordering space, sharded over the process group (one GPU per rank): each
+    rank keeps its shard's makespans in HBM (8 B per ordering), reductions and
+    selection histograms are combined with NCCL all_gather / all_reduce."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as tdist
+
+    from . import _capi
+
+    d = np.asarray(durs, dtype=np.float64).reshape(-1, 3)
+    n = d.shape[0]
+    total = math.factorial(n)
+    world, rank = tdist.get_world_size(group), tdist.get_rank(group)
+    lo, hi = shard(total, rank, world)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    L = _capi.load()
+    # library work and torch's reads of its outputs must share one stream; the
+    # legacy default stream (handle 0) would map to the library's own stream
+    st = torch.cuda.Stream(device=dev)
+    st.wait_stream(torch.cuda.current_stream())
+    prev = torch.cuda.current_stream()
+    torch.cuda.set_stream(st)
+    try:
+        return _stats_on_stream(L, C, torch, tdist, _capi, d, n, dma, sigma, threshold, group, lo, hi, world, dev, st)
+    finally:
+        torch.cuda.set_stream(prev)
+
+
+def _stats_on_stream(L, C, torch, tdist, _capi, d, n, dma, sigma, threshold, group, lo, hi, world, dev, st):
+    sp = C.c_void_p(st.cuda_stream)
+    dd = torch.from_numpy(d).to(dev)
+    out = torch.zeros(6, dtype=torch.float64, device=dev)
+    below = torch.zeros(1, dtype=torch.int64, device=dev)
+    ms = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=dev)
+    hist = torch.empty(1 << RADIX_BITS, dtype=torch.int32, device=dev)
+    fast = int(_capi.fast_eligible(d, sigma))
+    _capi.check(L.osim_exhaustive_ex_dev(C.c_void_p(dd.data_ptr()), n, int(dma), float(sigma), lo, hi, fast,
+                                         float(threshold), C.c_void_p(out.data_ptr()), C.c_void_p(below.data_ptr()),
+                                         C.c_void_p(ms.data_ptr()), sp))
+    bufs = [torch.empty_like(out) for _ in range(world)]
+    tdist.all_gather(bufs, out, group=group)
+    tdist.all_reduce(below, group=group)
+    summ = summary_from_dict(combine([unpack(b.cpu().numpy()) for b in bufs]), n)
+
+    def local_hist(prefix, pbits, dbits):
+        _capi.check(L.osim_radix_hist_dev(C.c_void_p(ms.data_ptr()), hi - lo, prefix, pbits, dbits,
+                                          C.c_void_p(hist.data_ptr()), sp))
+        return hist[: 1 << dbits].to(torch.int64).cpu().numpy()
+
+    med = median_distributed(local_hist, summ.count, group)
+    return summ, int(below.item()), med

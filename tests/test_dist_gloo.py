@@ -63,3 +63,43 @@ def test_gloo_sharded_exhaustive_matches_whole_space(world):
         assert close(sm, whole["sum"]) and close(sl, whole["sum_log"])
     # every rank holds the identical combined summary
     assert len({r[1:] for r in results}) == 1
+
+
+def _median_worker(rank, world, port, vals, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1806_10113_b200.dist import median_distributed, numpy_hist, select_kth_distributed, shard
+
+        lo, hi = shard(len(vals), rank, world)
+        mine = vals[lo:hi]
+        h = numpy_hist(mine)
+        med = median_distributed(h, len(vals))
+        k7 = select_kth_distributed(h, 7)
+        q.put((rank, med, k7))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("count", [5040, 5039])
+def test_gloo_sharded_median_selection(count):
+    # the makespans of a 7-task group (with ties) from the pinned oracle
+    c = load("c1_bk.json")["cases"][3]
+    d = np.concatenate([durs(c["durs"]), durs(c["durs"])[:3] * 1.25])
+    _, ms = O.exhaustive(d, c["dma"], F(c["sigma"]), threads=4, makespans=True)
+    vals = ms[:count].copy()
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_median_worker, args=(r, world, port, vals, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, med, k7 in res:
+        assert med == float(np.median(vals))
+        assert k7 == float(np.sort(vals)[7])

@@ -308,3 +308,29 @@ def test_heuristic_percentile_dropin():
     assert st.below == g["below_heuristic"]
     assert pct == 100.0 * g["below_heuristic"] / 3628800
     assert st.median == F(g["median"])
+
+
+def test_distributed_stats_single_rank_nccl():
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as tdist
+
+    from paper_1806_10113_b200 import dist as odist
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        g = load("c3_full.json")
+        h = g["heuristic_relabeled_t00"]
+        summ, below, med = odist.exhaustive_stats_distributed(durs(g["durs"]), 2, 0.5, threshold=F(h["makespan"]))
+        assert med == F(g["median"]) and below == g["below_heuristic"]
+        assert summ.best_rank == g["argmin"] and summ.count == 3628800
+    finally:
+        tdist.destroy_process_group()
