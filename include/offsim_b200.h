@@ -114,6 +114,27 @@ int osim_exhaustive_stats(const double* durs, int n, int dma, double sigma, uint
 int osim_timeline(const double* durs, int n, int dma, double sigma, const uint8_t* order,
                   double* start, double* end, double* makespan, double* idle);
 
+/* ---- NoReorder distribution (workload.py:259-327) */
+/* T workers x N dependent tasks: durs[T*N][3] with task (w, j) at w*N + j
+ * depending on (w, j-1).  Ranks index sorted(set(permutations(labels)))
+ * (the worker-label sequences, workload.py:262-265); each sequence is
+ * simulated as workload.simulate_sequence (deps gate; 1-DMA wave split,
+ * :277-304).  below/threshold as in osim_exhaustive_stats; makespans
+ * nullable [hi-lo]. */
+int osim_interleavings(const double* durs, int T, int N, int dma, double sigma, uint64_t rank_lo,
+                       uint64_t rank_hi, double threshold, int n_dev, osim_summary* out,
+                       uint64_t* below, double* makespans);
+/* Sampled mode: explicit worker-label rows labels[cnt][T*N]. */
+int osim_eval_sequences(const double* durs, int T, int N, int dma, double sigma,
+                        const uint8_t* labels, uint64_t cnt, int n_dev, double* makespans,
+                        osim_summary* out);
+/* engine.simulate(tasks, profile, deps) (waves = 0) or
+ * workload.simulate_sequence (waves = 1): dep[n] = prerequisite task index
+ * or -1 (nullable). */
+int osim_timeline_deps(const double* durs, int n, int dma, double sigma, const uint8_t* order,
+                       const int8_t* dep, int waves, double* start, double* end, double* makespan,
+                       double* idle);
+
 /* ---- device-resident variants (inputs already in HBM) ---------------- */
 /* fast = 1 asserts every stage is non-null and every duration and sigma
  * lies in [2^-60, 2^60] (osim_fast_eligible()); 0 selects the general path. */

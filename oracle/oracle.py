@@ -66,6 +66,12 @@ def lib():
         L.oracle_pysum.restype = C.c_double
         L.oracle_unrank.argtypes = [C.c_uint64, C.c_int, ip]
         L.oracle_stats_get.argtypes = [C.POINTER(C.c_int64)]
+        L.oracle_simulate_seq.argtypes = [dp, C.c_int, C.c_int, C.c_double, ip, C.c_int, ip, dp, dp, dp, dp]
+        L.oracle_unrank_labels.argtypes = [C.c_uint64, C.c_int, C.c_int, ip]
+        L.oracle_interleavings.argtypes = [dp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_uint64,
+                                           C.c_int, C.POINTER(OracleSummary), dp]
+        L.oracle_eval_sequences.argtypes = [dp, C.c_int, C.c_int, C.c_int, C.c_double, u8p, C.c_uint64, C.c_int,
+                                            dp, C.POINTER(OracleSummary)]
         L.oracle_op_stats.argtypes = [dp, C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_uint64,
                                       C.c_uint64, C.POINTER(C.c_int64)]
         _lib = L
@@ -193,3 +199,52 @@ def reorder_op_stats(durs, id_rank, dma, sigma, sum_mode):
     out = np.zeros(4, dtype=np.int64)
     lib().oracle_stats_get(_p(out, C.c_int64))
     return out
+
+
+def simulate_seq(durs, order, dma, sigma, dep=None) -> SimResult:
+    """workload.simulate_sequence: deps gate + 1-DMA wave split."""
+    d = _durs(durs)
+    n = d.shape[0]
+    o = np.ascontiguousarray(np.asarray(order, dtype=np.int32))
+    dp_ = None if dep is None else np.ascontiguousarray(np.asarray(dep, dtype=np.int32))
+    st, en, idle = np.empty((n, 3)), np.empty((n, 3)), np.empty(3)
+    ms = C.c_double()
+    rc = lib().oracle_simulate_seq(_p(d, C.c_double), n, int(dma), float(sigma), _p(o, C.c_int), len(o),
+                                   _p(dp_, C.c_int), _p(st, C.c_double), _p(en, C.c_double), C.byref(ms),
+                                   _p(idle, C.c_double))
+    if rc:
+        raise RuntimeError(f"oracle_simulate_seq rc={rc}")
+    return SimResult(ms.value, float("nan"), idle, st, en, -1)
+
+
+def unrank_labels(rank, T, N):
+    p = np.empty(T * N, dtype=np.int32)
+    lib().oracle_unrank_labels(rank, T, N, _p(p, C.c_int))
+    return p.tolist()
+
+
+def interleavings(durs, T, N, dma, sigma, lo=0, hi=None, threads=1, makespans=False):
+    import math
+
+    d = np.ascontiguousarray(np.asarray(durs, dtype=np.float64).reshape(-1, 3))
+    if hi is None:
+        hi = math.factorial(T * N) // math.factorial(N) ** T
+    out = OracleSummary()
+    ms = np.empty(hi - lo) if makespans else None
+    rc = lib().oracle_interleavings(_p(d, C.c_double), T, N, int(dma), float(sigma), lo, hi, threads,
+                                    C.byref(out), _p(ms, C.c_double))
+    if rc:
+        raise RuntimeError(f"oracle_interleavings rc={rc}")
+    return out.as_dict(), ms
+
+
+def eval_sequences(durs, T, N, dma, sigma, labels, threads=1):
+    d = np.ascontiguousarray(np.asarray(durs, dtype=np.float64).reshape(-1, 3))
+    lab = np.ascontiguousarray(np.asarray(labels, dtype=np.uint8).reshape(-1, T * N))
+    ms = np.empty(lab.shape[0])
+    out = OracleSummary()
+    rc = lib().oracle_eval_sequences(_p(d, C.c_double), T, N, int(dma), float(sigma), _p(lab, C.c_uint8),
+                                     lab.shape[0], threads, _p(ms, C.c_double), C.byref(out))
+    if rc:
+        raise RuntimeError(f"oracle_eval_sequences rc={rc}")
+    return out.as_dict(), ms

@@ -678,3 +678,170 @@ int oracle_reorder_batch(const double* durs, const uint8_t* id_rank, uint64_t B,
         if (jobs[t].err) return jobs[t].err;
     return 0;
 }
+
+
+/* ---- workload.py restatement: NoReorder interleavings (row f1) ------ */
+
+/* simulate_sequence (workload.py:277-304): 2-DMA or no deps -> one submit
+ * with the deps gate; 1-DMA with deps -> a new wave (a separate submit)
+ * whenever a task's prerequisite sits in the current wave. */
+int oracle_simulate_seq(const double* durs, int n_tasks, int dma, double sigma, const int* order, int n_order,
+                        const int* dep, double* start, double* end, double* makespan, double* idle) {
+    if (n_order < 1 || n_order > OR_MAXN || n_tasks > OR_MAXN) return -1;
+    if (dma != 2 && dep) {
+        or_sim s;
+        sim_init(&s, dma, sigma, dep, n_tasks);
+        int wave[OR_MAXN], nw = 0;
+        int in_wave[OR_MAXN];
+        for (int t = 0; t < n_tasks; ++t) in_wave[t] = 0;
+        for (int i = 0; i < n_order; ++i) {
+            int t = order[i];
+            int d = dep[t];
+            if (d >= 0 && in_wave[d]) { /* workload.py:296-298 */
+                if (sim_submit(&s, durs, wave, nw)) return -1;
+                for (int j = 0; j < nw; ++j) in_wave[wave[j]] = 0;
+                nw = 0;
+            }
+            wave[nw++] = t;
+            in_wave[t] = 1;
+        }
+        if (nw && sim_submit(&s, durs, wave, nw)) return -1;
+        while (!sim_drained(&s))
+            if (sim_step(&s) < 0) return -5;
+        double ms = 0.0;
+        for (int i = 0; i < s.n_cmd; ++i)
+            if (i == 0 || s.cmd[i].end > ms) ms = s.cmd[i].end;
+        if (makespan) *makespan = ms;
+        if (idle) {
+            idle[0] = idle_of_kind(&s, K_HTD);
+            idle[1] = idle_of_kind(&s, K_K);
+            idle[2] = idle_of_kind(&s, K_DTH);
+        }
+        if (start || end) {
+            for (int t = 0; t < n_tasks * 3; ++t) {
+                if (start) start[t] = -1.0;
+                if (end) end[t] = -1.0;
+            }
+            for (int i = 0; i < s.n_cmd; ++i) {
+                const or_cmd* c = &s.cmd[i];
+                if (start) start[3 * c->task + c->kind] = c->start;
+                if (end) end[3 * c->task + c->kind] = c->end;
+            }
+        }
+        return 0;
+    }
+    return oracle_simulate(durs, n_tasks, dma, sigma, order, n_order, dep, start, end, makespan, idle, NULL, NULL);
+}
+
+/* multinomial coefficient (sum c)! / prod c_i! for the remaining label counts */
+static uint64_t multinom(const int* c, int T) {
+    uint64_t r = 1;
+    int tot = 0;
+    for (int w = 0; w < T; ++w) {
+        for (int k = 1; k <= c[w]; ++k) {
+            ++tot;
+            r = r * (uint64_t)tot / (uint64_t)k; /* exact: running binomial products */
+        }
+    }
+    return r;
+}
+
+/* sorted(set(permutations(labels))) index -> label sequence (workload.py:262-265) */
+void oracle_unrank_labels(uint64_t rank, int T, int N, int* labels) {
+    int c[OR_MAXN];
+    for (int w = 0; w < T; ++w) c[w] = N;
+    for (int p = 0; p < T * N; ++p) {
+        for (int w = 0; w < T; ++w) {
+            if (!c[w]) continue;
+            c[w]--;
+            uint64_t m = multinom(c, T);
+            if (rank < m) { labels[p] = w; break; }
+            rank -= m;
+            c[w]++;
+        }
+    }
+}
+
+/* labels -> task order and chain deps: task (w, j) is index w*N + j and
+ * depends on (w, j-1) (noreorder_distribution, workload.py:310-326) */
+static void labels_to_order(const int* labels, int T, int N, int* order, int* dep) {
+    int cnt[OR_MAXN];
+    for (int w = 0; w < T; ++w) cnt[w] = 0;
+    for (int p = 0; p < T * N; ++p) order[p] = labels[p] * N + cnt[labels[p]]++;
+    for (int w = 0; w < T; ++w)
+        for (int j = 0; j < N; ++j) dep[w * N + j] = j ? w * N + j - 1 : -1;
+}
+
+typedef struct {
+    const double* durs;
+    int T, N, dma;
+    double sigma;
+    uint64_t lo, hi;
+    const uint8_t* labels; /* explicit mode */
+    double* makespans;
+    oracle_summary sum;
+    int err;
+} il_job;
+
+static void* il_worker(void* arg) {
+    il_job* j = (il_job*)arg;
+    summary_init(&j->sum);
+    comp_t cp = {0.0, 0.0};
+    int lab[OR_MAXN], order[OR_MAXN], dep[OR_MAXN];
+    const int n = j->T * j->N;
+    for (uint64_t r = j->lo; r < j->hi; ++r) {
+        if (j->labels) for (int i = 0; i < n; ++i) lab[i] = j->labels[r * (uint64_t)n + i];
+        else oracle_unrank_labels(r, j->T, j->N, lab);
+        labels_to_order(lab, j->T, j->N, order, dep);
+        double ms;
+        int rc = oracle_simulate_seq(j->durs, n, j->dma, j->sigma, order, n, dep, NULL, NULL, &ms, NULL);
+        if (rc) { j->err = rc; return NULL; }
+        if (j->makespans) j->makespans[r] = ms;
+        summary_add(&j->sum, &cp, ms, r);
+    }
+    j->sum.sum += cp.c_sum;
+    j->sum.sum_log += cp.c_log;
+    return NULL;
+}
+
+static int run_il(const double* durs, int T, int N, int dma, double sigma, uint64_t lo, uint64_t hi,
+                  const uint8_t* labels, int threads, double* makespans, oracle_summary* out) {
+    if (T < 1 || N < 1 || T * N > OR_MAXN) return -1;
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    uint64_t total = hi - lo;
+    if ((uint64_t)threads > total && total > 0) threads = (int)total;
+    il_job jobs[256];
+    pthread_t tid[256];
+    for (int t = 0; t < threads; ++t) {
+        il_job* j = &jobs[t];
+        memset(j, 0, sizeof(*j));
+        j->durs = durs; j->T = T; j->N = N; j->dma = dma; j->sigma = sigma; j->labels = labels;
+        j->lo = lo + total * (uint64_t)t / (uint64_t)threads;
+        j->hi = lo + total * (uint64_t)(t + 1) / (uint64_t)threads;
+        j->makespans = makespans ? makespans - lo : NULL;
+    }
+    if (threads == 1) il_worker(&jobs[0]);
+    else {
+        for (int t = 0; t < threads; ++t) pthread_create(&tid[t], NULL, il_worker, &jobs[t]);
+        for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+    }
+    oracle_summary acc;
+    summary_init(&acc);
+    for (int t = 0; t < threads; ++t) {
+        if (jobs[t].err) return jobs[t].err;
+        summary_merge(&acc, &jobs[t].sum);
+    }
+    if (out) *out = acc;
+    return 0;
+}
+
+int oracle_interleavings(const double* durs, int T, int N, int dma, double sigma, uint64_t lo, uint64_t hi,
+                         int threads, oracle_summary* out, double* makespans) {
+    return run_il(durs, T, N, dma, sigma, lo, hi, NULL, threads, makespans, out);
+}
+
+int oracle_eval_sequences(const double* durs, int T, int N, int dma, double sigma, const uint8_t* labels,
+                          uint64_t cnt, int threads, double* makespans, oracle_summary* out) {
+    return run_il(durs, T, N, dma, sigma, 0, cnt, labels, threads, makespans, out);
+}

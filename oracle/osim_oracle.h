@@ -78,6 +78,20 @@ int oracle_reorder_batch(const double* durs, const uint8_t* id_rank,
                          int sum_mode, int threads, uint8_t* order,
                          double* makespan, uint32_t* n_sims);
 
+/* workload.simulate_sequence (workload.py:277-304): deps gate, and on a
+ * 1-DMA device the wave split into separate submits. */
+int oracle_simulate_seq(const double* durs, int n_tasks, int dma, double sigma, const int* order, int n_order,
+                        const int* dep, double* start, double* end, double* makespan, double* idle);
+/* sorted(set(permutations(labels))) rank -> label sequence (workload.py:262-265). */
+void oracle_unrank_labels(uint64_t rank, int T, int N, int* labels);
+/* noreorder_distribution (workload.py:307-327) over label-sequence ranks
+ * [lo, hi); durs [T][N][3], task (w, j) depends on (w, j-1). */
+int oracle_interleavings(const double* durs, int T, int N, int dma, double sigma, uint64_t lo, uint64_t hi,
+                         int threads, oracle_summary* out, double* makespans);
+/* sampled mode: explicit label sequences labels[cnt][T*N]. */
+int oracle_eval_sequences(const double* durs, int T, int N, int dma, double sigma, const uint8_t* labels,
+                          uint64_t cnt, int threads, double* makespans, oracle_summary* out);
+
 /* CPython builtin sum() of doubles (bltinmodule.c, 3.12 Neumaier / <=3.11
  * naive), exposed for the tests. */
 double oracle_pysum(const double* x, int n, int sum_mode);

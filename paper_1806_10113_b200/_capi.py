@@ -26,7 +26,8 @@ EXPORTS = (
     "osim_exhaustive", "osim_eval_perms", "osim_exhaustive_batch", "osim_heuristic_batch",
     "osim_timeline", "osim_fast_eligible", "osim_exhaustive_dev", "osim_exhaustive_batch_dev",
     "osim_heuristic_batch_dev", "osim_selftest_div", "osim_fp64_peak", "osim_exhaustive_stats",
-    "osim_exhaustive_ex_dev", "osim_radix_hist_dev",
+    "osim_exhaustive_ex_dev", "osim_radix_hist_dev", "osim_interleavings", "osim_eval_sequences",
+    "osim_timeline_deps",
 )
 
 
@@ -56,7 +57,8 @@ class OsimError(RuntimeError):
 
 
 class StallError(RuntimeError):
-    """engine.py:239-241: simulation stalled with commands pending."""
+    """engine.py:239-241: simulation stalled with commands pending (the
+    reference raises RuntimeError; this is a subclass)."""
 
 
 _lib = None
@@ -96,6 +98,9 @@ def load(path: str = LIB_PATH):
             "osim_exhaustive_stats": ([dp, i, i, d, u64, u64, d, i, sp, C.POINTER(u64), dp], i),
             "osim_exhaustive_ex_dev": ([vp, i, i, d, u64, u64, i, d, vp, vp, vp, vp], i),
             "osim_radix_hist_dev": ([vp, u64, u64, i, i, vp, vp], i),
+            "osim_interleavings": ([dp, i, i, i, d, u64, u64, d, i, sp, C.POINTER(u64), dp], i),
+            "osim_eval_sequences": ([dp, i, i, i, d, u8p, u64, i, dp, sp], i),
+            "osim_timeline_deps": ([dp, i, i, d, u8p, C.POINTER(C.c_int8), i, dp, dp, dp, dp], i),
             "osim_fp64_peak": ([dp], i),
         }
         for name, (args, res) in sig.items():
@@ -230,3 +235,38 @@ def fp64_peak_tflops() -> float:
     t = C.c_double()
     check(load().osim_fp64_peak(C.byref(t)))
     return t.value
+
+
+def interleavings(durs, T, N, dma, sigma, lo, hi, threshold=float("-inf"), n_dev=1, want_makespans=False):
+    d = f64(durs, (-1, 3))
+    out = OsimSummary()
+    below = C.c_uint64()
+    ms = np.empty(hi - lo) if want_makespans else None
+    check(load().osim_interleavings(ptr(d, C.c_double), int(T), int(N), int(dma), float(sigma), int(lo), int(hi),
+                                    float(threshold), int(n_dev), C.byref(out), C.byref(below),
+                                    ptr(ms, C.c_double) if ms is not None else None))
+    return out.as_dict(), below.value, ms
+
+
+def eval_sequences(durs, T, N, dma, sigma, labels, n_dev=1):
+    d = f64(durs, (-1, 3))
+    lab = u8(labels, (-1, T * N))
+    ms = np.empty(lab.shape[0])
+    out = OsimSummary()
+    check(load().osim_eval_sequences(ptr(d, C.c_double), int(T), int(N), int(dma), float(sigma),
+                                     ptr(lab, C.c_uint8), lab.shape[0], int(n_dev), ptr(ms, C.c_double),
+                                     C.byref(out)))
+    return out.as_dict(), ms
+
+
+def timeline_deps(durs, dma, sigma, order, dep=None, waves=False):
+    d = f64(durs, (-1, 3))
+    n = d.shape[0]
+    o = u8(order)
+    dp_ = None if dep is None else np.ascontiguousarray(np.asarray(dep, dtype=np.int8))
+    st, en, idle = np.empty((n, 3)), np.empty((n, 3)), np.empty(3)
+    ms = C.c_double()
+    check(load().osim_timeline_deps(ptr(d, C.c_double), n, int(dma), float(sigma), ptr(o, C.c_uint8),
+                                    ptr(dp_, C.c_int8) if dp_ is not None else None, int(bool(waves)),
+                                    ptr(st, C.c_double), ptr(en, C.c_double), C.byref(ms), ptr(idle, C.c_double)))
+    return st, en, ms.value, idle

@@ -10,9 +10,11 @@
 #include <cstring>
 #include <algorithm>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
+#include "osim_deps.cuh"
 #include "osim_launch.cuh"
 
 using namespace osim;
@@ -103,17 +105,87 @@ int check_common(int n, int dma, double sigma) {
     return 0;
 }
 
-int check_durs(const double* durs, uint64_t tasks) {
-    if (!durs) return fail(OSIM_EINVAL, "durations pointer is NULL");
-    for (uint64_t t = 0; t < tasks; ++t) {
-        const double h = durs[3 * t], k = durs[3 * t + 1], d = durs[3 * t + 2];
-        if (!(h >= 0.0) || !(k >= 0.0) || !(d >= 0.0) || !std::isfinite(h) || !std::isfinite(k) ||
-            !std::isfinite(d))
-            return fail(OSIM_EINVAL, "task %llu: durations must be finite and non-negative",
-                        (unsigned long long)t);
-        if (h <= 0 && k <= 0 && d <= 0)
-            return fail(OSIM_EINVAL, "task %llu has no commands", (unsigned long long)t);
+// One pass over the durations: the reference's validity rules
+// (model.py:95-100, engine.py:129-130) and fast-path eligibility (every
+// stage non-null and in [2^-60, 2^60]); split over host threads for large
+// batches.  Reports the lowest offending task, as a serial scan would.
+struct ScanPart {
+    uint64_t bad = ~0ull;
+    int why = 0;  // 1 = negative / non-finite, 2 = no commands
+    bool fast = true;
+};
+
+void scan_range(const double* d, uint64_t t0, uint64_t t1, ScanPart& r) {
+    const double lo = 0x1p-60, hi = 0x1p60;
+    bool fast = true;
+    for (uint64_t t = t0; t < t1; ++t) {
+        const double h = d[3 * t], k = d[3 * t + 1], x = d[3 * t + 2];
+        if (!(h >= 0.0 && k >= 0.0 && x >= 0.0 && h <= 1.7976931348623157e308 && k <= 1.7976931348623157e308 &&
+              x <= 1.7976931348623157e308)) {
+            r.bad = t; r.why = 1; break;
+        }
+        if (h <= 0 && k <= 0 && x <= 0) { r.bad = t; r.why = 2; break; }
+        fast = fast && h >= lo && h <= hi && k >= lo && k <= hi && x >= lo && x <= hi;
     }
+    r.fast = fast;
+}
+
+int scan_durs(const double* durs, uint64_t tasks, double sigma, int* fast) {
+    if (!durs) return fail(OSIM_EINVAL, "durations pointer is NULL");
+    unsigned nt = tasks >= (1ull << 18) ? std::thread::hardware_concurrency() : 1u;
+    if (nt < 1) nt = 1;
+    if (nt > 32) nt = 32;
+    std::vector<ScanPart> parts(nt);
+    if (nt == 1) {
+        scan_range(durs, 0, tasks, parts[0]);
+    } else {
+        std::vector<std::thread> th;
+        for (unsigned i = 0; i < nt; ++i)
+            th.emplace_back(scan_range, durs, tasks * i / nt, tasks * (i + 1) / nt, std::ref(parts[i]));
+        for (auto& t : th) t.join();
+    }
+    bool f = sigma >= 0x1p-60;
+    for (const ScanPart& p : parts) {
+        if (p.bad != ~0ull) {
+            if (p.why == 1)
+                return fail(OSIM_EINVAL, "task %llu: durations must be finite and non-negative",
+                            (unsigned long long)p.bad);
+            return fail(OSIM_EINVAL, "task %llu has no commands", (unsigned long long)p.bad);
+        }
+        f = f && p.fast;
+    }
+    if (fast) *fast = f ? 1 : 0;
+    return 0;
+}
+
+int check_durs(const double* durs, uint64_t tasks) { return scan_durs(durs, tasks, 1.0, nullptr); }
+
+// each row of id ranks must be a permutation of range(n) (unique ids)
+int check_id_ranks(const uint8_t* id_rank, uint64_t B, int n) {
+    unsigned nt = B >= (1ull << 16) ? std::thread::hardware_concurrency() : 1u;
+    if (nt < 1) nt = 1;
+    if (nt > 32) nt = 32;
+    std::vector<uint64_t> bad(nt, ~0ull);
+    auto work = [&](unsigned i) {
+        for (uint64_t b = B * i / nt; b < B * (i + 1) / nt; ++b) {
+            unsigned seen = 0;
+            for (int j = 0; j < n; ++j) {
+                const unsigned v = id_rank[b * n + j];
+                if (v >= (unsigned)n || ((seen >> v) & 1u)) { bad[i] = b; return; }
+                seen |= 1u << v;
+            }
+        }
+    };
+    if (nt == 1) work(0);
+    else {
+        std::vector<std::thread> th;
+        for (unsigned i = 0; i < nt; ++i) th.emplace_back(work, i);
+        for (auto& t : th) t.join();
+    }
+    for (uint64_t b : bad)
+        if (b != ~0ull)
+            return fail(OSIM_EINVAL, "group %llu: id ranks must be a permutation (duplicate task id?)",
+                        (unsigned long long)b);
     return 0;
 }
 
@@ -629,11 +701,11 @@ int osim_exhaustive_batch(const double* durs, uint64_t B, int n, int dma, double
     int rc = check_common(n, dma, sigma);
     if (rc) return rc;
     if (n > 12) return fail(OSIM_EINVAL, "batched exhaustive search supports n <= 12");
-    if ((rc = check_durs(durs, B * (uint64_t)n))) return rc;
+    int fast = 0;
+    if ((rc = scan_durs(durs, B * (uint64_t)n, sigma, &fast))) return rc;
     if (!out && B) return fail(OSIM_EINVAL, "out is NULL");
     DevList dl;
     if ((rc = pick_devs(n_dev, dl))) return rc;
-    const int fast = fast_ok(durs, B * (uint64_t)n, sigma);
     const int G = (int)dl.v.size();
     std::vector<std::unique_lock<std::mutex>> locks;
     for (int gi = 0; gi < G; ++gi) {
@@ -679,21 +751,12 @@ int osim_heuristic_batch(const double* durs, const uint8_t* id_rank, uint64_t B,
                          uint32_t* n_sims) {
     int rc = check_common(n, dma, sigma);
     if (rc) return rc;
-    if ((rc = check_durs(durs, B * (uint64_t)n))) return rc;
+    int fast = 0;
+    if ((rc = scan_durs(durs, B * (uint64_t)n, sigma, &fast))) return rc;
     if (B && (!id_rank || !order || !makespan)) return fail(OSIM_EINVAL, "NULL buffer");
-    for (uint64_t b = 0; b < B; ++b) {  // id ranks must be a permutation (unique ids)
-        unsigned seen = 0;
-        for (int j = 0; j < n; ++j) {
-            const unsigned v = id_rank[b * n + j];
-            if (v >= (unsigned)n || ((seen >> v) & 1u))
-                return fail(OSIM_EINVAL, "group %llu: id ranks must be a permutation (duplicate task id?)",
-                            (unsigned long long)b);
-            seen |= 1u << v;
-        }
-    }
+    if ((rc = check_id_ranks(id_rank, B, n))) return rc;
     DevList dl;
     if ((rc = pick_devs(n_dev, dl))) return rc;
-    const int fast = fast_ok(durs, B * (uint64_t)n, sigma);
     const int G = (int)dl.v.size();
     std::vector<std::unique_lock<std::mutex>> locks;
     for (int gi = 0; gi < G; ++gi) {
@@ -782,6 +845,215 @@ int osim_timeline(const double* durs, int n, int dma, double sigma, const uint8_
     if ((rc = finish(c, c->stream))) return rc;
     if (makespan) *makespan = res[0];
     if (idle) { idle[0] = res[1]; idle[1] = res[2]; idle[2] = res[3]; }
+    return 0;
+}
+
+// ---- row f1: NoReorder interleavings (workload.py:259-327) ---------------
+
+static uint64_t multinomial_total(int T, int N) {  // (T*N)! / (N!)^T, exact
+    uint64_t r = 1;
+    int tot = 0;
+    for (int w = 0; w < T; ++w)
+        for (int k = 1; k <= N; ++k) {
+            ++tot;
+            r = r / (uint64_t)k * (uint64_t)tot + r % (uint64_t)k * (uint64_t)tot / (uint64_t)k;
+        }
+    return r;
+}
+
+int osim_interleavings(const double* durs, int T, int N, int dma, double sigma, uint64_t rank_lo,
+                       uint64_t rank_hi, double threshold, int n_dev, osim_summary* out, uint64_t* below,
+                       double* makespans) {
+    if (T < 1 || N < 1 || T * N > kMaxN) return fail(OSIM_EINVAL, "T*N must be in [1, %d]", kMaxN);
+    int rc = check_common(T * N, dma, sigma);
+    if (rc) return rc;
+    if ((rc = check_durs(durs, (uint64_t)(T * N)))) return rc;
+    if (!out) return fail(OSIM_EINVAL, "out is NULL");
+    const uint64_t total = multinomial_total(T, N);
+    if (rank_lo > rank_hi || rank_hi > total) return fail(OSIM_EINVAL, "rank range outside [0, %llu)",
+                                                          (unsigned long long)total);
+    DevList dl;
+    if ((rc = pick_devs(n_dev, dl))) return rc;
+    const int G = (int)dl.v.size();
+    const uint64_t span = rank_hi - rank_lo;
+    std::vector<osim_summary> res(G);
+    std::vector<unsigned long long> bel(G, 0);
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        locks.emplace_back(c->mu);
+        CK(cudaSetDevice(c->dev));
+        const uint64_t lo = rank_lo + span * (uint64_t)gi / (uint64_t)G;
+        const uint64_t hi = rank_lo + span * (uint64_t)(gi + 1) / (uint64_t)G;
+        const int mp = max_parts_for(c);
+        size_t off_parts = align_up(3 * kMaxN * sizeof(double));
+        size_t off_sum = off_parts + align_up(mp * sizeof(Part));
+        size_t off_bel = off_sum + align_up(sizeof(osim_summary));
+        size_t off_ms = off_bel + 256;
+        size_t bytes = off_ms + (makespans ? align_up((hi - lo) * sizeof(double)) : 0);
+        void* base;
+        if ((rc = scratch(c, bytes, &base))) return rc;
+        char* b = (char*)base;
+        CK(cudaMemcpyAsync(b, durs, 3 * T * N * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        double* d_ms = makespans ? (double*)(b + off_ms) : nullptr;
+        int g = 0;
+        if (hi > lo) {
+            const uint64_t blocks = (hi - lo + kBlock - 1) / kBlock;
+            if (dma == 2) {
+                g = grid_for(k_interleave<2>, kBlock, 0, c, blocks);
+                if (g > mp) g = mp;
+                k_interleave<2><<<g, kBlock, 0, c->stream>>>((double*)b, T, N, sigma, lo, hi, total, threshold,
+                                                             (Part*)(b + off_parts), d_ms, c->d_err);
+            } else {
+                g = grid_for(k_interleave<1>, kBlock, 0, c, blocks);
+                if (g > mp) g = mp;
+                k_interleave<1><<<g, kBlock, 0, c->stream>>>((double*)b, T, N, sigma, lo, hi, total, threshold,
+                                                             (Part*)(b + off_parts), d_ms, c->d_err);
+            }
+        }
+        k_final_reduce<<<1, kBlock, 0, c->stream>>>((Part*)(b + off_parts), g, (osim_summary*)(b + off_sum),
+                                                    (unsigned long long*)(b + off_bel));
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&res[gi], b + off_sum, sizeof(osim_summary), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(&bel[gi], b + off_bel, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+        if (makespans && hi > lo)
+            CK(cudaMemcpyAsync(makespans + (lo - rank_lo), d_ms, (hi - lo) * sizeof(double),
+                               cudaMemcpyDeviceToHost, c->stream));
+    }
+    osim_summary acc;
+    memset(&acc, 0, sizeof(acc));
+    uint64_t nb = 0;
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        CK(cudaSetDevice(c->dev));
+        if ((rc = finish(c, c->stream))) return rc;
+        merge_host(acc, res[gi]);
+        nb += bel[gi];
+    }
+    *out = acc;
+    if (below) *below = nb;
+    return 0;
+}
+
+int osim_eval_sequences(const double* durs, int T, int N, int dma, double sigma, const uint8_t* labels,
+                        uint64_t cnt, int n_dev, double* makespans, osim_summary* out) {
+    if (T < 1 || N < 1 || T * N > kMaxN) return fail(OSIM_EINVAL, "T*N must be in [1, %d]", kMaxN);
+    int rc = check_common(T * N, dma, sigma);
+    if (rc) return rc;
+    if ((rc = check_durs(durs, (uint64_t)(T * N)))) return rc;
+    if (cnt && (!labels || !makespans)) return fail(OSIM_EINVAL, "NULL buffer");
+    const int n = T * N;
+    for (uint64_t i = 0; i < cnt; ++i) {  // each row: every worker exactly N times
+        int c[kMaxN] = {0};
+        for (int p = 0; p < n; ++p) {
+            const int w = labels[i * n + p];
+            if (w >= T || ++c[w] > N)
+                return fail(OSIM_EINVAL, "row %llu is not an interleaving of %d workers x %d tasks",
+                            (unsigned long long)i, T, N);
+        }
+    }
+    DevList dl;
+    if ((rc = pick_devs(n_dev, dl))) return rc;
+    const int G = (int)dl.v.size();
+    std::vector<osim_summary> res(G);
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        locks.emplace_back(c->mu);
+        CK(cudaSetDevice(c->dev));
+        const uint64_t lo = cnt * (uint64_t)gi / (uint64_t)G, hi = cnt * (uint64_t)(gi + 1) / (uint64_t)G;
+        const uint64_t m = hi - lo;
+        const int mp = max_parts_for(c);
+        size_t off_parts = align_up(3 * kMaxN * sizeof(double));
+        size_t off_sum = off_parts + align_up(mp * sizeof(Part));
+        size_t off_ms = off_sum + align_up(sizeof(osim_summary));
+        size_t off_l = off_ms + align_up(m * sizeof(double) + 8);
+        size_t bytes = off_l + align_up(m * n + 8);
+        void* base;
+        if ((rc = scratch(c, bytes, &base))) return rc;
+        char* b = (char*)base;
+        CK(cudaMemcpyAsync(b, durs, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        int g = 0;
+        if (m) {
+            CK(cudaMemcpyAsync(b + off_l, labels + lo * n, m * n, cudaMemcpyHostToDevice, c->stream));
+            const uint64_t blocks = (m + kBlock - 1) / kBlock;
+            if (dma == 2) {
+                g = grid_for(k_eval_labels<2>, kBlock, 0, c, blocks);
+                if (g > mp) g = mp;
+                k_eval_labels<2><<<g, kBlock, 0, c->stream>>>((double*)b, T, N, sigma, (uint8_t*)(b + off_l), m,
+                                                              (Part*)(b + off_parts), (double*)(b + off_ms), c->d_err);
+            } else {
+                g = grid_for(k_eval_labels<1>, kBlock, 0, c, blocks);
+                if (g > mp) g = mp;
+                k_eval_labels<1><<<g, kBlock, 0, c->stream>>>((double*)b, T, N, sigma, (uint8_t*)(b + off_l), m,
+                                                              (Part*)(b + off_parts), (double*)(b + off_ms), c->d_err);
+            }
+        }
+        k_final_reduce<<<1, kBlock, 0, c->stream>>>((Part*)(b + off_parts), g, (osim_summary*)(b + off_sum), nullptr);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&res[gi], b + off_sum, sizeof(osim_summary), cudaMemcpyDeviceToHost, c->stream));
+        if (m) CK(cudaMemcpyAsync(makespans + lo, b + off_ms, m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    }
+    osim_summary acc;
+    memset(&acc, 0, sizeof(acc));
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        CK(cudaSetDevice(c->dev));
+        if ((rc = finish(c, c->stream))) return rc;
+        res[gi].best_rank += cnt * (uint64_t)gi / (uint64_t)G;
+        merge_host(acc, res[gi]);
+    }
+    if (out) *out = acc;
+    return 0;
+}
+
+int osim_timeline_deps(const double* durs, int n, int dma, double sigma, const uint8_t* order, const int8_t* dep,
+                       int waves, double* start, double* end, double* makespan, double* idle) {
+    int rc = check_common(n, dma, sigma);
+    if (rc) return rc;
+    if ((rc = check_durs(durs, (uint64_t)n))) return rc;
+    if (!order || !start || !end) return fail(OSIM_EINVAL, "NULL buffer");
+    unsigned seen = 0;
+    for (int j = 0; j < n; ++j) {
+        if (order[j] >= n || ((seen >> order[j]) & 1u)) return fail(OSIM_EINVAL, "order is not a permutation");
+        seen |= 1u << order[j];
+    }
+    if (dep)
+        for (int t = 0; t < n; ++t)
+            if (dep[t] >= n || dep[t] == t) return fail(OSIM_EINVAL, "bad dependency of task %d", t);
+    DevList dl;
+    if ((rc = pick_devs(1, dl))) return rc;
+    DevCtx* c = dl.v[0];
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->dev));
+    size_t off_o = align_up(3 * kMaxN * sizeof(double));
+    size_t off_dp = off_o + 256;
+    size_t off_s = off_dp + 256;
+    size_t off_e = off_s + align_up(3 * kMaxN * sizeof(double));
+    size_t off_r = off_e + align_up(3 * kMaxN * sizeof(double));
+    void* base;
+    if ((rc = scratch(c, off_r + 256, &base))) return rc;
+    char* b = (char*)base;
+    CK(cudaMemcpyAsync(b, durs, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(b + off_o, order, n, cudaMemcpyHostToDevice, c->stream));
+    if (dep) CK(cudaMemcpyAsync(b + off_dp, dep, n, cudaMemcpyHostToDevice, c->stream));
+    const int8_t* d_dep = dep ? (const int8_t*)(b + off_dp) : nullptr;
+    if (dma == 2)
+        k_timeline_dep<2><<<1, 64, 0, c->stream>>>((double*)b, n, sigma, (uint8_t*)(b + off_o), d_dep, waves,
+                                                   (double*)(b + off_s), (double*)(b + off_e), (double*)(b + off_r),
+                                                   c->d_err);
+    else
+        k_timeline_dep<1><<<1, 64, 0, c->stream>>>((double*)b, n, sigma, (uint8_t*)(b + off_o), d_dep, waves,
+                                                   (double*)(b + off_s), (double*)(b + off_e), (double*)(b + off_r),
+                                                   c->d_err);
+    CK(cudaGetLastError());
+    double res4[4];
+    CK(cudaMemcpyAsync(start, b + off_s, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(end, b + off_e, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(res4, b + off_r, sizeof(res4), cudaMemcpyDeviceToHost, c->stream));
+    if ((rc = finish(c, c->stream))) return rc;
+    if (makespan) *makespan = res4[0];
+    if (idle) { idle[0] = res4[1]; idle[1] = res4[2]; idle[2] = res4[3]; }
     return 0;
 }
 

@@ -1,0 +1,303 @@
+// osim_deps.cuh -- simulator with dependency gates and 1-DMA waves, for the
+// NoReorder interleaving distribution (SURVEY.md 8(f) row f1:
+// workload.py:259-327) and engine.simulate(..., deps=...).
+//
+// Queues are explicit per thread (task ids packed 4 bits each), built the
+// way DeviceSim.submit builds them (engine.py:115-156), one submit per wave:
+// simulate_sequence (workload.py:277-304) splits a 1-DMA sequence into a new
+// wave whenever a task's prerequisite sits in the current wave, and each
+// submit appends the wave's HtDs and then its DtHs to the shared XFER
+// queue.  Readiness adds the deps gate (engine.py:168-171): a command waits
+// until its task's prerequisite task has finalized all of its commands.
+// Arithmetic is the reference's op sequence with IEEE division (general
+// path), so results are bit-identical to the oracle.
+#pragma once
+
+#include "osim_kernels.cuh"
+
+namespace osim {
+
+struct Queue32 {  // up to 32 entries: 4-bit task id + 1 kind bit (XFER: 1 = DtH)
+    uint64_t t[2];
+    uint32_t kind;
+    int len;
+    __device__ __forceinline__ void clear() { t[0] = t[1] = 0; kind = 0; len = 0; }
+    __device__ __forceinline__ void push(int task, int isD) {
+        t[len >> 4] |= (uint64_t)task << (4 * (len & 15));
+        kind |= (uint32_t)isD << len;
+        ++len;
+    }
+    __device__ __forceinline__ int task(int i) const { return (int)((t[i >> 4] >> (4 * (i & 15))) & 0xF); }
+    __device__ __forceinline__ int isD(int i) const { return (kind >> i) & 1; }
+};
+
+// dep: nibble-packed (prerequisite task + 1) per task id, 0 = none
+template <int DMA>
+struct DepSim {
+    Durs D;
+    double sigma;
+    Queue32 q[3];  // 2-DMA: 0 HtD, 1 DtH, 2 K;  1-DMA: 0 XFER, 2 K
+    int h[3];
+    bool run[3];
+    int ck[3];     // task of the running command per lane
+    int kk[3];     // kind of the running command (0 HtD, 1 K, 2 DtH)
+    double rem[3], nd[3];
+    double now;
+    uint64_t dep;
+    unsigned doneH, doneK, doneD;
+    int ncmd;
+
+    __device__ __forceinline__ bool nonnull(int k, int t) const { return D.nd(k, t) > 0.0; }
+    __device__ __forceinline__ int depof(int t) const { return (int)((dep >> (4 * t)) & 0xF) - 1; }
+
+    // order: packed task ids, len positions; waves: split as simulate_sequence
+    __device__ void init(const Durs& d, double sg, uint64_t order, int len, uint64_t dp, bool waves,
+                         int ntask) {
+        D = d;
+        sigma = sg;
+        dep = dp;
+        now = 0.0;
+        for (int l = 0; l < 3; ++l) { q[l].clear(); h[l] = 0; run[l] = false; rem[l] = 1.0; nd[l] = 1.0; }
+        doneH = doneK = doneD = 0;
+        for (int t = 0; t < ntask; ++t) {  // null stages are done from the start (engine.py:133-135)
+            if (!nonnull(0, t)) doneH |= 1u << t;
+            if (!nonnull(1, t)) doneK |= 1u << t;
+            if (!nonnull(2, t)) doneD |= 1u << t;
+        }
+        ncmd = 0;
+        int w0 = 0;          // first position of the current wave
+        unsigned inw = 0;    // tasks of the current wave
+        for (int p = 0; p <= len; ++p) {
+            const int t = p < len ? nib(order, p) : 0;
+            const bool flush = p == len || (DMA == 1 && waves && depof(t) >= 0 && ((inw >> depof(t)) & 1u));
+            if (flush) {  // DeviceSim.submit of positions [w0, p)
+                for (int i = w0; i < p; ++i) {
+                    const int u = nib(order, i);
+                    if (nonnull(0, u)) { q[0].push(u, 0); ++ncmd; }
+                    if (nonnull(1, u)) { q[2].push(u, 0); ++ncmd; }
+                    if (nonnull(2, u) && DMA == 2) { q[1].push(u, 0); ++ncmd; }
+                }
+                if (DMA == 1)
+                    for (int i = w0; i < p; ++i) {
+                        const int u = nib(order, i);
+                        if (nonnull(2, u)) { q[0].push(u, 1); ++ncmd; }
+                    }
+                w0 = p;
+                inw = 0;
+            }
+            if (p < len) inw |= 1u << t;
+        }
+    }
+
+    __device__ __forceinline__ bool finished(int t) const {
+        return (((doneH & doneK & doneD) >> t) & 1u) != 0;
+    }
+    __device__ __forceinline__ bool ready(int kind, int t) const {
+        const int pd = depof(t);
+        if (pd >= 0 && !finished(pd)) return false;  // engine.py:169-171
+        if (kind == 1) return (doneH >> t) & 1u;
+        if (kind == 2) return ((doneK & doneH) >> t) & 1u;
+        return true;
+    }
+
+    __device__ __forceinline__ bool drained() const {
+        return h[0] >= q[0].len && h[1] >= q[1].len && h[2] >= q[2].len;
+    }
+
+    // returns false when nothing runs and nothing can start (a stall)
+    __device__ bool step(TimelineOut* tl) {
+        for (int l = 0; l < 3; ++l) {  // engine.py:188-194
+            if (run[l] || h[l] >= q[l].len) continue;
+            const int t = q[l].task(h[l]);
+            const int kind = (l == 2) ? 1 : ((l == 1) ? 2 : (q[l].isD(h[l]) ? 2 : 0));
+            if (!ready(kind, t)) continue;
+            run[l] = true;
+            ck[l] = t;
+            kk[l] = kind;
+            nd[l] = D.nd(kind, t);
+            rem[l] = nd[l];
+            if (tl) tl->start[3 * t + kind] = now;
+        }
+        if (!run[0] && !run[1] && !run[2]) return false;
+        const bool ov = DMA == 2 && run[0] && run[1];
+        double dt = 0.0;
+        bool first = true;
+        double rate[3];
+        for (int l = 0; l < 3; ++l) {  // engine.py:207-210 (lane order HtD, DtH, K)
+            const int ll = (l == 1) ? 1 : l;
+            rate[ll] = (ov && ll != 2) ? sigma : 1.0;
+        }
+        const int order3[3] = {0, 1, 2};
+        for (int i = 0; i < 3; ++i) {
+            const int l = order3[i];
+            if (!run[l]) continue;
+            const double v = __ddiv_rn(rem[l], rate[l]);
+            if (first || v < dt) dt = v;
+            first = false;
+        }
+        now = __dadd_rn(now, dt);
+        for (int l = 0; l < 3; ++l) {
+            if (!run[l]) continue;
+            const double left = __dsub_rn(rem[l], __dmul_rn(dt, rate[l]));
+            rem[l] = __dmul_rn(__ddiv_rn(pymax0(left), nd[l]), nd[l]);
+        }
+        for (int l = 0; l < 3; ++l) {  // engine.py:216-231
+            if (!run[l] || rem[l] > kEndEps) continue;
+            run[l] = false;
+            ++h[l];
+            const int t = ck[l];
+            if (kk[l] == 0) doneH |= 1u << t;
+            else if (kk[l] == 1) doneK |= 1u << t;
+            else doneD |= 1u << t;
+            if (tl) tl->end[3 * t + kk[l]] = now;
+        }
+        return true;
+    }
+
+    __device__ bool run_all(TimelineOut* tl = nullptr) {
+        for (int s = 0; s < ncmd + 1 && !drained(); ++s)
+            if (!step(tl)) return false;
+        return drained();
+    }
+};
+
+// sorted(set(permutations(labels))) rank -> packed task order (task (w, j) =
+// w*N + j): multinomial unranking, M(c - e_w) = M(c) * c_w / |c| exactly.
+__device__ __forceinline__ uint64_t unrank_labels(uint64_t r, int T, int N, uint64_t mtotal) {
+    int c[16];
+    for (int w = 0; w < T; ++w) c[w] = N;
+    int rem = T * N;
+    uint64_t M = mtotal;
+    uint64_t order = 0;
+    int cnt[16];
+    for (int w = 0; w < T; ++w) cnt[w] = 0;
+    for (int p = 0; p < T * N; ++p) {
+        for (int w = 0; w < T; ++w) {
+            if (!c[w]) continue;
+            const uint64_t m = M / (uint64_t)rem * (uint64_t)c[w] + (M % (uint64_t)rem) * (uint64_t)c[w] / (uint64_t)rem;
+            if (r < m) {
+                order |= (uint64_t)(w * N + cnt[w]) << (4 * p);
+                ++cnt[w];
+                --c[w];
+                --rem;
+                M = m;
+                break;
+            }
+            r -= m;
+        }
+    }
+    return order;
+}
+
+__device__ __forceinline__ uint64_t chain_deps(int T, int N) {
+    uint64_t dep = 0;
+    for (int w = 0; w < T; ++w)
+        for (int j = 1; j < N; ++j) dep |= (uint64_t)(w * N + j) << (4 * (w * N + j));  // (t-1)+1 = t
+    return dep;
+}
+
+template <int DMA>
+__global__ void __launch_bounds__(kBlock) k_interleave(const double* __restrict__ durs, int T, int N, double sigma,
+                                                       uint64_t lo, uint64_t hi, uint64_t mtotal, double thr,
+                                                       Part* __restrict__ parts, double* __restrict__ ms_out,
+                                                       int* __restrict__ err) {
+    __shared__ double sd[3 * kStride], sr[3 * kStride];
+    __shared__ Part sh[32];
+    const int n = T * N;
+    stage_durs(durs, n, sd, sr);
+    __syncthreads();
+    const Durs Dd{sd, sr, 1};
+    const uint64_t dep = chain_deps(T, N);
+    Part acc;
+    part_init(acc);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = lo + (uint64_t)blockIdx.x * blockDim.x; base < hi; base += stride) {
+        const uint64_t r = base + threadIdx.x;
+        if (r >= hi) continue;
+        DepSim<DMA> s;
+        s.init(Dd, sigma, unrank_labels(r, T, N, mtotal), n, dep, true, n);
+        if (!s.run_all()) atomicExch(err, OSIM_ESTALL);
+        part_add<true>(acc, s.now, r, thr);
+        if (ms_out) ms_out[r - lo] = s.now;
+    }
+    acc = block_reduce(acc, sh);
+    if (threadIdx.x == 0) parts[blockIdx.x] = acc;
+}
+
+template <int DMA>
+__global__ void __launch_bounds__(kBlock) k_eval_labels(const double* __restrict__ durs, int T, int N, double sigma,
+                                                        const uint8_t* __restrict__ labels, uint64_t cnt,
+                                                        Part* __restrict__ parts, double* __restrict__ ms_out,
+                                                        int* __restrict__ err) {
+    __shared__ double sd[3 * kStride], sr[3 * kStride];
+    __shared__ Part sh[32];
+    const int n = T * N;
+    stage_durs(durs, n, sd, sr);
+    __syncthreads();
+    const Durs Dd{sd, sr, 1};
+    const uint64_t dep = chain_deps(T, N);
+    Part acc;
+    part_init(acc);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += stride) {
+        int c[16];
+        for (int w = 0; w < T; ++w) c[w] = 0;
+        uint64_t order = 0;
+        for (int p = 0; p < n; ++p) {
+            const int w = labels[i * n + p];
+            order |= (uint64_t)(w * N + c[w]++) << (4 * p);
+        }
+        DepSim<DMA> s;
+        s.init(Dd, sigma, order, n, dep, true, n);
+        if (!s.run_all()) atomicExch(err, OSIM_ESTALL);
+        part_add<true>(acc, s.now, i, -kBig);
+        ms_out[i] = s.now;
+    }
+    acc = block_reduce(acc, sh);
+    if (threadIdx.x == 0) parts[blockIdx.x] = acc;
+}
+
+// engine.simulate(tasks, profile, deps) / workload.simulate_sequence: one
+// ordering with an explicit dep array and optional 1-DMA waves.
+template <int DMA>
+__global__ void k_timeline_dep(const double* __restrict__ durs, int n, double sigma,
+                               const uint8_t* __restrict__ order, const int8_t* __restrict__ dep, int waves,
+                               double* start, double* end, double* res, int* err) {
+    __shared__ double sd[3 * kStride], sr[3 * kStride];
+    stage_durs(durs, n, sd, sr);
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int i = 0; i < 3 * n; ++i) { start[i] = -1.0; end[i] = -1.0; }
+    uint64_t seq = 0, dp = 0;
+    for (int j = 0; j < n; ++j) seq |= (uint64_t)(order[j] & 0xF) << (4 * j);
+    for (int t = 0; t < n; ++t)
+        if (dep && dep[t] >= 0) dp |= (uint64_t)(dep[t] + 1) << (4 * t);
+    DepSim<DMA> s;
+    s.init(Durs{sd, sr, 1}, sigma, seq, n, dp, waves != 0, n);
+    TimelineOut tl{start, end};
+    if (!s.run_all(&tl)) { *err = OSIM_ESTALL; return; }
+    res[0] = s.now;
+    // idle_report (engine.py:68-80): spans of a kind sorted by (start, end)
+    for (int k = 0; k < 3; ++k) {
+        double idle = 0.0, prev_end = 0.0;
+        int done = 0;
+        for (int it = 0; it < n; ++it) {  // selection in (start, end) order
+            int best = -1;
+            for (int t = 0; t < n; ++t) {
+                const double st = start[3 * t + k];
+                if (st < 0.0 || ((done >> t) & 1)) continue;
+                if (best < 0 || st < start[3 * best + k] ||
+                    (st == start[3 * best + k] && end[3 * t + k] < end[3 * best + k]))
+                    best = t;
+            }
+            if (best < 0) break;
+            const double st = start[3 * best + k];
+            if (it > 0 && st > prev_end) idle = __dadd_rn(idle, __dsub_rn(st, prev_end));
+            prev_end = end[3 * best + k];
+            done |= 1 << best;
+        }
+        res[1 + k] = idle;
+    }
+}
+
+}  // namespace osim

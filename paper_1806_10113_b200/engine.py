@@ -71,13 +71,33 @@ def simulate(tasks: Sequence[TaskSpec], profile: DeviceProfile,
     """Simulate one ordered task group on the GPU and return its timeline."""
     if not tasks:
         raise ValueError("task group must be non-empty")
-    if deps:
-        raise NotImplementedError("dependency-gated simulation (deps=) is not on the B200 path yet")
+    return _simulate(tasks, profile, deps, waves=False)
+
+
+def _simulate(tasks: Sequence[TaskSpec], profile: DeviceProfile, deps: Optional[Dict[str, str]],
+              waves: bool) -> Timeline:
+    """One ordered group on the GPU; deps -> osim_timeline_deps (waves: the
+    1-DMA split of workload.simulate_sequence)."""
     if len(tasks) > MAX_TASKS:
         raise NotImplementedError(f"groups of more than {MAX_TASKS} tasks are not supported on the B200 path")
     durs = resolve_group(tasks, profile)
     n = len(tasks)
-    start, end, makespan, idle = _capi.timeline(durs, profile.dma_engines, profile.overlap_sigma, list(range(n)))
+    if deps:
+        index = {t.id: i for i, t in enumerate(tasks)}
+        dep = [-1] * n
+        for i, t in enumerate(tasks):
+            d = deps.get(t.id)
+            if d is not None:
+                if d not in index:
+                    # never finishes -> the task's commands never become ready
+                    # (engine.py:169-171) -> DeviceSim.run stalls (:239-241)
+                    raise RuntimeError("simulation stalled with commands pending")
+                dep[i] = index[d]
+        start, end, makespan, idle = _capi.timeline_deps(durs, profile.dma_engines, profile.overlap_sigma,
+                                                         list(range(n)), dep, waves)
+    else:
+        start, end, makespan, idle = _capi.timeline(durs, profile.dma_engines, profile.overlap_sigma,
+                                                    list(range(n)))
     cmds: List[Command] = []
     for i, t in enumerate(tasks):
         for k, kind in enumerate(KINDS):

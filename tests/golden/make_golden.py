@@ -359,6 +359,69 @@ def gen_sampled():
     dump("sampled.json", {"dma": 2, "sigma": H(0.5), "cases": cases})
 
 
+# ------------------------------------------------- row f1: NoReorder (deps)
+def gen_noreorder():
+    from offsim import workload
+    from offsim.workload import Scenario
+
+    cases = []
+    for (T, N, bk, seed, pname, cap) in [(2, 2, "BK50", 1, "2dma", 10_000), (2, 2, "BK50", 1, "1dma", 10_000),
+                                         (3, 2, "BK25", 2, "2dma", 10_000), (3, 2, "BK75", 3, "1dma", 10_000),
+                                         (2, 3, "BK0", 4, "1dma", 10_000), (2, 4, "BK100", 5, "2dma", 10_000),
+                                         (4, 2, "BK50", 6, "2dma", 10_000), (4, 2, "BK50", 6, "1dma", 10_000),
+                                         (3, 3, "BK25", 7, "1dma", 2_000), (4, 3, "BK75", 8, "2dma", 1_000)]:
+        p = load_profile_arg(pname)
+        sc = Scenario(workers=T, batch_depth=N, pool=load_bk_benchmark(bk), seed=seed, profile=p)
+        wt = workload._draw_worker_tasks(sc)
+        rep = workload.noreorder_distribution(sc, wt, cap)
+        ms = np.asarray(rep.makespans)
+        idx = {wt[w][j].id: (w, j) for w in range(T) for j in range(N)}
+        labels = [[idx[i][0] for i in o] for o in rep.orderings]
+        cases.append({
+            "T": T, "N": N, "bk": bk, "seed": seed, "profile": pname, "cap": cap,
+            "dma": p.dma_engines, "sigma": H(p.overlap_sigma),
+            "durs": [[[H(float(x)) for x in offsim.stage_times(wt[w][j], p)] for j in range(N)] for w in range(T)],
+            "count": len(ms), "exhaustive": rep.exhaustive,
+            "labels_head": labels[:200],
+            "labels_sha256": hashlib.sha256(np.asarray(labels, dtype=np.uint8).tobytes()).hexdigest(),
+            "makespans_head": [H(float(m)) for m in ms[:200]],
+            "makespans_sha256": hashlib.sha256(ms.astype("<f8").tobytes()).hexdigest(),
+            "best": H(rep.best), "argmin": int(np.argmin(ms)), "worst": H(rep.worst),
+            "median": H(rep.median), "geomean": H(rep.geomean),
+        })
+        print("noreorder", T, N, pname, len(ms), rep.exhaustive)
+    # simulate_sequence timelines with deps (1-DMA waves and 2-DMA gates),
+    # random worker interleavings incl. null stages
+    rng = np.random.default_rng(99)
+    seqs = []
+    for c in range(300):
+        T = int(rng.integers(1, 4)); N = int(rng.integers(1, 4))
+        dma = 1 + c % 2
+        sigma = [0.5, 0.375, 1.0][c % 3]
+        p = prof(dma, sigma)
+        d = rand_task_durs(rng, T * N, ["int", "mixed", "real"][c % 3])
+        tasks = [[TaskSpec(id=f"w{w}.{j}", fixed_durations=tuple(d[w * N + j])) for j in range(N)] for w in range(T)]
+        labels = [int(x) for x in rng.permutation([w for w in range(T) for _ in range(N)])]
+        cnt = [0] * T
+        seq = []
+        for w in labels:
+            seq.append(tasks[w][cnt[w]]); cnt[w] += 1
+        deps = {tasks[w][j].id: tasks[w][j - 1].id for w in range(T) for j in range(1, N)}
+        tl = workload.simulate_sequence(seq, p, deps)
+        flat = [t for row in tasks for t in row]
+        ix = {t.id: i for i, t in enumerate(flat)}
+        kinds = {engine.KIND_HTD: 0, engine.KIND_K: 1, engine.KIND_DTH: 2}
+        start = [[None] * 3 for _ in flat]
+        end = [[None] * 3 for _ in flat]
+        for cmd in tl.commands:
+            start[ix[cmd.task_id]][kinds[cmd.kind]] = H(cmd.start)
+            end[ix[cmd.task_id]][kinds[cmd.kind]] = H(cmd.end)
+        seqs.append({"T": T, "N": N, "dma": dma, "sigma": H(sigma), "labels": labels,
+                     "durs": [[H(x) for x in r] for r in d], "makespan": H(tl.makespan),
+                     "idle": [H(tl.idle[k]) for k in engine.KINDS], "start": start, "end": end})
+    dump("noreorder.json", {"cases": cases, "sequences": seqs})
+
+
 # ---------------------------------------------------------------- C3
 def _c3_chunk(args):
     lo, hi = args
@@ -402,7 +465,7 @@ if __name__ == "__main__":
         gen_c3()
         sys.exit(0)
     gens = {"c1": gen_c1, "sim": gen_sim_random, "heur": gen_heuristic_random, "c2": gen_c2,
-            "c4": gen_c4, "c5": gen_c5, "sampled": gen_sampled}
+            "c4": gen_c4, "c5": gen_c5, "sampled": gen_sampled, "noreorder": gen_noreorder}
     for k, g in gens.items():
         if not a.only or k in a.only.split(","):
             g()

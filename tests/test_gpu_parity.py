@@ -334,3 +334,80 @@ def test_distributed_stats_single_rank_nccl():
         assert summ.best_rank == g["argmin"] and summ.count == 3628800
     finally:
         tdist.destroy_process_group()
+
+
+
+# ---- row f1: NoReorder interleavings (deps + 1-DMA waves) -----------------
+
+def test_simulate_sequence_timelines_bit_exact():
+    g = load("noreorder.json")
+    for c in g["sequences"]:
+        T, N = c["T"], c["N"]
+        cnt = [0] * T
+        order = []
+        for w in c["labels"]:
+            order.append(w * N + cnt[w])
+            cnt[w] += 1
+        dep = [(w * N + j - 1 if j else -1) for w in range(T) for j in range(N)]
+        st, en, ms, idle = _capi.timeline_deps(durs(c["durs"]), c["dma"], F(c["sigma"]), order, dep,
+                                               waves=(c["dma"] == 1))
+        assert ms == F(c["makespan"]) and idle.tolist() == fl(c["idle"])
+        for t in range(T * N):
+            for k in range(3):
+                s = c["start"][t][k]
+                if s is None:
+                    assert st[t, k] == -1.0
+                else:
+                    assert st[t, k] == F(s) and en[t, k] == F(c["end"][t][k])
+
+
+def test_noreorder_distributions_bit_exact():
+    import hashlib
+
+    from paper_1806_10113_b200 import noreorder as nr
+
+    g = load("noreorder.json")
+    for c in g["cases"]:
+        d = np.array([[[F(x) for x in r] for r in row] for row in c["durs"]])
+        labels, ms, summ, exhaustive = nr.distribution_durs(d, c["dma"], F(c["sigma"]), c["cap"], c["seed"])
+        assert exhaustive == c["exhaustive"] and len(ms) == c["count"]
+        assert hashlib.sha256(ms.astype("<f8").tobytes()).hexdigest() == c["makespans_sha256"]
+        assert summ["best_rank"] == c["argmin"] and summ["best"] == F(c["best"]) and summ["worst"] == F(c["worst"])
+        assert float(np.median(ms)) == F(c["median"])
+
+
+def test_noreorder_large_space_vs_oracle():
+    # 4 workers x 3 tasks: 369,600 interleavings, 1-DMA waves and 2-DMA
+    rng = np.random.default_rng(5)
+    d = rng.uniform(0.2, 5.0, (4, 3, 3))
+    total = 369600
+    for dma, sigma in ((1, 1.0), (2, 0.375)):
+        s, below, ms = _capi.interleavings(d.reshape(-1, 3), 4, 3, dma, sigma, 0, total, threshold=20.0,
+                                           want_makespans=True)
+        o, oms = O.interleavings(d.reshape(-1, 3), 4, 3, dma, sigma, threads=8, makespans=True)
+        assert np.array_equal(ms, oms)
+        assert_summary_vs_oracle(s, o)
+        assert below == int((oms < 20.0).sum())
+
+
+def test_simulate_with_deps_dropin():
+    p2 = osim.DeviceProfile("2dma", 2, 0.0, 1.0, 0.0, 1.0, overlap_sigma=0.5)
+    p1 = osim.DeviceProfile("1dma", 1, 0.0, 1.0, 0.0, 1.0)
+    tasks = [osim.TaskSpec(f"t{i}", fixed_durations=(1.0 + i, 2.0, 0.5 * i + 0.25)) for i in range(5)]
+    deps = {"t3": "t1", "t4": "t0"}
+    dep = [-1, -1, -1, 1, 0]
+    for p in (p2, p1):
+        if p.dma_engines == 2:
+            tl = osim.simulate(tasks, p, deps=deps)
+            r = O.simulate([t.fixed_durations for t in tasks], list(range(5)), 2, p.overlap_sigma, dep=dep)
+            assert tl.makespan == r.makespan
+        else:
+            # one 1-DMA submit: HtD(t3) waits for DtH(t1), queued behind it ->
+            # the reference stalls (engine.py:239-241), and so must we
+            with pytest.raises(RuntimeError):
+                osim.simulate(tasks, p, deps=deps)
+            with pytest.raises(RuntimeError):
+                O.simulate([t.fixed_durations for t in tasks], list(range(5)), 1, 1.0, dep=dep)
+        seq_tl = osim.simulate_sequence(tasks, p, deps)
+        rs = O.simulate_seq([t.fixed_durations for t in tasks], list(range(5)), p.dma_engines, p.overlap_sigma, dep)
+        assert seq_tl.makespan == rs.makespan

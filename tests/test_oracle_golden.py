@@ -167,3 +167,39 @@ def sha_u8(a):
     import hashlib
 
     return hashlib.sha256(np.ascontiguousarray(a, dtype=np.uint8).tobytes()).hexdigest()
+
+
+def test_noreorder_oracle_pinned():
+    import hashlib
+
+    g = load("noreorder.json")
+    for c in g["sequences"]:
+        T, N = c["T"], c["N"]
+        cnt = [0] * T
+        order = []
+        for w in c["labels"]:
+            order.append(w * N + cnt[w])
+            cnt[w] += 1
+        dep = [(w * N + j - 1 if j else -1) for w in range(T) for j in range(N)]
+        r = O.simulate_seq(durs(c["durs"]), order, c["dma"], F(c["sigma"]), dep)
+        assert r.makespan == F(c["makespan"]) and r.idle.tolist() == fl(c["idle"])
+        for t in range(T * N):
+            for k in range(3):
+                s = c["start"][t][k]
+                if s is None:
+                    assert r.start[t, k] == -1.0
+                else:
+                    assert r.start[t, k] == F(s) and r.end[t, k] == F(c["end"][t][k])
+    for c in g["cases"]:
+        T, N = c["T"], c["N"]
+        d = np.array(c["durs"], dtype=object)
+        d = np.array([[[F(x) for x in r] for r in row] for row in c["durs"]]).reshape(-1, 3)
+        if c["exhaustive"]:
+            s, ms = O.interleavings(d, T, N, c["dma"], F(c["sigma"]), threads=8, makespans=True)
+        else:
+            from paper_1806_10113_b200.noreorder import sample_interleavings
+
+            s, ms = O.eval_sequences(d, T, N, c["dma"], F(c["sigma"]), sample_interleavings(T, N, c["cap"], c["seed"]))
+        assert hashlib.sha256(ms.astype("<f8").tobytes()).hexdigest() == c["makespans_sha256"]
+        assert s["best_rank"] == c["argmin"] and s["best"] == F(c["best"]) and s["worst"] == F(c["worst"])
+        assert float(np.median(ms)) == F(c["median"])
