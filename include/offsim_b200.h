@@ -135,6 +135,15 @@ int osim_timeline_deps(const double* durs, int n, int dma, double sigma, const u
                        const int8_t* dep, int waves, double* start, double* end, double* makespan,
                        double* idle);
 
+/* ---- micro-step validation oracle ------------- */
+/* oracle.micro_simulate's fixed-dt tick loop (_micro.py:19-143,
+ * oracle.py:60-95) for the orderings of ranks [lo, hi): makespans[hi-lo]. */
+int osim_micro(const double* durs, int n, int dma, double sigma, double dt, uint64_t rank_lo,
+               uint64_t rank_hi, int n_dev, double* makespans);
+/* One ordering with its quantized timeline (start/end[n][3] by task, -1 = none). */
+int osim_micro_timeline(const double* durs, int n, int dma, double sigma, double dt,
+                        const uint8_t* order, double* start, double* end, double* makespan);
+
 /* ---- device-resident variants (inputs already in HBM) ---------------- */
 /* fast = 1 asserts every stage is non-null and every duration and sigma
  * lies in [2^-60, 2^60] (osim_fast_eligible()); 0 selects the general path. */

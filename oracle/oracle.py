@@ -66,6 +66,7 @@ def lib():
         L.oracle_pysum.restype = C.c_double
         L.oracle_unrank.argtypes = [C.c_uint64, C.c_int, ip]
         L.oracle_stats_get.argtypes = [C.POINTER(C.c_int64)]
+        L.oracle_micro.argtypes = [dp, C.c_int, C.c_int, C.c_double, C.c_double, ip, dp, dp, dp]
         L.oracle_simulate_seq.argtypes = [dp, C.c_int, C.c_int, C.c_double, ip, C.c_int, ip, dp, dp, dp, dp]
         L.oracle_unrank_labels.argtypes = [C.c_uint64, C.c_int, C.c_int, ip]
         L.oracle_interleavings.argtypes = [dp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_uint64,
@@ -248,3 +249,17 @@ def eval_sequences(durs, T, N, dma, sigma, labels, threads=1):
     if rc:
         raise RuntimeError(f"oracle_eval_sequences rc={rc}")
     return out.as_dict(), ms
+
+
+def micro(durs, order, dma, sigma, dt):
+    """_micro_core: (makespan, start[n][3], end[n][3]) by task index."""
+    d = _durs(durs)
+    n = d.shape[0]
+    o = np.ascontiguousarray(np.asarray(order, dtype=np.int32))
+    st, en = np.empty((n, 3)), np.empty((n, 3))
+    ms = C.c_double()
+    rc = lib().oracle_micro(_p(d, C.c_double), n, int(dma), float(sigma), float(dt), _p(o, C.c_int),
+                            _p(st, C.c_double), _p(en, C.c_double), C.byref(ms))
+    if rc:
+        raise RuntimeError(f"oracle_micro rc={rc}")
+    return ms.value, st, en

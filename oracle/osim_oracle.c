@@ -845,3 +845,64 @@ int oracle_eval_sequences(const double* durs, int T, int N, int dma, double sigm
                           uint64_t cnt, int threads, double* makespans, oracle_summary* out) {
     return run_il(durs, T, N, dma, sigma, 0, cnt, labels, threads, makespans, out);
 }
+
+/* ---- _micro.py restatement (row f4): fixed-dt tick loop ------------- */
+
+/* _micro_core (_micro.py:19-143) over the tasks in `order`; start/end by
+ * task index (-1 = no command). */
+int oracle_micro(const double* durs, int n, int dma, double sigma, double dt, const int* order, double* start,
+                 double* end, double* makespan) {
+    if (n < 1 || n > OR_MAXN || !(dt > 0)) return -1;
+    const double TOL = 1e-9; /* _micro.py:16 */
+    int qh[OR_MAXN], qd[OR_MAXN], qk[OR_MAXN], nh = 0, nd = 0, nk = 0;
+    double th[OR_MAXN], tk[OR_MAXN], td[OR_MAXN];
+    for (int i = 0; i < n; ++i) { /* the sequence as micro_simulate sees it */
+        const double* d = durs + 3 * order[i];
+        th[i] = d[0]; tk[i] = d[1]; td[i] = d[2];
+    }
+    for (int i = 0; i < n; ++i) if (th[i] > 0.0) qh[nh++] = i;
+    for (int i = 0; i < n; ++i) if (td[i] > 0.0) qd[nd++] = i;
+    for (int i = 0; i < n; ++i) if (tk[i] > 0.0) qk[nk++] = i;
+    double rem[3][OR_MAXN];
+    int done[3][OR_MAXN];
+    double st[3][OR_MAXN], en[3][OR_MAXN];
+    for (int i = 0; i < n; ++i) {
+        rem[0][i] = th[i]; rem[1][i] = tk[i]; rem[2][i] = td[i];
+        done[0][i] = th[i] <= 0.0; done[1][i] = tk[i] <= 0.0; done[2][i] = td[i] <= 0.0;
+        for (int k = 0; k < 3; ++k) st[k][i] = en[k][i] = -1.0;
+    }
+    int hh = 0, hd = 0, hk = 0;
+    double t = 0.0, ms = 0.0;
+    int64_t step = 0;
+    for (;;) {
+        int eh = -1, ed = -1, ek = -1;
+        if (dma == 2) {
+            if (hh < nh) eh = qh[hh];
+            if (hd < nd) { int i = qd[hd]; if (done[1][i] && done[0][i]) ed = i; }
+        } else {
+            if (hh < nh) eh = qh[hh];
+            else if (hd < nd) { int i = qd[hd]; if (done[1][i] && done[0][i]) ed = i; }
+        }
+        if (hk < nk) { int i = qk[hk]; if (done[0][i]) ek = i; }
+        if (eh < 0 && ed < 0 && ek < 0) break;
+        double rate = (dma == 2 && eh >= 0 && ed >= 0) ? sigma : 1.0;
+        step += 1;
+        double tick_end = (double)step * dt;
+        if (eh >= 0) { if (st[0][eh] < 0.0) st[0][eh] = t; rem[0][eh] -= dt * rate; }
+        if (ed >= 0) { if (st[2][ed] < 0.0) st[2][ed] = t; rem[2][ed] -= dt * rate; }
+        if (ek >= 0) { if (st[1][ek] < 0.0) st[1][ek] = t; rem[1][ek] -= dt; }
+        t = tick_end;
+        if (eh >= 0 && rem[0][eh] <= TOL) { en[0][eh] = t; done[0][eh] = 1; hh++; ms = t; }
+        if (ed >= 0 && rem[2][ed] <= TOL) { en[2][ed] = t; done[2][ed] = 1; hd++; ms = t; }
+        if (ek >= 0 && rem[1][ek] <= TOL) { en[1][ek] = t; done[1][ek] = 1; hk++; ms = t; }
+    }
+    if (makespan) *makespan = ms;
+    for (int i = 0; i < n; ++i) {
+        const int task = order[i];
+        for (int k = 0; k < 3; ++k) {
+            if (start) start[3 * task + k] = st[k][i];
+            if (end) end[3 * task + k] = en[k][i];
+        }
+    }
+    return 0;
+}

@@ -92,6 +92,11 @@ int oracle_interleavings(const double* durs, int T, int N, int dma, double sigma
 int oracle_eval_sequences(const double* durs, int T, int N, int dma, double sigma, const uint8_t* labels,
                           uint64_t cnt, int threads, double* makespans, oracle_summary* out);
 
+/* oracle.micro_simulate's core (_micro.py:19-143): fixed-dt tick loop over
+ * the tasks in `order`; start/end by task index. */
+int oracle_micro(const double* durs, int n, int dma, double sigma, double dt, const int* order, double* start,
+                 double* end, double* makespan);
+
 /* CPython builtin sum() of doubles (bltinmodule.c, 3.12 Neumaier / <=3.11
  * naive), exposed for the tests. */
 double oracle_pysum(const double* x, int n, int sum_mode);

@@ -41,6 +41,7 @@ from .model import (
     fit_kernel_model,
     stage_times,
 )
+from .micro import micro_simulate, validate
 from .noreorder import noreorder_distribution, simulate_sequence
 from .search import (
     DEFAULT_CAP,
@@ -66,7 +67,7 @@ __all__ = [
     "Timeline", "UnresolvableDuration", "classify_task", "DEFAULT_CAP", "estimate_kernel",
     "estimate_transfer", "exhaustive_search", "exhaustive_summary", "exhaustive_summary_batch",
     "exhaustive_summary_durs", "exhaustive_stats", "exhaustive_stats_durs", "fit_kernel_model",
-    "heuristic_percentile", "idle_report", "noreorder_distribution", "simulate_sequence", "make_report", "recompute_overlap",
+    "heuristic_percentile", "idle_report", "micro_simulate", "validate", "noreorder_distribution", "simulate_sequence", "make_report", "recompute_overlap",
     "reorder_batch", "reorder_batch_many", "reorder_durs", "sample_permutations", "select_first_task",
     "select_last_tasks", "select_next_task", "simulate", "stage_times",
 ]

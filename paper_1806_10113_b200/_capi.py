@@ -27,7 +27,7 @@ EXPORTS = (
     "osim_timeline", "osim_fast_eligible", "osim_exhaustive_dev", "osim_exhaustive_batch_dev",
     "osim_heuristic_batch_dev", "osim_selftest_div", "osim_fp64_peak", "osim_exhaustive_stats",
     "osim_exhaustive_ex_dev", "osim_radix_hist_dev", "osim_interleavings", "osim_eval_sequences",
-    "osim_timeline_deps",
+    "osim_timeline_deps", "osim_micro", "osim_micro_timeline",
 )
 
 
@@ -100,6 +100,8 @@ def load(path: str = LIB_PATH):
             "osim_radix_hist_dev": ([vp, u64, u64, i, i, vp, vp], i),
             "osim_interleavings": ([dp, i, i, i, d, u64, u64, d, i, sp, C.POINTER(u64), dp], i),
             "osim_eval_sequences": ([dp, i, i, i, d, u8p, u64, i, dp, sp], i),
+            "osim_micro": ([dp, i, i, d, d, u64, u64, i, dp], i),
+            "osim_micro_timeline": ([dp, i, i, d, d, u8p, dp, dp, dp], i),
             "osim_timeline_deps": ([dp, i, i, d, u8p, C.POINTER(C.c_int8), i, dp, dp, dp, dp], i),
             "osim_fp64_peak": ([dp], i),
         }
@@ -270,3 +272,22 @@ def timeline_deps(durs, dma, sigma, order, dep=None, waves=False):
                                     ptr(dp_, C.c_int8) if dp_ is not None else None, int(bool(waves)),
                                     ptr(st, C.c_double), ptr(en, C.c_double), C.byref(ms), ptr(idle, C.c_double)))
     return st, en, ms.value, idle
+
+
+def micro(durs, dma, sigma, dt, lo, hi, n_dev=1):
+    d = f64(durs, (-1, 3))
+    ms = np.empty(hi - lo)
+    check(load().osim_micro(ptr(d, C.c_double), d.shape[0], int(dma), float(sigma), float(dt), int(lo), int(hi),
+                            int(n_dev), ptr(ms, C.c_double)))
+    return ms
+
+
+def micro_timeline(durs, dma, sigma, dt, order):
+    d = f64(durs, (-1, 3))
+    n = d.shape[0]
+    o = u8(order)
+    st, en = np.empty((n, 3)), np.empty((n, 3))
+    ms = C.c_double()
+    check(load().osim_micro_timeline(ptr(d, C.c_double), n, int(dma), float(sigma), float(dt), ptr(o, C.c_uint8),
+                                     ptr(st, C.c_double), ptr(en, C.c_double), C.byref(ms)))
+    return st, en, ms.value

@@ -16,6 +16,7 @@
 
 #include "osim_deps.cuh"
 #include "osim_launch.cuh"
+#include "osim_micro.cuh"
 
 using namespace osim;
 
@@ -1054,6 +1055,108 @@ int osim_timeline_deps(const double* durs, int n, int dma, double sigma, const u
     if ((rc = finish(c, c->stream))) return rc;
     if (makespan) *makespan = res4[0];
     if (idle) { idle[0] = res4[1]; idle[1] = res4[2]; idle[2] = res4[3]; }
+    return 0;
+}
+
+// ---- row f4: micro-step tick oracle (_micro.py, oracle.py:60-95) ----------
+
+static long long micro_max_ticks(const double* durs, int n, double sigma, double dt) {
+    double work = 0.0;  // every command runs at rate >= sigma: ticks <= total / (dt * sigma) + commands
+    for (int i = 0; i < 3 * n; ++i) work += durs[i] > 0.0 ? durs[i] : 0.0;
+    const double ticks = work / (dt * sigma) + 3.0 * n + 16.0;
+    return ticks > 9.0e18 ? (long long)9.0e18 : (long long)ticks;
+}
+
+int osim_micro(const double* durs, int n, int dma, double sigma, double dt, uint64_t rank_lo, uint64_t rank_hi,
+               int n_dev, double* makespans) {
+    int rc = check_common(n, dma, sigma);
+    if (rc) return rc;
+    if (!(dt > 0.0)) return fail(OSIM_EINVAL, "dt must be positive");
+    if ((rc = check_durs(durs, (uint64_t)n))) return rc;
+    if (!makespans && rank_hi > rank_lo) return fail(OSIM_EINVAL, "makespans is NULL");
+    if (rank_lo > rank_hi || rank_hi > factorial(n)) return fail(OSIM_EINVAL, "bad rank range");
+    const long long mt = micro_max_ticks(durs, n, sigma, dt);
+    if ((double)mt * (double)(rank_hi - rank_lo) > 5e13)
+        return fail(OSIM_EINVAL, "dt too small for this sweep (%lld ticks per ordering)", mt);
+    DevList dl;
+    if ((rc = pick_devs(n_dev, dl))) return rc;
+    const int G = (int)dl.v.size();
+    const uint64_t span = rank_hi - rank_lo;
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        locks.emplace_back(c->mu);
+        CK(cudaSetDevice(c->dev));
+        const uint64_t lo = rank_lo + span * (uint64_t)gi / (uint64_t)G;
+        const uint64_t hi = rank_lo + span * (uint64_t)(gi + 1) / (uint64_t)G;
+        if (hi <= lo) continue;
+        size_t off_ms = align_up(3 * kMaxN * sizeof(double));
+        void* base;
+        if ((rc = scratch(c, off_ms + align_up((hi - lo) * sizeof(double)), &base))) return rc;
+        char* b = (char*)base;
+        CK(cudaMemcpyAsync(b, durs, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        const unsigned blocks = (unsigned)((hi - lo + kBlock - 1) / kBlock);
+        if (dma == 2)
+            k_micro<2><<<blocks, kBlock, 0, c->stream>>>((double*)b, n, sigma, dt, lo, hi, mt, (double*)(b + off_ms),
+                                                         c->d_err);
+        else
+            k_micro<1><<<blocks, kBlock, 0, c->stream>>>((double*)b, n, sigma, dt, lo, hi, mt, (double*)(b + off_ms),
+                                                         c->d_err);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(makespans + (lo - rank_lo), b + off_ms, (hi - lo) * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+    }
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        CK(cudaSetDevice(c->dev));
+        if ((rc = finish(c, c->stream))) return rc;
+    }
+    return 0;
+}
+
+int osim_micro_timeline(const double* durs, int n, int dma, double sigma, double dt, const uint8_t* order,
+                        double* start, double* end, double* makespan) {
+    int rc = check_common(n, dma, sigma);
+    if (rc) return rc;
+    if (!(dt > 0.0)) return fail(OSIM_EINVAL, "dt must be positive");
+    if ((rc = check_durs(durs, (uint64_t)n))) return rc;
+    if (!order || !start || !end) return fail(OSIM_EINVAL, "NULL buffer");
+    unsigned seen = 0;
+    for (int j = 0; j < n; ++j) {
+        if (order[j] >= n || ((seen >> order[j]) & 1u)) return fail(OSIM_EINVAL, "order is not a permutation");
+        seen |= 1u << order[j];
+    }
+    const long long mt = micro_max_ticks(durs, n, sigma, dt);
+    if (mt > 4000000000ll) return fail(OSIM_EINVAL, "dt too small (%lld ticks)", mt);
+    DevList dl;
+    if ((rc = pick_devs(1, dl))) return rc;
+    DevCtx* c = dl.v[0];
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->dev));
+    size_t off_o = align_up(3 * kMaxN * sizeof(double));
+    size_t off_s = off_o + 256;
+    size_t off_e = off_s + align_up(3 * kMaxN * sizeof(double));
+    size_t off_r = off_e + align_up(3 * kMaxN * sizeof(double));
+    void* base;
+    if ((rc = scratch(c, off_r + 256, &base))) return rc;
+    char* b = (char*)base;
+    CK(cudaMemcpyAsync(b, durs, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(b + off_o, order, n, cudaMemcpyHostToDevice, c->stream));
+    if (dma == 2)
+        k_micro_timeline<2><<<1, 64, 0, c->stream>>>((double*)b, n, sigma, dt, (uint8_t*)(b + off_o), mt,
+                                                     (double*)(b + off_s), (double*)(b + off_e), (double*)(b + off_r),
+                                                     c->d_err);
+    else
+        k_micro_timeline<1><<<1, 64, 0, c->stream>>>((double*)b, n, sigma, dt, (uint8_t*)(b + off_o), mt,
+                                                     (double*)(b + off_s), (double*)(b + off_e), (double*)(b + off_r),
+                                                     c->d_err);
+    CK(cudaGetLastError());
+    double r0;
+    CK(cudaMemcpyAsync(start, b + off_s, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(end, b + off_e, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&r0, b + off_r, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if ((rc = finish(c, c->stream))) return rc;
+    if (makespan) *makespan = r0;
     return 0;
 }
 

@@ -422,6 +422,45 @@ def gen_noreorder():
     dump("noreorder.json", {"cases": cases, "sequences": seqs})
 
 
+# ------------------------------------------- row f4: micro-step tick oracle
+def gen_micro():
+    from offsim.oracle import micro_simulate
+
+    cases = []
+    for name in BK_NAMES:
+        tasks = list(load_bk_benchmark(name).tasks)
+        for pname in ("1dma", "2dma"):
+            p = load_profile_arg(pname)
+            ms = []
+            for perm in permutations(range(4)):
+                tl = micro_simulate([tasks[i] for i in perm], p, dt=0.001)
+                ms.append(H(tl.makespan))
+            cases.append({"bk": name, "profile": pname, "dma": p.dma_engines, "sigma": H(p.overlap_sigma),
+                          "dt": H(0.001), "durs": durs_of(tasks, p), "makespans": ms})
+    rng = np.random.default_rng(4242)
+    rand = []
+    for c in range(120):
+        n = int(rng.integers(1, 6))
+        dma = 1 + c % 2
+        sigma = [0.5, 0.375, 1.0][c % 3]
+        dt = [0.01, 0.005, 0.001, 0.0025][c % 4]
+        d = rand_task_durs(rng, n, ["int", "mixed", "real"][c % 3])
+        tasks = [TaskSpec(id=f"t{i}", fixed_durations=tuple(d[i])) for i in range(n)]
+        order = [int(x) for x in rng.permutation(n)]
+        tl = micro_simulate([tasks[i] for i in order], prof(dma, sigma), dt=dt)
+        kinds = {engine.KIND_HTD: 0, engine.KIND_K: 1, engine.KIND_DTH: 2}
+        start = [[None] * 3 for _ in range(n)]
+        end = [[None] * 3 for _ in range(n)]
+        for cmd in tl.commands:
+            i = int(cmd.task_id[1:])
+            start[i][kinds[cmd.kind]] = H(cmd.start)
+            end[i][kinds[cmd.kind]] = H(cmd.end)
+        rand.append({"n": n, "dma": dma, "sigma": H(sigma), "dt": H(dt), "durs": [[H(x) for x in r] for r in d],
+                     "order": order, "makespan": H(tl.makespan), "start": start, "end": end,
+                     "idle": [H(tl.idle[k]) for k in engine.KINDS]})
+    dump("micro.json", {"cases": cases, "random": rand})
+
+
 # ---------------------------------------------------------------- C3
 def _c3_chunk(args):
     lo, hi = args
@@ -465,7 +504,8 @@ if __name__ == "__main__":
         gen_c3()
         sys.exit(0)
     gens = {"c1": gen_c1, "sim": gen_sim_random, "heur": gen_heuristic_random, "c2": gen_c2,
-            "c4": gen_c4, "c5": gen_c5, "sampled": gen_sampled, "noreorder": gen_noreorder}
+            "c4": gen_c4, "c5": gen_c5, "sampled": gen_sampled, "noreorder": gen_noreorder,
+            "micro": gen_micro}
     for k, g in gens.items():
         if not a.only or k in a.only.split(","):
             g()

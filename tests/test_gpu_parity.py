@@ -411,3 +411,41 @@ def test_simulate_with_deps_dropin():
         seq_tl = osim.simulate_sequence(tasks, p, deps)
         rs = O.simulate_seq([t.fixed_durations for t in tasks], list(range(5)), p.dma_engines, p.overlap_sigma, dep)
         assert seq_tl.makespan == rs.makespan
+
+
+# ---- row f4: micro-step tick oracle -----------------------------------------
+
+def test_micro_bit_exact_vs_reference():
+    g = load("micro.json")
+    for c in g["cases"]:
+        ms = _capi.micro(durs(c["durs"]), c["dma"], F(c["sigma"]), F(c["dt"]), 0, 24)
+        assert ms.tolist() == fl(c["makespans"])
+    for c in g["random"]:
+        st, en, ms = _capi.micro_timeline(durs(c["durs"]), c["dma"], F(c["sigma"]), F(c["dt"]), c["order"])
+        assert ms == F(c["makespan"])
+        for t in range(c["n"]):
+            for k in range(3):
+                s = c["start"][t][k]
+                if s is None:
+                    assert st[t, k] == -1.0
+                else:
+                    assert st[t, k] == F(s) and en[t, k] == F(c["end"][t][k])
+
+
+def test_micro_simulate_dropin_and_validate_sweep():
+    c = load("micro.json")["random"][7]
+    tasks = [osim.TaskSpec(f"t{i}", fixed_durations=tuple(r)) for i, r in enumerate(durs(c["durs"]).tolist())]
+    ordered = [tasks[i] for i in c["order"]]
+    p = osim.DeviceProfile("p", c["dma"], 0.0, 1.0, 0.0, 1.0, overlap_sigma=F(c["sigma"]))
+    tl = osim.micro_simulate(ordered, p, dt=F(c["dt"]))
+    assert tl.makespan == F(c["makespan"])
+    assert [tl.idle[k] for k in osim.KINDS] == fl(c["idle"])
+    checked, dev, ok = osim.validate(dt=0.001)
+    assert checked == 240 and ok and dev <= 0.002
+
+
+def test_micro_c2_group_vs_oracle():
+    d = synth.c2_batch(1)[0]
+    ms = _capi.micro(d, 2, 0.5, 0.001, 0, 40320)
+    for r in range(0, 40320, 997):
+        assert ms[r] == O.micro(d, O.unrank(r, 8), 2, 0.5, 0.001)[0]

@@ -203,3 +203,23 @@ def test_noreorder_oracle_pinned():
         assert hashlib.sha256(ms.astype("<f8").tobytes()).hexdigest() == c["makespans_sha256"]
         assert s["best_rank"] == c["argmin"] and s["best"] == F(c["best"]) and s["worst"] == F(c["worst"])
         assert float(np.median(ms)) == F(c["median"])
+
+
+def test_micro_oracle_pinned():
+    from itertools import permutations
+
+    g = load("micro.json")
+    for c in g["cases"]:
+        d = durs(c["durs"])
+        ms = [O.micro(d, list(p), c["dma"], F(c["sigma"]), F(c["dt"]))[0] for p in permutations(range(4))]
+        assert ms == fl(c["makespans"])
+    for c in g["random"]:
+        ms, st, en = O.micro(durs(c["durs"]), c["order"], c["dma"], F(c["sigma"]), F(c["dt"]))
+        assert ms == F(c["makespan"])
+        for t in range(c["n"]):
+            for k in range(3):
+                s = c["start"][t][k]
+                if s is None:
+                    assert st[t, k] == -1.0
+                else:
+                    assert st[t, k] == F(s) and en[t, k] == F(c["end"][t][k])
