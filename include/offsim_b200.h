@@ -135,6 +135,16 @@ int osim_timeline_deps(const double* durs, int n, int dma, double sigma, const u
                        const int8_t* dep, int waves, double* start, double* end, double* makespan,
                        double* idle);
 
+/* ---- proxy-thread scenario harness ----------- */
+/* workload._run_heuristic_schedule (workload.py:197-256) for S independent
+ * scenarios of T workers x N tasks: durs[S][T*N][3] (task (w, j) at w*N+j),
+ * id_rank[S][T*N] = sorted() order of each scenario's task ids.  Outputs
+ * makespan[S], n_groups[S], tg_sizes[S][T*N] (nullable; first n_groups
+ * entries), start/end[S][T*N][3] (nullable; -1 = null stage). */
+int osim_harness_batch(const double* durs, const uint8_t* id_rank, uint64_t S, int T, int N, int dma,
+                       double sigma, int sum_mode, int n_dev, double* makespan, uint8_t* n_groups,
+                       uint8_t* tg_sizes, double* start, double* end);
+
 /* ---- micro-step validation oracle ------------- */
 /* oracle.micro_simulate's fixed-dt tick loop (_micro.py:19-143,
  * oracle.py:60-95) for the orderings of ranks [lo, hi): makespans[hi-lo]. */

@@ -906,3 +906,89 @@ int oracle_micro(const double* durs, int n, int dma, double sigma, double dt, co
     }
     return 0;
 }
+
+/* ---- workload.py restatement: proxy-thread harness (row f3) --------- */
+
+/* _run_heuristic_schedule (workload.py:197-256) for one scenario: T workers
+ * x N tasks, durs [T][N][3] (task (w, j) = index w*N + j), id_rank [T*N] =
+ * position of each task id in sorted() order of all ids.  Returns the
+ * timeline makespan, the number of groups and their sizes. */
+int oracle_harness(const double* durs, const uint8_t* id_rank, int T, int N, int dma, double sigma, int sum_mode,
+                   double* makespan, int* n_groups, int* tg_sizes) {
+    const int n = T * N;
+    if (T < 1 || N < 1 || n > OR_MAXN || T > 16) return -1;
+    or_sim s;
+    sim_init(&s, dma, sigma, NULL, n);
+    int next_idx[16], avail[16], n_avail = 0, ng = 0;
+    for (int w = 0; w < T; ++w) { next_idx[w] = 0; avail[n_avail++] = w; }
+    int polling = 1, watched = -1;
+    /* submit_group (workload.py:219-233) */
+#define SUBMIT_GROUP()                                                                      \
+    do {                                                                                    \
+        int ws[16], m = 0;                                                                  \
+        for (int w = 0; w < T; ++w)                                                         \
+            for (int a = 0; a < n_avail; ++a)                                               \
+                if (avail[a] == w) ws[m++] = w;                                             \
+        int tg[16];                                                                         \
+        double td[16 * 3];                                                                  \
+        uint8_t tr[16], sub[16], order8[16];                                                \
+        for (int i = 0; i < m; ++i) {                                                       \
+            tg[i] = ws[i] * N + next_idx[ws[i]];                                            \
+            next_idx[ws[i]]++;                                                              \
+            for (int k = 0; k < 3; ++k) td[3 * i + k] = durs[3 * tg[i] + k];                \
+        }                                                                                   \
+        for (int i = 0; i < m; ++i) { /* ranks of the ids within the group */               \
+            int r = 0;                                                                      \
+            for (int j = 0; j < m; ++j) r += id_rank[tg[j]] < id_rank[tg[i]];               \
+            tr[i] = (uint8_t)r;                                                             \
+        }                                                                                   \
+        n_avail = 0;                                                                        \
+        if (oracle_reorder(td, tr, m, dma, sigma, sum_mode, order8, NULL, NULL)) return -1; \
+        int ord[16];                                                                        \
+        for (int i = 0; i < m; ++i) ord[i] = tg[order8[i]];                                 \
+        (void)sub;                                                                          \
+        int before = s.n_cmd;                                                               \
+        if (sim_submit(&s, durs, ord, m)) return -1;                                        \
+        if (tg_sizes) tg_sizes[ng] = m;                                                     \
+        ng++;                                                                               \
+        watched = -1;                                                                       \
+        for (int c = before; c < s.n_cmd; ++c)                                              \
+            if (s.cmd[c].kind == K_HTD) watched = c; /* htds[-1] */                         \
+        polling = watched < 0;                                                              \
+    } while (0)
+
+    SUBMIT_GROUP();
+    for (;;) {
+        if (polling && n_avail) SUBMIT_GROUP();
+        /* sim.step() with the finalized commands (engine.py:182-232) */
+        int prev_exec[3];
+        for (int l = 0; l < 3; ++l) prev_exec[l] = s.exec[l];
+        (void)prev_exec;
+        int before_done[3 * OR_MAXN];
+        for (int c = 0; c < s.n_cmd; ++c) before_done[c] = s.cmd[c].end >= 0.0;
+        int nf = sim_step(&s);
+        if (nf < 0) {
+            int remaining = 0;
+            for (int w = 0; w < T; ++w) remaining |= next_idx[w] < N;
+            if (remaining || !sim_drained(&s)) return -5; /* "harness stalled" */
+            break;
+        }
+        /* finalized commands in _FINALIZE_ORDER (only sets/flags depend on them) */
+        for (int c = 0; c < s.n_cmd; ++c) {
+            if (before_done[c] || s.cmd[c].end < 0.0) continue;
+            if (c == watched) polling = 1;
+            const int t = s.cmd[c].task;
+            if (s.finished[t]) {
+                const int w = t / N, j = t % N;
+                if (j + 1 < N) avail[n_avail++] = w;
+            }
+        }
+    }
+#undef SUBMIT_GROUP
+    double ms = 0.0;
+    for (int i = 0; i < s.n_cmd; ++i)
+        if (i == 0 || s.cmd[i].end > ms) ms = s.cmd[i].end;
+    if (makespan) *makespan = ms;
+    if (n_groups) *n_groups = ng;
+    return 0;
+}

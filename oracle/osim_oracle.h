@@ -97,6 +97,12 @@ int oracle_eval_sequences(const double* durs, int T, int N, int dma, double sigm
 int oracle_micro(const double* durs, int n, int dma, double sigma, double dt, const int* order, double* start,
                  double* end, double* makespan);
 
+/* workload._run_heuristic_schedule (workload.py:197-256): proxy-thread
+ * harness of one scenario; durs [T][N][3], id_rank [T*N] (sorted() order of
+ * all task ids); tg_sizes nullable [T*N]. */
+int oracle_harness(const double* durs, const uint8_t* id_rank, int T, int N, int dma, double sigma, int sum_mode,
+                   double* makespan, int* n_groups, int* tg_sizes);
+
 /* CPython builtin sum() of doubles (bltinmodule.c, 3.12 Neumaier / <=3.11
  * naive), exposed for the tests. */
 double oracle_pysum(const double* x, int n, int sum_mode);

@@ -43,6 +43,15 @@ from .model import (
 )
 from .micro import micro_simulate, validate
 from .noreorder import noreorder_distribution, simulate_sequence
+from .workload import (
+    Benchmark,
+    Scenario,
+    ScenarioResult,
+    load_bk_benchmark,
+    load_table2_tasks,
+    run_scenario,
+    sample_real_tasks,
+)
 from .search import (
     DEFAULT_CAP,
     OrderingStats,
@@ -62,6 +71,8 @@ from .search import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "Benchmark", "Scenario", "ScenarioResult", "load_bk_benchmark", "load_table2_tasks", "run_scenario",
+    "sample_real_tasks",
     "Command", "DeviceProfile", "Direction", "InsufficientSamples", "KINDS", "NegativeFitWarning",
     "OffsimError", "OrderingStats", "OrderingSummary", "PermutationReport", "SUM_MODE", "TaskDominance", "TaskSpec",
     "Timeline", "UnresolvableDuration", "classify_task", "DEFAULT_CAP", "estimate_kernel",

@@ -27,7 +27,7 @@ EXPORTS = (
     "osim_timeline", "osim_fast_eligible", "osim_exhaustive_dev", "osim_exhaustive_batch_dev",
     "osim_heuristic_batch_dev", "osim_selftest_div", "osim_fp64_peak", "osim_exhaustive_stats",
     "osim_exhaustive_ex_dev", "osim_radix_hist_dev", "osim_interleavings", "osim_eval_sequences",
-    "osim_timeline_deps", "osim_micro", "osim_micro_timeline",
+    "osim_timeline_deps", "osim_micro", "osim_micro_timeline", "osim_harness_batch",
 )
 
 
@@ -101,6 +101,7 @@ def load(path: str = LIB_PATH):
             "osim_interleavings": ([dp, i, i, i, d, u64, u64, d, i, sp, C.POINTER(u64), dp], i),
             "osim_eval_sequences": ([dp, i, i, i, d, u8p, u64, i, dp, sp], i),
             "osim_micro": ([dp, i, i, d, d, u64, u64, i, dp], i),
+            "osim_harness_batch": ([dp, u8p, u64, i, i, i, d, i, i, dp, u8p, u8p, dp, dp], i),
             "osim_micro_timeline": ([dp, i, i, d, d, u8p, dp, dp, dp], i),
             "osim_timeline_deps": ([dp, i, i, d, u8p, C.POINTER(C.c_int8), i, dp, dp, dp, dp], i),
             "osim_fp64_peak": ([dp], i),
@@ -291,3 +292,21 @@ def micro_timeline(durs, dma, sigma, dt, order):
     check(load().osim_micro_timeline(ptr(d, C.c_double), n, int(dma), float(sigma), float(dt), ptr(o, C.c_uint8),
                                      ptr(st, C.c_double), ptr(en, C.c_double), C.byref(ms)))
     return st, en, ms.value
+
+
+def harness_batch(durs, id_rank, T, N, dma, sigma, sum_mode, n_dev=1, timeline=False):
+    """(makespan [S], n_groups [S], tg_sizes [S][T*N], start/end [S][T*N][3] or None)."""
+    d = f64(durs).reshape(-1, T * N, 3)
+    S = d.shape[0]
+    r = u8(id_rank, (S, T * N))
+    ms = np.empty(S)
+    ng = np.empty(S, dtype=np.uint8)
+    sz = np.zeros((S, T * N), dtype=np.uint8)
+    st = np.empty((S, T * N, 3)) if timeline else None
+    en = np.empty((S, T * N, 3)) if timeline else None
+    check(load().osim_harness_batch(ptr(d, C.c_double), ptr(r, C.c_uint8), S, int(T), int(N), int(dma),
+                                    float(sigma), int(sum_mode), int(n_dev), ptr(ms, C.c_double),
+                                    ptr(ng, C.c_uint8), ptr(sz, C.c_uint8),
+                                    ptr(st, C.c_double) if timeline else None,
+                                    ptr(en, C.c_double) if timeline else None))
+    return ms, ng, sz, st, en

@@ -17,6 +17,7 @@
 #include "osim_deps.cuh"
 #include "osim_launch.cuh"
 #include "osim_micro.cuh"
+#include "osim_harness.cuh"
 
 using namespace osim;
 
@@ -1157,6 +1158,73 @@ int osim_micro_timeline(const double* durs, int n, int dma, double sigma, double
     CK(cudaMemcpyAsync(&r0, b + off_r, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     if ((rc = finish(c, c->stream))) return rc;
     if (makespan) *makespan = r0;
+    return 0;
+}
+
+// ---- row f3: proxy-thread scenario harness (workload.py:197-256) ----------
+
+int osim_harness_batch(const double* durs, const uint8_t* id_rank, uint64_t S, int T, int N, int dma, double sigma,
+                       int sum_mode, int n_dev, double* makespan, uint8_t* n_groups, uint8_t* tg_sizes,
+                       double* start, double* end) {
+    if (T < 1 || N < 1 || T * N > kMaxN) return fail(OSIM_EINVAL, "T*N must be in [1, %d]", kMaxN);
+    const int n = T * N;
+    int rc = check_common(n, dma, sigma);
+    if (rc) return rc;
+    if ((rc = check_durs(durs, S * (uint64_t)n))) return rc;
+    if (S && (!id_rank || !makespan || !n_groups)) return fail(OSIM_EINVAL, "NULL buffer");
+    if ((rc = check_id_ranks(id_rank, S, n))) return rc;
+    DevList dl;
+    if ((rc = pick_devs(n_dev, dl))) return rc;
+    const int G = (int)dl.v.size();
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        locks.emplace_back(c->mu);
+        CK(cudaSetDevice(c->dev));
+        const uint64_t lo = S * (uint64_t)gi / (uint64_t)G, hi = S * (uint64_t)(gi + 1) / (uint64_t)G;
+        const uint64_t m = hi - lo;
+        if (!m) continue;
+        const bool tl = start && end;
+        size_t off_r = align_up(m * n * 3 * sizeof(double));
+        size_t off_ms = off_r + align_up(m * n);
+        size_t off_ng = off_ms + align_up(m * sizeof(double));
+        size_t off_sz = off_ng + align_up(m);
+        size_t off_st = off_sz + align_up(m * n);
+        size_t off_en = off_st + (tl ? align_up(m * n * 3 * sizeof(double)) : 0);
+        size_t bytes = off_en + (tl ? align_up(m * n * 3 * sizeof(double)) : 0);
+        void* base;
+        if ((rc = scratch(c, bytes, &base))) return rc;
+        char* b = (char*)base;
+        CK(cudaMemcpyAsync(b, durs + lo * n * 3, m * n * 3 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(b + off_r, id_rank + lo * n, m * n, cudaMemcpyHostToDevice, c->stream));
+        const unsigned blocks = (unsigned)((m + 127) / 128);
+        double* d_st = tl ? (double*)(b + off_st) : nullptr;
+        double* d_en = tl ? (double*)(b + off_en) : nullptr;
+        if (dma == 2)
+            k_harness<2><<<blocks, 128, 0, c->stream>>>((double*)b, (uint8_t*)(b + off_r), m, T, N, sigma, sum_mode,
+                                                        (double*)(b + off_ms), (uint8_t*)(b + off_ng),
+                                                        (uint8_t*)(b + off_sz), d_st, d_en, c->d_err);
+        else
+            k_harness<1><<<blocks, 128, 0, c->stream>>>((double*)b, (uint8_t*)(b + off_r), m, T, N, sigma, sum_mode,
+                                                        (double*)(b + off_ms), (uint8_t*)(b + off_ng),
+                                                        (uint8_t*)(b + off_sz), d_st, d_en, c->d_err);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(makespan + lo, b + off_ms, m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(n_groups + lo, b + off_ng, m, cudaMemcpyDeviceToHost, c->stream));
+        if (tg_sizes) CK(cudaMemcpyAsync(tg_sizes + lo * n, b + off_sz, m * n, cudaMemcpyDeviceToHost, c->stream));
+        if (tl) {
+            CK(cudaMemcpyAsync(start + lo * n * 3, d_st, m * n * 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(end + lo * n * 3, d_en, m * n * 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        }
+    }
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        CK(cudaSetDevice(c->dev));
+        if ((rc = finish(c, c->stream))) {
+            if (rc == OSIM_ESTALL) return fail(OSIM_ESTALL, "harness stalled with tasks remaining");
+            return rc;
+        }
+    }
     return 0;
 }
 

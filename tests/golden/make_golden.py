@@ -461,6 +461,54 @@ def gen_micro():
     dump("micro.json", {"cases": cases, "random": rand})
 
 
+# ------------------------------------------ row f3: proxy-thread harness
+def gen_harness():
+    from offsim import workload
+    from offsim.workload import Scenario
+
+    cases = []
+    rng = np.random.default_rng(2024)
+    for c in range(60):
+        T = int(rng.integers(1, 9))
+        N = int(rng.integers(1, 5))
+        while T * N > 16:
+            N -= 1
+        bk = BK_NAMES[c % 5]
+        pname = ["1dma", "2dma"][c % 2]
+        p = load_profile_arg(pname)
+        seed = int(rng.integers(0, 10_000))
+        sc = Scenario(workers=T, batch_depth=N, pool=load_bk_benchmark(bk), seed=seed, profile=p)
+        wt = workload._draw_worker_tasks(sc)
+        res = workload.run_scenario(sc, evaluate_noreorder=False)
+        flat = [t for row in wt for t in row]
+        order = sorted(range(len(flat)), key=lambda i: flat[i].id)
+        rank = [0] * len(flat)
+        for r, i in enumerate(order):
+            rank[i] = r
+        cases.append({"T": T, "N": N, "bk": bk, "profile": pname, "seed": seed, "dma": p.dma_engines,
+                      "sigma": H(p.overlap_sigma), "ids": [t.id for t in flat], "id_rank": rank,
+                      "durs": [[H(float(x)) for x in offsim.stage_times(t, p)] for t in flat],
+                      "makespan": H(res.heuristic_makespan), "tg_sizes": res.tg_sizes})
+    # real-task pools with ids beyond w9 (string order != numeric order)
+    for c in range(20):
+        T, N = 10 + c % 6, 1
+        pool = workload.make_benchmark("real", sample_real_tasks("K20", 8, seed=c))
+        p = [load_profile_arg("2dma"), prof(2, 0.375), load_profile_arg("1dma")][c % 3]
+        sc = Scenario(workers=T, batch_depth=N, pool=pool, seed=c, profile=p)
+        wt = workload._draw_worker_tasks(sc)
+        res = workload.run_scenario(sc, evaluate_noreorder=False)
+        flat = [t for row in wt for t in row]
+        order = sorted(range(len(flat)), key=lambda i: flat[i].id)
+        rank = [0] * len(flat)
+        for r, i in enumerate(order):
+            rank[i] = r
+        cases.append({"T": T, "N": N, "bk": "real", "profile": str(c % 3), "seed": c, "dma": p.dma_engines,
+                      "sigma": H(p.overlap_sigma), "ids": [t.id for t in flat], "id_rank": rank,
+                      "durs": [[H(float(x)) for x in offsim.stage_times(t, p)] for t in flat],
+                      "makespan": H(res.heuristic_makespan), "tg_sizes": res.tg_sizes})
+    dump("harness.json", {"cases": cases})
+
+
 # ---------------------------------------------------------------- C3
 def _c3_chunk(args):
     lo, hi = args
@@ -505,7 +553,7 @@ if __name__ == "__main__":
         sys.exit(0)
     gens = {"c1": gen_c1, "sim": gen_sim_random, "heur": gen_heuristic_random, "c2": gen_c2,
             "c4": gen_c4, "c5": gen_c5, "sampled": gen_sampled, "noreorder": gen_noreorder,
-            "micro": gen_micro}
+            "micro": gen_micro, "harness": gen_harness}
     for k, g in gens.items():
         if not a.only or k in a.only.split(","):
             g()

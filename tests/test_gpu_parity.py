@@ -449,3 +449,56 @@ def test_micro_c2_group_vs_oracle():
     ms = _capi.micro(d, 2, 0.5, 0.001, 0, 40320)
     for r in range(0, 40320, 997):
         assert ms[r] == O.micro(d, O.unrank(r, 8), 2, 0.5, 0.001)[0]
+
+
+# ---- row f3: proxy-thread scenario harness ----------------------------------
+
+def test_harness_batch_bit_exact():
+    g = load("harness.json")
+    groups = {}
+    for c in g["cases"]:
+        groups.setdefault((c["T"], c["N"], c["dma"], c["sigma"]), []).append(c)
+    for (T, N, dma, sig), cs in groups.items():
+        d = np.stack([durs(c["durs"]) for c in cs])
+        r = np.array([c["id_rank"] for c in cs], dtype=np.uint8)
+        ms, ng, sz, _, _ = _capi.harness_batch(d, r, T, N, dma, F(sig), g["meta"]["sum_mode"])
+        for i, c in enumerate(cs):
+            assert ms[i] == F(c["makespan"]), (T, N, c["bk"], c["seed"])
+            assert sz[i, : ng[i]].tolist() == c["tg_sizes"]
+
+
+def test_run_scenario_dropin():
+    from paper_1806_10113_b200 import workload as wl
+
+    g = load("harness.json")
+    c = g["cases"][4]
+    p = osim.DeviceProfile("p", c["dma"], 0.0, 1.0, 0.0, 1.0, overlap_sigma=F(c["sigma"]))
+    sc = wl.Scenario(c["T"], c["N"], wl.load_bk_benchmark(c["bk"]), c["seed"], p)
+    res = wl.run_scenario(sc, evaluate_noreorder=c["T"] * c["N"] <= 8)
+    assert res.heuristic_makespan == F(c["makespan"]) and res.tg_sizes == c["tg_sizes"]
+    assert res.timeline.makespan == max(cmd.end for cmd in res.timeline.commands)
+    if res.noreorder is not None:
+        assert res.speedup_best >= res.speedup_median >= 1.0
+
+
+def test_harness_many_scenarios_vs_oracle():
+    import ctypes as C
+
+    from paper_1806_10113_b200 import workload as wl
+
+    L = O.lib()
+    L.oracle_harness.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_int,
+                                 C.c_double, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    T, N = 4, 3
+    for pname, (dev, dma, sigma) in synth.PROFILES.items():
+        S = 2000
+        d = np.stack([synth.real_group(dev, T * N, 10_000 + s)[1] for s in range(S)])
+        r = np.tile(np.argsort(np.argsort([f"w{w}.{j}" for w in range(T) for j in range(N)])).astype(np.uint8),
+                    (S, 1))
+        ms, ng, sz, _, _ = _capi.harness_batch(d, r, T, N, dma, sigma, osim.SUM_MODE)
+        for s in range(0, S, 97):
+            om, ong, osz = C.c_double(), C.c_int(), np.zeros(64, dtype=np.int32)
+            rc = L.oracle_harness(np.ascontiguousarray(d[s]).ctypes.data_as(C.POINTER(C.c_double)),
+                                  np.ascontiguousarray(r[s]).ctypes.data_as(C.POINTER(C.c_uint8)), T, N, dma, sigma,
+                                  osim.SUM_MODE, C.byref(om), C.byref(ong), osz.ctypes.data_as(C.POINTER(C.c_int)))
+            assert rc == 0 and ms[s] == om.value and sz[s, : ng[s]].tolist() == osz[: ong.value].tolist()

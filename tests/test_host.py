@@ -165,3 +165,17 @@ def test_noreorder_host_enumeration_matches_reference():
         else:
             lab = nr.sample_interleavings(T, N, c["cap"], c["seed"])
             assert hashlib.sha256(lab.tobytes()).hexdigest() == c["labels_sha256"]
+
+
+def test_worker_task_draws_match_reference():
+    from paper_1806_10113_b200 import workload as wl
+
+    g = load("harness.json")
+    for c in g["cases"]:
+        if c["bk"] == "real":
+            continue
+        p = model.DeviceProfile("p", c["dma"], 0.0, 1.0, 0.0, 1.0, overlap_sigma=F(c["sigma"]))
+        sc = wl.Scenario(c["T"], c["N"], wl.load_bk_benchmark(c["bk"]), c["seed"], p)
+        flat = [t for row in wl.draw_worker_tasks(sc) for t in row]
+        assert [t.id for t in flat] == c["ids"]
+        assert [list(t.fixed_durations) for t in flat] == durs(c["durs"]).tolist()

@@ -223,3 +223,20 @@ def test_micro_oracle_pinned():
                     assert st[t, k] == -1.0
                 else:
                     assert st[t, k] == F(s) and en[t, k] == F(c["end"][t][k])
+
+
+def test_harness_oracle_pinned():
+    import ctypes as C
+
+    L = O.lib()
+    L.oracle_harness.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_int,
+                                 C.c_double, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    g = load("harness.json")
+    for c in g["cases"]:
+        d = np.ascontiguousarray(durs(c["durs"]))
+        r = np.array(c["id_rank"], dtype=np.uint8)
+        ms, ng, sizes = C.c_double(), C.c_int(), np.zeros(64, dtype=np.int32)
+        rc = L.oracle_harness(d.ctypes.data_as(C.POINTER(C.c_double)), r.ctypes.data_as(C.POINTER(C.c_uint8)),
+                              c["T"], c["N"], c["dma"], F(c["sigma"]), sum_mode_of(g), C.byref(ms), C.byref(ng),
+                              sizes.ctypes.data_as(C.POINTER(C.c_int)))
+        assert rc == 0 and ms.value == F(c["makespan"]) and sizes[: ng.value].tolist() == c["tg_sizes"]
