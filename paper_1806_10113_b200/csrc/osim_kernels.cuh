@@ -27,6 +27,7 @@ struct Part {
     unsigned long long rank;
     double worst;
     double sum;
+    double csum;  // Neumaier compensation of sum
     double lpm;
     long long lpe;
     unsigned long long count;
@@ -38,6 +39,7 @@ __device__ __forceinline__ void part_init(Part& a) {
     a.rank = ~0ull;
     a.worst = -__longlong_as_double(0x7ff0000000000000ll);
     a.sum = 0.0;
+    a.csum = 0.0;
     a.lpm = 1.0;
     a.lpe = 0;
     a.count = 0;
@@ -58,6 +60,14 @@ __device__ __forceinline__ void renorm(double& m, long long& e) {
     }
 }
 
+// compensated accumulation: s + c carries the exact running sum to ~1 ulp
+// (10^8 orderings per thread block in the batch kernel at n = 12)
+__device__ __forceinline__ void neumaier(double& s, double& c, double x) {
+    const double t = __dadd_rn(s, x);
+    c = __dadd_rn(c, (fabs(s) >= fabs(x)) ? __dadd_rn(__dsub_rn(s, t), x) : __dadd_rn(__dsub_rn(x, t), s));
+    s = t;
+}
+
 // per-thread add, ranks visited in increasing order -> strict < keeps the
 // first of equal makespans (np.argmin)
 template <bool EXACT>
@@ -65,7 +75,7 @@ __device__ __forceinline__ void part_add(Part& a, double ms, unsigned long long 
     if (ms < a.best) { a.best = ms; a.rank = r; }
     a.below += (ms < thr) ? 1ull : 0ull;
     a.worst = fmax(a.worst, ms);
-    a.sum = __dadd_rn(a.sum, ms);
+    neumaier(a.sum, a.csum, ms);
     a.lpm = __dmul_rn(a.lpm, ms);
     renorm<EXACT>(a.lpm, a.lpe);
     a.count += 1;
@@ -75,7 +85,8 @@ __device__ __forceinline__ void part_add(Part& a, double ms, unsigned long long 
 __device__ __forceinline__ void part_merge(Part& a, const Part& b) {
     if (b.best < a.best || (b.best == a.best && b.rank < a.rank)) { a.best = b.best; a.rank = b.rank; }
     a.worst = fmax(a.worst, b.worst);
-    a.sum = __dadd_rn(a.sum, b.sum);
+    neumaier(a.sum, a.csum, b.sum);
+    a.csum = __dadd_rn(a.csum, b.csum);
     a.lpm = __dmul_rn(a.lpm, b.lpm);
     a.lpe += b.lpe;
     renorm<false>(a.lpm, a.lpe);
@@ -89,6 +100,7 @@ __device__ __forceinline__ Part part_shfl(const Part& a, int m) {
     b.rank = __shfl_xor_sync(kFull, a.rank, m);
     b.worst = __shfl_xor_sync(kFull, a.worst, m);
     b.sum = __shfl_xor_sync(kFull, a.sum, m);
+    b.csum = __shfl_xor_sync(kFull, a.csum, m);
     b.lpm = __shfl_xor_sync(kFull, a.lpm, m);
     b.lpe = __shfl_xor_sync(kFull, a.lpe, m);
     b.count = __shfl_xor_sync(kFull, a.count, m);
@@ -128,7 +140,7 @@ __device__ __forceinline__ osim_summary part_to_summary(const Part& a) {
     s.best = a.best;
     s.best_rank = a.rank;
     s.worst = a.worst;
-    s.sum = a.sum;
+    s.sum = __dadd_rn(a.sum, a.csum);
     s.sum_log = a.count ? log(a.lpm) + (double)a.lpe * 0.6931471805599453094 : 0.0;
     s.count = a.count;
     return s;

@@ -502,3 +502,45 @@ def test_harness_many_scenarios_vs_oracle():
                                   np.ascontiguousarray(r[s]).ctypes.data_as(C.POINTER(C.c_uint8)), T, N, dma, sigma,
                                   osim.SUM_MODE, C.byref(om), C.byref(ong), osz.ctypes.data_as(C.POINTER(C.c_int)))
             assert rc == 0 and ms[s] == om.value and sz[s, : ng[s]].tolist() == osz[: ong.value].tolist()
+
+
+# ---- every instantiation: n = 1..16 windows, both DMA modes, sigma pow2 or not ---
+
+@pytest.mark.parametrize("n", list(range(1, 17)))
+def test_exhaustive_every_n_window_vs_oracle(n):
+    rng = np.random.default_rng(100 + n)
+    d = rng.uniform(0.05, 6.0, (n, 3))
+    total = math.factorial(n)
+    span = min(total, 200_000)
+    lo = (total - span) // 3 + (7 if total > span + 7 else 0)
+    for dma, sigma in ((2, 0.5), (2, 0.375), (1, 1.0)):
+        s, ms = _capi.exhaustive(d, dma, sigma, lo, lo + span, want_makespans=True)
+        o, oms = O.exhaustive(d, dma, sigma, lo, lo + span, threads=8, makespans=True)
+        assert np.array_equal(ms, oms), (n, dma, sigma)
+        assert_summary_vs_oracle(s, o)
+
+
+@pytest.mark.parametrize("n", list(range(1, 13)))
+def test_batch_every_n_vs_oracle(n):
+    rng = np.random.default_rng(200 + n)
+    B = 3 if n >= 10 else 12
+    d = rng.uniform(0.05, 6.0, (B, n, 3))
+    for dma, sigma in ((2, 0.5), (2, 0.375), (1, 1.0)):
+        out = _capi.exhaustive_batch(d, dma, sigma)
+        for b in range(B):
+            if n >= 11 and b > 0:
+                break
+            o, _ = O.exhaustive(d[b], dma, sigma, threads=8)
+            assert_summary_vs_oracle({k: out[b][k].item() for k in out.dtype.names}, o)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 9, 13, 16])
+def test_heuristic_every_size_vs_oracle(n):
+    rng = np.random.default_rng(300 + n)
+    B = 500
+    d = rng.uniform(0.05, 6.0, (B, n, 3))
+    r = np.stack([rng.permutation(n) for _ in range(B)]).astype(np.uint8)
+    for dma, sigma in ((2, 0.5), (2, 0.375), (1, 1.0)):
+        order, ms, sims = _capi.heuristic_batch(d, r, dma, sigma, osim.SUM_MODE)
+        oo, om, osims = O.reorder_batch(d, r, dma, sigma, osim.SUM_MODE, threads=8)
+        assert np.array_equal(order, oo) and np.array_equal(ms, om) and np.array_equal(sims, osims)
