@@ -318,8 +318,28 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
         }
         ck_load(K, threadIdx.x, s);
         s.set_seq(pre | suf);
+        if constexpr (DMA == 2) {
+            // full steps while any lane of the warp still has an HtD to run,
+            // then K+DtH steps, then DtH-only steps (FastSim::step_kd/step_d)
+            int st = 0;
+#pragma unroll 1
+            for (; st < rest; st += 2) {
+                if (__all_sync(kFull, s.s0 >= s.n4)) break;
+                s.step(sigma, rsig);
+                s.step(sigma, rsig);
+            }
+#pragma unroll 1
+            for (; st < rest; st += 2) {
+                if (__all_sync(kFull, s.s2 >= s.n4)) break;
+                s.step_kd();
+                s.step_kd();
+            }
 #pragma unroll 2
-        for (int st = 0; st < rest; ++st) s.step(sigma, rsig);
+            for (; st < rest; ++st) s.step_d();
+        } else {
+#pragma unroll 2
+            for (int st = 0; st < rest; ++st) s.step(sigma, rsig);
+        }
         const uint64_t r = P * LF + (uint64_t)j;
         if (validP && r >= lo && r < hi) {
             part_add<false>(acc, s.now, r, thr);

@@ -414,6 +414,38 @@ struct FastSim {
         return __dmul_rn(divq<true>(__dsub_rn(rem, dd), nd, rc), nd);
     }
 
+    // ---- phase-specialized steps (2-DMA, TRACK off).  Once every HtD has
+    // finalized the HtD lane stays idle (rem = sentinel), so no transfer
+    // overlap exists (rate 1 everywhere, engine.py:200-208) and step() reduces
+    // exactly to step_kd(); once every K has finalized too it reduces to
+    // step_d().  Same operations, same order, on the lanes that can run.
+    __device__ __forceinline__ void step_kd() {
+        static_assert(DMA == 2 && !TRACK, "2-DMA exhaustive path only");
+        const bool st2 = idle(r2) && s2 < n4;
+        const bool st1 = idle(r1) && s1 < s2;
+        start_if(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
+        start_if(st1, base + 512 + task_off<PRE>(seq, s1), d1, c1, r1);
+        const double dt = dmin(r1, r2);
+        now = __dadd_rn(now, dt);
+        r2 = upd(r2, dt, d2, c2);
+        r1 = upd(r1, dt, d1, c1);
+        const bool f1 = r1 <= kEndEps;
+        r1 = retire_or_drain(f1, r1, s1 + 4 >= n4);
+        s1 += f1 ? 4 : 0;
+        if (r2 <= kEndEps) { r2 = retire(r2); s2 += 4; }
+    }
+    __device__ __forceinline__ void step_d() {
+        static_assert(DMA == 2 && !TRACK, "2-DMA exhaustive path only");
+        const bool st1 = idle(r1) && s1 < n4;
+        start_if(st1, base + 512 + task_off<PRE>(seq, s1), d1, c1, r1);
+        const double dt = r1;  // the only lane that can run (rem ~0 once drained)
+        now = __dadd_rn(now, dt);
+        r1 = upd(r1, dt, d1, c1);
+        const bool f1 = r1 <= kEndEps;
+        r1 = retire_or_drain(f1, r1, s1 + 4 >= n4);
+        s1 += f1 ? 4 : 0;
+    }
+
     __device__ __forceinline__ void k_idle_gap(bool st2) {
         if constexpr (TRACK) {
             // idle_report (engine.py:68-80) over K spans in FIFO (= sorted) order
