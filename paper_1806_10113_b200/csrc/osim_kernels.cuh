@@ -14,7 +14,7 @@ namespace osim {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kBlock = 256;
 #ifndef OSIM_PFX_MINB
-#define OSIM_PFX_MINB 5  // min resident CTAs per SM for the prefix kernels (48 registers)
+#define OSIM_PFX_MINB 4  // min resident CTAs per SM for the prefix kernels (64 registers)
 #endif
 
 // ---------------------------------------------------------------------------
