@@ -318,28 +318,9 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
         }
         ck_load(K, threadIdx.x, s);
         s.set_seq(pre | suf);
-        if constexpr (DMA == 2) {
-            // full steps while any lane of the warp still has an HtD to run,
-            // then K+DtH steps, then DtH-only steps (FastSim::step_kd/step_d)
-            int st = 0;
-#pragma unroll 1
-            for (; st < rest; st += 2) {
-                if (__all_sync(kFull, s.s0 >= s.n4)) break;
-                s.step(sigma, rsig);
-                s.step(sigma, rsig);
-            }
-#pragma unroll 1
-            for (; st < rest; st += 2) {
-                if (__all_sync(kFull, s.s2 >= s.n4)) break;
-                s.step_kd();
-                s.step_kd();
-            }
-#pragma unroll 2
-            for (; st < rest; ++st) s.step_d();
-        } else {
-#pragma unroll 2
-            for (int st = 0; st < rest; ++st) s.step(sigma, rsig);
-        }
+        // full steps while any lane of the warp still has an HtD to run, then
+        // K+DtH steps, then DtH-only steps (FastSim::run_phased)
+        s.run_phased(rest, sigma, rsig);
         const uint64_t r = P * LF + (uint64_t)j;
         if (validP && r >= lo && r < hi) {
             part_add<false>(acc, s.now, r, thr);
@@ -868,8 +849,7 @@ __global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict
             s.init(gbase(g), S.ot[g] | ((uint64_t)c << (4 * k)), k + 1);
             s.load(S.ck[g]);
             const int rest = __reduce_max_sync(kFull, 3 * (k + 1) - s.finalized());
-#pragma unroll 1
-            for (int st = 0; st < rest; ++st) s.step(sigma, rsig);
+            s.run_phased(rest, sigma, rsig);
             // _completion_estimate (heuristic.py:34-49): builtin sum of the
             // rest's t_k in rt order (cand[] is rt in input order), min t_dth.
             // Warp-uniform loop over the m candidates, skipping j.
@@ -952,8 +932,7 @@ __global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict
             s.init(gbase(g), S.ot[g] | (x << (4 * kl)) | (y << (4 * (kl + 1))), n);
             s.load(S.ck[g]);
             const int rest = __reduce_max_sync(kFull, 3 * n - s.finalized());
-#pragma unroll 1
-            for (int st = 0; st < rest; ++st) s.step(sigma, rsig);
+            s.run_phased(rest, sigma, rsig);
             if (valid) S.ka[g * kMaxN + w] = s.now;
         }
         __syncwarp();

@@ -414,15 +414,16 @@ struct FastSim {
         return __dmul_rn(divq<true>(__dsub_rn(rem, dd), nd, rc), nd);
     }
 
-    // ---- phase-specialized steps (2-DMA, TRACK off).  Once every HtD has
+    // ---- phase-specialized steps (2-DMA).  Once every HtD has
     // finalized the HtD lane stays idle (rem = sentinel), so no transfer
     // overlap exists (rate 1 everywhere, engine.py:200-208) and step() reduces
     // exactly to step_kd(); once every K has finalized too it reduces to
     // step_d().  Same operations, same order, on the lanes that can run.
     __device__ __forceinline__ void step_kd() {
-        static_assert(DMA == 2 && !TRACK, "2-DMA exhaustive path only");
+        static_assert(DMA == 2, "2-DMA only");
         const bool st2 = idle(r2) && s2 < n4;
         const bool st1 = idle(r1) && s1 < s2;
+        k_idle_gap(st2);
         start_if(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
         start_if(st1, base + 512 + task_off<PRE>(seq, s1), d1, c1, r1);
         const double dt = dmin(r1, r2);
@@ -432,10 +433,14 @@ struct FastSim {
         const bool f1 = r1 <= kEndEps;
         r1 = retire_or_drain(f1, r1, s1 + 4 >= n4);
         s1 += f1 ? 4 : 0;
-        if (r2 <= kEndEps) { r2 = retire(r2); s2 += 4; }
+        if (r2 <= kEndEps) {
+            r2 = retire(r2);
+            s2 += 4;
+            if constexpr (TRACK) kEnd = now;
+        }
     }
     __device__ __forceinline__ void step_d() {
-        static_assert(DMA == 2 && !TRACK, "2-DMA exhaustive path only");
+        static_assert(DMA == 2, "2-DMA only");
         const bool st1 = idle(r1) && s1 < n4;
         start_if(st1, base + 512 + task_off<PRE>(seq, s1), d1, c1, r1);
         const double dt = r1;  // the only lane that can run (rem ~0 once drained)
@@ -444,6 +449,31 @@ struct FastSim {
         const bool f1 = r1 <= kEndEps;
         r1 = retire_or_drain(f1, r1, s1 + 4 >= n4);
         s1 += f1 ? 4 : 0;
+    }
+
+    // `rest` steps in warp lock-step, switching to the specialized steps as
+    // soon as the whole warp has drained its HtD (then K) lanes
+    __device__ __forceinline__ void run_phased(int rest, double sigma, double rsig) {
+        int st = 0;
+        if constexpr (DMA == 2) {
+#pragma unroll 1
+            for (; st < rest; st += 2) {
+                if (__all_sync(0xffffffffu, s0 >= n4)) break;
+                step(sigma, rsig);
+                step(sigma, rsig);
+            }
+#pragma unroll 1
+            for (; st < rest; st += 2) {
+                if (__all_sync(0xffffffffu, s2 >= n4)) break;
+                step_kd();
+                step_kd();
+            }
+#pragma unroll 2
+            for (; st < rest; ++st) step_d();
+        } else {
+#pragma unroll 2
+            for (; st < rest; ++st) step(sigma, rsig);
+        }
     }
 
     __device__ __forceinline__ void k_idle_gap(bool st2) {
