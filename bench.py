@@ -278,6 +278,8 @@ def run_ours(a):
     cpu = None
     if D.rank == 0 and D.world == 1 and not a.no_cpu:
         cpu = cpu_baseline(a.cpu_seconds)
+        if secondary:
+            secondary["cpu_port_c5_nvidia_decisions_per_s"] = cpu_heuristic_rate(4.0)
 
     if D.rank == 0:
         line = {
@@ -448,6 +450,26 @@ def cpu_rate(seconds):
     O.exhaustive(d, DMA, SIGMA, start, start + m, threads=threads)
     el = time.perf_counter() - t0
     return m / el, threads, m, start
+
+
+def cpu_heuristic_rate(seconds):
+    """CPU port of reorder_batch (oracle/, all host threads) on config-5
+    groups (NVIDIA-style profile), sized to ~`seconds`."""
+    from oracle import oracle as O
+    from paper_1806_10113_b200 import synth
+
+    threads = os.cpu_count() or 1
+    d, r = synth.c5_batch_fast("nvidia", 20_000, seed=77)
+    probe = 16 * threads
+    t0 = time.perf_counter()
+    O.reorder_batch(d[:probe], r[:probe], 2, 0.5, 1, threads=threads)
+    rate = probe / (time.perf_counter() - t0)
+    m = int(min(len(d), max(probe, rate * seconds)))
+    t0 = time.perf_counter()
+    O.reorder_batch(d[:m], r[:m], 2, 0.5, 1, threads=threads)
+    el = time.perf_counter() - t0
+    return {"value": m / el, "unit": "TG decisions/s", "cores": threads, "kind": "port",
+            "sample": f"{m} config-5 16-task groups (NVIDIA-style) through oracle/osim_oracle.c reorder"}
 
 
 def cpu_baseline(seconds):
