@@ -258,78 +258,99 @@ __device__ __forceinline__ void stage_dr(const double* __restrict__ g, int n, do
     }
 }
 
-// Per-thread checkpoint slot in shared memory, structure-of-arrays so that
+// Per-thread checkpoint slots in shared memory, structure-of-arrays so that
 // the 32 lanes of a warp touch 32 consecutive 8-byte words (conflict-free);
-// keeping it out of registers lifts occupancy (the register state is halved).
+// keeping them out of registers lifts occupancy.  At a checkpoint the HtD lane
+// has just finalized (rem = sentinel, head known to the caller), so only the
+// DtH and K lanes and the clock are stored: 7 doubles + 2 ints per thread.
+template <int SLOTS>
 struct CkSlots {
-    double v[12][kBlock];  // now, r0..r2, d0..d2, c0..c2, kEnd, idleK
-    int h[3][kBlock];      // s0..s2
+    double v[SLOTS][7][kBlock];  // now, r1, r2, d1, d2, c1, c2
+    int h[SLOTS][2][kBlock];     // s1, s2
 };
 
-template <class FS>
-__device__ __forceinline__ void ck_store(CkSlots& K, int i, const FS& s) {
-    K.v[0][i] = s.now; K.v[1][i] = s.r0; K.v[2][i] = s.r1; K.v[3][i] = s.r2;
-    K.v[4][i] = s.d0; K.v[5][i] = s.d1; K.v[6][i] = s.d2;
-    K.v[7][i] = s.c0; K.v[8][i] = s.c1; K.v[9][i] = s.c2;
-    K.h[0][i] = s.s0; K.h[1][i] = s.s1; K.h[2][i] = s.s2;
+template <int SLOTS, class FS>
+__device__ __forceinline__ void ck_store(CkSlots<SLOTS>& K, int slot, int i, const FS& s) {
+    K.v[slot][0][i] = s.now; K.v[slot][1][i] = s.r1; K.v[slot][2][i] = s.r2;
+    K.v[slot][3][i] = s.d1; K.v[slot][4][i] = s.d2; K.v[slot][5][i] = s.c1; K.v[slot][6][i] = s.c2;
+    K.h[slot][0][i] = s.s1; K.h[slot][1][i] = s.s2;
 }
+// restore; the HtD lane is idle with `hdone` HtDs finalized
+template <int SLOTS, class FS>
+__device__ __forceinline__ void ck_load(const CkSlots<SLOTS>& K, int slot, int i, FS& s, int hdone) {
+    s.now = K.v[slot][0][i]; s.r1 = K.v[slot][1][i]; s.r2 = K.v[slot][2][i];
+    s.d1 = K.v[slot][3][i]; s.d2 = K.v[slot][4][i]; s.c1 = K.v[slot][5][i]; s.c2 = K.v[slot][6][i];
+    s.s1 = K.h[slot][0][i]; s.s2 = K.h[slot][1][i];
+    s.r0 = kBig;
+    s.s0 = 4 * hdone;
+}
+
+// Advance every lane of the warp to the checkpoint "htd_done() == target";
+// returns this lane's step count.
 template <class FS>
-__device__ __forceinline__ void ck_load(const CkSlots& K, int i, FS& s) {
-    s.now = K.v[0][i]; s.r0 = K.v[1][i]; s.r1 = K.v[2][i]; s.r2 = K.v[3][i];
-    s.d0 = K.v[4][i]; s.d1 = K.v[5][i]; s.d2 = K.v[6][i];
-    s.c0 = K.v[7][i]; s.c1 = K.v[8][i]; s.c2 = K.v[9][i];
-    s.s0 = K.h[0][i]; s.s1 = K.h[1][i]; s.s2 = K.h[2][i];
+__device__ __forceinline__ int advance_to(FS& s, int target, double sigma, double rsig) {
+    int n = 0;
+#pragma unroll 1
+    while (__any_sync(kFull, s.htd_done() < target)) {
+        if (s.htd_done() < target) {
+            s.step(sigma, rsig);
+            ++n;
+        }
+    }
+    return n;
 }
 
 // Simulate prefix P of length M and every suffix; accumulate leaves that
 // fall inside [lo, hi).  All threads of the warp must call together.
-template <int N, int DMA, bool SIGP2, int L, bool WRITE_MS>
+// (A second checkpoint level two positions later was measured slower on B200:
+// its middle segment runs in divergent advance loops shared by only two
+// leaves.)
+template <int N, int DMA, bool SIGP2, int L, bool WRITE_MS, int SLOTS>
 __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double rsig, uint64_t P,
                                            bool validP, uint64_t lo, uint64_t hi, double thr, Part& acc,
-                                           double* __restrict__ ms_out, uint64_t ms_base, CkSlots& K) {
+                                           double* __restrict__ ms_out, uint64_t ms_base, CkSlots<SLOTS>& K) {
     constexpr int M = N - L;
     constexpr uint64_t LF = Fact<L>::v;
     const uint64_t seq0 = unrank<N>(P * LF);  // prefix + ascending remainder
     using FS = FastSim<DMA, SIGP2, false, (N <= 15)>;
     FS s;
     s.init(base, seq0, N);
-    int sa = 0;
-    if constexpr (M > 0) {
-#pragma unroll 1
-        while (__any_sync(kFull, s.htd_done() < M)) {
-            if (s.htd_done() < M) {
-                s.step(sigma, rsig);
-                ++sa;
-            }
-        }
-    }
-    const int rest = 3 * N - __reduce_min_sync(kFull, sa);
-    ck_store(K, threadIdx.x, s);
+    const int sa = (M > 0) ? advance_to(s, M, sigma, rsig) : 0;
+    const int ti = threadIdx.x;
     const uint64_t pre = (M > 0) ? (seq0 & ((1ull << (4 * M)) - 1ull)) : 0ull;
     const uint64_t rem = seq0 >> (4 * M);  // L ascending task ids
+    {
+        const int rest = 3 * N - __reduce_min_sync(kFull, sa);
+        ck_store(K, 0, ti, s);
 #pragma unroll 1
-    for (int j = 0; j < (int)LF; ++j) {
-        const uint64_t idx = unrank<L>((uint64_t)j);
-        uint64_t suf = 0;
+        for (int j = 0; j < (int)LF; ++j) {
+            const uint64_t idx = unrank<L>((uint64_t)j);
+            uint64_t suf = 0;
 #pragma unroll
-        for (int i = 0; i < L; ++i) {
-            const uint32_t id = (uint32_t)(idx >> (4 * i)) & 0xFu;
-            suf |= ((rem >> (4 * id)) & 0xFull) << (4 * (M + i));
-        }
-        ck_load(K, threadIdx.x, s);
-        s.set_seq(pre | suf);
-        // full steps while any lane of the warp still has an HtD to run, then
-        // K+DtH steps, then DtH-only steps (FastSim::run_phased)
-        s.run_phased(rest, sigma, rsig);
-        const uint64_t r = P * LF + (uint64_t)j;
-        if (validP && r >= lo && r < hi) {
-            part_add<false>(acc, s.now, r, thr);
-            if constexpr (WRITE_MS) {
-                if (ms_out) ms_out[r - ms_base] = s.now;
+            for (int i = 0; i < L; ++i) {
+                const uint32_t id = (uint32_t)(idx >> (4 * i)) & 0xFu;
+                suf |= ((rem >> (4 * id)) & 0xFull) << (4 * (M + i));
+            }
+            ck_load(K, 0, ti, s, M);
+            s.set_seq(pre | suf);
+            // full steps while any lane of the warp still has an HtD to run, then
+            // K+DtH steps, then DtH-only steps (FastSim::run_phased)
+            s.run_phased(rest, sigma, rsig);
+            const uint64_t r = P * LF + (uint64_t)j;
+            if (validP && r >= lo && r < hi) {
+                part_add<false>(acc, s.now, r, thr);
+                if constexpr (WRITE_MS) {
+                    if (ms_out) ms_out[r - ms_base] = s.now;
+                }
             }
         }
     }
 }
+
+template <int DMA, int L>
+struct PfxSlots {
+    static constexpr int v = 1;
+};
 
 template <int N, int DMA, bool SIGP2, int L>
 __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const double* __restrict__ durs, double sigma,
@@ -337,7 +358,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
                                                            double* __restrict__ ms_out) {
     __shared__ double2 sdr[3 * kStride];
     __shared__ Part sh[32];
-    __shared__ CkSlots K;
+    __shared__ CkSlots<PfxSlots<DMA, L>::v> K;
     stage_dr(durs, N, sdr);
     __syncthreads();
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
@@ -350,7 +371,8 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
     for (uint64_t pb = p_lo + (uint64_t)blockIdx.x * blockDim.x; pb < p_hi; pb += stride) {
         const uint64_t P = pb + threadIdx.x;
         const bool validP = P < p_hi;
-        pfx_leaves<N, DMA, SIGP2, L, true>(base, sigma, rsig, validP ? P : p_lo, validP, lo, hi, thr, acc, ms_out, lo, K);
+        pfx_leaves<N, DMA, SIGP2, L, true, PfxSlots<DMA, L>::v>(base, sigma, rsig, validP ? P : p_lo, validP, lo, hi,
+                                                               thr, acc, ms_out, lo, K);
     }
     acc = block_reduce(acc, sh);
     if (threadIdx.x == 0) parts[blockIdx.x] = acc;
@@ -362,7 +384,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_batch_pfx(
                                                                  double sigma, osim_summary* __restrict__ out) {
     __shared__ double2 sdr[3 * kStride];
     __shared__ Part sh[32];
-    __shared__ CkSlots K;
+    __shared__ CkSlots<PfxSlots<DMA, L>::v> K;
     constexpr uint64_t total = Fact<N>::v;
     constexpr uint64_t NP = total / Fact<L>::v;
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
@@ -375,8 +397,8 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_batch_pfx(
         for (uint64_t pb = 0; pb < NP; pb += blockDim.x) {
             const uint64_t P = pb + threadIdx.x;
             const bool validP = P < NP;
-            pfx_leaves<N, DMA, SIGP2, L, false>(base, sigma, rsig, validP ? P : 0, validP, 0, total, -kBig, acc,
-                                                nullptr, 0, K);
+            pfx_leaves<N, DMA, SIGP2, L, false, PfxSlots<DMA, L>::v>(base, sigma, rsig, validP ? P : 0, validP, 0,
+                                                                     total, -kBig, acc, nullptr, 0, K);
         }
         acc = block_reduce(acc, sh);  // ends with __syncthreads: smem reusable
         if (threadIdx.x == 0) out[b] = part_to_summary(acc);

@@ -511,7 +511,7 @@ def test_exhaustive_every_n_window_vs_oracle(n):
     rng = np.random.default_rng(100 + n)
     d = rng.uniform(0.05, 6.0, (n, 3))
     total = math.factorial(n)
-    span = min(total, 200_000)
+    span = min(total, 60_000)
     lo = (total - span) // 3 + (7 if total > span + 7 else 0)
     for dma, sigma in ((2, 0.5), (2, 0.375), (1, 1.0)):
         s, ms = _capi.exhaustive(d, dma, sigma, lo, lo + span, want_makespans=True)
@@ -537,7 +537,7 @@ def test_batch_every_n_vs_oracle(n):
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 9, 13, 16])
 def test_heuristic_every_size_vs_oracle(n):
     rng = np.random.default_rng(300 + n)
-    B = 500
+    B = 200
     d = rng.uniform(0.05, 6.0, (B, n, 3))
     r = np.stack([rng.permutation(n) for _ in range(B)]).astype(np.uint8)
     for dma, sigma in ((2, 0.5), (2, 0.375), (1, 1.0)):
