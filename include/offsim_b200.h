@@ -155,8 +155,9 @@ int osim_micro_timeline(const double* durs, int n, int dma, double sigma, double
                         const uint8_t* order, double* start, double* end, double* makespan);
 
 /* ---- device-resident variants (inputs already in HBM) ---------------- */
-/* fast = 1 asserts every stage is non-null and every duration and sigma
- * lies in [2^-60, 2^60] (osim_fast_eligible()); 0 selects the general path. */
+/* fast = 1 asserts every stage is non-null, every duration lies in
+ * [2^-60, 2^22) ms and sigma >= 2^-60 (osim_fast_eligible()); 0 selects the
+ * general path. */
 int osim_fast_eligible(const double* durs, uint64_t count /* tasks */, double sigma);
 
 int osim_exhaustive_dev(const double* d_durs, int n, int dma, double sigma, uint64_t rank_lo,

@@ -109,7 +109,7 @@ int check_common(int n, int dma, double sigma) {
 
 // One pass over the durations: the reference's validity rules
 // (model.py:95-100, engine.py:129-130) and fast-path eligibility (every
-// stage non-null and in [2^-60, 2^60]); split over host threads for large
+// stage non-null and in [2^-60, 2^22)); split over host threads for large
 // batches.  Reports the lowest offending task, as a serial scan would.
 struct ScanPart {
     uint64_t bad = ~0ull;
@@ -118,7 +118,7 @@ struct ScanPart {
 };
 
 void scan_range(const double* d, uint64_t t0, uint64_t t1, ScanPart& r) {
-    const double lo = 0x1p-60, hi = 0x1p60;
+    const double lo = 0x1p-60, hi = 0x1p22;  // see kFastHi (osim_sim.cuh)
     bool fast = true;
     for (uint64_t t = t0; t < t1; ++t) {
         const double h = d[3 * t], k = d[3 * t + 1], x = d[3 * t + 2];
@@ -127,7 +127,7 @@ void scan_range(const double* d, uint64_t t0, uint64_t t1, ScanPart& r) {
             r.bad = t; r.why = 1; break;
         }
         if (h <= 0 && k <= 0 && x <= 0) { r.bad = t; r.why = 2; break; }
-        fast = fast && h >= lo && h <= hi && k >= lo && k <= hi && x >= lo && x <= hi;
+        fast = fast && h >= lo && h < hi && k >= lo && k < hi && x >= lo && x < hi;
     }
     r.fast = fast;
 }
@@ -309,10 +309,10 @@ int finish(DevCtx* c, cudaStream_t st) {
 }
 
 bool fast_ok(const double* durs, uint64_t tasks, double sigma) {
-    const double lo = std::ldexp(1.0, -60), hi = std::ldexp(1.0, 60);
+    const double lo = std::ldexp(1.0, -60), hi = std::ldexp(1.0, 22);  // kFastHi
     if (!(sigma >= lo)) return false;
     for (uint64_t i = 0; i < 3 * tasks; ++i)
-        if (!(durs[i] >= lo && durs[i] <= hi)) return false;
+        if (!(durs[i] >= lo && durs[i] < hi)) return false;
     return true;
 }
 

@@ -155,7 +155,7 @@ struct DepSim {
     }
 
     __device__ bool run_all(TimelineOut* tl = nullptr) {
-        for (int s = 0; s < ncmd + 1 && !drained(); ++s)
+        for (int s = 0; s < (ncmd + 1) * kSlowSteps && !drained(); ++s)
             if (!step(tl)) return false;
         return drained();
     }

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(128) k_harness(const double* __restrict__ durs
     if (tl)
         for (int i = 0; i < 3 * n; ++i) { tl->start[i] = -1.0; tl->end[i] = -1.0; }
     submit_group();
-    for (int guard = 0; guard < 4 * n + 4; ++guard) {
+    for (int guard = 0; guard < (3 * n + 1) * kSlowSteps + n + 1; ++guard) {
         if (polling && avail) submit_group();
         int hb[3];
         for (int l = 0; l < 3; ++l) hb[l] = s.h[l];

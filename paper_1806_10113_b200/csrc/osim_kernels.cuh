@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kBlock) k_exhaustive_gen(const double* __restr
         const bool valid = r < hi;
         Sim<DMA, false, false, false> s;
         s.init(D, unrank_rt(valid ? r : lo, n), n, sigma, 1.0, nH, nK, nD);
-        run_warp(s, 3 * n);
+        run_warp(s, 3 * n * kSlowSteps);
         if (!s.drained()) atomicExch(err, OSIM_ESTALL);
         if (valid) {
             part_add<true>(acc, s.now, r, thr);
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(kBlock) k_eval_perms(const double* __restrict_
         for (int j = 0; j < n; ++j) seq |= (uint64_t)(p[j] & 0xF) << (4 * j);
         Sim<DMA, FAST, FAST, false> s;
         s.init(D, seq, n, sigma, rsig, nH, nK, nD);
-        run_warp(s, 3 * n);
+        run_warp(s, 3 * n * kSlowSteps);
         if (!s.drained()) atomicExch(err, OSIM_ESTALL);
         if (valid) {
             part_add<!FAST>(acc, s.now, i, thr);
@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(kBlock) k_exhaustive_batch_gen(const double* _
             const bool valid = r < total;
             Sim<DMA, false, false, false> s;
             s.init(D, unrank_rt(valid ? r : 0, n), n, sigma, 1.0, nH, nK, nD);
-            run_warp(s, 3 * n);
+            run_warp(s, 3 * n * kSlowSteps);
             if (!s.drained()) atomicExch(err, OSIM_ESTALL);
             if (valid) part_add<true>(acc, s.now, r, -kBig);
         }
@@ -566,7 +566,7 @@ struct HeurRun {
             const double* p = reinterpret_cast<const double*>(&S.dr[g * kHS]);
             Sim<DMA, false, false, TRACK> s;
             s.init(Durs{p, p + 1, 2}, seq, len, sigma, rsig, S.nH[g], S.nK[g], S.nD[g]);
-            run_warp(s, 3 * len);
+            run_warp(s, 3 * len * kSlowSteps);
             ms = s.now; kEnd = s.kEnd; idleK = s.idleK; ok = s.drained();
         }
     }
@@ -1039,7 +1039,7 @@ static __global__ void k_selftest_div(uint64_t samples, uint64_t seed, unsigned 
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < samples; i += stride) {
         const uint64_t a = splitmix(st), b = splitmix(st), c = splitmix(st);
-        // y: durations / sigma in [2^-60, 2^60], random mantissa (sometimes all ones)
+        // y: durations / sigma in [2^-60, 2^60] (a superset of the fast range), random mantissa
         int ey = (int)(a % 121) - 60;
         uint64_t my = (b & 0xFFFFFFFFFFFFFull);
         if ((c & 7) == 0) my = 0xFFFFFFFFFFFFFull;

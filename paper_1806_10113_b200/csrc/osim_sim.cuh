@@ -25,7 +25,7 @@
 // q = fma(e, r, q0)), which returns the correctly rounded quotient for
 // operands whose quotient and remainder stay clear of the subnormal range;
 // the host only selects it when every duration and sigma lies in
-// [2^-60, 2^60] (see osim_capi.cu), and the GPU self-test compares it with
+// [2^-60, 2^22) (see kFastHi and osim_capi.cu), and the GPU self-test compares it with
 // IEEE division.  The general path (null stages, out-of-range inputs)
 // uses IEEE division (__ddiv_rn).
 #pragma once
@@ -35,6 +35,16 @@
 namespace osim {
 
 constexpr double kEndEps = 1e-9;  // engine.py:26 _END_EPS
+
+// Step bounds.  The command that sets dt leaves left = rem - RN(RN(rem/r)*r),
+// which is 0 for rate 1 and at most 2^-52 * rem for rate sigma; with every
+// duration below kFastHi = 2^22 ms that is < 1e-9, so each step finalizes at
+// least one command and 3n steps drain a group (the fast path relies on it;
+// the host selects it only for durations in [2^-60, 2^22)).  Beyond that a
+// command may need a few more steps (rem shrinks by ~2^-52 per extra step),
+// so the general path allows kSlowSteps steps per command.
+constexpr double kFastHi = 0x1p22;
+constexpr int kSlowSteps = 24;
 constexpr int kMaxN = 16;         // 4-bit positions in a u64 sequence
 constexpr int kStride = 16;       // doubles per kind row in shared memory
 
@@ -286,11 +296,10 @@ struct Sim {
         }
     }
 
-    // DeviceSim.run (engine.py:237-241).  Every step finalizes at least the
-    // command that set dt, so 3*len steps always suffice; returns false on
-    // a stall (cannot happen without deps, kept as a guard).
+    // DeviceSim.run (engine.py:237-241); returns false on a stall (cannot
+    // happen without deps, kept as a guard).  Bound: see kSlowSteps.
     __device__ __forceinline__ bool run(TimelineOut* tl = nullptr) {
-        const int max_steps = 3 * len;
+        const int max_steps = 3 * len * kSlowSteps;
         for (int s = 0; s < max_steps; ++s) {
             if (drained()) break;
             step(tl);
@@ -305,7 +314,7 @@ struct Sim {
 // arithmetic as Sim<FAST=true>; the differences are representational:
 //  * idle lanes hold rem = 2^900 instead of a running flag in the dt min and
 //    the update (no selects; 2^900 * (1/nd) cannot overflow for durations in
-//    [2^-60, 2^60], and 2^900 - dt == 2^900);
+//    [2^-60, 2^22), and 2^900 - dt == 2^900);
 //  * max(left, 0.0) (engine.py:214) is dropped: when left <= 0 the command
 //    finalizes in this step with or without it (rw*nd <= 0 <= 1e-9), and a
 //    finalized command's rw is never read again (engine.py:223);

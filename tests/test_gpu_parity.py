@@ -544,3 +544,20 @@ def test_heuristic_every_size_vs_oracle(n):
         order, ms, sims = _capi.heuristic_batch(d, r, dma, sigma, osim.SUM_MODE)
         oo, om, osims = O.reorder_batch(d, r, dma, sigma, osim.SUM_MODE, threads=8)
         assert np.array_equal(order, oo) and np.array_equal(ms, om) and np.array_equal(sims, osims)
+
+
+def test_out_of_fast_range_durations_take_the_general_path():
+    # non-null stages outside [2^-60, 2^60] (and sigma = 1) select the IEEE-division path
+    rng = np.random.default_rng(9)
+    for scale in (1e-22, 1e22):
+        d = rng.uniform(0.5, 4.0, (6, 3)) * scale
+        assert not _capi.fast_eligible(d, 0.5)
+        for dma, sigma in ((2, 0.5), (2, 0.3), (1, 1.0)):
+            s, ms = _capi.exhaustive(d, dma, sigma, 0, 720, want_makespans=True)
+            o, oms = O.exhaustive(d, dma, sigma, makespans=True)
+            assert np.array_equal(ms, oms)
+            assert_summary_vs_oracle(s, o)
+            r = np.arange(6, dtype=np.uint8)
+            order, hm, _ = _capi.heuristic_batch(d[None], r[None], dma, sigma, osim.SUM_MODE)
+            oo, om, _ = O.reorder(d, r, dma, sigma, osim.SUM_MODE)
+            assert order[0].tolist() == oo and hm[0] == om
