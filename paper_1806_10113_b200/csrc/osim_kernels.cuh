@@ -873,26 +873,23 @@ __global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict
             const int rest = __reduce_max_sync(kFull, 3 * (k + 1) - s.finalized());
             s.run_phased(rest, sigma, rsig);
             // _completion_estimate (heuristic.py:34-49): builtin sum of the
-            // rest's t_k in rt order (cand[] is rt in input order), min t_dth.
-            // Warp-uniform loop over the m candidates, skipping j.
+            // rest's t_k in rt order (cand[] is rt in input order, rest skips
+            // position j), min t_dth.  Warp-uniform loop over the m-1 rest.
             double f = 0.0, cmp = 0.0, tail = kBig;
+            const uint8_t* cl = &S.cand[g * kMaxN];
 #pragma unroll 1
-            for (int i = 0; i < m; ++i) {
-                const int t = S.cand[g * kMaxN + i];
-                const double x = DV(g, 1, t), d = DV(g, 2, t);
-                const bool use = i != j;
+            for (int i = 0; i < m - 1; ++i) {
+                const int t = cl[i + (i >= j ? 1 : 0)];
+                const double2 kd = make_double2(DV(g, 1, t), DV(g, 2, t));
+                const double x = kd.x;
                 const double tt = __dadd_rn(f, x);
-                double e;
                 if (sum_mode) {  // Neumaier (CPython >= 3.12); f = 0 first is 0 + x0
-                    e = (fabs(f) >= fabs(x)) ? __dadd_rn(__dsub_rn(f, tt), x) : __dadd_rn(__dsub_rn(x, tt), f);
-                } else {
-                    e = 0.0;
+                    const bool fb = fabs(f) >= fabs(x);
+                    const double big = fb ? f : x, small = fb ? x : f;
+                    cmp = __dadd_rn(cmp, __dadd_rn(__dsub_rn(big, tt), small));
                 }
-                if (use) {
-                    cmp = __dadd_rn(cmp, e);
-                    f = tt;
-                    tail = dmin(d, tail);
-                }
+                f = tt;
+                tail = dmin(kd.y, tail);
             }
             if (sum_mode && cmp != 0.0 && isfinite(cmp)) f = __dadd_rn(f, cmp);
             const double bound = __dadd_rn(__dadd_rn(s.kEnd, f), tail);
