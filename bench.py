@@ -351,6 +351,25 @@ def run_secondary(a, D, torch, dev, sp, flush, ops, peak_ops, L):
                                  "workload": "C3: K20 seed 10, 10 tasks, 10! orderings x20 per step",
                                  "frac_fp64": ops["c3"]["ops"] * (hi - lo) * reps * K / tk / 1e12 / peak_ops}
 
+    # C4 variants: sigma 0.375 (true-divide path) and 1-DMA
+    d4v = torch.from_numpy(synth.c4_group()).to(dev)
+    o4v = torch.zeros(6, dtype=torch.float64, device=dev)
+    lo4, hi4 = odist.shard(TOTAL12, D.rank, D.world)
+    for name, dma_v, sig_v, opkey in (("c4_sigma0.375_orderings_per_s", 2, 0.375, "c4_sigma0.375"),
+                                      ("c4_1dma_orderings_per_s", 1, 1.0, None)):
+        def s4(ev=None, dma_v=dma_v, sig_v=sig_v):
+            _capi.check(L.osim_exhaustive_dev(C.c_void_p(d4v.data_ptr()), 12, dma_v, sig_v, lo4, hi4, 1,
+                                              C.c_void_p(o4v.data_ptr()), None, sp))
+            if ev is not None:
+                ev.record()
+
+        t, tk = timed_steps(s4, K, W, flush, sync)
+        t = D.max(t)
+        out[name] = {"value": TOTAL12 * K / t, "unit": "orderings/s",
+                     "workload": f"C4 group, {dma_v}-DMA sigma {sig_v}, all 12! orderings"}
+        if opkey:
+            out[name]["frac_fp64"] = ops[opkey]["ops"] * (hi4 - lo4) * K / tk / 1e12 / peak_ops
+
     # row f2 on the headline space: exact median + percentile count of all 12!
     # makespans kept in HBM (single GPU; multi-rank uses dist.exhaustive_stats_distributed)
     if D.world == 1:
@@ -459,7 +478,7 @@ def cpu_heuristic_rate(seconds):
     from paper_1806_10113_b200 import synth
 
     threads = os.cpu_count() or 1
-    d, r = synth.c5_batch_fast("nvidia", 20_000, seed=77)
+    d, r = synth.c5_batch_fast("nvidia", 400_000, seed=77)
     probe = 16 * threads
     t0 = time.perf_counter()
     O.reorder_batch(d[:probe], r[:probe], 2, 0.5, 1, threads=threads)
