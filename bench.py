@@ -506,7 +506,7 @@ def run_reference(a):
 
     threads = os.cpu_count() or 1
     d = synth.c4_group()
-    v, _, m, start = cpu_rate(2.0)  # calibrate: each step ~2 s of wall time
+    v, _, m, start = cpu_rate(float(os.environ.get("OSIM_REF_STEP_SECONDS", "2.0")))  # each step ~2 s
     for _ in range(a.warmup):
         O.exhaustive(d, DMA, SIGMA, start, start + m // 4, threads=threads)
     t0 = time.perf_counter()
