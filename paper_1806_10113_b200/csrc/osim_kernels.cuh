@@ -789,6 +789,15 @@ struct HeurWarpShared {
     uint8_t pa[kWG], pb[kWG];
 };
 
+// (estimate, idle_K, id rank) key of select_next_task (heuristic.py:74-76)
+__device__ __forceinline__ bool key_less(double e, double d, int r, double be, double bd, int br) {
+    if (e < be) return true;
+    if (be < e) return false;
+    if (d < bd) return true;
+    if (bd < d) return false;
+    return r < br;
+}
+
 template <int DMA, bool SP2>
 __global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict__ durs,
                                                         const uint8_t* __restrict__ id_rank, uint64_t B, int n,
@@ -900,21 +909,33 @@ __global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict
             }
         }
         __syncwarp();
+        // argmin of the key over the m candidates: 4 lanes per group, each
+        // scanning every 4th candidate, then a 2-level shuffle reduction
+        // (the key is a strict total order, so the tree order is immaterial)
+        int bj;
+        {
+            const int g = lane >> 2, part = lane & 3;
+            int lj = -1;
+            double le = 0, ld = 0;
+            int lr = 0;
+            if (g < Gv) {
+                for (int j = part; j < m; j += 4) {
+                    const double e = S.ka[g * kMaxN + j], d = S.kb[g * kMaxN + j];
+                    const int r = S.idr[g * kMaxN + S.cand[g * kMaxN + j]];
+                    if (lj < 0 || key_less(e, d, r, le, ld, lr)) { lj = j; le = e; ld = d; lr = r; }
+                }
+            }
+#pragma unroll
+            for (int off = 1; off <= 2; off <<= 1) {
+                const int oj = __shfl_xor_sync(kFull, lj, off);
+                const double oe = __shfl_xor_sync(kFull, le, off), od = __shfl_xor_sync(kFull, ld, off);
+                const int orr = __shfl_xor_sync(kFull, lr, off);
+                if (oj >= 0 && (lj < 0 || key_less(oe, od, orr, le, ld, lr))) { lj = oj; le = oe; ld = od; lr = orr; }
+            }
+            bj = __shfl_sync(kFull, lj, (lane & 7) << 2);  // group `lane` (< 8) result
+        }
         if (lane < Gv) {
             const int g = lane;
-            int bj = 0;
-            for (int j = 1; j < m; ++j) {
-                const double e = S.ka[g * kMaxN + j], be = S.ka[g * kMaxN + bj];
-                const double d = S.kb[g * kMaxN + j], bd = S.kb[g * kMaxN + bj];
-                bool less;
-                if (e < be) less = true;
-                else if (be < e) less = false;
-                else if (d < bd) less = true;
-                else if (bd < d) less = false;
-                else less = S.idr[g * kMaxN + S.cand[g * kMaxN + j]] <
-                            S.idr[g * kMaxN + S.cand[g * kMaxN + bj]];
-                if (less) bj = j;
-            }
             const int c = S.cand[g * kMaxN + bj];
             S.ot[g] |= (uint64_t)c << (4 * k);
             S.rmask[g] &= ~(1u << c);
