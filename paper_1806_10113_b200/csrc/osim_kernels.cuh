@@ -772,6 +772,7 @@ __global__ void __launch_bounds__(kHT) k_heuristic(const double* __restrict__ du
 // unchanged, so every estimate, idle time and makespan is bit-identical.
 // ---------------------------------------------------------------------------
 constexpr int kWG = 8;                 // groups per warp
+constexpr int kKeyN = kMaxN - 1;       // candidates per greedy round (n - k, k >= 1)
 constexpr int kWPB = 4;                // warps per CTA (kHT threads)
 static_assert(kWG * kWPB == kHG, "groups per CTA");
 
@@ -780,8 +781,8 @@ struct HeurWarpShared {
     using FS = FastSim<DMA, SP2, true, false>;
     double2 dr[kWG * kHS];
     typename FS::Ck ck[kWG];
-    double ka[kWG * kMaxN];
-    double kb[kWG * kMaxN];
+    double ka[kWG * kKeyN];  // per-candidate keys (m <= 15 per round)
+    double kb[kWG * kKeyN];
     uint64_t ot[kWG];
     unsigned rmask[kWG];
     uint8_t idr[kWG * kMaxN];
@@ -904,8 +905,8 @@ __global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict
             const double bound = __dadd_rn(__dadd_rn(s.kEnd, f), tail);
             const double est = (bound > s.now) ? bound : s.now;
             if (valid) {
-                S.ka[g * kMaxN + j] = est;
-                S.kb[g * kMaxN + j] = s.idleK;
+                S.ka[g * kKeyN + j] = est;
+                S.kb[g * kKeyN + j] = s.idleK;
             }
         }
         __syncwarp();
@@ -920,7 +921,7 @@ __global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict
             int lr = 0;
             if (g < Gv) {
                 for (int j = part; j < m; j += 4) {
-                    const double e = S.ka[g * kMaxN + j], d = S.kb[g * kMaxN + j];
+                    const double e = S.ka[g * kKeyN + j], d = S.kb[g * kKeyN + j];
                     const int r = S.idr[g * kMaxN + S.cand[g * kMaxN + j]];
                     if (lj < 0 || key_less(e, d, r, le, ld, lr)) { lj = j; le = e; ld = d; lr = r; }
                 }
@@ -973,7 +974,7 @@ __global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict
             s.load(S.ck[g]);
             const int rest = __reduce_max_sync(kFull, 3 * n - s.finalized());
             s.run_phased(rest, sigma, rsig);
-            if (valid) S.ka[g * kMaxN + w] = s.now;
+            if (valid) S.ka[g * kKeyN + w] = s.now;
         }
         __syncwarp();
     }
@@ -982,7 +983,7 @@ __global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict
         double ms;
         if (n >= 2) {
             const int a = S.pa[g], b = S.pb[g];
-            const double m_ab = S.ka[g * kMaxN + 0], m_ba = S.ka[g * kMaxN + 1];
+            const double m_ab = S.ka[g * kKeyN + 0], m_ba = S.ka[g * kKeyN + 1];
             bool ab;
             if (m_ab < m_ba) ab = true;
             else if (m_ba < m_ab) ab = false;
