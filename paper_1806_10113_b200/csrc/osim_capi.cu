@@ -47,6 +47,8 @@ struct DevCtx {
     int dev = 0;
     int sms = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t stream2 = nullptr;  // second copy/compute stream for pipelined host calls
+    cudaEvent_t ev = nullptr;
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
     int* d_err = nullptr;
@@ -69,6 +71,8 @@ int ensure_init() {
         CK(cudaSetDevice(d));
         CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, d));
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming));
         CK(cudaMalloc(&c->d_err, sizeof(int)));
         CK(cudaMemset(c->d_err, 0, sizeof(int)));
         g_devs.push_back(c);
@@ -415,6 +419,8 @@ int osim_shutdown(void) {
         if (c->scratch) cudaFree(c->scratch);
         if (c->d_err) cudaFree(c->d_err);
         if (c->stream) cudaStreamDestroy(c->stream);
+        if (c->stream2) cudaStreamDestroy(c->stream2);
+        if (c->ev) cudaEventDestroy(c->ev);
         delete c;
     }
     g_devs.clear();
@@ -753,22 +759,31 @@ int osim_heuristic_batch(const double* durs, const uint8_t* id_rank, uint64_t B,
                          uint32_t* n_sims) {
     int rc = check_common(n, dma, sigma);
     if (rc) return rc;
-    int fast = 0;
-    if ((rc = scan_durs(durs, B * (uint64_t)n, sigma, &fast))) return rc;
-    if (B && (!id_rank || !order || !makespan)) return fail(OSIM_EINVAL, "NULL buffer");
-    if ((rc = check_id_ranks(id_rank, B, n))) return rc;
+    if (B && (!durs || !id_rank || !order || !makespan)) return fail(OSIM_EINVAL, "NULL buffer");
     DevList dl;
     if ((rc = pick_devs(n_dev, dl))) return rc;
     const int G = (int)dl.v.size();
     std::vector<std::unique_lock<std::mutex>> locks;
+    std::vector<unsigned long long*> d_chk(G, nullptr);
+    std::vector<char*> bases(G, nullptr);
+    std::vector<uint64_t> los(G), ms_(G);
+    std::vector<size_t> offs_idr(G), offs_ord(G), offs_ms(G), offs_ns(G);
+    const bool fast_first = sigma >= 0x1p-60;
+    // Inputs are validated on the device (a check kernel per chunk) while the
+    // fast kernel runs optimistically on them -- it is memory-safe for any
+    // values; a batch that turns out not to be fast-eligible is re-run through
+    // the general kernel, and invalid input returns the reference's error.
     for (int gi = 0; gi < G; ++gi) {
         DevCtx* c = dl.v[gi];
         locks.emplace_back(c->mu);
         CK(cudaSetDevice(c->dev));
         const uint64_t lo = B * (uint64_t)gi / (uint64_t)G, hi = B * (uint64_t)(gi + 1) / (uint64_t)G;
         const uint64_t m = hi - lo;
+        los[gi] = lo;
+        ms_[gi] = m;
         if (!m) continue;
-        size_t off_idr = align_up(m * 3 * n * sizeof(double));
+        size_t off_chk = align_up(m * 3 * n * sizeof(double));
+        size_t off_idr = off_chk + 256;
         size_t off_ord = off_idr + align_up(m * n);
         size_t off_ms = off_ord + align_up(m * n);
         size_t off_ns = off_ms + align_up(m * sizeof(double));
@@ -776,20 +791,75 @@ int osim_heuristic_batch(const double* durs, const uint8_t* id_rank, uint64_t B,
         void* base;
         if ((rc = scratch(c, bytes, &base))) return rc;
         char* b = (char*)base;
-        CK(cudaMemcpyAsync(b, durs + lo * 3 * n, m * 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(b + off_idr, id_rank + lo * n, m * n, cudaMemcpyHostToDevice, c->stream));
-        if ((rc = enqueue_heuristic(c, c->stream, (double*)b, (uint8_t*)(b + off_idr), m, n, dma, sigma,
-                                    sum_mode, fast, (uint8_t*)(b + off_ord), (double*)(b + off_ms),
-                                    (uint32_t*)(b + off_ns))))
-            return rc;
-        CK(cudaMemcpyAsync(order + lo * n, b + off_ord, m * n, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(makespan + lo, b + off_ms, m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        if (n_sims)
-            CK(cudaMemcpyAsync(n_sims + lo, b + off_ns, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+        bases[gi] = b;
+        offs_idr[gi] = off_idr; offs_ord[gi] = off_ord; offs_ms[gi] = off_ms; offs_ns[gi] = off_ns;
+        unsigned long long* chk = (unsigned long long*)(b + off_chk);
+        d_chk[gi] = chk;
+        const unsigned long long init[3] = {~0ull, ~0ull, 0ull};
+        CK(cudaMemcpyAsync(chk, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));  // `init` is a stack buffer
+        CK(cudaEventRecord(c->ev, c->stream));
+        CK(cudaStreamWaitEvent(c->stream2, c->ev, 0));
+        // large batches: chunks alternate between two streams so the H2D of
+        // chunk i+1 and the D2H of chunk i-1 overlap the kernel of chunk i
+        // (effective when the caller's buffers are pinned)
+        const uint64_t nchunk = m >= (1ull << 17) ? 8 : 1;
+        for (uint64_t ci = 0; ci < nchunk; ++ci) {
+            const uint64_t a = m * ci / nchunk, e = m * (ci + 1) / nchunk, mm = e - a;
+            if (!mm) continue;
+            cudaStream_t st = (ci & 1) ? c->stream2 : c->stream;
+            double* d_durs = (double*)b + a * 3 * n;
+            uint8_t* d_idr = (uint8_t*)(b + off_idr) + a * n;
+            uint8_t* d_ord = (uint8_t*)(b + off_ord) + a * n;
+            double* d_ms = (double*)(b + off_ms) + a;
+            uint32_t* d_ns = (uint32_t*)(b + off_ns) + a;
+            CK(cudaMemcpyAsync(d_durs, durs + (lo + a) * 3 * n, mm * 3 * n * sizeof(double),
+                               cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(d_idr, id_rank + (lo + a) * n, mm * n, cudaMemcpyHostToDevice, st));
+            const unsigned cg = (unsigned)((mm + 255) / 256 < (uint64_t)c->sms * 4 ? (mm + 255) / 256 : c->sms * 4);
+            k_check_batch<<<cg, 256, 0, st>>>(d_durs, d_idr, mm, n, (lo + a) * n, lo + a, chk);
+            if ((rc = enqueue_heuristic(c, st, d_durs, d_idr, mm, n, dma, sigma, sum_mode, fast_first, d_ord, d_ms, d_ns)))
+                return rc;
+            CK(cudaMemcpyAsync(order + (lo + a) * n, d_ord, mm * n, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(makespan + lo + a, d_ms, mm * sizeof(double), cudaMemcpyDeviceToHost, st));
+            if (n_sims)
+                CK(cudaMemcpyAsync(n_sims + lo + a, d_ns, mm * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        }
     }
     for (int gi = 0; gi < G; ++gi) {
         DevCtx* c = dl.v[gi];
+        if (!ms_[gi]) continue;
         CK(cudaSetDevice(c->dev));
+        CK(cudaStreamSynchronize(c->stream2));
+        CK(cudaStreamSynchronize(c->stream));
+        unsigned long long res[3];
+        CK(cudaMemcpy(res, d_chk[gi], sizeof(res), cudaMemcpyDeviceToHost));
+        if (res[0] != ~0ull || res[1] != ~0ull || (fast_first && res[2]))
+            CK(cudaMemset(c->d_err, 0, sizeof(int)));  // the optimistic pass ran on ineligible data
+        if (res[0] != ~0ull) {  // the reason, for the reference's message
+            const uint64_t t = res[0];
+            const double* d = durs + 3 * t;
+            if (d[0] == 0.0 && d[1] == 0.0 && d[2] == 0.0)
+                return fail(OSIM_EINVAL, "task %llu has no commands", (unsigned long long)t);
+            return fail(OSIM_EINVAL, "task %llu: durations must be finite and non-negative", (unsigned long long)t);
+        }
+        if (res[1] != ~0ull)
+            return fail(OSIM_EINVAL, "group %llu: id ranks must be a permutation (duplicate task id?)", res[1]);
+        if (fast_first && res[2]) {
+            // not fast-eligible: recompute this shard with the general kernel
+            const uint64_t m = ms_[gi];
+            char* b = bases[gi];
+            if ((rc = enqueue_heuristic(c, c->stream, (double*)b, (uint8_t*)(b + offs_idr[gi]), m, n, dma, sigma,
+                                        sum_mode, 0, (uint8_t*)(b + offs_ord[gi]), (double*)(b + offs_ms[gi]),
+                                        (uint32_t*)(b + offs_ns[gi]))))
+                return rc;
+            const uint64_t lo = los[gi];
+            CK(cudaMemcpyAsync(order + lo * n, b + offs_ord[gi], m * n, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(makespan + lo, b + offs_ms[gi], m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            if (n_sims)
+                CK(cudaMemcpyAsync(n_sims + lo, b + offs_ns[gi], m * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                   c->stream));
+        }
         if ((rc = finish(c, c->stream))) return rc;
     }
     return 0;

@@ -291,8 +291,9 @@ template <class FS>
 __device__ __forceinline__ int advance_to(FS& s, int target, double sigma, double rsig) {
     int n = 0;
 #pragma unroll 1
-    while (__any_sync(kFull, s.htd_done() < target)) {
-        if (s.htd_done() < target) {
+    // (<= 3n steps on fast-eligible data; the bound keeps ineligible input finite)
+    while (__any_sync(kFull, s.htd_done() < target && n < 3 * kMaxN)) {
+        if (s.htd_done() < target && n < 3 * kMaxN) {
             s.step(sigma, rsig);
             ++n;
         }
@@ -854,7 +855,7 @@ __global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict
             S.ot[g] = (uint64_t)best;
             S.rmask[g] = all & ~(1u << best);
             s.init(gbase(g), S.ot[g], 1);
-            while (s.htd_done() < 1) s.step(sigma, rsig);
+            for (int q = 0; q < 3 * kMaxN && s.htd_done() < 1; ++q) s.step(sigma, rsig);
         } else {
             S.ot[g] = 0;
             S.rmask[g] = all;
@@ -947,7 +948,8 @@ __global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict
             FS s;
             s.init(gbase(g), S.ot[g], k + 1);
             s.load(S.ck[g]);
-            while (s.htd_done() < k + 1) s.step(sigma, rsig);
+            // bounded: the optimistic host pass may run this on ineligible input
+            for (int q = 0; q < 3 * kMaxN && s.htd_done() < k + 1; ++q) s.step(sigma, rsig);
             s.save(S.ck[g]);
         }
         __syncwarp();
@@ -1004,6 +1006,39 @@ __global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict
         const int g = i / n, p = i % n;
         order_out[(g0 + g) * (uint64_t)n + p] = (uint8_t)nib(S.ot[g], p);
     }
+}
+
+// ---------------------------------------------------------------------------
+// Device-side input validation for the batched host APIs (same rules as the
+// host scan in osim_capi.cu: model.py:95-100, engine.py:129-130, unique ids):
+// out[0] = lowest offending task index (durations), out[1] = lowest group with
+// bad id ranks, out[2] = 1 if any stage is outside the fast range.
+// ---------------------------------------------------------------------------
+static __global__ void k_check_batch(const double* __restrict__ durs, const uint8_t* __restrict__ idr,
+                                     uint64_t B, int n, uint64_t task0, uint64_t group0,
+                                     unsigned long long* __restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    bool notfast = false;
+    for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B; b += stride) {
+        unsigned seen = 0;
+        bool badr = false;
+        for (int j = 0; j < n; ++j) {
+            const double* d = durs + (b * n + j) * 3;
+            const double h = d[0], k = d[1], x = d[2];
+            const bool ok = h >= 0.0 && k >= 0.0 && x >= 0.0 && h <= 1.7976931348623157e308 &&
+                            k <= 1.7976931348623157e308 && x <= 1.7976931348623157e308 &&
+                            !(h <= 0 && k <= 0 && x <= 0);
+            if (!ok) atomicMin(&out[0], (unsigned long long)(task0 + b * n + j));
+            notfast |= !(h >= 0x1p-60 && h < kFastHi && k >= 0x1p-60 && k < kFastHi && x >= 0x1p-60 && x < kFastHi);
+            if (idr) {
+                const unsigned v = idr[b * n + j];
+                badr |= v >= (unsigned)n || ((seen >> v) & 1u);
+                seen |= 1u << (v & 31u);
+            }
+        }
+        if (badr) atomicMin(&out[1], (unsigned long long)(group0 + b));
+    }
+    if (__any_sync(kFull, notfast) && (threadIdx.x & 31) == 0) atomicExch(&out[2], 1ull);
 }
 
 // ---------------------------------------------------------------------------

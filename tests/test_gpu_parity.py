@@ -563,3 +563,37 @@ def test_out_of_fast_range_durations_take_the_general_path():
             order, hm, _ = _capi.heuristic_batch(d[None], r[None], dma, sigma, osim.SUM_MODE)
             oo, om, _ = O.reorder(d, r, dma, sigma, osim.SUM_MODE)
             assert order[0].tolist() == oo and hm[0] == om
+
+
+def test_heuristic_large_batch_device_validation_and_fallback():
+    # >= 2^17 groups: chunked two-stream pipeline, inputs validated on the
+    # device while the fast kernel runs optimistically
+    rng = np.random.default_rng(77)
+    B, n = (1 << 17) + 5, 4
+    d = rng.uniform(0.05, 6.0, (B, n, 3))
+    r = np.stack([rng.permutation(n) for _ in range(64)]).astype(np.uint8)[rng.integers(0, 64, B)]
+    # one group outside the fast range -> the whole shard reruns on the general kernel
+    d[70001] *= 1e23
+    for dma, sigma in ((2, 0.5), (1, 1.0)):
+        order, ms, sims = _capi.heuristic_batch(d, r, dma, sigma, osim.SUM_MODE)
+        oo, om, osims = O.reorder_batch(d, r, dma, sigma, osim.SUM_MODE, threads=16)
+        assert np.array_equal(order, oo) and np.array_equal(ms, om) and np.array_equal(sims, osims)
+    # invalid inputs in an interior chunk: the lowest offending task / group is reported
+    bad = d.copy()
+    bad[90000, 2, 1] = -1.0
+    bad[100000, 1, 0] = np.nan
+    with pytest.raises(ValueError, match=f"task {90000 * n + 2}:"):
+        _capi.heuristic_batch(bad, r, 2, 0.5, osim.SUM_MODE)
+    bad = d.copy()
+    bad[120000, 3] = 0.0
+    with pytest.raises(osim.UnresolvableDuration, match=f"task {120000 * n + 3} has"):
+        _capi.heuristic_batch(bad, r, 2, 0.5, osim.SUM_MODE)
+    rr = r.copy()
+    rr[100001] = [0, 1, 1, 3]
+    rr[110000] = [0, 1, 2, 9]
+    with pytest.raises(ValueError, match="group 100001:"):
+        _capi.heuristic_batch(d, rr, 2, 0.5, osim.SUM_MODE)
+    # the context is clean afterwards
+    order, ms, _ = _capi.heuristic_batch(d[:1000], r[:1000], 2, 0.5, osim.SUM_MODE)
+    oo, om, _ = O.reorder_batch(d[:1000], r[:1000], 2, 0.5, osim.SUM_MODE, threads=8)
+    assert np.array_equal(order, oo) and np.array_equal(ms, om)
