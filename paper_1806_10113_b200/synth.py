@@ -130,8 +130,19 @@ def c4_group() -> np.ndarray:
     return real_group("AMD", 12, 12)[1]
 
 
-def c5_batch(profile: str, count: int, start: int = 0) -> Tuple[np.ndarray, np.ndarray]:
-    """Config 5: group b = sample_real_tasks(dev, 16, seed=b)."""
+def c5_batch(profile: str, count: int, start: int = 0, workers: int = 1) -> Tuple[np.ndarray, np.ndarray]:
+    """Config 5: group b = sample_real_tasks(dev, 16, seed=b).  One
+    generator per group (~0.2 ms each), so large batches can be drawn by
+    `workers` processes over contiguous seed ranges."""
+    if workers > 1 and count >= 4 * workers:
+        import multiprocessing as mp
+        from concurrent.futures import ProcessPoolExecutor
+
+        cuts = [count * i // workers for i in range(workers + 1)]
+        with ProcessPoolExecutor(workers, mp_context=mp.get_context("spawn")) as ex:
+            parts = list(ex.map(c5_batch, [profile] * workers, [cuts[i + 1] - cuts[i] for i in range(workers)],
+                                [start + cuts[i] for i in range(workers)]))
+        return np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts])
     dev = PROFILES[profile][0]
     d = np.empty((count, 16, 3))
     r = np.empty((count, 16), dtype=np.uint8)

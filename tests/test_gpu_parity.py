@@ -4,6 +4,7 @@ orderings and simulation counts; 1e-12 relative for mean and geomean
 (north_star tolerance)."""
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -96,7 +97,9 @@ def test_c2_tgs_full_space():
 
 
 def test_c2_batch_vs_oracle():
-    d = synth.c2_batch(512)
+    # the full config-2 batch (10^5 x 8-task groups); SURVEY 8(d) parity bar:
+    # groups 0-255 plus 256 seeded-random indices against the oracle
+    d = synth.c2_batch(100_000)
     out = _capi.exhaustive_batch(d, 2, 0.5)
     g = load("c2_tg.json")
     for tg in g["tgs"]:
@@ -104,13 +107,15 @@ def test_c2_batch_vs_oracle():
         assert o["best"] == F(tg["best"]) and o["best_rank"] == tg["argmin"] and o["worst"] == F(tg["worst"])
         assert close(o["sum"] / o["count"], F(tg["mean"]), REL)
     rng = np.random.default_rng(3)
-    for b in rng.choice(512, 24, replace=False):
-        o, _ = O.exhaustive(d[b], 2, 0.5, threads=8)
+    idx = np.concatenate([np.arange(256), rng.choice(np.arange(256, 100_000), 256, replace=False)])
+    cpus = os.cpu_count() or 4
+    for b in idx:
+        o, _ = O.exhaustive(d[b], 2, 0.5, threads=cpus)
         assert_summary_vs_oracle({k: out[b][k].item() for k in out.dtype.names}, o)
     # 1-DMA on the same groups
-    out1 = _capi.exhaustive_batch(d[:16], 1, 1.0)
-    for b in range(0, 16, 5):
-        o, _ = O.exhaustive(d[b], 1, 1.0, threads=8)
+    out1 = _capi.exhaustive_batch(d[:4096], 1, 1.0)
+    for b in list(range(0, 64)) + list(rng.choice(4096, 64, replace=False)):
+        o, _ = O.exhaustive(d[b], 1, 1.0, threads=cpus)
         assert_summary_vs_oracle({k: out1[b][k].item() for k in out1.dtype.names}, o)
 
 
@@ -147,6 +152,48 @@ def test_c4_sampled_ranks_and_subrange():
         assert_summary_vs_oracle(s, o)
 
 
+def _unrank_many(ranks, n):
+    """Vectorized Lehmer unranking (lexicographic permutation index)."""
+    ranks = np.asarray(ranks, dtype=np.int64).copy()
+    avail = np.ones((len(ranks), n), dtype=bool)
+    out = np.empty((len(ranks), n), dtype=np.uint8)
+    for p in range(n):
+        f = math.factorial(n - 1 - p)
+        dgt = ranks // f
+        ranks -= dgt * f
+        pick = np.argmax(np.cumsum(avail, axis=1) == (dgt + 1)[:, None], axis=1)
+        out[:, p] = pick
+        avail[np.arange(len(ranks)), pick] = False
+    return out
+
+
+def test_c4_strided_ranks_bit_exact():
+    # SURVEY 8(d) C4 parity bar: 10^6 strided ranks r = k * floor(12!/10^6)
+    d = synth.c4_group()
+    step = math.factorial(12) // 1_000_000
+    perms = _unrank_many(np.arange(1_000_000) * step, 12)
+    assert perms[1].tolist() == O.unrank(step, 12)
+    cpus = os.cpu_count() or 4
+    for sig in (0.5, 0.375):
+        s, ms = _capi.eval_perms(d, 2, sig, perms)
+        o, oms = O.eval_perms(d, 2, sig, perms, threads=cpus)
+        assert np.array_equal(ms, oms)
+        assert_summary_vs_oracle(s, o)
+    s, ms = _capi.eval_perms(d, 1, 1.0, perms)
+    o, oms = O.eval_perms(d, 1, 1.0, perms, threads=cpus)
+    assert np.array_equal(ms, oms)
+
+
+def test_c4_full_space_vs_oracle():
+    # the whole 12! space of the headline group against the C restatement
+    # (~1 min of host time on 16 threads)
+    d = synth.c4_group()
+    total = math.factorial(12)
+    s, _ = _capi.exhaustive(d, 2, 0.5, 0, total)
+    o, _ = O.exhaustive(d, 2, 0.5, 0, total, threads=os.cpu_count() or 4)
+    assert_summary_vs_oracle(s, o)
+
+
 def test_c4_full_space_consistency():
     d = synth.c4_group()
     total = math.factorial(12)
@@ -179,10 +226,13 @@ def test_c5_heuristic_rows_bit_exact():
 
 @pytest.mark.parametrize("profile", ["nvidia", "amd", "phi"])
 def test_c5_heuristic_vs_oracle_many(profile):
-    d, r = synth.c5_batch(profile, 3000, start=500_000)
+    # SURVEY 8(d) C5 parity bar: >= 10^5 groups per profile (seeds 0..99999),
+    # order, makespan and simulation count bit-exact
+    cpus = os.cpu_count() or 4
+    d, r = synth.c5_batch(profile, 100_000, start=0, workers=min(cpus, 32))
     _, dma, sigma = synth.PROFILES[profile]
     order, ms, sims = _capi.heuristic_batch(d, r, dma, sigma, osim.SUM_MODE)
-    o_order, o_ms, o_sims = O.reorder_batch(d, r, dma, sigma, osim.SUM_MODE, threads=8)
+    o_order, o_ms, o_sims = O.reorder_batch(d, r, dma, sigma, osim.SUM_MODE, threads=cpus)
     assert np.array_equal(order, o_order)
     assert np.array_equal(ms, o_ms)
     assert np.array_equal(sims, o_sims)
