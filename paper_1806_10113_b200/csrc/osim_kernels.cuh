@@ -301,23 +301,89 @@ __device__ __forceinline__ int advance_to(FS& s, int target, double sigma, doubl
     return n;
 }
 
+// Phase-B lanes of a warp run in lock-step for 3N - min(sa) steps, sa being
+// a lane's phase-A step count, so lanes with a larger sa idle through no-op
+// steps.  After phase A the block therefore reassigns its 256 checkpoints in
+// ascending-sa order (a deterministic counting sort: per-warp bins from
+// __match_any_sync, ties by thread index), so that each warp gets prefixes of
+// nearly equal remaining length (C4: executed/needed steps 1.095 -> 1.015).
+constexpr int kSaBins = 64;  // sa <= 3 * kMaxN
+struct PfxSort {
+    uint64_t seq[kBlock];
+    uint64_t P[kBlock];  // ~0: no prefix (tail of the range)
+    int sa[kBlock];
+    int cnt[kBlock / 32][kSaBins];
+    int base[kSaBins];
+    short order[kBlock];
+};
+
+// Returns the thread index whose phase-A result this thread takes over.
+__device__ __forceinline__ int pfx_sort(PfxSort& S, int sa) {
+    const int ti = threadIdx.x, lane = ti & 31, w = ti >> 5;
+    for (int i = lane; i < kSaBins; i += 32) S.cnt[w][i] = 0;
+    __syncwarp();
+    const unsigned same = __match_any_sync(kFull, sa);
+    if (lane == __ffs(same) - 1) S.cnt[w][sa] = __popc(same);
+    __syncthreads();
+    if (w == 0) {
+        int carry = 0;
+#pragma unroll
+        for (int b0 = 0; b0 < kSaBins; b0 += 32) {
+            const int b = b0 + lane;
+            int t = 0;
+#pragma unroll
+            for (int ww = 0; ww < kBlock / 32; ++ww) t += S.cnt[ww][b];
+            int x = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(kFull, x, o);
+                if (lane >= o) x += y;
+            }
+            S.base[b] = carry + x - t;
+            carry += __shfl_sync(kFull, x, 31);
+        }
+    }
+    __syncthreads();
+    int rank = S.base[sa] + __popc(same & ((1u << lane) - 1u));
+    for (int ww = 0; ww < w; ++ww) rank += S.cnt[ww][sa];
+    S.order[rank] = (short)ti;
+    __syncthreads();
+    return S.order[ti];
+}
+
 // Simulate prefix P of length M and every suffix; accumulate leaves that
-// fall inside [lo, hi).  All threads of the warp must call together.
+// fall inside [lo, hi).  All threads of the block must call together.
 // (A second checkpoint level two positions later was measured slower on B200:
 // its middle segment runs in divergent advance loops shared by only two
 // leaves.)
 template <int N, int DMA, bool SIGP2, int L, bool WRITE_MS, int SLOTS>
 __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double rsig, uint64_t P,
                                            bool validP, uint64_t lo, uint64_t hi, double thr, Part& acc,
-                                           double* __restrict__ ms_out, uint64_t ms_base, CkSlots<SLOTS>& K) {
+                                           double* __restrict__ ms_out, uint64_t ms_base, CkSlots<SLOTS>& K,
+                                           PfxSort& S) {
     constexpr int M = N - L;
     constexpr uint64_t LF = Fact<L>::v;
-    const uint64_t seq0 = unrank<N>(P * LF);  // prefix + ascending remainder
+    uint64_t seq0 = unrank<N>(P * LF);  // prefix + ascending remainder
     using FS = FastSim<DMA, SIGP2, false, (N <= 15)>;
     FS s;
     s.init(base, seq0, N);
-    const int sa = (M > 0) ? advance_to(s, M, sigma, rsig) : 0;
+    int sa = (M > 0) ? advance_to(s, M, sigma, rsig) : 0;
     const int ti = threadIdx.x;
+    if constexpr (M > 0) {
+        // hand the checkpoints out in ascending-sa order (pfx_sort)
+        ck_store(K, 0, ti, s);
+        S.seq[ti] = seq0;
+        S.P[ti] = validP ? P : ~0ull;
+        S.sa[ti] = sa;
+        const int src = pfx_sort(S, sa);
+        ck_load(K, 0, src, s, M);
+        seq0 = S.seq[src];
+        P = S.P[src];
+        validP = P != ~0ull;
+        sa = S.sa[src];
+        __syncthreads();  // every source slot has been read
+        if (!validP) P = 0;
+    }
     const uint64_t pre = (M > 0) ? (seq0 & ((1ull << (4 * M)) - 1ull)) : 0ull;
     const uint64_t rem = seq0 >> (4 * M);  // L ascending task ids
     {
@@ -346,6 +412,7 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
             }
         }
     }
+    if constexpr (M > 0) __syncthreads();  // K and S are rewritten by the next call
 }
 
 template <int DMA, int L>
@@ -360,6 +427,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
     __shared__ double2 sdr[3 * kStride];
     __shared__ Part sh[32];
     __shared__ CkSlots<PfxSlots<DMA, L>::v> K;
+    __shared__ PfxSort S;
     stage_dr(durs, N, sdr);
     __syncthreads();
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
@@ -373,7 +441,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
         const uint64_t P = pb + threadIdx.x;
         const bool validP = P < p_hi;
         pfx_leaves<N, DMA, SIGP2, L, true, PfxSlots<DMA, L>::v>(base, sigma, rsig, validP ? P : p_lo, validP, lo, hi,
-                                                               thr, acc, ms_out, lo, K);
+                                                               thr, acc, ms_out, lo, K, S);
     }
     acc = block_reduce(acc, sh);
     if (threadIdx.x == 0) parts[blockIdx.x] = acc;
@@ -386,6 +454,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_batch_pfx(
     __shared__ double2 sdr[3 * kStride];
     __shared__ Part sh[32];
     __shared__ CkSlots<PfxSlots<DMA, L>::v> K;
+    __shared__ PfxSort S;
     constexpr uint64_t total = Fact<N>::v;
     constexpr uint64_t NP = total / Fact<L>::v;
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
@@ -399,7 +468,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_batch_pfx(
             const uint64_t P = pb + threadIdx.x;
             const bool validP = P < NP;
             pfx_leaves<N, DMA, SIGP2, L, false, PfxSlots<DMA, L>::v>(base, sigma, rsig, validP ? P : 0, validP, 0,
-                                                                     total, -kBig, acc, nullptr, 0, K);
+                                                                     total, -kBig, acc, nullptr, 0, K, S);
         }
         acc = block_reduce(acc, sh);  // ends with __syncthreads: smem reusable
         if (threadIdx.x == 0) out[b] = part_to_summary(acc);

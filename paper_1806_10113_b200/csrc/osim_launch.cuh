@@ -22,6 +22,11 @@ int grid_for_sms(K kernel, int threads, size_t smem, int sms, uint64_t work_bloc
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
     if (per_sm < 1) per_sm = 1;
+    // OSIM_CTAS_PER_SM=<k> caps the resident CTAs per SM (tuning only)
+    if (const char* e = std::getenv("OSIM_CTAS_PER_SM")) {
+        const int k = std::atoi(e);
+        if (k >= 1 && k < per_sm) per_sm = k;
+    }
     uint64_t g = (uint64_t)per_sm * sms;
     if (work_blocks < g) g = work_blocks;
     if (g < 1) g = 1;
