@@ -518,11 +518,20 @@ struct FastSim {
         if constexpr (DMA == 2) {
             const bool ov = !idle(r0) && !idle(r1);
             double m = dmin(r0, r1);
-            if constexpr (SIGP2) mul_if(ov, m, rsig);
-            else if (ov) m = divq<true>(m, sigma, rsig);
-            dt = dmin(m, r2);
-            dd = dt;
-            mul_if(ov, dd, sigma);
+            if constexpr (SIGP2) {
+                // sigma, 1/sigma and 1.0 are powers of two (low word 0): select
+                // the factor's high word and multiply unconditionally
+                // (x * 1.0 == x exactly), one integer select instead of a
+                // 64-bit select of the product
+                m = __dmul_rn(m, __hiloint2double(ov ? __double2hiint(rsig) : 0x3FF00000, 0));
+                dt = dmin(m, r2);
+                dd = __dmul_rn(dt, __hiloint2double(ov ? __double2hiint(sigma) : 0x3FF00000, 0));
+            } else {
+                if (ov) m = divq<true>(m, sigma, rsig);
+                dt = dmin(m, r2);
+                dd = dt;
+                mul_if(ov, dd, sigma);
+            }
         } else {
             dt = dmin(r0, r2);
             dd = dt;
