@@ -13,9 +13,10 @@ int exh_t(const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo,
     auto k = k_exhaustive_pfx<N, OSIM_DMA, OSIM_SP2, L>;
     constexpr uint64_t LF = Fact<L>::v;
     const uint64_t prefixes = (hi + LF - 1) / LF - lo / LF;
-    int g = grid_for_sms(k, kBlock, 0, cfg.sms, (prefixes + kBlock - 1) / kBlock);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPfxDynSmem);
+    int g = grid_for_sms(k, kBlock, kPfxDynSmem, cfg.sms, (prefixes + kPfxQ * kBlock - 1) / (kPfxQ * kBlock));
     if (g > max_parts) g = max_parts;
-    k<<<g, kBlock, 0, cfg.st>>>(d_durs, sigma, lo, hi, thr, parts, d_ms);
+    k<<<g, kBlock, kPfxDynSmem, cfg.st>>>(d_durs, sigma, lo, hi, thr, parts, d_ms);
     *grid_out = g;
     return 0;
 }

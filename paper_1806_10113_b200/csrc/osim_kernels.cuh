@@ -68,11 +68,11 @@ __device__ __forceinline__ void neumaier(double& s, double& c, double x) {
     s = t;
 }
 
-// per-thread add, ranks visited in increasing order -> strict < keeps the
-// first of equal makespans (np.argmin)
+// per-thread add; the lower rank wins a tie (np.argmin keeps the first of
+// equal makespans), so threads may visit ranks in any order
 template <bool EXACT>
 __device__ __forceinline__ void part_add(Part& a, double ms, unsigned long long r, double thr) {
-    if (ms < a.best) { a.best = ms; a.rank = r; }
+    if (ms < a.best || (ms == a.best && r < a.rank)) { a.best = ms; a.rank = r; }
     a.below += (ms < thr) ? 1ull : 0ull;
     a.worst = fmax(a.worst, ms);
     neumaier(a.sum, a.csum, ms);
@@ -303,27 +303,39 @@ __device__ __forceinline__ int advance_to(FS& s, int target, double sigma, doubl
 
 // Phase-B lanes of a warp run in lock-step for 3N - min(sa) steps, sa being
 // a lane's phase-A step count, so lanes with a larger sa idle through no-op
-// steps.  After phase A the block therefore reassigns its 256 checkpoints in
-// ascending-sa order (a deterministic counting sort: per-warp bins from
-// __match_any_sync, ties by thread index), so that each warp gets prefixes of
-// nearly equal remaining length (C4: executed/needed steps 1.095 -> 1.015).
-constexpr int kSaBins = 64;  // sa <= 3 * kMaxN
+// steps.  Each call therefore takes kPfxQ = 2 prefixes per thread (512 per
+// CTA), sorts the 512 checkpoints by sa (a deterministic counting sort:
+// per-warp bins from __match_any_sync, ties by entry index) and cuts the
+// sorted list into 16 chunks of 32; warp w replays chunk w and chunk 15 - w,
+// so lanes of a chunk have nearly equal remaining length (C4: executed /
+// needed replay steps 1.095 -> ~1.01) while every warp gets a similar total
+// (one long and one short chunk), which keeps the CTA's barrier waits short.
+// Entries without a prefix (range tails) sort last; all-empty chunks are
+// skipped.
+constexpr int kSaBins = 64;  // sa <= 3 * kMaxN; bin kSaBins - 1 = no prefix
+constexpr int kPfxQ = 2;
+constexpr int kNW = kBlock / 32;
 struct PfxSort {
-    uint64_t seq[kBlock];
-    uint64_t P[kBlock];  // ~0: no prefix (tail of the range)
-    int sa[kBlock];
-    int cnt[kBlock / 32][kSaBins];
+    uint64_t seq[kPfxQ * kBlock];
+    uint64_t P[kPfxQ * kBlock];  // ~0: no prefix
+    int sa[kPfxQ * kBlock];
+    int cnt[kPfxQ][kNW][kSaBins];
     int base[kSaBins];
-    short order[kBlock];
+    short order[kPfxQ * kBlock];
 };
 
-// Returns the thread index whose phase-A result this thread takes over.
-__device__ __forceinline__ int pfx_sort(PfxSort& S, int sa) {
+// Sort this CTA's kPfxQ * 256 entries (entry e = q * 256 + thread) by sa;
+// returns the entries this thread replays (chunks w and 2 * kNW - 1 - w).
+__device__ __forceinline__ int2 pfx_sort(PfxSort& S, int sa0, int sa1) {
     const int ti = threadIdx.x, lane = ti & 31, w = ti >> 5;
-    for (int i = lane; i < kSaBins; i += 32) S.cnt[w][i] = 0;
+    for (int i = lane; i < kSaBins; i += 32) {
+        S.cnt[0][w][i] = 0;
+        S.cnt[1][w][i] = 0;
+    }
     __syncwarp();
-    const unsigned same = __match_any_sync(kFull, sa);
-    if (lane == __ffs(same) - 1) S.cnt[w][sa] = __popc(same);
+    const unsigned m0 = __match_any_sync(kFull, sa0), m1 = __match_any_sync(kFull, sa1);
+    if (lane == __ffs(m0) - 1) S.cnt[0][w][sa0] = __popc(m0);
+    if (lane == __ffs(m1) - 1) S.cnt[1][w][sa1] = __popc(m1);
     __syncthreads();
     if (w == 0) {
         int carry = 0;
@@ -332,7 +344,9 @@ __device__ __forceinline__ int pfx_sort(PfxSort& S, int sa) {
             const int b = b0 + lane;
             int t = 0;
 #pragma unroll
-            for (int ww = 0; ww < kBlock / 32; ++ww) t += S.cnt[ww][b];
+            for (int q = 0; q < kPfxQ; ++q)
+#pragma unroll
+                for (int ww = 0; ww < kNW; ++ww) t += S.cnt[q][ww][b];
             int x = t;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -344,51 +358,90 @@ __device__ __forceinline__ int pfx_sort(PfxSort& S, int sa) {
         }
     }
     __syncthreads();
-    int rank = S.base[sa] + __popc(same & ((1u << lane) - 1u));
-    for (int ww = 0; ww < w; ++ww) rank += S.cnt[ww][sa];
-    S.order[rank] = (short)ti;
+    const unsigned lt = (1u << lane) - 1u;
+    int r0 = S.base[sa0] + __popc(m0 & lt);
+    int r1 = S.base[sa1] + __popc(m1 & lt);
+    for (int ww = 0; ww < kNW; ++ww) {
+        if (ww < w) r0 += S.cnt[0][ww][sa0];
+        r1 += S.cnt[0][ww][sa1] + (ww < w ? S.cnt[1][ww][sa1] : 0);
+    }
+    S.order[r0] = (short)ti;
+    S.order[r1] = (short)(kBlock + ti);
     __syncthreads();
-    return S.order[ti];
+    return make_int2(S.order[32 * w + lane], S.order[32 * (2 * kNW - 1 - w) + lane]);
 }
 
-// Simulate prefix P of length M and every suffix; accumulate leaves that
-// fall inside [lo, hi).  All threads of the block must call together.
+// Simulate this CTA's prefixes P0 + t and P0 + 256 + t (t = thread) of
+// length M and every suffix; accumulate leaves that fall inside [lo, hi) and
+// below prefix p_end.  All threads of the CTA must call together.
 // (A second checkpoint level two positions later was measured slower on B200:
 // its middle segment runs in divergent advance loops shared by only two
 // leaves.)
-template <int N, int DMA, bool SIGP2, int L, bool WRITE_MS, int SLOTS>
-__device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double rsig, uint64_t P,
-                                           bool validP, uint64_t lo, uint64_t hi, double thr, Part& acc,
-                                           double* __restrict__ ms_out, uint64_t ms_base, CkSlots<SLOTS>& K,
+template <int N, int DMA, bool SIGP2, int L, bool WRITE_MS>
+__device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double rsig, uint64_t P0, uint64_t p_end,
+                                           uint64_t lo, uint64_t hi, double thr, Part& acc,
+                                           double* __restrict__ ms_out, uint64_t ms_base, CkSlots<kPfxQ>& K,
                                            PfxSort& S) {
     constexpr int M = N - L;
     constexpr uint64_t LF = Fact<L>::v;
-    uint64_t seq0 = unrank<N>(P * LF);  // prefix + ascending remainder
     using FS = FastSim<DMA, SIGP2, false, (N <= 15)>;
-    FS s;
-    s.init(base, seq0, N);
-    int sa = (M > 0) ? advance_to(s, M, sigma, rsig) : 0;
     const int ti = threadIdx.x;
-    if constexpr (M > 0) {
-        // hand the checkpoints out in ascending-sa order (pfx_sort)
-        ck_store(K, 0, ti, s);
-        S.seq[ti] = seq0;
-        S.P[ti] = validP ? P : ~0ull;
-        S.sa[ti] = sa;
-        const int src = pfx_sort(S, sa);
-        ck_load(K, 0, src, s, M);
-        seq0 = S.seq[src];
-        P = S.P[src];
-        validP = P != ~0ull;
-        sa = S.sa[src];
-        __syncthreads();  // every source slot has been read
-        if (!validP) P = 0;
+    FS s;
+    // ---- phase A: both prefixes to their checkpoints
+    int sa[kPfxQ];
+#pragma unroll
+    for (int q = 0; q < kPfxQ; ++q) {
+        const uint64_t P = P0 + (uint64_t)q * kBlock + ti;
+        const bool valid = P < p_end;
+        const uint64_t seq0 = unrank<N>((valid ? P : P0) * LF);  // prefix + ascending remainder
+        s.init(base, seq0, N);
+        int a = 0;
+        if constexpr (M > 0) {
+            a = advance_to(s, valid ? M : 0, sigma, rsig);
+            ck_store(K, q, ti, s);
+        }
+        sa[q] = valid ? a : kSaBins - 1;
+        S.seq[q * kBlock + ti] = seq0;
+        S.P[q * kBlock + ti] = valid ? P : ~0ull;
+        S.sa[q * kBlock + ti] = sa[q];
     }
-    const uint64_t pre = (M > 0) ? (seq0 & ((1ull << (4 * M)) - 1ull)) : 0ull;
-    const uint64_t rem = seq0 >> (4 * M);  // L ascending task ids
+    // ---- reassign: this thread replays entries e.x then e.y
+    const int2 e = pfx_sort(S, sa[0], sa[1]);
+    uint64_t seqq[kPfxQ], Pq[kPfxQ];
+    double tv[7];
+    int th[2];
     {
-        const int rest = 3 * N - __reduce_min_sync(kFull, sa);
-        ck_store(K, 0, ti, s);
+        const int ex = e.x & (kBlock - 1), qx = e.x >> 8;
+        const int ey = e.y & (kBlock - 1), qy = e.y >> 8;
+        static_assert(kBlock == 256, "entry index split");
+        seqq[0] = S.seq[e.x]; Pq[0] = S.P[e.x]; sa[0] = S.sa[e.x];
+        seqq[1] = S.seq[e.y]; Pq[1] = S.P[e.y]; sa[1] = S.sa[e.y];
+        if constexpr (M > 0) {
+            ck_load(K, qx, ex, s, M);
+#pragma unroll
+            for (int k = 0; k < 7; ++k) tv[k] = K.v[qy][k][ey];
+            th[0] = K.h[qy][0][ey];
+            th[1] = K.h[qy][1][ey];
+        }
+        __syncthreads();  // every source slot has been read
+        if constexpr (M > 0) {
+            ck_store(K, 0, ti, s);
+#pragma unroll
+            for (int k = 0; k < 7; ++k) K.v[1][k][ti] = tv[k];
+            K.h[1][0][ti] = th[0];
+            K.h[1][1][ti] = th[1];
+        }
+    }
+    // ---- phase B: replay the L! suffixes of each taken prefix
+#pragma unroll 1
+    for (int q = 0; q < kPfxQ; ++q) {
+        const bool validP = Pq[q] != ~0ull;
+        if (!__any_sync(kFull, validP)) continue;  // all-empty chunk (range tail)
+        const uint64_t P = validP ? Pq[q] : 0ull;
+        const uint64_t seq0 = seqq[q];
+        const uint64_t pre = (M > 0) ? (seq0 & ((1ull << (4 * M)) - 1ull)) : 0ull;
+        const uint64_t rem = seq0 >> (4 * M);  // L ascending task ids
+        const int rest = 3 * N - __reduce_min_sync(kFull, validP ? sa[q] : 3 * N);
 #pragma unroll 1
         for (int j = 0; j < (int)LF; ++j) {
             const uint64_t idx = unrank<L>((uint64_t)j);
@@ -398,7 +451,8 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
                 const uint32_t id = (uint32_t)(idx >> (4 * i)) & 0xFu;
                 suf |= ((rem >> (4 * id)) & 0xFull) << (4 * (M + i));
             }
-            ck_load(K, 0, ti, s, M);
+            if constexpr (M > 0) ck_load(K, q, ti, s, M);
+            else s.init(base, 0, N);
             s.set_seq(pre | suf);
             // full steps while any lane of the warp still has an HtD to run, then
             // K+DtH steps, then DtH-only steps (FastSim::run_phased)
@@ -412,13 +466,14 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
             }
         }
     }
-    if constexpr (M > 0) __syncthreads();  // K and S are rewritten by the next call
+    // No trailing barrier: after the copy above every K slot is read only by
+    // its owner, and the shared arrays pfx_sort reads across threads are
+    // rewritten in the next call only after that call's first barrier -- a
+    // warp done early runs its next phase A meanwhile.
 }
 
-template <int DMA, int L>
-struct PfxSlots {
-    static constexpr int v = 1;
-};
+// dynamic shared memory of the prefix kernels (checkpoint slots + sort)
+constexpr size_t kPfxDynSmem = sizeof(CkSlots<kPfxQ>) + sizeof(PfxSort);
 
 template <int N, int DMA, bool SIGP2, int L>
 __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const double* __restrict__ durs, double sigma,
@@ -426,8 +481,9 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
                                                            double* __restrict__ ms_out) {
     __shared__ double2 sdr[3 * kStride];
     __shared__ Part sh[32];
-    __shared__ CkSlots<PfxSlots<DMA, L>::v> K;
-    __shared__ PfxSort S;
+    extern __shared__ __align__(16) unsigned char pfx_dsm[];
+    CkSlots<kPfxQ>& K = *reinterpret_cast<CkSlots<kPfxQ>*>(pfx_dsm);
+    PfxSort& S = *reinterpret_cast<PfxSort*>(pfx_dsm + sizeof(CkSlots<kPfxQ>));
     stage_dr(durs, N, sdr);
     __syncthreads();
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
@@ -436,13 +492,10 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
     const uint64_t p_lo = lo / LF, p_hi = (hi + LF - 1) / LF;
     Part acc;
     part_init(acc);
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t pb = p_lo + (uint64_t)blockIdx.x * blockDim.x; pb < p_hi; pb += stride) {
-        const uint64_t P = pb + threadIdx.x;
-        const bool validP = P < p_hi;
-        pfx_leaves<N, DMA, SIGP2, L, true, PfxSlots<DMA, L>::v>(base, sigma, rsig, validP ? P : p_lo, validP, lo, hi,
-                                                               thr, acc, ms_out, lo, K, S);
-    }
+    constexpr uint64_t kPer = (uint64_t)kPfxQ * kBlock;  // prefixes per CTA call
+    const uint64_t stride = (uint64_t)gridDim.x * kPer;
+    for (uint64_t pb = p_lo + (uint64_t)blockIdx.x * kPer; pb < p_hi; pb += stride)
+        pfx_leaves<N, DMA, SIGP2, L, true>(base, sigma, rsig, pb, p_hi, lo, hi, thr, acc, ms_out, lo, K, S);
     acc = block_reduce(acc, sh);
     if (threadIdx.x == 0) parts[blockIdx.x] = acc;
 }
@@ -453,10 +506,12 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_batch_pfx(
                                                                  double sigma, osim_summary* __restrict__ out) {
     __shared__ double2 sdr[3 * kStride];
     __shared__ Part sh[32];
-    __shared__ CkSlots<PfxSlots<DMA, L>::v> K;
-    __shared__ PfxSort S;
+    extern __shared__ __align__(16) unsigned char pfx_dsm[];
+    CkSlots<kPfxQ>& K = *reinterpret_cast<CkSlots<kPfxQ>*>(pfx_dsm);
+    PfxSort& S = *reinterpret_cast<PfxSort*>(pfx_dsm + sizeof(CkSlots<kPfxQ>));
     constexpr uint64_t total = Fact<N>::v;
     constexpr uint64_t NP = total / Fact<L>::v;
+    constexpr uint64_t kPer = (uint64_t)kPfxQ * kBlock;
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
     const double rsig = __ddiv_rn(1.0, sigma);
     for (uint64_t b = blockIdx.x; b < B; b += gridDim.x) {
@@ -464,12 +519,8 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_batch_pfx(
         __syncthreads();
         Part acc;
         part_init(acc);
-        for (uint64_t pb = 0; pb < NP; pb += blockDim.x) {
-            const uint64_t P = pb + threadIdx.x;
-            const bool validP = P < NP;
-            pfx_leaves<N, DMA, SIGP2, L, false, PfxSlots<DMA, L>::v>(base, sigma, rsig, validP ? P : 0, validP, 0,
-                                                                     total, -kBig, acc, nullptr, 0, K, S);
-        }
+        for (uint64_t pb = 0; pb < NP; pb += kPer)
+            pfx_leaves<N, DMA, SIGP2, L, false>(base, sigma, rsig, pb, NP, 0, total, -kBig, acc, nullptr, 0, K, S);
         acc = block_reduce(acc, sh);  // ends with __syncthreads: smem reusable
         if (threadIdx.x == 0) out[b] = part_to_summary(acc);
     }
