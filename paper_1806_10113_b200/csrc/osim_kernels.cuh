@@ -1015,9 +1015,12 @@ __global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict
                 const double x = kd.x;
                 const double tt = __dadd_rn(f, x);
                 if (sum_mode) {  // Neumaier (CPython >= 3.12); f = 0 first is 0 + x0
-                    const bool fb = fabs(f) >= fabs(x);
-                    const double big = fb ? f : x, small = fb ? x : f;
-                    cmp = __dadd_rn(cmp, __dadd_rn(__dsub_rn(big, tt), small));
+                    // CPython adds the exact rounding error of f + x, computed
+                    // by Fast2Sum on the (larger, smaller) magnitude pair;
+                    // TwoSum yields the same exact error without the select
+                    const double bp = __dsub_rn(tt, f);
+                    const double e = __dadd_rn(__dsub_rn(f, __dsub_rn(tt, bp)), __dsub_rn(x, bp));
+                    cmp = __dadd_rn(cmp, e);
                 }
                 f = tt;
                 tail = dmin(kd.y, tail);
