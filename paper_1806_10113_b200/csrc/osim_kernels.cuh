@@ -493,6 +493,10 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
     Part acc;
     part_init(acc);
     constexpr uint64_t kPer = (uint64_t)kPfxQ * kBlock;  // prefixes per CTA call
+    // grid-stride over calls of 512 prefixes.  (An even split of the ragged
+    // last round over all CTAs measured slower: a CTA left alone on an SM by
+    // the partial wave runs ~3x faster than one sharing it, so the grid-stride
+    // tail costs only a fraction of a call.)
     const uint64_t stride = (uint64_t)gridDim.x * kPer;
     for (uint64_t pb = p_lo + (uint64_t)blockIdx.x * kPer; pb < p_hi; pb += stride)
         pfx_leaves<N, DMA, SIGP2, L, true>(base, sigma, rsig, pb, p_hi, lo, hi, thr, acc, ms_out, lo, K, S);

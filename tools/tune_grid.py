@@ -25,11 +25,12 @@ def main():
     c2 = synth.c2_batch(100_000)
     h, r = synth.c5_batch_fast("nvidia", 1_000_000)
     t4 = best_of(lambda: _capi.exhaustive(d4, 2, 0.5, 0, 479001600))
+    t48 = best_of(lambda: _capi.exhaustive(d4, 2, 0.5, 0, 479001600 // 8))
     t3 = best_of(lambda: _capi.exhaustive(d3, 2, 0.5, 0, 3628800), 20)
     t2 = best_of(lambda: _capi.exhaustive_batch(c2, 2, 0.5), 3)
     t5 = best_of(lambda: _capi.heuristic_batch(h, r, 2, 0.5, 1), 3)
     print(f"env={os.environ.get('OSIM_CTAS_PER_SM', '-')} c4 {479001600 / t4 / 1e9:.2f}G/s ({t4 * 1e3:.2f} ms) "
-          f"c3 {3628800 / t3 / 1e9:.2f}G/s c2 {4.032e9 / t2 / 1e9:.2f}G/s c5 {1e6 / t5 / 1e6:.1f}M/s", flush=True)
+          f"c4/8-shard {479001600 / 8 / t48 / 1e9:.2f}G/s c3 {3628800 / t3 / 1e9:.2f}G/s c2 {4.032e9 / t2 / 1e9:.2f}G/s c5 {1e6 / t5 / 1e6:.1f}M/s", flush=True)
 
 
 if __name__ == "__main__":
