@@ -6,6 +6,7 @@
 
 #include <cstdint>
 
+#include "osim_suftab.h"
 #include "osim_sim.cuh"
 #include "../../include/offsim_b200.h"
 
@@ -444,7 +445,13 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
         const int rest = 3 * N - __reduce_min_sync(kFull, validP ? sa[q] : 3 * N);
 #pragma unroll 1
         for (int j = 0; j < (int)LF; ++j) {
-            const uint64_t idx = unrank<L>((uint64_t)j);
+            // suffix order: for L >= 4 a constant-table load replaces ~35
+            // uniform-datapath instructions per leaf (+1 % at N = 12); for
+            // short suffixes the inline unrank measured faster (the load's
+            // latency sits on the shorter replays' critical path)
+            uint64_t idx;
+            if constexpr (L >= 4) idx = suf_tab<L>(j);
+            else idx = unrank<L>((uint64_t)j);
             uint64_t suf = 0;
 #pragma unroll
             for (int i = 0; i < L; ++i) {
