@@ -10,7 +10,9 @@ namespace {
 template <int N, int L>
 int exh_t(const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo, uint64_t hi, double thr,
           Part* parts, int max_parts, double* d_ms, int* grid_out) {
-    auto k = k_exhaustive_pfx<N, OSIM_DMA, OSIM_SP2, L>;
+    // makespans out or a positive threshold need the stats variant
+    auto k = (d_ms || thr > 0.0) ? k_exhaustive_pfx<N, OSIM_DMA, OSIM_SP2, L, true>
+                                 : k_exhaustive_pfx<N, OSIM_DMA, OSIM_SP2, L, false>;
     constexpr uint64_t LF = Fact<L>::v;
     const uint64_t prefixes = (hi + LF - 1) / LF - lo / LF;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPfxDynSmem);

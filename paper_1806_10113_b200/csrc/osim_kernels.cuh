@@ -82,6 +82,17 @@ __device__ __forceinline__ void part_add(Part& a, double ms, unsigned long long 
     a.count += 1;
 }
 
+// prefix-kernel leaf: part_add without the count (added per prefix) and the
+// renormalization (every 4 leaves); the threshold count only when STATS
+template <bool STATS>
+__device__ __forceinline__ void leaf_add(Part& a, double ms, unsigned long long r, double thr) {
+    if (ms < a.best || (ms == a.best && r < a.rank)) { a.best = ms; a.rank = r; }
+    if constexpr (STATS) a.below += (ms < thr) ? 1ull : 0ull;
+    a.worst = fmax(a.worst, ms);
+    neumaier(a.sum, a.csum, ms);
+    a.lpm = __dmul_rn(a.lpm, ms);
+}
+
 // order-independent for best/rank (lexicographic), fixed tree order for sums
 __device__ __forceinline__ void part_merge(Part& a, const Part& b) {
     if (b.best < a.best || (b.best == a.best && b.rank < a.rank)) { a.best = b.best; a.rank = b.rank; }
@@ -378,7 +389,7 @@ __device__ __forceinline__ int2 pfx_sort(PfxSort& S, int sa0, int sa1) {
 // (A second checkpoint level two positions later was measured slower on B200:
 // its middle segment runs in divergent advance loops shared by only two
 // leaves.)
-template <int N, int DMA, bool SIGP2, int L, bool WRITE_MS>
+template <int N, int DMA, bool SIGP2, int L, bool STATS>
 __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double rsig, uint64_t P0, uint64_t p_end,
                                            uint64_t lo, uint64_t hi, double thr, Part& acc,
                                            double* __restrict__ ms_out, uint64_t ms_base, CkSlots<kPfxQ>& K,
@@ -443,6 +454,11 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
         const uint64_t pre = (M > 0) ? (seq0 & ((1ull << (4 * M)) - 1ull)) : 0ull;
         const uint64_t rem = seq0 >> (4 * M);  // L ascending task ids
         const int rest = 3 * N - __reduce_min_sync(kFull, validP ? sa[q] : 3 * N);
+        // leaves [r0, r0 + L!) of this prefix that fall inside [lo, hi)
+        const uint64_t r0 = P * LF;
+        const bool any_in = validP && r0 + LF > lo && r0 < hi;
+        const bool all_in = validP && r0 >= lo && r0 + LF <= hi;
+        if (any_in) acc.count += (r0 + LF < hi ? r0 + LF : hi) - (r0 > lo ? r0 : lo);
 #pragma unroll 1
         for (int j = 0; j < (int)LF; ++j) {
             // suffix order: for L >= 4 a constant-table load replaces ~35
@@ -464,13 +480,17 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
             // full steps while any lane of the warp still has an HtD to run, then
             // K+DtH steps, then DtH-only steps (FastSim::run_phased)
             s.run_phased(rest, sigma, rsig);
-            const uint64_t r = P * LF + (uint64_t)j;
-            if (validP && r >= lo && r < hi) {
-                part_add<false>(acc, s.now, r, thr);
-                if constexpr (WRITE_MS) {
+            const uint64_t r = r0 + (uint64_t)j;
+            if (all_in || (any_in && r >= lo && r < hi)) {
+                leaf_add<STATS>(acc, s.now, r, thr);
+                if constexpr (STATS) {
                     if (ms_out) ms_out[r - ms_base] = s.now;
                 }
             }
+            // the log-product's exponent is split off every 4 leaves (exact:
+            // only the binary exponent moves; 4 fast-path makespans stay
+            // within [2^-240, 2^120])
+            if ((j & 3) == 3 || j == (int)LF - 1) renorm<false>(acc.lpm, acc.lpe);
         }
     }
     // No trailing barrier: after the copy above every K slot is read only by
@@ -482,7 +502,7 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
 // dynamic shared memory of the prefix kernels (checkpoint slots + sort)
 constexpr size_t kPfxDynSmem = sizeof(CkSlots<kPfxQ>) + sizeof(PfxSort);
 
-template <int N, int DMA, bool SIGP2, int L>
+template <int N, int DMA, bool SIGP2, int L, bool STATS>
 __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const double* __restrict__ durs, double sigma,
                                                            uint64_t lo, uint64_t hi, double thr, Part* __restrict__ parts,
                                                            double* __restrict__ ms_out) {
@@ -506,7 +526,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
     // tail costs only a fraction of a call.)
     const uint64_t stride = (uint64_t)gridDim.x * kPer;
     for (uint64_t pb = p_lo + (uint64_t)blockIdx.x * kPer; pb < p_hi; pb += stride)
-        pfx_leaves<N, DMA, SIGP2, L, true>(base, sigma, rsig, pb, p_hi, lo, hi, thr, acc, ms_out, lo, K, S);
+        pfx_leaves<N, DMA, SIGP2, L, STATS>(base, sigma, rsig, pb, p_hi, lo, hi, thr, acc, ms_out, lo, K, S);
     acc = block_reduce(acc, sh);
     if (threadIdx.x == 0) parts[blockIdx.x] = acc;
 }
