@@ -460,6 +460,44 @@ struct FastSim {
         s1 += f1 ? 4 : 0;
     }
 
+    // ---- 1-DMA phase-specialized steps.  Once the XFER queue is past every
+    // HtD (s0 >= n4) step() has isH false, and K(s2) is always ready
+    // (s2 < n4 <= s0); once every K has finalized too the K lane stays idle
+    // and only the XFER lane (the DtH block) runs.  Same operations, same
+    // order, on the lanes that can run.
+    __device__ __forceinline__ void step_1d() {
+        static_assert(DMA == 1, "1-DMA only");
+        const int ps = s0 - n4;
+        const bool st0 = idle(r0) && s0 < 2 * n4 && s2 > ps;
+        const bool st2 = idle(r2) && s2 < n4;
+        k_idle_gap(st2);
+        start_if(st0, base + 512u + task_off<PRE>(seq, ps), d0, c0, r0);
+        start_if(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
+        const double dt = dmin(r0, r2);
+        now = __dadd_rn(now, dt);
+        r0 = upd(r0, dt, d0, c0);
+        r2 = upd(r2, dt, d2, c2);
+        const bool f0 = r0 <= kEndEps;
+        r0 = retire_or_drain(f0, r0, s0 + 4 >= 2 * n4);
+        s0 += f0 ? 4 : 0;
+        if (r2 <= kEndEps) {
+            r2 = retire(r2);
+            s2 += 4;
+            if constexpr (TRACK) kEnd = now;
+        }
+    }
+    __device__ __forceinline__ void step_1dd() {
+        static_assert(DMA == 1, "1-DMA only");
+        const bool st0 = idle(r0) && s0 < 2 * n4;
+        start_if(st0, base + 512u + task_off<PRE>(seq, s0 - n4), d0, c0, r0);
+        const double dt = r0;  // the only lane that can run (rem ~0 once drained)
+        now = __dadd_rn(now, dt);
+        r0 = upd(r0, dt, d0, c0);
+        const bool f0 = r0 <= kEndEps;
+        r0 = retire_or_drain(f0, r0, s0 + 4 >= 2 * n4);
+        s0 += f0 ? 4 : 0;
+    }
+
     // `rest` steps in warp lock-step, switching to the specialized steps as
     // soon as the whole warp has drained its HtD (then K) lanes
     __device__ __forceinline__ void run_phased(int rest, double sigma, double rsig) {
@@ -480,8 +518,20 @@ struct FastSim {
 #pragma unroll 2
             for (; st < rest; ++st) step_d();
         } else {
+#pragma unroll 1
+            for (; st < rest; st += 2) {
+                if (__all_sync(0xffffffffu, s0 >= n4)) break;
+                step(sigma, rsig);
+                step(sigma, rsig);
+            }
+#pragma unroll 1
+            for (; st < rest; st += 2) {
+                if (__all_sync(0xffffffffu, s2 >= n4)) break;
+                step_1d();
+                step_1d();
+            }
 #pragma unroll 2
-            for (; st < rest; ++st) step(sigma, rsig);
+            for (; st < rest; ++st) step_1dd();
         }
     }
 
