@@ -280,6 +280,8 @@ def run_ours(a):
         cpu = cpu_baseline(a.cpu_seconds)
         if secondary:
             secondary["cpu_port_c5_nvidia_decisions_per_s"] = cpu_heuristic_rate(4.0)
+    if secondary and D.world == 1:
+        secondary.update(run_rows(a, cpu=not a.no_cpu))
 
     if D.rank == 0:
         line = {
@@ -447,6 +449,86 @@ def run_secondary(a, D, torch, dev, sp, flush, ops, peak_ops, L):
                 "value": B5 * K / te, "unit": "TG decisions/s", "api": "_capi.heuristic_batch (pinned host buffers)",
                 "h2d_bytes_per_step": dh.nbytes + rh.nbytes, "d2h_bytes_per_step": B5 * (16 + 8 + 4)}
         del dd, rr, oo, mm, ns
+    return out
+
+
+# ---------------------------------------------------------------- rows f1, f3, f4
+def run_rows(a, cpu):
+    """SURVEY 8(f) rows through the public C-ABI wrappers with host buffers
+    (wall clock, best of 3 after a warm-up), each beside the CPU oracle on a
+    bounded sample when `cpu` (rank 0, N = 1: the cpu_baseline leg)."""
+    import ctypes as C
+
+    from paper_1806_10113_b200 import _capi, synth
+
+    def best(f, k=3):
+        f()
+        ts = []
+        for _ in range(k):
+            t0 = time.perf_counter()
+            f()
+            ts.append(time.perf_counter() - t0)
+        return min(ts)
+
+    out = {}
+    threads = os.cpu_count() or 1
+    # f1: NoReorder interleavings, 4 workers x 4 tasks (16!/(4!^4) = 63,063,000)
+    W, T = 4, 4
+    d1 = synth.real_group("K20", W * T, 41)[1]
+    tot1 = 63_063_000
+    t = best(lambda: _capi.interleavings(d1, W, T, 2, 0.5, 0, tot1))
+    out["f1_noreorder_interleavings_per_s"] = {
+        "value": tot1 / t, "unit": "interleavings/s",
+        "workload": "f1: all 63,063,000 interleavings of 4 workers x 4 in-order tasks (K20-style, 2-DMA, "
+                    "sigma 0.5) -> summary; osim_interleavings host call"}
+    # f3: proxy-thread scenario harness, 10^5 scenarios of 4 workers x 3 tasks
+    S3, W3, T3 = 100_000, 4, 3
+    d3 = np.stack([synth.real_group("K20", W3 * T3, 20_000 + s)[1] for s in range(2000)])
+    d3 = np.ascontiguousarray(np.tile(d3, (S3 // 2000, 1, 1)))
+    r3 = np.tile(np.argsort(np.argsort([f"w{w}.{j}" for w in range(W3) for j in range(T3)])).astype(np.uint8), (S3, 1))
+    sm = 1 if sys.version_info >= (3, 12) else 0
+    t = best(lambda: _capi.harness_batch(d3, r3, W3, T3, 2, 0.5, sm))
+    out["f3_harness_scenarios_per_s"] = {
+        "value": S3 / t, "unit": "scenarios/s",
+        "workload": "f3: 10^5 proxy-thread scenarios (4 workers x 3 tasks, K20-style, 2-DMA, sigma 0.5, "
+                    "Algorithm 1 per submitted group); osim_harness_batch host call"}
+    # f4: micro-step tick oracle, all 8! orderings of a config-2 group at dt = 1 us
+    d4 = synth.c2_batch(1)[0]
+    t = best(lambda: _capi.micro(d4, 2, 0.5, 0.001, 0, 40320), 2)
+    out["f4_micro_orderings_per_s"] = {
+        "value": 40320 / t, "unit": "orderings/s",
+        "workload": "f4: fixed-dt (1 us) tick simulation of all 8! orderings of a config-2 group "
+                    "(2-DMA, sigma 0.5); osim_micro host call"}
+    if cpu:
+        from oracle import oracle as O
+
+        m1 = 400_000
+        t0 = time.perf_counter()
+        O.interleavings(d1, W, T, 2, 0.5, 0, m1, threads=threads)
+        out["f1_noreorder_interleavings_per_s"]["cpu_port"] = {
+            "value": m1 / (time.perf_counter() - t0), "cores": threads,
+            "sample": f"interleavings [0, {m1}) through oracle_interleavings"}
+        L = O.lib()
+        L.oracle_harness.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_int,
+                                     C.c_double, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int),
+                                     C.POINTER(C.c_int)]
+        om, ong, osz = C.c_double(), C.c_int(), np.zeros(64, dtype=np.int32)
+        m3 = 2000
+        t0 = time.perf_counter()
+        for s_ in range(m3):
+            L.oracle_harness(d3[s_].ctypes.data_as(C.POINTER(C.c_double)),
+                             r3[s_].ctypes.data_as(C.POINTER(C.c_uint8)), W3, T3, 2, 0.5, sm, C.byref(om),
+                             C.byref(ong), osz.ctypes.data_as(C.POINTER(C.c_int)))
+        out["f3_harness_scenarios_per_s"]["cpu_port"] = {
+            "value": m3 / (time.perf_counter() - t0), "cores": 1,
+            "sample": f"{m3} scenarios through oracle_harness, one thread"}
+        m4 = 40
+        t0 = time.perf_counter()
+        for r_ in range(m4):
+            O.micro(d4, O.unrank(r_ * 1000, 8), 2, 0.5, 0.001)
+        out["f4_micro_orderings_per_s"]["cpu_port"] = {
+            "value": m4 / (time.perf_counter() - t0), "cores": 1,
+            "sample": f"{m4} orderings through oracle_micro, one thread"}
     return out
 
 
