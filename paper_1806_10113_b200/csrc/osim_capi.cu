@@ -939,7 +939,8 @@ int osim_interleavings(const double* durs, int T, int N, int dma, double sigma, 
     if (T < 1 || N < 1 || T * N > kMaxN) return fail(OSIM_EINVAL, "T*N must be in [1, %d]", kMaxN);
     int rc = check_common(T * N, dma, sigma);
     if (rc) return rc;
-    if ((rc = check_durs(durs, (uint64_t)(T * N)))) return rc;
+    int fast = 0;
+    if ((rc = scan_durs(durs, (uint64_t)(T * N), sigma, &fast))) return rc;
     if (!out) return fail(OSIM_EINVAL, "out is NULL");
     const uint64_t total = multinomial_total(T, N);
     if (rank_lo > rank_hi || rank_hi > total) return fail(OSIM_EINVAL, "rank range outside [0, %llu)",
@@ -971,7 +972,14 @@ int osim_interleavings(const double* durs, int T, int N, int dma, double sigma, 
         int g = 0;
         if (hi > lo) {
             const uint64_t blocks = (hi - lo + kBlock - 1) / kBlock;
-            if (dma == 2) {
+            if (dma == 2 && fast) {
+                auto k = sigma_pow2(sigma) ? (T * N <= 15 ? k_interleave_fast<true, true> : k_interleave_fast<true, false>)
+                                           : (T * N <= 15 ? k_interleave_fast<false, true> : k_interleave_fast<false, false>);
+                g = grid_for(k, kBlock, 0, c, blocks);
+                if (g > mp) g = mp;
+                k<<<g, kBlock, 0, c->stream>>>((double*)b, T, N, sigma, lo, hi, total, threshold,
+                                               (Part*)(b + off_parts), d_ms, c->d_err);
+            } else if (dma == 2) {
                 g = grid_for(k_interleave<2>, kBlock, 0, c, blocks);
                 if (g > mp) g = mp;
                 k_interleave<2><<<g, kBlock, 0, c->stream>>>((double*)b, T, N, sigma, lo, hi, total, threshold,

@@ -224,6 +224,73 @@ __global__ void __launch_bounds__(kBlock) k_interleave(const double* __restrict_
     if (threadIdx.x == 0) parts[blockIdx.x] = acc;
 }
 
+// Same unranking, also returning the packed NoReorder prerequisite of each
+// position (1 + position of the same worker's previous task, 0 for a
+// worker's first task).
+__device__ __forceinline__ uint64_t unrank_labels_dep(uint64_t r, int T, int N, uint64_t mtotal, uint64_t& dseq) {
+    int c[16], last[16];
+    for (int w = 0; w < T; ++w) { c[w] = N; last[w] = -1; }
+    int rem = T * N;
+    uint64_t M = mtotal;
+    uint64_t order = 0;
+    dseq = 0;
+    for (int p = 0; p < T * N; ++p) {
+        for (int w = 0; w < T; ++w) {
+            if (!c[w]) continue;
+            const uint64_t m = M / (uint64_t)rem * (uint64_t)c[w] + (M % (uint64_t)rem) * (uint64_t)c[w] / (uint64_t)rem;
+            if (r < m) {
+                order |= (uint64_t)(w * N + (N - c[w])) << (4 * p);
+                dseq |= (uint64_t)(last[w] + 1) << (4 * p);
+                last[w] = p;
+                --c[w];
+                --rem;
+                M = m;
+                break;
+            }
+            r -= m;
+        }
+    }
+    return order;
+}
+
+// Fast path of the NoReorder distribution (2-DMA, every stage non-null and
+// in the FastSim range): one thread per interleaving, FastSim with the
+// prerequisite gate, phase-specialized steps, Markstein division -- the
+// same op sequence as DepSim, so makespans are bit-identical.
+template <bool SIGP2, bool PRE>
+__global__ void __launch_bounds__(kBlock) k_interleave_fast(const double* __restrict__ durs, int T, int N,
+                                                            double sigma, uint64_t lo, uint64_t hi, uint64_t mtotal,
+                                                            double thr, Part* __restrict__ parts,
+                                                            double* __restrict__ ms_out, int* __restrict__ err) {
+    __shared__ double2 sdr[3 * kStride];
+    __shared__ Part sh[32];
+    const int n = T * N;
+    stage_dr(durs, n, sdr);
+    __syncthreads();
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
+    const double rsig = __ddiv_rn(1.0, sigma);
+    Part acc;
+    part_init(acc);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t b0 = lo + (uint64_t)blockIdx.x * blockDim.x; b0 < hi; b0 += stride) {
+        const uint64_t r = b0 + threadIdx.x;
+        const bool valid = r < hi;
+        uint64_t dseq;
+        const uint64_t order = unrank_labels_dep(valid ? r : lo, T, N, mtotal, dseq);
+        FastSim<2, SIGP2, false, PRE, true> s;
+        s.init(base, order, n);
+        s.dseq = PRE ? (dseq << 4) : dseq;
+        s.run_phased(3 * n, sigma, rsig);
+        if (valid) {
+            if (!s.drained()) atomicExch(err, OSIM_ESTALL);
+            part_add<true>(acc, s.now, r, thr);
+            if (ms_out) ms_out[r - lo] = s.now;
+        }
+    }
+    acc = block_reduce(acc, sh);
+    if (threadIdx.x == 0) parts[blockIdx.x] = acc;
+}
+
 template <int DMA>
 __global__ void __launch_bounds__(kBlock) k_eval_labels(const double* __restrict__ durs, int T, int N, double sigma,
                                                         const uint8_t* __restrict__ labels, uint64_t cnt,

@@ -369,10 +369,17 @@ __device__ __forceinline__ uint32_t task_off(uint64_t seq, int sh) {
     else return ((uint32_t)(seq >> sh) & 0xFu) << 4;
 }
 
-template <int DMA, bool SIGP2, bool TRACK, bool PRE>
+// DEPS (2-DMA only): each task may wait for a prerequisite task to finish
+// (engine.py:168-171, the NoReorder chains of workload.py:313-317); `dseq`
+// holds, per position, 1 + the prerequisite's position (0: none), packed
+// like `seq`.  With every stage non-null a task is finished exactly when its
+// DtH finalized, and DtHs finalize in sequence order, so the gate is one
+// extra condition on the HtD start: s1 >= 4 * (1 + prerequisite position).
+template <int DMA, bool SIGP2, bool TRACK, bool PRE, bool DEPS = false>
 struct FastSim {
     uint32_t base;
     uint64_t seq;   // packed ordering (pre-shifted by 4 when PRE)
+    uint64_t dseq;  // DEPS: packed 1 + prerequisite position (pre-shifted like seq)
     int n4;         // 4*n
     double now;
     double r0, r1, r2;  // 2-DMA: HtD, DtH, K;  1-DMA: XFER, -, K.  kBig = idle
@@ -547,7 +554,8 @@ struct FastSim {
         // ---- start phase (engine.py:188-194); readiness in the all-non-null
         // case: K(p) needs HtD(p) finalized, DtH(p) needs K(p) finalized
         if constexpr (DMA == 2) {
-            const bool st0 = idle(r0) && s0 < n4;
+            bool st0 = idle(r0) && s0 < n4;
+            if constexpr (DEPS) st0 = st0 && s1 >= (int)(task_off<PRE>(dseq, s0) >> 2);
             const bool st2 = idle(r2) && s2 < s0;
             const bool st1 = idle(r1) && s1 < s2;
             k_idle_gap(st2);

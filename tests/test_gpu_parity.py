@@ -440,6 +440,20 @@ def test_noreorder_large_space_vs_oracle():
         assert below == int((oms < 20.0).sum())
 
 
+def test_noreorder_fast_path_4x4_vs_oracle():
+    # 2-DMA, every stage non-null: the FastSim interleaving kernel (n = 16:
+    # unshifted packing); a 300k window of the 63,063,000 interleavings
+    d = synth.real_group("K20", 16, 41)[1]
+    lo, hi = 31_000_000, 31_300_000
+    cpus = os.cpu_count() or 4
+    for sigma in (0.5, 0.375):
+        s, below, ms = _capi.interleavings(d, 4, 4, 2, sigma, lo, hi, threshold=90.0, want_makespans=True)
+        o, oms = O.interleavings(d, 4, 4, 2, sigma, lo, hi, threads=cpus, makespans=True)
+        assert np.array_equal(ms, oms)
+        assert_summary_vs_oracle(s, o)
+        assert below == int((oms < 90.0).sum())
+
+
 def test_simulate_with_deps_dropin():
     p2 = osim.DeviceProfile("2dma", 2, 0.0, 1.0, 0.0, 1.0, overlap_sigma=0.5)
     p1 = osim.DeviceProfile("1dma", 1, 0.0, 1.0, 0.0, 1.0)
