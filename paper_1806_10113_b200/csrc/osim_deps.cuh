@@ -161,6 +161,13 @@ struct DepSim {
     }
 };
 
+// M(c - e_w) = M(c) * c_w / |c|: an exact integer below 2^53 (M <= 16!), so
+// one correctly rounded FP64 multiply and divide give it exactly -- far
+// cheaper than 64-bit integer division.
+__device__ __forceinline__ uint64_t mult_next(uint64_t M, int cw, int rem) {
+    return (uint64_t)__ddiv_rn(__dmul_rn((double)M, (double)cw), (double)rem);
+}
+
 // sorted(set(permutations(labels))) rank -> packed task order (task (w, j) =
 // w*N + j): multinomial unranking, M(c - e_w) = M(c) * c_w / |c| exactly.
 __device__ __forceinline__ uint64_t unrank_labels(uint64_t r, int T, int N, uint64_t mtotal) {
@@ -174,7 +181,7 @@ __device__ __forceinline__ uint64_t unrank_labels(uint64_t r, int T, int N, uint
     for (int p = 0; p < T * N; ++p) {
         for (int w = 0; w < T; ++w) {
             if (!c[w]) continue;
-            const uint64_t m = M / (uint64_t)rem * (uint64_t)c[w] + (M % (uint64_t)rem) * (uint64_t)c[w] / (uint64_t)rem;
+            const uint64_t m = mult_next(M, c[w], rem);
             if (r < m) {
                 order |= (uint64_t)(w * N + cnt[w]) << (4 * p);
                 ++cnt[w];
@@ -237,7 +244,7 @@ __device__ __forceinline__ uint64_t unrank_labels_dep(uint64_t r, int T, int N, 
     for (int p = 0; p < T * N; ++p) {
         for (int w = 0; w < T; ++w) {
             if (!c[w]) continue;
-            const uint64_t m = M / (uint64_t)rem * (uint64_t)c[w] + (M % (uint64_t)rem) * (uint64_t)c[w] / (uint64_t)rem;
+            const uint64_t m = mult_next(M, c[w], rem);
             if (r < m) {
                 order |= (uint64_t)(w * N + (N - c[w])) << (4 * p);
                 dseq |= (uint64_t)(last[w] + 1) << (4 * p);
