@@ -12,6 +12,7 @@
 namespace osim {
 
 constexpr double kMicroTol = 1e-9;  // _micro.py:16
+constexpr long long kMicroBurst = 1ll << 20;  // ticks per inner burst (runaway bound granularity)
 
 template <int DMA>
 struct MicroSim {
@@ -24,6 +25,7 @@ struct MicroSim {
     double rh, rd, rk;
     double t, ms;
     long long step;
+    long long ticks;  // ticks executed (the caller's runaway bound)
 
     __device__ __forceinline__ int skip(int p, unsigned nm) const {
         while (p < n && ((nm >> nib(seq, p)) & 1u)) ++p;
@@ -48,6 +50,7 @@ struct MicroSim {
         t = 0.0;
         ms = 0.0;
         step = 0;
+        ticks = 0;
     }
 
     // one tick; false once nothing can execute (the loop's break)
@@ -61,21 +64,32 @@ struct MicroSim {
         const bool ek = hk < n && ((doneH >> nib(seq, hk)) & 1u);
         if (!eh && !ed && !ek) return false;
         const double rate = (DMA == 2 && eh && ed) ? sigma : 1.0;
-        step += 1;
-        const double tick_end = __dmul_rn((double)step, dt);
-        if (eh) {
-            if (tl && tl->start[3 * nib(seq, hh) + 0] < 0.0) tl->start[3 * nib(seq, hh) + 0] = t;
-            rh = __dsub_rn(rh, __dmul_rn(dt, rate));
+        if (tl) {
+            if (eh && tl->start[3 * nib(seq, hh) + 0] < 0.0) tl->start[3 * nib(seq, hh) + 0] = t;
+            if (ed && tl->start[3 * nib(seq, hd) + 2] < 0.0) tl->start[3 * nib(seq, hd) + 2] = t;
+            if (ek && tl->start[3 * nib(seq, hk) + 1] < 0.0) tl->start[3 * nib(seq, hk) + 1] = t;
         }
-        if (ed) {
-            if (tl && tl->start[3 * nib(seq, hd) + 2] < 0.0) tl->start[3 * nib(seq, hd) + 2] = t;
-            rd = __dsub_rn(rd, __dmul_rn(dt, rate));
-        }
-        if (ek) {
-            if (tl && tl->start[3 * nib(seq, hk) + 1] < 0.0) tl->start[3 * nib(seq, hk) + 1] = t;
-            rk = __dsub_rn(rk, dt);
-        }
-        t = tick_end;
+        // Ticks up to the next finalization: the enabled lanes and the rate
+        // only change when a command finalizes, and t = step * dt is read
+        // only then, so the reference's per-tick `rem -= dt * rate` runs in a
+        // tight loop (same operations on the same values, tick by tick).
+        const double xt = __dmul_rn(dt, rate);
+        const double big = 0x1p1000;  // a lane that is not executing never finalizes
+        double ah = eh ? rh : big, ad = ed ? rd : big, ak = ek ? rk : big;
+        const double xh = eh ? xt : 0.0, xd = ed ? xt : 0.0, xk = ek ? dt : 0.0;
+        long long k = 0;
+        do {
+            ah = __dsub_rn(ah, xh);
+            ad = __dsub_rn(ad, xd);
+            ak = __dsub_rn(ak, xk);
+            ++k;
+        } while (ah > kMicroTol && ad > kMicroTol && ak > kMicroTol && k < kMicroBurst);
+        if (eh) rh = ah;
+        if (ed) rd = ad;
+        if (ek) rk = ak;
+        step += k;
+        ticks += k;
+        t = __dmul_rn((double)step, dt);
         if (eh && rh <= kMicroTol) {
             const int i = nib(seq, hh);
             if (tl) tl->end[3 * i + 0] = t;
@@ -115,9 +129,8 @@ __global__ void __launch_bounds__(kBlock) k_micro(const double* __restrict__ dur
     if (r >= hi) return;
     MicroSim<DMA> s;
     s.init(Durs{sd, sr, 1}, unrank_rt(r, n), n);
-    long long k = 0;
     while (s.tick(sigma, dt, nullptr))
-        if (++k > max_ticks) { atomicExch(err, OSIM_ESTALL); break; }
+        if (s.ticks > max_ticks) { atomicExch(err, OSIM_ESTALL); break; }
     ms_out[r - lo] = s.ms;
 }
 
@@ -135,9 +148,8 @@ __global__ void k_micro_timeline(const double* __restrict__ durs, int n, double 
     MicroSim<DMA> s;
     s.init(Durs{sd, sr, 1}, seq, n);
     TimelineOut tl{start, end};
-    long long k = 0;
     while (s.tick(sigma, dt, &tl))
-        if (++k > max_ticks) { *err = OSIM_ESTALL; return; }
+        if (s.ticks > max_ticks) { *err = OSIM_ESTALL; return; }
     res[0] = s.ms;
 }
 
