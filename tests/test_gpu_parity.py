@@ -661,3 +661,45 @@ def test_heuristic_large_batch_device_validation_and_fallback():
     order, ms, _ = _capi.heuristic_batch(d[:1000], r[:1000], 2, 0.5, osim.SUM_MODE)
     oo, om, _ = O.reorder_batch(d[:1000], r[:1000], 2, 0.5, osim.SUM_MODE, threads=8)
     assert np.array_equal(order, oo) and np.array_equal(ms, om)
+
+
+def _gpu_shard_worker(rank, world, port, q):
+    import torch.distributed as tdist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1806_10113_b200.dist import exhaustive_summary_distributed
+
+        s = exhaustive_summary_distributed(synth.c3_group(), 2, 0.5)  # shard on cuda:0 via the library
+        q.put((rank, s.best, s.best_ordering, s.worst, s.mean, s.geomean))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_two_rank_shards_through_the_library_combine_exactly():
+    # the N>1 path's sharding and combine with real GPU shards: two ranks
+    # (gloo for the 48-byte exchange) each reduce their half of 10! on the
+    # device independently; no rank waits on another's kernels
+    import socket
+
+    import torch.multiprocessing as mp
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gpu_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    whole = osim.exhaustive_summary_durs(synth.c3_group(), 2, 0.5)
+    for _, best, order, worst, mean, geo in res:
+        assert best == whole.best and tuple(order) == tuple(whole.best_ordering) and worst == whole.worst
+        assert close(mean, whole.mean, REL) and close(geo, whole.geomean, REL)
