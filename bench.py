@@ -248,7 +248,9 @@ def run_ours(a):
                            "flops/DFMA), i.e. FP64-pipe issue capacity in ops/s" % (ops_per, peak_tflops)),
             "kernel": "k_exhaustive_pfx<12,2,sigma-pow2,L=4>", "launch_ms": kern_avg * 1e3,
             "ncu_executed": {k: v for k, v in profile_headline().items()
-                             if k in ("issue_active_pct", "fp64_pipe_active_pct", "warp_exec_efficiency", "source")}}
+                             if k in ("issue_active_pct", "fp64_pipe_active_pct", "alu_pipe_active_pct",
+                                      "warp_exec_efficiency", "achieved_occupancy_pct",
+                                      "theoretical_occupancy_pct", "source")}}
 
     # ---- e2e through the public API (host buffers) ---------------------------
     e2e_steps = max(3, a.steps // 2)

@@ -25,6 +25,9 @@ KEYS = [
     "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__maximum_warps_per_active_cycle_pct",
 ]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
@@ -54,8 +57,13 @@ def main(rep, out, label, headline=False):
                    "issue_active_pct": float(k["sm__inst_issued.avg.pct_of_peak_sustained_active"].split()[0]),
                    "fp64_pipe_active_pct": float(
                        k["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"].split()[0]),
+                   "alu_pipe_active_pct": float(
+                       k["sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"].split()[0]),
                    "warp_exec_efficiency": float(
                        k["smsp__thread_inst_executed_per_inst_executed.ratio"].split()[0]) / 32,
+                   "achieved_occupancy_pct": float(
+                       k["sm__warps_active.avg.pct_of_peak_sustained_active"].split()[0]),
+                   "theoretical_occupancy_pct": float(k["sm__maximum_warps_per_active_cycle_pct"].split()[0]),
                    "source": out}, open("profiles/ncu_headline.json", "w"), indent=1)
     print(json.dumps(kernels, indent=1)[:3000])
 
