@@ -703,3 +703,20 @@ def test_two_rank_shards_through_the_library_combine_exactly():
     for _, best, order, worst, mean, geo in res:
         assert best == whole.best and tuple(order) == tuple(whole.best_ordering) and worst == whole.worst
         assert close(mean, whole.mean, REL) and close(geo, whole.geomean, REL)
+
+
+def test_sigma_at_the_fast_range_boundary():
+    # sigma = 2^-60 is the smallest fast-path sigma; just below it the
+    # general (IEEE division) path runs; both bit-exact with the oracle
+    rng = np.random.default_rng(17)
+    d = rng.uniform(0.5, 4.0, (6, 3))
+    r = np.arange(6, dtype=np.uint8)
+    for sigma in (2.0 ** -60, np.nextafter(2.0 ** -60, 0.0), 1e-20, 2.0 ** -59 * 3):
+        assert _capi.fast_eligible(d, sigma) == (sigma >= 2.0 ** -60)
+        s, ms = _capi.exhaustive(d, 2, sigma, 0, 720, want_makespans=True)
+        o, oms = O.exhaustive(d, 2, sigma, makespans=True)
+        assert np.array_equal(ms, oms)
+        assert_summary_vs_oracle(s, o)
+        order, hm, sims = _capi.heuristic_batch(d[None], r[None], 2, sigma, osim.SUM_MODE)
+        oo, om, osims = O.reorder(d, r, 2, sigma, osim.SUM_MODE)
+        assert order[0].tolist() == oo and hm[0] == om
