@@ -18,6 +18,7 @@
 #include "osim_launch.cuh"
 #include "osim_micro.cuh"
 #include "osim_harness.cuh"
+#include "osim_null.cuh"
 
 using namespace osim;
 
@@ -246,8 +247,15 @@ int enqueue_exhaustive(DevCtx* c, cudaStream_t st, const double* d_durs, int n, 
     int g = 1;
     int rc = 0;
     if (hi > lo) {
-        if (fast) {
+        if (fast == 1) {
             rc = launch_exh_fast_dispatch(dma, n, c, st, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, &g);
+        } else if (fast == 2) {  // null stages in the fast range: NullSim
+            uint64_t blocks = (hi - lo + kBlock - 1) / kBlock;
+            auto k = dma == 2 ? (sigma_pow2(sigma) ? k_exhaustive_null<2, true> : k_exhaustive_null<2, false>)
+                              : k_exhaustive_null<1, false>;
+            g = grid_for(k, kBlock, 0, c, blocks);
+            if (g > max_parts) g = max_parts;
+            k<<<g, kBlock, 0, st>>>(d_durs, n, sigma, lo, hi, thr, parts, d_ms, c->d_err);
         } else {
             uint64_t blocks = (hi - lo + kBlock - 1) / kBlock;
             if (dma == 2) {
@@ -310,6 +318,15 @@ int finish(DevCtx* c, cudaStream_t st) {
         return fail(h_err, "simulation stalled with commands pending");
     }
     return 0;
+}
+
+// Null stages allowed: every stage 0 or in the FastSim range (NullSim path).
+bool null_fast_ok(const double* durs, uint64_t tasks, double sigma) {
+    const double lo = std::ldexp(1.0, -60), hi = std::ldexp(1.0, 22);
+    if (!(sigma >= lo)) return false;
+    for (uint64_t i = 0; i < 3 * tasks; ++i)
+        if (!(durs[i] == 0.0 || (durs[i] >= lo && durs[i] < hi))) return false;
+    return true;
 }
 
 bool fast_ok(const double* durs, uint64_t tasks, double sigma) {
@@ -455,7 +472,7 @@ int osim_exhaustive(const double* durs, int n, int dma, double sigma, uint64_t r
                     (unsigned long long)rank_hi, (unsigned long long)total);
     DevList dl;
     if ((rc = pick_devs(n_dev, dl))) return rc;
-    const int fast = fast_ok(durs, n, sigma);
+    const int fast = fast_ok(durs, n, sigma) ? 1 : (null_fast_ok(durs, n, sigma) ? 2 : 0);
     const int G = (int)dl.v.size();
     const uint64_t span = rank_hi - rank_lo;
     std::vector<osim_summary> res(G);
@@ -525,7 +542,7 @@ int osim_exhaustive_stats(const double* durs, int n, int dma, double sigma, uint
     if (rank_lo > rank_hi || rank_hi > total) return fail(OSIM_EINVAL, "bad rank range");
     DevList dl;
     if ((rc = pick_devs(n_dev, dl))) return rc;
-    const int fast = fast_ok(durs, n, sigma);
+    const int fast = fast_ok(durs, n, sigma) ? 1 : (null_fast_ok(durs, n, sigma) ? 2 : 0);
     const int G = (int)dl.v.size();
     const uint64_t span = rank_hi - rank_lo;
     std::vector<osim_summary> res(G);

@@ -720,3 +720,22 @@ def test_sigma_at_the_fast_range_boundary():
         order, hm, sims = _capi.heuristic_batch(d[None], r[None], 2, sigma, osim.SUM_MODE)
         oo, om, osims = O.reorder(d, r, 2, sigma, osim.SUM_MODE)
         assert order[0].tolist() == oo and hm[0] == om
+
+
+@pytest.mark.parametrize("n", [4, 7, 10, 12])
+def test_null_stage_fast_path_vs_oracle(n):
+    # every stage either 0 (no command) or in the fast range: NullSim path
+    rng = np.random.default_rng(400 + n)
+    d = rng.uniform(0.1, 5.0, (n, 3))
+    d[rng.random((n, 3)) < 0.25] = 0.0
+    for t in range(n):  # a task keeps at least one command
+        if not d[t].any():
+            d[t, 1] = 1.5
+    total = math.factorial(n)
+    lo, hi = (0, total) if total <= 400_000 else (total // 3, total // 3 + 400_000)
+    assert not _capi.fast_eligible(d, 0.5)
+    for dma, sigma in ((2, 0.5), (2, 0.375), (1, 1.0)):
+        s, ms = _capi.exhaustive(d, dma, sigma, lo, hi, want_makespans=True)
+        o, oms = O.exhaustive(d, dma, sigma, lo, hi, threads=os.cpu_count() or 4, makespans=True)
+        assert np.array_equal(ms, oms), (n, dma, sigma)
+        assert_summary_vs_oracle(s, o)
