@@ -249,13 +249,10 @@ int enqueue_exhaustive(DevCtx* c, cudaStream_t st, const double* d_durs, int n, 
     if (hi > lo) {
         if (fast == 1) {
             rc = launch_exh_fast_dispatch(dma, n, c, st, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, &g);
-        } else if (fast == 2) {  // null stages in the fast range: NullSim
-            uint64_t blocks = (hi - lo + kBlock - 1) / kBlock;
-            auto k = dma == 2 ? (sigma_pow2(sigma) ? k_exhaustive_null<2, true> : k_exhaustive_null<2, false>)
-                              : k_exhaustive_null<1, false>;
-            g = grid_for(k, kBlock, 0, c, blocks);
-            if (g > max_parts) g = max_parts;
-            k<<<g, kBlock, 0, st>>>(d_durs, n, sigma, lo, hi, thr, parts, d_ms, c->d_err);
+        } else if (fast == 2) {  // null stages in the fast range: NullSim with prefix sharing
+            if (null_pfx_launch(n, dma, sigma_pow2(sigma), LaunchCfg{c->sms, st}, d_durs, sigma, lo, hi, thr, parts,
+                                max_parts, d_ms, c->d_err, &g))
+                return fail(OSIM_EINVAL, "unsupported n=%d", n);
         } else {
             uint64_t blocks = (hi - lo + kBlock - 1) / kBlock;
             if (dma == 2) {

@@ -61,6 +61,11 @@ int batch_fast_launch_d2(int n, int L, bool sp2, const LaunchCfg& cfg, const dou
 int batch_fast_launch_d1(int n, int L, const LaunchCfg& cfg, const double* d_durs, uint64_t B, double sigma,
                          osim_summary* d_out);
 
+// exhaustive search with null stages in the fast range (osim_null.cu):
+// prefix sharing with the prefix-world checkpoint, L = default_pfx_l(n)
+int null_pfx_launch(int n, int dma, bool sp2, const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo,
+                    uint64_t hi, double thr, Part* parts, int max_parts, double* d_ms, int* d_err, int* g);
+
 void heuristic_launch(int dma, bool fast, const LaunchCfg& cfg, const double* d_durs, const uint8_t* d_idr,
                       uint64_t B, int n, double sigma, int sum_mode, uint8_t* d_order, double* d_ms,
                       uint32_t* d_ns, int* d_err);

@@ -142,43 +142,113 @@ struct NullSim {
     }
 };
 
-// Exhaustive search over lexicographic ranks [lo, hi) with null stages in the
-// fast range: one thread per ordering from time 0.
+// ---------------------------------------------------------------------------
+// Prefix sharing with null stages.  With nulls a suffix command can start
+// before the HtD lane reaches position M (K(M) is ready at once if HtD(M) is
+// null), so the checkpoint is taken in a prefix-only world (the first M
+// positions): the state is prefix-determined up to the first step whose
+// start phase finds some lane idle with its head at or past M -- only then
+// could a position >= M command start.  Replaying a suffix restores every
+// lane, rebuilds the position null masks for the full ordering, and moves
+// each head that sat at M to the first non-null slot >= M of the full
+// ordering (1-DMA: the prefix world's XFER slot M is the full world's HtD(M)).
+// ---------------------------------------------------------------------------
 template <int DMA, bool SIGP2>
-__global__ void __launch_bounds__(kBlock) k_exhaustive_null(const double* __restrict__ durs, int n, double sigma,
-                                                            uint64_t lo, uint64_t hi, double thr,
-                                                            Part* __restrict__ parts, double* __restrict__ ms_out,
-                                                            int* __restrict__ err) {
+__device__ __forceinline__ bool null_at_ck(const NullSim<DMA, SIGP2>& s) {
+    const bool a = idle(s.r0) && s.s0 >= s.n4;  // 1-DMA prefix world: XFER at its DtH part
+    const bool c = idle(s.r2) && s.s2 >= s.n4;
+    if constexpr (DMA == 2) return a || c || (idle(s.r1) && s.s1 >= s.n4);
+    else return a || c;
+}
+
+struct NullCk {  // structure-of-arrays checkpoint slots (conflict-free)
+    double v[10][kBlock];  // now, r0, r1, r2, d0, d1, d2, c0, c1, c2
+    int h[3][kBlock];      // s0, s1, s2 (prefix-world heads)
+};
+
+template <int N, int DMA, bool SIGP2, int L>
+__global__ void __launch_bounds__(kBlock) k_exhaustive_null_pfx(const double* __restrict__ durs, double sigma,
+                                                                uint64_t lo, uint64_t hi, double thr,
+                                                                Part* __restrict__ parts,
+                                                                double* __restrict__ ms_out,
+                                                                int* __restrict__ err) {
+    constexpr int M = N - L;
+    constexpr uint64_t LF = Fact<L>::v;
     __shared__ double2 sdr[3 * kStride];
     __shared__ Part sh[32];
-    stage_dr(durs, n, sdr);
+    __shared__ NullCk K;
+    stage_dr(durs, N, sdr);
     __syncthreads();
     unsigned tH = 0, tK = 0, tD = 0;
-    for (int t = 0; t < n; ++t) {
+    for (int t = 0; t < N; ++t) {
         tH |= (sdr[t].x > 0.0 ? 0u : 1u) << t;
         tK |= (sdr[kStride + t].x > 0.0 ? 0u : 1u) << t;
         tD |= (sdr[2 * kStride + t].x > 0.0 ? 0u : 1u) << t;
     }
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
     const double rsig = __ddiv_rn(1.0, sigma);
+    const int ti = threadIdx.x;
+    const uint64_t p_lo = lo / LF, p_hi = (hi + LF - 1) / LF;
     Part acc;
     part_init(acc);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t b0 = lo + (uint64_t)blockIdx.x * blockDim.x; b0 < hi; b0 += stride) {
-        const uint64_t r = b0 + threadIdx.x;
-        const bool valid = r < hi;
+    for (uint64_t pb = p_lo + (uint64_t)blockIdx.x * blockDim.x; pb < p_hi; pb += stride) {
+        const uint64_t P = pb + ti;
+        const bool validP = P < p_hi;
+        const uint64_t seq0 = unrank<N>((validP ? P : p_lo) * LF);
         NullSim<DMA, SIGP2> s;
-        s.init(base, unrank_rt(valid ? r : lo, n), n, tH, tK, tD);
+        // ---- phase A in the prefix-only world
+        s.init(base, seq0, M, tH, tK, tD);
+        int sa = 0;
 #pragma unroll 1
-        for (int st = 0; st < 3 * n; st += 2) {
-            if (__all_sync(kFull, s.drained())) break;
-            s.step(sigma, rsig);
-            s.step(sigma, rsig);
+        while (__any_sync(kFull, !null_at_ck(s) && sa < 3 * N)) {
+            if (!null_at_ck(s) && sa < 3 * N) {
+                s.step(sigma, rsig);
+                ++sa;
+            }
         }
-        if (valid) {
-            if (!s.drained()) atomicExch(err, OSIM_ESTALL);
-            part_add<true>(acc, s.now, r, thr);
-            if (ms_out) ms_out[r - lo] = s.now;
+        K.v[0][ti] = s.now; K.v[1][ti] = s.r0; K.v[2][ti] = s.r1; K.v[3][ti] = s.r2;
+        K.v[4][ti] = s.d0; K.v[5][ti] = s.d1; K.v[6][ti] = s.d2;
+        K.v[7][ti] = s.c0; K.v[8][ti] = s.c1; K.v[9][ti] = s.c2;
+        K.h[0][ti] = s.s0; K.h[1][ti] = s.s1; K.h[2][ti] = s.s2;
+        const uint64_t pre = seq0 & ((1ull << (4 * M)) - 1ull);
+        const uint64_t rem = seq0 >> (4 * M);
+        const int rest = 3 * N - __reduce_min_sync(kFull, validP ? sa : 3 * N);
+#pragma unroll 1
+        for (int j = 0; j < (int)LF; ++j) {
+            uint64_t idx;
+            if constexpr (L >= 4) idx = suf_tab<L>(j);
+            else idx = unrank<L>((uint64_t)j);
+            uint64_t suf = 0;
+#pragma unroll
+            for (int i = 0; i < L; ++i)
+                suf |= ((rem >> (4 * ((idx >> (4 * i)) & 0xF))) & 0xFull) << (4 * (M + i));
+            // ---- restore into the full world
+            s.init(base, pre | suf, N, tH, tK, tD);  // full-ordering masks; heads reset below
+            s.now = K.v[0][ti]; s.r0 = K.v[1][ti]; s.r1 = K.v[2][ti]; s.r2 = K.v[3][ti];
+            s.d0 = K.v[4][ti]; s.d1 = K.v[5][ti]; s.d2 = K.v[6][ti];
+            s.c0 = K.v[7][ti]; s.c1 = K.v[8][ti]; s.c2 = K.v[9][ti];
+            const int h0 = K.h[0][ti], h1 = K.h[1][ti], h2 = K.h[2][ti];
+            constexpr int M4 = 4 * M;
+            if constexpr (DMA == 2) {
+                s.s0 = h0 >= M4 ? NullSim<DMA, SIGP2>::next(s.mH, M4 - 4, N) : h0;
+                s.s1 = h1 >= M4 ? NullSim<DMA, SIGP2>::next(s.mX, M4 - 4, N) : h1;
+            } else {
+                s.s0 = h0 >= M4 ? NullSim<DMA, SIGP2>::next(s.mX, M4 - 4, 2 * N) : h0;
+            }
+            s.s2 = h2 >= M4 ? NullSim<DMA, SIGP2>::next(s.mK, M4 - 4, N) : h2;
+#pragma unroll 1
+            for (int st = 0; st < rest; st += 2) {
+                if (__all_sync(kFull, s.drained())) break;
+                s.step(sigma, rsig);
+                s.step(sigma, rsig);
+            }
+            const uint64_t r = P * LF + (uint64_t)j;
+            if (validP && r >= lo && r < hi) {
+                if (!s.drained()) atomicExch(err, OSIM_ESTALL);
+                part_add<true>(acc, s.now, r, thr);
+                if (ms_out) ms_out[r - lo] = s.now;
+            }
         }
     }
     acc = block_reduce(acc, sh);

@@ -722,7 +722,7 @@ def test_sigma_at_the_fast_range_boundary():
         assert order[0].tolist() == oo and hm[0] == om
 
 
-@pytest.mark.parametrize("n", [4, 7, 10, 12])
+@pytest.mark.parametrize("n", [4, 7, 10, 12, 14, 16])
 def test_null_stage_fast_path_vs_oracle(n):
     # every stage either 0 (no command) or in the fast range: NullSim path
     rng = np.random.default_rng(400 + n)
