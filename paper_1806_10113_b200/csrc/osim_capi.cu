@@ -119,12 +119,13 @@ int check_common(int n, int dma, double sigma) {
 struct ScanPart {
     uint64_t bad = ~0ull;
     int why = 0;  // 1 = negative / non-finite, 2 = no commands
-    bool fast = true;
+    bool fast = true;   // every stage in the FastSim range
+    bool nfast = true;  // every stage 0 or in the FastSim range (NullSim)
 };
 
 void scan_range(const double* d, uint64_t t0, uint64_t t1, ScanPart& r) {
     const double lo = 0x1p-60, hi = 0x1p22;  // see kFastHi (osim_sim.cuh)
-    bool fast = true;
+    bool fast = true, nfast = true;
     for (uint64_t t = t0; t < t1; ++t) {
         const double h = d[3 * t], k = d[3 * t + 1], x = d[3 * t + 2];
         if (!(h >= 0.0 && k >= 0.0 && x >= 0.0 && h <= 1.7976931348623157e308 && k <= 1.7976931348623157e308 &&
@@ -133,8 +134,11 @@ void scan_range(const double* d, uint64_t t0, uint64_t t1, ScanPart& r) {
         }
         if (h <= 0 && k <= 0 && x <= 0) { r.bad = t; r.why = 2; break; }
         fast = fast && h >= lo && h < hi && k >= lo && k < hi && x >= lo && x < hi;
+        nfast = nfast && (h == 0.0 || (h >= lo && h < hi)) && (k == 0.0 || (k >= lo && k < hi)) &&
+                (x == 0.0 || (x >= lo && x < hi));
     }
     r.fast = fast;
+    r.nfast = nfast;
 }
 
 int scan_durs(const double* durs, uint64_t tasks, double sigma, int* fast) {
@@ -151,7 +155,7 @@ int scan_durs(const double* durs, uint64_t tasks, double sigma, int* fast) {
             th.emplace_back(scan_range, durs, tasks * i / nt, tasks * (i + 1) / nt, std::ref(parts[i]));
         for (auto& t : th) t.join();
     }
-    bool f = sigma >= 0x1p-60;
+    bool f = sigma >= 0x1p-60, nf = f;
     for (const ScanPart& p : parts) {
         if (p.bad != ~0ull) {
             if (p.why == 1)
@@ -160,8 +164,10 @@ int scan_durs(const double* durs, uint64_t tasks, double sigma, int* fast) {
             return fail(OSIM_EINVAL, "task %llu has no commands", (unsigned long long)p.bad);
         }
         f = f && p.fast;
+        nf = nf && p.nfast;
     }
-    if (fast) *fast = f ? 1 : 0;
+    // 1: FastSim path; 2: null stages in the fast range (NullSim); 0: general
+    if (fast) *fast = f ? 1 : (nf ? 2 : 0);
     return 0;
 }
 
@@ -280,8 +286,12 @@ int enqueue_batch(DevCtx* c, cudaStream_t st, const double* d_durs, uint64_t B, 
                   double sigma, int fast, osim_summary* d_out) {
     if (B == 0) return 0;
     int rc = 0;
-    if (fast) {
+    if (fast == 1) {
         rc = launch_batch_fast_dispatch(dma, n, c, st, d_durs, B, sigma, d_out);
+    } else if (fast == 2) {
+        int g = 0;
+        if (null_batch_launch(n, dma, sigma_pow2(sigma), LaunchCfg{c->sms, st}, d_durs, B, sigma, d_out, c->d_err, &g))
+            return fail(OSIM_EINVAL, "unsupported n=%d", n);
     } else if (dma == 2) {
         int g = grid_for(k_exhaustive_batch_gen<2>, kBlock, 0, c, B);
         k_exhaustive_batch_gen<2><<<g, kBlock, 0, st>>>(d_durs, B, n, sigma, d_out, c->d_err);
@@ -986,7 +996,7 @@ int osim_interleavings(const double* durs, int T, int N, int dma, double sigma, 
         int g = 0;
         if (hi > lo) {
             const uint64_t blocks = (hi - lo + kBlock - 1) / kBlock;
-            if (dma == 2 && fast) {
+            if (dma == 2 && fast == 1) {
                 auto k = sigma_pow2(sigma) ? (T * N <= 15 ? k_interleave_fast<true, true> : k_interleave_fast<true, false>)
                                            : (T * N <= 15 ? k_interleave_fast<false, true> : k_interleave_fast<false, false>);
                 g = grid_for(k, kBlock, 0, c, blocks);

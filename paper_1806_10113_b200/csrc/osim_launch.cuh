@@ -66,6 +66,9 @@ int batch_fast_launch_d1(int n, int L, const LaunchCfg& cfg, const double* d_dur
 int null_pfx_launch(int n, int dma, bool sp2, const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo,
                     uint64_t hi, double thr, Part* parts, int max_parts, double* d_ms, int* d_err, int* g);
 
+int null_batch_launch(int n, int dma, bool sp2, const LaunchCfg& cfg, const double* d_durs, uint64_t B, double sigma,
+                      osim_summary* d_out, int* d_err, int* g);
+
 void heuristic_launch(int dma, bool fast, const LaunchCfg& cfg, const double* d_durs, const uint8_t* d_idr,
                       uint64_t B, int n, double sigma, int sum_mode, uint8_t* d_order, double* d_ms,
                       uint32_t* d_ns, int* d_err);

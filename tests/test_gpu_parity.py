@@ -739,3 +739,19 @@ def test_null_stage_fast_path_vs_oracle(n):
         o, oms = O.exhaustive(d, dma, sigma, lo, hi, threads=os.cpu_count() or 4, makespans=True)
         assert np.array_equal(ms, oms), (n, dma, sigma)
         assert_summary_vs_oracle(s, o)
+
+
+@pytest.mark.parametrize("n", [7, 8])
+def test_batch_null_stages_vs_oracle(n):
+    # batched groups with null stages in the fast range: one CTA per group, NullSim
+    rng = np.random.default_rng(500 + n)
+    B = 64
+    d = rng.uniform(0.1, 5.0, (B, n, 3))
+    d[rng.random((B, n, 3)) < 0.2] = 0.0
+    d[(d == 0).all(axis=2), 1] = 2.0
+    cpus = os.cpu_count() or 4
+    for dma, sigma in ((2, 0.5), (2, 0.375), (1, 1.0)):
+        out = _capi.exhaustive_batch(d, dma, sigma)
+        for b in range(0, B, 3):
+            o, _ = O.exhaustive(d[b], dma, sigma, threads=cpus)
+            assert_summary_vs_oracle({k: out[b][k].item() for k in out.dtype.names}, o)
