@@ -755,3 +755,27 @@ def test_batch_null_stages_vs_oracle(n):
         for b in range(0, B, 3):
             o, _ = O.exhaustive(d[b], dma, sigma, threads=cpus)
             assert_summary_vs_oracle({k: out[b][k].item() for k in out.dtype.names}, o)
+
+
+def test_concurrent_host_calls_from_threads():
+    # ctypes releases the GIL: several Python threads drive the library at
+    # once; the per-device mutex keeps scratch/streams consistent
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.default_rng(23)
+    groups = [rng.uniform(0.2, 4.0, (9, 3)) for _ in range(8)]
+    expect = [_capi.exhaustive(g, 2, 0.5, 0, 362880)[0] for g in groups]
+    hd, hr = synth.c5_batch_fast("amd", 4096, seed=5)
+    h_expect = _capi.heuristic_batch(hd, hr, 2, 0.375, osim.SUM_MODE)
+
+    def work(i):
+        if i % 3 == 2:
+            o, m, s_ = _capi.heuristic_batch(hd, hr, 2, 0.375, osim.SUM_MODE)
+            return ("h", np.array_equal(o, h_expect[0]) and np.array_equal(m, h_expect[1]))
+        g = i % len(groups)
+        s, _ = _capi.exhaustive(groups[g], 2, 0.5, 0, 362880)
+        return ("e", s == expect[g])
+
+    with ThreadPoolExecutor(6) as ex:
+        res = list(ex.map(work, range(36)))
+    assert all(ok for _, ok in res)
