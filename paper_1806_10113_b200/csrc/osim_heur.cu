@@ -11,10 +11,11 @@ void heuristic_launch(int dma, bool fast, const LaunchCfg& cfg, const double* d_
     const unsigned grid = (unsigned)((B + kHG - 1) / kHG);
     const size_t sm = sizeof(HeurShared);
     if (fast) {
+        const unsigned gridf = (unsigned)((B + kHGF - 1) / kHGF);
         int e;
         const bool sp2 = std::frexp(sigma, &e) == 0.5;
 #define OSIM_HF(D, P)                                                                                       \
-    k_heuristic_fast<D, P><<<grid, kHT, kWPB * sizeof(HeurWarpShared<D, P>), cfg.st>>>(d_durs, d_idr, B, n, sigma, \
+    k_heuristic_fast<D, P><<<gridf, kHTF, kWPB * sizeof(HeurWarpShared<D, P>), cfg.st>>>(d_durs, d_idr, B, n, sigma, \
                                                                                  sum_mode, d_order, d_ms, d_ns)
         if (dma == 2) { if (sp2) OSIM_HF(2, true); else OSIM_HF(2, false); }
         else OSIM_HF(1, false);

@@ -923,10 +923,16 @@ __global__ void __launch_bounds__(kHT) k_heuristic(const double* __restrict__ du
 // makespan of the chosen ordering.  Per-simulation operation sequences are
 // unchanged, so every estimate, idle time and makespan is bit-identical.
 // ---------------------------------------------------------------------------
-constexpr int kWG = 8;                 // groups per warp
+#ifndef OSIM_HWG
+#define OSIM_HWG 8
+#endif
+constexpr int kWG = OSIM_HWG;          // groups per warp
+constexpr int kLPG = 32 / kWG;         // lanes per group in the key argmin
 constexpr int kKeyN = kMaxN - 1;       // candidates per greedy round (n - k, k >= 1)
-constexpr int kWPB = 4;                // warps per CTA (kHT threads)
-static_assert(kWG * kWPB == kHG, "groups per CTA");
+constexpr int kWPB = 32 / kWG;         // warps per CTA
+constexpr int kHGF = kWG * kWPB;       // groups per CTA (fast kernel)
+constexpr int kHTF = 32 * kWPB;        // threads per CTA (fast kernel)
+static_assert(kLPG * kWG == 32 && kWG <= 16, "groups per warp");
 
 template <int DMA, bool SP2>
 struct HeurWarpShared {
@@ -952,7 +958,7 @@ __device__ __forceinline__ bool key_less(double e, double d, int r, double be, d
 }
 
 template <int DMA, bool SP2>
-__global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict__ durs,
+__global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restrict__ durs,
                                                         const uint8_t* __restrict__ id_rank, uint64_t B, int n,
                                                         double sigma, int sum_mode,
                                                         uint8_t* __restrict__ order_out,
@@ -1065,30 +1071,30 @@ __global__ void __launch_bounds__(kHT) k_heuristic_fast(const double* __restrict
             }
         }
         __syncwarp();
-        // argmin of the key over the m candidates: 4 lanes per group, each
-        // scanning every 4th candidate, then a 2-level shuffle reduction
+        // argmin of the key over the m candidates: kLPG lanes per group, each
+        // scanning every kLPG-th candidate, then a shuffle reduction
         // (the key is a strict total order, so the tree order is immaterial)
         int bj;
         {
-            const int g = lane >> 2, part = lane & 3;
+            const int g = lane / kLPG, part = lane % kLPG;
             int lj = -1;
             double le = 0, ld = 0;
             int lr = 0;
             if (g < Gv) {
-                for (int j = part; j < m; j += 4) {
+                for (int j = part; j < m; j += kLPG) {
                     const double e = S.ka[g * kKeyN + j], d = S.kb[g * kKeyN + j];
                     const int r = S.idr[g * kMaxN + S.cand[g * kMaxN + j]];
                     if (lj < 0 || key_less(e, d, r, le, ld, lr)) { lj = j; le = e; ld = d; lr = r; }
                 }
             }
 #pragma unroll
-            for (int off = 1; off <= 2; off <<= 1) {
+            for (int off = 1; off < kLPG; off <<= 1) {
                 const int oj = __shfl_xor_sync(kFull, lj, off);
                 const double oe = __shfl_xor_sync(kFull, le, off), od = __shfl_xor_sync(kFull, ld, off);
                 const int orr = __shfl_xor_sync(kFull, lr, off);
                 if (oj >= 0 && (lj < 0 || key_less(oe, od, orr, le, ld, lr))) { lj = oj; le = oe; ld = od; lr = orr; }
             }
-            bj = __shfl_sync(kFull, lj, (lane & 7) << 2);  // group `lane` (< 8) result
+            bj = __shfl_sync(kFull, lj, (lane % kWG) * kLPG);  // group `lane` (< kWG) result
         }
         if (lane < Gv) {
             const int g = lane;
