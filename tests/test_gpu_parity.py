@@ -722,12 +722,13 @@ def test_sigma_at_the_fast_range_boundary():
         assert order[0].tolist() == oo and hm[0] == om
 
 
-@pytest.mark.parametrize("n", [4, 7, 10, 12, 14, 16])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 7, 10, 12, 14, 16])
 def test_null_stage_fast_path_vs_oracle(n):
     # every stage either 0 (no command) or in the fast range: NullSim path
     rng = np.random.default_rng(400 + n)
     d = rng.uniform(0.1, 5.0, (n, 3))
     d[rng.random((n, 3)) < 0.25] = 0.0
+    d[0, 0] = 0.0  # at least one null stage
     for t in range(n):  # a task keeps at least one command
         if not d[t].any():
             d[t, 1] = 1.5
