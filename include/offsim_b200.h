@@ -157,9 +157,9 @@ int osim_micro_timeline(const double* durs, int n, int dma, double sigma, double
 /* ---- device-resident variants (inputs already in HBM) ---------------- */
 /* fast = 1 asserts every stage is non-null, every duration lies in
  * [2^-60, 2^22) ms and sigma >= 2^-60 (osim_fast_eligible()); for the
- * exhaustive entry points fast = 2 asserts the same with null (0) stages
- * allowed (the null-stage fast simulator); 0 selects the general path.  The
- * host entry points choose the mode themselves. */
+ * exhaustive and heuristic entry points fast = 2 asserts the same with null
+ * (0) stages allowed (the null-stage fast simulator); 0 selects the general
+ * path.  The host entry points choose the mode themselves. */
 int osim_fast_eligible(const double* durs, uint64_t count /* tasks */, double sigma);
 
 int osim_exhaustive_dev(const double* d_durs, int n, int dma, double sigma, uint64_t rank_lo,

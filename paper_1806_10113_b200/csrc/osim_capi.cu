@@ -309,7 +309,7 @@ int enqueue_heuristic(DevCtx* c, cudaStream_t st, const double* d_durs, const ui
                       uint8_t* d_order, double* d_ms, uint32_t* d_ns) {
     if (B == 0) return 0;
     if ((B + kHG - 1) / kHG > 0x7fffffffull) return fail(OSIM_EINVAL, "batch too large");
-    heuristic_launch(dma, fast != 0, LaunchCfg{c->sms, st}, d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms,
+    heuristic_launch(dma, fast, LaunchCfg{c->sms, st}, d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms,
                      d_ns, c->d_err);
     CK(cudaGetLastError());
     return 0;
@@ -819,7 +819,7 @@ int osim_heuristic_batch(const double* durs, const uint8_t* id_rank, uint64_t B,
         offs_idr[gi] = off_idr; offs_ord[gi] = off_ord; offs_ms[gi] = off_ms; offs_ns[gi] = off_ns;
         unsigned long long* chk = (unsigned long long*)(b + off_chk);
         d_chk[gi] = chk;
-        const unsigned long long init[3] = {~0ull, ~0ull, 0ull};
+        const unsigned long long init[4] = {~0ull, ~0ull, 0ull, 0ull};
         CK(cudaMemcpyAsync(chk, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
         CK(cudaStreamSynchronize(c->stream));  // `init` is a stack buffer
         CK(cudaEventRecord(c->ev, c->stream));
@@ -856,7 +856,7 @@ int osim_heuristic_batch(const double* durs, const uint8_t* id_rank, uint64_t B,
         CK(cudaSetDevice(c->dev));
         CK(cudaStreamSynchronize(c->stream2));
         CK(cudaStreamSynchronize(c->stream));
-        unsigned long long res[3];
+        unsigned long long res[4];
         CK(cudaMemcpy(res, d_chk[gi], sizeof(res), cudaMemcpyDeviceToHost));
         if (res[0] != ~0ull || res[1] != ~0ull || (fast_first && res[2]))
             CK(cudaMemset(c->d_err, 0, sizeof(int)));  // the optimistic pass ran on ineligible data
@@ -870,12 +870,13 @@ int osim_heuristic_batch(const double* durs, const uint8_t* id_rank, uint64_t B,
         if (res[1] != ~0ull)
             return fail(OSIM_EINVAL, "group %llu: id ranks must be a permutation (duplicate task id?)", res[1]);
         if (fast_first && res[2]) {
-            // not fast-eligible: recompute this shard with the general kernel
+            // not fast-eligible: recompute this shard with the null-stage
+            // kernel (every stage 0 or in range) or the general one
             const uint64_t m = ms_[gi];
             char* b = bases[gi];
             if ((rc = enqueue_heuristic(c, c->stream, (double*)b, (uint8_t*)(b + offs_idr[gi]), m, n, dma, sigma,
-                                        sum_mode, 0, (uint8_t*)(b + offs_ord[gi]), (double*)(b + offs_ms[gi]),
-                                        (uint32_t*)(b + offs_ns[gi]))))
+                                        sum_mode, res[3] ? 0 : 2, (uint8_t*)(b + offs_ord[gi]),
+                                        (double*)(b + offs_ms[gi]), (uint32_t*)(b + offs_ns[gi]))))
                 return rc;
             const uint64_t lo = los[gi];
             CK(cudaMemcpyAsync(order + lo * n, b + offs_ord[gi], m * n, cudaMemcpyDeviceToHost, c->stream));

@@ -5,12 +5,12 @@
 
 namespace osim {
 
-void heuristic_launch(int dma, bool fast, const LaunchCfg& cfg, const double* d_durs, const uint8_t* d_idr,
+void heuristic_launch(int dma, int mode, const LaunchCfg& cfg, const double* d_durs, const uint8_t* d_idr,
                       uint64_t B, int n, double sigma, int sum_mode, uint8_t* d_order, double* d_ms,
                       uint32_t* d_ns, int* d_err) {
     const unsigned grid = (unsigned)((B + kHG - 1) / kHG);
     const size_t sm = sizeof(HeurShared);
-    if (fast) {
+    if (mode == 1) {
         const unsigned gridf = (unsigned)((B + kHGF - 1) / kHGF);
         int e;
         const bool sp2 = std::frexp(sigma, &e) == 0.5;
@@ -22,9 +22,13 @@ void heuristic_launch(int dma, bool fast, const LaunchCfg& cfg, const double* d_
 #undef OSIM_HF
         return;
     }
-#define OSIM_HL(D) \
-    k_heuristic<D, false><<<grid, kHT, sm, cfg.st>>>(d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms, d_ns, d_err)
-    if (dma == 2) OSIM_HL(2); else OSIM_HL(1);
+#define OSIM_HL(D, M) \
+    k_heuristic<D, M><<<grid, kHT, sm, cfg.st>>>(d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms, d_ns, d_err)
+    if (mode == 2) {  // null stages in the fast range: NullSim per candidate
+        if (dma == 2) OSIM_HL(2, 2); else OSIM_HL(1, 2);
+    } else {
+        if (dma == 2) OSIM_HL(2, 0); else OSIM_HL(1, 0);
+    }
 #undef OSIM_HL
 }
 

@@ -692,14 +692,16 @@ struct HeurShared {
     uint8_t pa[kHG], pb[kHG];
 };
 
-// One simulation of `seq` (len positions) of group g; FAST uses FastSim.
-template <int DMA, bool FAST, bool TRACK>
+// One simulation of `seq` (len positions) of group g from time 0.  MODE 1:
+// FastSim (no null stage); MODE 2: NullSim (null stages, fast range); MODE 0:
+// the general simulator (IEEE division, any durations).
+template <int DMA, int MODE, bool TRACK>
 struct HeurRun {
     double ms, kEnd, idleK;
     bool ok;
     __device__ __forceinline__ void run(HeurShared& S, uint32_t sbase, int g, uint64_t seq, int len, double sigma,
                                         double rsig, bool sp2) {
-        if constexpr (FAST) {
+        if constexpr (MODE == 1) {
             const uint32_t base = sbase + (uint32_t)(g * kHS * sizeof(double2));
             if (sp2 && DMA == 2) {
                 FastSim<DMA, true, TRACK, false> s;
@@ -714,6 +716,21 @@ struct HeurRun {
                 for (int st = 0; st < 3 * len; ++st) s.step(sigma, rsig);
                 ms = s.now; kEnd = s.kEnd; idleK = s.idleK; ok = s.drained();
             }
+        } else if constexpr (MODE == 2) {
+            const uint32_t base = sbase + (uint32_t)(g * kHS * sizeof(double2));
+            if (sp2 && DMA == 2) {
+                NullSim<DMA, true, TRACK> s;
+                s.init(base, seq, len, S.nH[g], S.nK[g], S.nD[g]);
+#pragma unroll 1
+                for (int st = 0; st < 3 * len; ++st) s.step(sigma, rsig);
+                ms = s.now; kEnd = s.kEnd; idleK = s.idleK; ok = s.drained();
+            } else {
+                NullSim<DMA, false, TRACK> s;
+                s.init(base, seq, len, S.nH[g], S.nK[g], S.nD[g]);
+#pragma unroll 1
+                for (int st = 0; st < 3 * len; ++st) s.step(sigma, rsig);
+                ms = s.now; kEnd = s.kEnd; idleK = s.idleK; ok = s.drained();
+            }
         } else {
             const double* p = reinterpret_cast<const double*>(&S.dr[g * kHS]);
             Sim<DMA, false, false, TRACK> s;
@@ -724,7 +741,7 @@ struct HeurRun {
     }
 };
 
-template <int DMA, bool FAST>
+template <int DMA, int MODE>
 __global__ void __launch_bounds__(kHT) k_heuristic(const double* __restrict__ durs,
                                                    const uint8_t* __restrict__ id_rank, uint64_t B,
                                                    int n, double sigma, int sum_mode,
@@ -808,7 +825,7 @@ __global__ void __launch_bounds__(kHT) k_heuristic(const double* __restrict__ du
             const int j = valid ? i % m : 0;
             const int c = S.cand[g * kMaxN + j];
             const uint64_t seq = S.ot[g] | ((uint64_t)c << (4 * k));
-            HeurRun<DMA, FAST, true> hr;
+            HeurRun<DMA, MODE, true> hr;
             hr.run(S, sbase, g, seq, k + 1, sigma, rsig, sp2);
             // _completion_estimate (heuristic.py:34-49); rest in rt order
             PySum ps;
@@ -873,7 +890,7 @@ __global__ void __launch_bounds__(kHT) k_heuristic(const double* __restrict__ du
             const int w = i & 1;
             const uint64_t x = w ? S.pb[g] : S.pa[g], y = w ? S.pa[g] : S.pb[g];
             const uint64_t seq = S.ot[g] | (x << (4 * kl)) | (y << (4 * (kl + 1)));
-            HeurRun<DMA, FAST, false> hr;
+            HeurRun<DMA, MODE, false> hr;
             hr.run(S, sbase, g, seq, n, sigma, rsig, sp2);
             if (valid) S.ka[g * kMaxN + w] = hr.ms;
         }
@@ -896,7 +913,7 @@ __global__ void __launch_bounds__(kHT) k_heuristic(const double* __restrict__ du
         const int i = i0 + tid;
         const bool valid = i < Gv;
         const int g = valid ? i : 0;
-        HeurRun<DMA, FAST, false> hr;
+        HeurRun<DMA, MODE, false> hr;
         hr.run(S, sbase, g, S.ot[g], n, sigma, rsig, sp2);
         if (!hr.ok) atomicExch(err, OSIM_ESTALL);
         if (valid) {
@@ -1172,13 +1189,14 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
 // Device-side input validation for the batched host APIs (same rules as the
 // host scan in osim_capi.cu: model.py:95-100, engine.py:129-130, unique ids):
 // out[0] = lowest offending task index (durations), out[1] = lowest group with
-// bad id ranks, out[2] = 1 if any stage is outside the fast range.
+// bad id ranks, out[2] = 1 if any stage is outside the fast range, out[3] = 1
+// if any stage is neither null nor in the fast range.
 // ---------------------------------------------------------------------------
 static __global__ void k_check_batch(const double* __restrict__ durs, const uint8_t* __restrict__ idr,
                                      uint64_t B, int n, uint64_t task0, uint64_t group0,
                                      unsigned long long* __restrict__ out) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    bool notfast = false;
+    bool notfast = false, notnull = false;
     for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B; b += stride) {
         unsigned seen = 0;
         bool badr = false;
@@ -1190,6 +1208,8 @@ static __global__ void k_check_batch(const double* __restrict__ durs, const uint
                             !(h <= 0 && k <= 0 && x <= 0);
             if (!ok) atomicMin(&out[0], (unsigned long long)(task0 + b * n + j));
             notfast |= !(h >= 0x1p-60 && h < kFastHi && k >= 0x1p-60 && k < kFastHi && x >= 0x1p-60 && x < kFastHi);
+            notnull |= !((h == 0.0 || (h >= 0x1p-60 && h < kFastHi)) && (k == 0.0 || (k >= 0x1p-60 && k < kFastHi)) &&
+                         (x == 0.0 || (x >= 0x1p-60 && x < kFastHi)));
             if (idr) {
                 const unsigned v = idr[b * n + j];
                 badr |= v >= (unsigned)n || ((seen >> v) & 1u);
@@ -1199,6 +1219,7 @@ static __global__ void k_check_batch(const double* __restrict__ durs, const uint
         if (badr) atomicMin(&out[1], (unsigned long long)(group0 + b));
     }
     if (__any_sync(kFull, notfast) && (threadIdx.x & 31) == 0) atomicExch(&out[2], 1ull);
+    if (__any_sync(kFull, notnull) && (threadIdx.x & 31) == 0) atomicExch(&out[3], 1ull);
 }
 
 // ---------------------------------------------------------------------------

@@ -69,7 +69,7 @@ int null_pfx_launch(int n, int dma, bool sp2, const LaunchCfg& cfg, const double
 int null_batch_launch(int n, int dma, bool sp2, const LaunchCfg& cfg, const double* d_durs, uint64_t B, double sigma,
                       osim_summary* d_out, int* d_err, int* g);
 
-void heuristic_launch(int dma, bool fast, const LaunchCfg& cfg, const double* d_durs, const uint8_t* d_idr,
+void heuristic_launch(int dma, int mode /* 0 general, 1 fast, 2 null stages */, const LaunchCfg& cfg, const double* d_durs, const uint8_t* d_idr,
                       uint64_t B, int n, double sigma, int sum_mode, uint8_t* d_order, double* d_ms,
                       uint32_t* d_ns, int* d_err);
 

@@ -18,129 +18,13 @@
 //    idle dt is clamped to 0 and the remaining lock-step steps are no-ops.
 // Fast-range conditions as FastSim: every non-null stage in [2^-60, 2^22)
 // ms and sigma >= 2^-60, so every step finalizes at least one command.
+// (NullSim itself is defined in osim_sim.cuh, next to FastSim, so the
+// heuristic kernels can use it too.)
 #pragma once
 
 #include "osim_kernels.cuh"
 
 namespace osim {
-
-template <int DMA, bool SIGP2>
-struct NullSim {
-    uint32_t base;
-    uint64_t seq;
-    int n, n4;
-    unsigned mH, mK, mX;  // position null masks (HtD, K; mX: 1-DMA XFER slots, 2-DMA DtH)
-    double now;
-    double r0, r1, r2, d0, d1, d2, c0, c1, c2;
-    int s0, s1, s2;  // 4 * head position: HtD (1-DMA: XFER slot), DtH, K
-
-    // next non-null slot after s (4x units) in mask m over `lim` slots
-    __device__ __forceinline__ static int next(unsigned m, int s, int lim) {
-        const int p = s >> 2;
-        const unsigned above = p >= 31 ? 0u : (~0u << (p + 1));
-        const unsigned in = lim >= 32 ? ~0u : ((1u << lim) - 1u);
-        const unsigned c = ~m & above & in;
-        return 4 * (c ? __ffs(c) - 1 : lim);
-    }
-    __device__ __forceinline__ static int first(unsigned m, int lim) {
-        const unsigned in = lim >= 32 ? ~0u : ((1u << lim) - 1u);
-        const unsigned c = ~m & in;
-        return 4 * (c ? __ffs(c) - 1 : lim);
-    }
-    __device__ __forceinline__ bool nul(unsigned m, int s) const { return (m >> (s >> 2)) & 1u; }
-
-    // tH/tK/tD: null-stage masks by task id
-    __device__ __forceinline__ void init(uint32_t b, uint64_t sq, int nn, unsigned tH, unsigned tK, unsigned tD) {
-        base = b;
-        seq = sq;
-        n = nn;
-        n4 = 4 * nn;
-        unsigned pH = 0, pK = 0, pD = 0;
-        for (int p = 0; p < nn; ++p) {
-            const int t = nib(sq, p);
-            pH |= ((tH >> t) & 1u) << p;
-            pK |= ((tK >> t) & 1u) << p;
-            pD |= ((tD >> t) & 1u) << p;
-        }
-        mH = pH;
-        mK = pK;
-        now = 0.0;
-        r0 = r1 = r2 = kBig;
-        d0 = d1 = d2 = c0 = c1 = c2 = 1.0;
-        s2 = first(pK, nn);
-        if constexpr (DMA == 2) {
-            mX = pD;
-            s0 = first(pH, nn);
-            s1 = first(pD, nn);
-        } else {
-            mX = pH | (pD << nn);
-            s0 = first(mX, 2 * nn);
-            s1 = 0;
-        }
-    }
-
-    __device__ __forceinline__ bool drained() const {
-        if constexpr (DMA == 2) return s0 >= n4 && s1 >= n4 && s2 >= n4 && idle(r0) && idle(r1) && idle(r2);
-        else return s0 >= 2 * n4 && s2 >= n4 && idle(r0) && idle(r2);
-    }
-
-    __device__ __forceinline__ double upd(double rem, double dd, double nd, double rc) const {
-        return __dmul_rn(divq<true>(__dsub_rn(rem, dd), nd, rc), nd);
-    }
-
-    __device__ __forceinline__ void step(double sigma, double rsig) {
-        // ---- start phase (engine.py:188-194)
-        if constexpr (DMA == 2) {
-            const bool st0 = idle(r0) && s0 < n4;
-            const bool st2 = idle(r2) && s2 < n4 && (s2 < s0 || nul(mH, s2));
-            const bool st1 = idle(r1) && s1 < n4 && (s1 < s2 || nul(mK, s1)) && (s1 < s0 || nul(mH, s1));
-            start_if(st0, base + task_off<false>(seq, s0), d0, c0, r0);
-            start_if(st2, base + 256 + task_off<false>(seq, s2), d2, c2, r2);
-            start_if(st1, base + 512 + task_off<false>(seq, s1), d1, c1, r1);
-        } else {
-            const bool isH = s0 < n4;
-            const int ps = isH ? s0 : s0 - n4;
-            const bool st0 = idle(r0) && s0 < 2 * n4 && (isH || ps < s2 || nul(mK, ps));
-            const bool st2 = idle(r2) && s2 < n4 && (s2 < s0 || nul(mH, s2));
-            start_if(st0, base + (isH ? 0u : 512u) + task_off<false>(seq, ps), d0, c0, r0);
-            start_if(st2, base + 256 + task_off<false>(seq, s2), d2, c2, r2);
-        }
-        // ---- dt (engine.py:200-210); every lane idle (drained): dt = 0
-        double dt, dd;
-        if constexpr (DMA == 2) {
-            const bool ov = !idle(r0) && !idle(r1);
-            double m = dmin(r0, r1);
-            if constexpr (SIGP2) {
-                m = __dmul_rn(m, __hiloint2double(ov ? __double2hiint(rsig) : 0x3FF00000, 0));
-                dt = dmin(m, r2);
-                dd = __dmul_rn(dt, __hiloint2double(ov ? __double2hiint(sigma) : 0x3FF00000, 0));
-            } else {
-                if (ov) m = divq<true>(m, sigma, rsig);
-                dt = dmin(m, r2);
-                dd = dt;
-                mul_if(ov, dd, sigma);
-            }
-        } else {
-            dt = dmin(r0, r2);
-            dd = dt;
-        }
-        if (idle(dt)) { dt = 0.0; dd = 0.0; }
-        now = __dadd_rn(now, dt);  // engine.py:211
-        // ---- update + finalize (engine.py:212-231)
-        r0 = upd(r0, dd, d0, c0);
-        r2 = upd(r2, dt, d2, c2);
-        if constexpr (DMA == 2) r1 = upd(r1, dd, d1, c1);
-        if (r0 <= kEndEps) {
-            r0 = retire(r0);
-            if constexpr (DMA == 2) s0 = next(mH, s0, n);
-            else s0 = next(mX, s0, 2 * n);
-        }
-        if constexpr (DMA == 2) {
-            if (r1 <= kEndEps) { r1 = retire(r1); s1 = next(mX, s1, n); }
-        }
-        if (r2 <= kEndEps) { r2 = retire(r2); s2 = next(mK, s2, n); }
-    }
-};
 
 // ---------------------------------------------------------------------------
 // Prefix sharing with null stages.  With nulls a suffix command can start
@@ -153,8 +37,8 @@ struct NullSim {
 // each head that sat at M to the first non-null slot >= M of the full
 // ordering (1-DMA: the prefix world's XFER slot M is the full world's HtD(M)).
 // ---------------------------------------------------------------------------
-template <int DMA, bool SIGP2>
-__device__ __forceinline__ bool null_at_ck(const NullSim<DMA, SIGP2>& s) {
+template <int DMA, bool SIGP2, bool TRACK>
+__device__ __forceinline__ bool null_at_ck(const NullSim<DMA, SIGP2, TRACK>& s) {
     const bool a = idle(s.r0) && s.s0 >= s.n4;  // 1-DMA prefix world: XFER at its DtH part
     const bool c = idle(s.r2) && s.s2 >= s.n4;
     if constexpr (DMA == 2) return a || c || (idle(s.r1) && s.s1 >= s.n4);

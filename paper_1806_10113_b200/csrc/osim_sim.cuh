@@ -621,6 +621,149 @@ struct FastSim {
     }
 };
 
+// FastSim generalized to null stages (see osim_null.cuh for the contract):
+// position heads, find-first-set skipping over per-sequence null masks,
+// "head passed or stage null" readiness, dt clamped to 0 once all lanes idle.
+template <int DMA, bool SIGP2, bool TRACK = false>
+struct NullSim {
+    uint32_t base;
+    uint64_t seq;
+    int n, n4;
+    unsigned mH, mK, mX;  // position null masks (HtD, K; mX: 1-DMA XFER slots, 2-DMA DtH)
+    double now;
+    double r0, r1, r2, d0, d1, d2, c0, c1, c2;
+    int s0, s1, s2;  // 4 * head position: HtD (1-DMA: XFER slot), DtH, K
+    double kEnd, idleK;  // TRACK: last K end, idle_report's K gaps (engine.py:68-80)
+    bool kfin;           // TRACK: some K has finalized
+
+    // next non-null slot after s (4x units) in mask m over `lim` slots
+    __device__ __forceinline__ static int next(unsigned m, int s, int lim) {
+        const int p = s >> 2;
+        const unsigned above = p >= 31 ? 0u : (~0u << (p + 1));
+        const unsigned in = lim >= 32 ? ~0u : ((1u << lim) - 1u);
+        const unsigned c = ~m & above & in;
+        return 4 * (c ? __ffs(c) - 1 : lim);
+    }
+    __device__ __forceinline__ static int first(unsigned m, int lim) {
+        const unsigned in = lim >= 32 ? ~0u : ((1u << lim) - 1u);
+        const unsigned c = ~m & in;
+        return 4 * (c ? __ffs(c) - 1 : lim);
+    }
+    __device__ __forceinline__ bool nul(unsigned m, int s) const { return (m >> (s >> 2)) & 1u; }
+
+    // tH/tK/tD: null-stage masks by task id
+    __device__ __forceinline__ void init(uint32_t b, uint64_t sq, int nn, unsigned tH, unsigned tK, unsigned tD) {
+        base = b;
+        seq = sq;
+        n = nn;
+        n4 = 4 * nn;
+        unsigned pH = 0, pK = 0, pD = 0;
+        for (int p = 0; p < nn; ++p) {
+            const int t = nib(sq, p);
+            pH |= ((tH >> t) & 1u) << p;
+            pK |= ((tK >> t) & 1u) << p;
+            pD |= ((tD >> t) & 1u) << p;
+        }
+        mH = pH;
+        mK = pK;
+        now = 0.0;
+        r0 = r1 = r2 = kBig;
+        d0 = d1 = d2 = c0 = c1 = c2 = 1.0;
+        kEnd = 0.0;
+        idleK = 0.0;
+        kfin = false;
+        s2 = first(pK, nn);
+        if constexpr (DMA == 2) {
+            mX = pD;
+            s0 = first(pH, nn);
+            s1 = first(pD, nn);
+        } else {
+            mX = pH | (pD << nn);
+            s0 = first(mX, 2 * nn);
+            s1 = 0;
+        }
+    }
+
+    __device__ __forceinline__ bool drained() const {
+        if constexpr (DMA == 2) return s0 >= n4 && s1 >= n4 && s2 >= n4 && idle(r0) && idle(r1) && idle(r2);
+        else return s0 >= 2 * n4 && s2 >= n4 && idle(r0) && idle(r2);
+    }
+
+    __device__ __forceinline__ double upd(double rem, double dd, double nd, double rc) const {
+        return __dmul_rn(divq<true>(__dsub_rn(rem, dd), nd, rc), nd);
+    }
+
+    __device__ __forceinline__ void step(double sigma, double rsig) {
+        // ---- start phase (engine.py:188-194)
+        if constexpr (DMA == 2) {
+            const bool st0 = idle(r0) && s0 < n4;
+            const bool st2 = idle(r2) && s2 < n4 && (s2 < s0 || nul(mH, s2));
+            const bool st1 = idle(r1) && s1 < n4 && (s1 < s2 || nul(mK, s1)) && (s1 < s0 || nul(mH, s1));
+            k_idle_gap(st2);
+            start_if(st0, base + task_off<false>(seq, s0), d0, c0, r0);
+            start_if(st2, base + 256 + task_off<false>(seq, s2), d2, c2, r2);
+            start_if(st1, base + 512 + task_off<false>(seq, s1), d1, c1, r1);
+        } else {
+            const bool isH = s0 < n4;
+            const int ps = isH ? s0 : s0 - n4;
+            const bool st0 = idle(r0) && s0 < 2 * n4 && (isH || ps < s2 || nul(mK, ps));
+            const bool st2 = idle(r2) && s2 < n4 && (s2 < s0 || nul(mH, s2));
+            k_idle_gap(st2);
+            start_if(st0, base + (isH ? 0u : 512u) + task_off<false>(seq, ps), d0, c0, r0);
+            start_if(st2, base + 256 + task_off<false>(seq, s2), d2, c2, r2);
+        }
+        // ---- dt (engine.py:200-210); every lane idle (drained): dt = 0
+        double dt, dd;
+        if constexpr (DMA == 2) {
+            const bool ov = !idle(r0) && !idle(r1);
+            double m = dmin(r0, r1);
+            if constexpr (SIGP2) {
+                m = __dmul_rn(m, __hiloint2double(ov ? __double2hiint(rsig) : 0x3FF00000, 0));
+                dt = dmin(m, r2);
+                dd = __dmul_rn(dt, __hiloint2double(ov ? __double2hiint(sigma) : 0x3FF00000, 0));
+            } else {
+                if (ov) m = divq<true>(m, sigma, rsig);
+                dt = dmin(m, r2);
+                dd = dt;
+                mul_if(ov, dd, sigma);
+            }
+        } else {
+            dt = dmin(r0, r2);
+            dd = dt;
+        }
+        if (idle(dt)) { dt = 0.0; dd = 0.0; }
+        now = __dadd_rn(now, dt);  // engine.py:211
+        // ---- update + finalize (engine.py:212-231)
+        r0 = upd(r0, dd, d0, c0);
+        r2 = upd(r2, dt, d2, c2);
+        if constexpr (DMA == 2) r1 = upd(r1, dd, d1, c1);
+        if (r0 <= kEndEps) {
+            r0 = retire(r0);
+            if constexpr (DMA == 2) s0 = next(mH, s0, n);
+            else s0 = next(mX, s0, 2 * n);
+        }
+        if constexpr (DMA == 2) {
+            if (r1 <= kEndEps) { r1 = retire(r1); s1 = next(mX, s1, n); }
+        }
+        if (r2 <= kEndEps) {
+            r2 = retire(r2);
+            s2 = next(mK, s2, n);
+            if constexpr (TRACK) {
+                kEnd = now;
+                kfin = true;
+            }
+        }
+    }
+
+    // idle_report over K spans in FIFO (= sorted) order, as FastSim
+    __device__ __forceinline__ void k_idle_gap(bool st2) {
+        if constexpr (TRACK) {
+            const double gap = __dsub_rn(now, kEnd);
+            add_if(st2 && kfin && now > kEnd, idleK, gap);
+        }
+    }
+};
+
 // Lexicographic unrank of `r` into a packed sequence (itertools.permutations
 // order == Lehmer rank order, oracle.py:125).
 template <int N>

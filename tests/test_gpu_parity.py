@@ -780,3 +780,18 @@ def test_concurrent_host_calls_from_threads():
     with ThreadPoolExecutor(6) as ex:
         res = list(ex.map(work, range(36)))
     assert all(ok for _, ok in res)
+
+
+@pytest.mark.parametrize("profile", ["nvidia", "amd", "phi"])
+def test_heuristic_null_stages_vs_oracle(profile):
+    # 16-task groups with null stages (the device check reroutes the batch to
+    # the NullSim heuristic): order, makespan and simulation count bit-exact
+    d, r = synth.c5_batch_fast(profile, 2000, seed=91)
+    rng = np.random.default_rng(92)
+    d = d.copy()
+    d[rng.random(d.shape) < 0.1] = 0.0
+    d[(d == 0).all(axis=2), 1] = 1.0
+    _, dma, sigma = synth.PROFILES[profile]
+    order, ms, sims = _capi.heuristic_batch(d, r, dma, sigma, osim.SUM_MODE)
+    o_order, o_ms, o_sims = O.reorder_batch(d, r, dma, sigma, osim.SUM_MODE, threads=os.cpu_count() or 4)
+    assert np.array_equal(order, o_order) and np.array_equal(ms, o_ms) and np.array_equal(sims, o_sims)
