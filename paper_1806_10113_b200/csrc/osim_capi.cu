@@ -1004,6 +1004,12 @@ int osim_interleavings(const double* durs, int T, int N, int dma, double sigma, 
                 if (g > mp) g = mp;
                 k<<<g, kBlock, 0, c->stream>>>((double*)b, T, N, sigma, lo, hi, total, threshold,
                                                (Part*)(b + off_parts), d_ms, c->d_err);
+            } else if (dma == 1 && fast == 1) {
+                auto k = T * N <= 15 ? k_interleave_fast1<true> : k_interleave_fast1<false>;
+                g = grid_for(k, kBlock, 0, c, blocks);
+                if (g > mp) g = mp;
+                k<<<g, kBlock, 0, c->stream>>>((double*)b, T, N, lo, hi, total, threshold, (Part*)(b + off_parts),
+                                               d_ms, c->d_err);
             } else if (dma == 2) {
                 g = grid_for(k_interleave<2>, kBlock, 0, c, blocks);
                 if (g > mp) g = mp;

@@ -298,6 +298,142 @@ __global__ void __launch_bounds__(kBlock) k_interleave_fast(const double* __rest
     if (threadIdx.x == 0) parts[blockIdx.x] = acc;
 }
 
+// 1-DMA NoReorder fast path.  simulate_sequence (workload.py:277-304) cuts
+// the sequence into waves -- a task whose prerequisite (the same worker's
+// previous task) sits in the current wave opens a new one -- and each submit
+// appends the wave's HtDs, then its DtHs, to the XFER queue; the K queue
+// keeps sequence order.  With a wave [a, b) the XFER slot of HtD(p) is
+// p + a and of DtH(p) is p + b.  A prerequisite always lies in an earlier
+// wave, whose DtH block the XFER lane has passed before this wave's HtDs,
+// so the deps gate never binds; readiness is K(p): XFER slot count > p +
+// ws(p); XFER DtH(p): K head > p.  Every stage non-null and in the FastSim
+// range; same op sequence as DepSim.
+template <bool PRE>
+struct WaveSim {
+    uint32_t base;
+    uint64_t seq;
+    uint64_t wsq, weq;  // per position: wave start, wave end - 1 (nibbles)
+    int n4;
+    double now, r0, r2, d0, d2, c0, c2;
+    int x;       // 4 * XFER slots finalized
+    int p0, h0;  // XFER current position and kind (0 HtD, 1 DtH)
+    int s2;      // 4 * K head position
+
+    __device__ __forceinline__ void init(uint32_t b, uint64_t sq, int n, uint64_t ws, uint64_t we) {
+        base = b;
+        seq = PRE ? (sq << 4) : sq;
+        wsq = ws;
+        weq = we;
+        n4 = 4 * n;
+        now = 0.0;
+        r0 = r2 = kBig;
+        d0 = d2 = c0 = c2 = 1.0;
+        x = 0;
+        p0 = 0;
+        h0 = 0;
+        s2 = 0;
+    }
+    __device__ __forceinline__ int wsof(int p) const { return (int)((wsq >> (4 * p)) & 0xF); }
+    __device__ __forceinline__ int weof(int p) const { return (int)((weq >> (4 * p)) & 0xF) + 1; }
+
+    __device__ __forceinline__ void step() {
+        const bool st0 = idle(r0) && x < 2 * n4 && (h0 == 0 || s2 > 4 * p0);
+        const bool st2 = idle(r2) && s2 < n4 && x > 4 * ((s2 >> 2) + wsof(s2 >> 2));
+        start_if(st0, base + (h0 ? 512u : 0u) + task_off<PRE>(seq, 4 * p0), d0, c0, r0);
+        start_if(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
+        const double dt = dmin(r0, r2);  // no overlap on one DMA engine: rate 1
+        now = __dadd_rn(now, dt);
+        r0 = __dmul_rn(divq<true>(__dsub_rn(r0, dt), d0, c0), d0);
+        r2 = __dmul_rn(divq<true>(__dsub_rn(r2, dt), d2, c2), d2);
+        const bool f0 = r0 <= kEndEps;
+        r0 = retire_or_drain(f0, r0, x + 4 >= 2 * n4);
+        if (f0) {
+            x += 4;
+            const int e = weof(p0);
+            if (p0 + 1 < e) ++p0;
+            else if (h0 == 0) { h0 = 1; p0 = wsof(p0); }
+            else { h0 = 0; p0 = e; }
+        }
+        if (r2 <= kEndEps) { r2 = retire(r2); s2 += 4; }
+    }
+    __device__ __forceinline__ bool drained() const { return x >= 2 * n4; }
+};
+
+// labels rank -> task order plus the wave bounds of simulate_sequence
+__device__ __forceinline__ uint64_t unrank_labels_waves(uint64_t r, int T, int N, uint64_t mtotal, uint64_t& wsq,
+                                                        uint64_t& weq) {
+    int c[16], last[16];
+    for (int w = 0; w < T; ++w) { c[w] = N; last[w] = -1; }
+    int rem = T * N;
+    uint64_t M = mtotal;
+    uint64_t order = 0;
+    unsigned starts = 0;
+    int w0 = 0;
+    for (int p = 0; p < T * N; ++p) {
+        for (int w = 0; w < T; ++w) {
+            if (!c[w]) continue;
+            const uint64_t m = mult_next(M, c[w], rem);
+            if (r < m) {
+                order |= (uint64_t)(w * N + (N - c[w])) << (4 * p);
+                if (p == 0 || last[w] >= w0) { starts |= 1u << p; w0 = p; }  // prerequisite in the wave
+                last[w] = p;
+                --c[w];
+                --rem;
+                M = m;
+                break;
+            }
+            r -= m;
+        }
+    }
+    const int n = T * N;
+    wsq = weq = 0;
+    int ws = 0;
+    for (int p = 0; p < n; ++p) {
+        if ((starts >> p) & 1u) ws = p;
+        const unsigned after = (p + 1 < 32) ? (starts & ~((2u << p) - 1u)) : 0u;
+        const int we = after ? __ffs(after) - 1 : n;
+        wsq |= (uint64_t)ws << (4 * p);
+        weq |= (uint64_t)(we - 1) << (4 * p);
+    }
+    return order;
+}
+
+template <bool PRE>
+__global__ void __launch_bounds__(kBlock) k_interleave_fast1(const double* __restrict__ durs, int T, int N,
+                                                             uint64_t lo, uint64_t hi, uint64_t mtotal, double thr,
+                                                             Part* __restrict__ parts, double* __restrict__ ms_out,
+                                                             int* __restrict__ err) {
+    __shared__ double2 sdr[3 * kStride];
+    __shared__ Part sh[32];
+    const int n = T * N;
+    stage_dr(durs, n, sdr);
+    __syncthreads();
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
+    Part acc;
+    part_init(acc);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t b0 = lo + (uint64_t)blockIdx.x * blockDim.x; b0 < hi; b0 += stride) {
+        const uint64_t r = b0 + threadIdx.x;
+        const bool valid = r < hi;
+        uint64_t wsq, weq;
+        const uint64_t order = unrank_labels_waves(valid ? r : lo, T, N, mtotal, wsq, weq);
+        WaveSim<PRE> s;
+        s.init(base, order, n, wsq, weq);
+#pragma unroll 1
+        for (int st = 0; st < 3 * n; st += 2) {
+            s.step();
+            s.step();
+        }
+        if (valid) {
+            if (!s.drained()) atomicExch(err, OSIM_ESTALL);
+            part_add<true>(acc, s.now, r, thr);
+            if (ms_out) ms_out[r - lo] = s.now;
+        }
+    }
+    acc = block_reduce(acc, sh);
+    if (threadIdx.x == 0) parts[blockIdx.x] = acc;
+}
+
 template <int DMA>
 __global__ void __launch_bounds__(kBlock) k_eval_labels(const double* __restrict__ durs, int T, int N, double sigma,
                                                         const uint8_t* __restrict__ labels, uint64_t cnt,

@@ -446,9 +446,10 @@ def test_noreorder_fast_path_4x4_vs_oracle():
     d = synth.real_group("K20", 16, 41)[1]
     lo, hi = 31_000_000, 31_300_000
     cpus = os.cpu_count() or 4
-    for sigma in (0.5, 0.375):
-        s, below, ms = _capi.interleavings(d, 4, 4, 2, sigma, lo, hi, threshold=90.0, want_makespans=True)
-        o, oms = O.interleavings(d, 4, 4, 2, sigma, lo, hi, threads=cpus, makespans=True)
+    for dma, sigma in ((2, 0.5), (2, 0.375), (1, 1.0)):
+        # 1-DMA: the wave-split fast kernel (k_interleave_fast1)
+        s, below, ms = _capi.interleavings(d, 4, 4, dma, sigma, lo, hi, threshold=90.0, want_makespans=True)
+        o, oms = O.interleavings(d, 4, 4, dma, sigma, lo, hi, threads=cpus, makespans=True)
         assert np.array_equal(ms, oms)
         assert_summary_vs_oracle(s, o)
         assert below == int((oms < 90.0).sum())
