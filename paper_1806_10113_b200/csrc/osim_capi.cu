@@ -213,6 +213,17 @@ int grid_for(K kernel, int threads, size_t smem, const DevCtx* c, uint64_t work_
     return osim::grid_for_sms(kernel, threads, smem, c->sms, work_blocks);
 }
 
+// NoReorder prefix-sharing run length (ranks per thread); OSIM_F1_RUN
+// overrides it for tuning (tools/f1_speed.py)
+int f1_run_len() {
+    static const int v = [] {
+        const char* e = std::getenv("OSIM_F1_RUN");
+        const int x = e ? std::atoi(e) : 0;
+        return (x >= 1 && x <= 4096) ? x : 32;
+    }();
+    return v;
+}
+
 bool sigma_pow2(double sigma) {
     int e;
     double m = std::frexp(sigma, &e);
@@ -998,18 +1009,23 @@ int osim_interleavings(const double* durs, int T, int N, int dma, double sigma, 
         if (hi > lo) {
             const uint64_t blocks = (hi - lo + kBlock - 1) / kBlock;
             if (dma == 2 && fast == 1) {
-                auto k = sigma_pow2(sigma) ? (T * N <= 15 ? k_interleave_fast<true, true> : k_interleave_fast<true, false>)
-                                           : (T * N <= 15 ? k_interleave_fast<false, true> : k_interleave_fast<false, false>);
-                g = grid_for(k, kBlock, 0, c, blocks);
+                // runs of kRun consecutive ranks share their common label prefix
+                const int run = f1_run_len();
+                const uint64_t rb = ((hi - lo + run - 1) / run + kBlock - 1) / kBlock;
+                auto k = sigma_pow2(sigma) ? (T * N <= 15 ? k_interleave_pfx<true, true> : k_interleave_pfx<true, false>)
+                                           : (T * N <= 15 ? k_interleave_pfx<false, true> : k_interleave_pfx<false, false>);
+                g = grid_for(k, kBlock, 0, c, rb);
                 if (g > mp) g = mp;
-                k<<<g, kBlock, 0, c->stream>>>((double*)b, T, N, sigma, lo, hi, total, threshold,
+                k<<<g, kBlock, 0, c->stream>>>((double*)b, T, N, sigma, lo, hi, total, run, threshold,
                                                (Part*)(b + off_parts), d_ms, c->d_err);
             } else if (dma == 1 && fast == 1) {
-                auto k = T * N <= 15 ? k_interleave_fast1<true> : k_interleave_fast1<false>;
-                g = grid_for(k, kBlock, 0, c, blocks);
+                const int run = f1_run_len();
+                const uint64_t rb = ((hi - lo + run - 1) / run + kBlock - 1) / kBlock;
+                auto k = T * N <= 15 ? k_interleave_pfx1<true> : k_interleave_pfx1<false>;
+                g = grid_for(k, kBlock, 0, c, rb);
                 if (g > mp) g = mp;
-                k<<<g, kBlock, 0, c->stream>>>((double*)b, T, N, lo, hi, total, threshold, (Part*)(b + off_parts),
-                                               d_ms, c->d_err);
+                k<<<g, kBlock, 0, c->stream>>>((double*)b, T, N, lo, hi, total, run, threshold,
+                                               (Part*)(b + off_parts), d_ms, c->d_err);
             } else if (dma == 2) {
                 g = grid_for(k_interleave<2>, kBlock, 0, c, blocks);
                 if (g > mp) g = mp;

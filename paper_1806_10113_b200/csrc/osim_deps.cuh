@@ -231,73 +231,6 @@ __global__ void __launch_bounds__(kBlock) k_interleave(const double* __restrict_
     if (threadIdx.x == 0) parts[blockIdx.x] = acc;
 }
 
-// Same unranking, also returning the packed NoReorder prerequisite of each
-// position (1 + position of the same worker's previous task, 0 for a
-// worker's first task).
-__device__ __forceinline__ uint64_t unrank_labels_dep(uint64_t r, int T, int N, uint64_t mtotal, uint64_t& dseq) {
-    int c[16], last[16];
-    for (int w = 0; w < T; ++w) { c[w] = N; last[w] = -1; }
-    int rem = T * N;
-    uint64_t M = mtotal;
-    uint64_t order = 0;
-    dseq = 0;
-    for (int p = 0; p < T * N; ++p) {
-        for (int w = 0; w < T; ++w) {
-            if (!c[w]) continue;
-            const uint64_t m = mult_next(M, c[w], rem);
-            if (r < m) {
-                order |= (uint64_t)(w * N + (N - c[w])) << (4 * p);
-                dseq |= (uint64_t)(last[w] + 1) << (4 * p);
-                last[w] = p;
-                --c[w];
-                --rem;
-                M = m;
-                break;
-            }
-            r -= m;
-        }
-    }
-    return order;
-}
-
-// Fast path of the NoReorder distribution (2-DMA, every stage non-null and
-// in the FastSim range): one thread per interleaving, FastSim with the
-// prerequisite gate, phase-specialized steps, Markstein division -- the
-// same op sequence as DepSim, so makespans are bit-identical.
-template <bool SIGP2, bool PRE>
-__global__ void __launch_bounds__(kBlock) k_interleave_fast(const double* __restrict__ durs, int T, int N,
-                                                            double sigma, uint64_t lo, uint64_t hi, uint64_t mtotal,
-                                                            double thr, Part* __restrict__ parts,
-                                                            double* __restrict__ ms_out, int* __restrict__ err) {
-    __shared__ double2 sdr[3 * kStride];
-    __shared__ Part sh[32];
-    const int n = T * N;
-    stage_dr(durs, n, sdr);
-    __syncthreads();
-    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
-    const double rsig = __ddiv_rn(1.0, sigma);
-    Part acc;
-    part_init(acc);
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t b0 = lo + (uint64_t)blockIdx.x * blockDim.x; b0 < hi; b0 += stride) {
-        const uint64_t r = b0 + threadIdx.x;
-        const bool valid = r < hi;
-        uint64_t dseq;
-        const uint64_t order = unrank_labels_dep(valid ? r : lo, T, N, mtotal, dseq);
-        FastSim<2, SIGP2, false, PRE, true> s;
-        s.init(base, order, n);
-        s.dseq = PRE ? (dseq << 4) : dseq;
-        s.run_phased(3 * n, sigma, rsig);
-        if (valid) {
-            if (!s.drained()) atomicExch(err, OSIM_ESTALL);
-            part_add<true>(acc, s.now, r, thr);
-            if (ms_out) ms_out[r - lo] = s.now;
-        }
-    }
-    acc = block_reduce(acc, sh);
-    if (threadIdx.x == 0) parts[blockIdx.x] = acc;
-}
-
 // 1-DMA NoReorder fast path.  simulate_sequence (workload.py:277-304) cuts
 // the sequence into waves -- a task whose prerequisite (the same worker's
 // previous task) sits in the current wave opens a new one -- and each submit
@@ -359,24 +292,36 @@ struct WaveSim {
     __device__ __forceinline__ bool drained() const { return x >= 2 * n4; }
 };
 
-// labels rank -> task order plus the wave bounds of simulate_sequence
-__device__ __forceinline__ uint64_t unrank_labels_waves(uint64_t r, int T, int N, uint64_t mtotal, uint64_t& wsq,
-                                                        uint64_t& weq) {
-    int c[16], last[16];
-    for (int w = 0; w < T; ++w) { c[w] = N; last[w] = -1; }
+// ---------------------------------------------------------------------------
+// Prefix sharing for the NoReorder distribution.  Interleavings are ranked in
+// lexicographic order of their worker-label sequences, so a run of K
+// consecutive ranks [r0, r0 + K) shares the first M = lcp(seq(r0),
+// seq(r0 + K - 1)) labels -- the same M tasks, the same prerequisites.  Up to
+// the step in which HtD(M - 1) finalizes no command of a position >= M can
+// have started (the HtD lane is a FIFO; K(p) waits for HtD(p), DtH(p) for
+// K(p); the deps gate only delays starts), so that state is common to the
+// whole run: each thread simulates it once, stores it in its shared-memory
+// slot and replays the K suffixes from it, stepping to the next sequence by
+// a multiset next-permutation of the label suffix (no per-rank unranking).
+// Per-sequence operation sequences are unchanged, so makespans are
+// bit-identical to DepSim's (FastSim with the prerequisite gate on the HtD
+// start: with every stage non-null a task is finished exactly when its DtH
+// finalized, and DtHs finalize in sequence order).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int lab_at(uint64_t lab, int p) { return (int)((lab >> (4 * p)) & 0xF); }
+
+// labels of rank r (multinomial unranking, as unrank_labels)
+__device__ __forceinline__ uint64_t unrank_lab(uint64_t r, int T, int N, uint64_t mtotal) {
+    int c[16];
+    for (int w = 0; w < T; ++w) c[w] = N;
     int rem = T * N;
-    uint64_t M = mtotal;
-    uint64_t order = 0;
-    unsigned starts = 0;
-    int w0 = 0;
+    uint64_t M = mtotal, lab = 0;
     for (int p = 0; p < T * N; ++p) {
         for (int w = 0; w < T; ++w) {
             if (!c[w]) continue;
             const uint64_t m = mult_next(M, c[w], rem);
             if (r < m) {
-                order |= (uint64_t)(w * N + (N - c[w])) << (4 * p);
-                if (p == 0 || last[w] >= w0) { starts |= 1u << p; w0 = p; }  // prerequisite in the wave
-                last[w] = p;
+                lab |= (uint64_t)w << (4 * p);
                 --c[w];
                 --rem;
                 M = m;
@@ -385,49 +330,209 @@ __device__ __forceinline__ uint64_t unrank_labels_waves(uint64_t r, int T, int N
             r -= m;
         }
     }
-    const int n = T * N;
-    wsq = weq = 0;
-    int ws = 0;
-    for (int p = 0; p < n; ++p) {
-        if ((starts >> p) & 1u) ws = p;
-        const unsigned after = (p + 1 < 32) ? (starts & ~((2u << p) - 1u)) : 0u;
-        const int we = after ? __ffs(after) - 1 : n;
-        wsq |= (uint64_t)ws << (4 * p);
-        weq |= (uint64_t)(we - 1) << (4 * p);
-    }
-    return order;
+    return lab;
 }
 
-template <bool PRE>
-__global__ void __launch_bounds__(kBlock) k_interleave_fast1(const double* __restrict__ durs, int T, int N,
-                                                             uint64_t lo, uint64_t hi, uint64_t mtotal, double thr,
-                                                             Part* __restrict__ parts, double* __restrict__ ms_out,
-                                                             int* __restrict__ err) {
+// next sequence in lexicographic order (std::next_permutation on a multiset);
+// the pivot lies at a position >= the run's common prefix
+__device__ __forceinline__ uint64_t lab_next(uint64_t lab, int n) {
+    int i = n - 2;
+    while (i >= 0 && lab_at(lab, i) >= lab_at(lab, i + 1)) --i;
+    if (i < 0) return lab;
+    const int a = lab_at(lab, i);
+    int j = n - 1;
+    while (lab_at(lab, j) <= a) --j;
+    const int b = lab_at(lab, j);
+    lab = (lab & ~(0xFull << (4 * i)) & ~(0xFull << (4 * j))) | ((uint64_t)b << (4 * i)) | ((uint64_t)a << (4 * j));
+    // reverse positions i+1 .. n-1
+    uint64_t out = lab & ((i + 1 >= 16) ? ~0ull : ((1ull << (4 * (i + 1))) - 1ull));
+    for (int p = i + 1, q = n - 1; p < n; ++p, --q) out |= (uint64_t)lab_at(lab, q) << (4 * p);
+    return out;
+}
+
+// task order and packed prerequisites (1 + position of the worker's previous
+// task) of positions [M, n), from the counters of the prefix [0, M)
+__device__ __forceinline__ void lab_tasks(uint64_t lab, int N, int M, int n, uint64_t cnt, uint64_t last,
+                                          uint64_t& order, uint64_t& dseq) {
+    const uint64_t keep = (M >= 16) ? ~0ull : ((1ull << (4 * M)) - 1ull);
+    order &= keep;
+    dseq &= keep;
+    for (int p = M; p < n; ++p) {
+        const int w = lab_at(lab, p), sh = 4 * w;
+        const int c = (int)((cnt >> sh) & 0xF);
+        order |= (uint64_t)(w * N + c) << (4 * p);
+        dseq |= ((last >> sh) & 0xFull) << (4 * p);
+        cnt += 1ull << sh;
+        last = (last & ~(0xFull << sh)) | ((uint64_t)((p + 1) & 0xF) << sh);
+    }
+}
+
+template <bool SIGP2, bool PRE>
+__global__ void __launch_bounds__(kBlock) k_interleave_pfx(const double* __restrict__ durs, int T, int N,
+                                                           double sigma, uint64_t lo, uint64_t hi, uint64_t mtotal,
+                                                           int K, double thr, Part* __restrict__ parts,
+                                                           double* __restrict__ ms_out, int* __restrict__ err) {
     __shared__ double2 sdr[3 * kStride];
     __shared__ Part sh[32];
+    __shared__ CkSlots<1> ck;
     const int n = T * N;
     stage_dr(durs, n, sdr);
     __syncthreads();
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
+    const double rsig = __ddiv_rn(1.0, sigma);
+    const int ti = threadIdx.x;
     Part acc;
     part_init(acc);
+    const uint64_t runs = (hi - lo + (uint64_t)K - 1) / (uint64_t)K;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t b0 = lo + (uint64_t)blockIdx.x * blockDim.x; b0 < hi; b0 += stride) {
-        const uint64_t r = b0 + threadIdx.x;
-        const bool valid = r < hi;
+    for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < runs; b0 += stride) {
+        const uint64_t run = b0 + ti;
+        const bool valid = run < runs;
+        const uint64_t r0 = lo + (valid ? run : 0) * (uint64_t)K;
+        const uint64_t r1 = (r0 + (uint64_t)K < hi) ? r0 + (uint64_t)K : hi;
+        uint64_t lab = unrank_lab(r0, T, N, mtotal);
+        const uint64_t x = lab ^ unrank_lab(r1 - 1, T, N, mtotal);
+        const int M = x ? (__ffsll((long long)x) - 1) >> 2 : n;
+        // prefix counters: occurrences and 1 + last position per worker
+        uint64_t cnt = 0, last = 0, order = 0, dseq = 0;
+        lab_tasks(lab, N, 0, n, 0, 0, order, dseq);
+        for (int p = 0; p < M; ++p) {
+            const int sh4 = 4 * lab_at(lab, p);
+            cnt += 1ull << sh4;
+            last = (last & ~(0xFull << sh4)) | ((uint64_t)((p + 1) & 0xF) << sh4);
+        }
+        FastSim<2, SIGP2, false, PRE, true> s;
+        s.init(base, order, n);
+        s.dseq = PRE ? (dseq << 4) : dseq;
+        const int sa = advance_to(s, M, sigma, rsig);
+        ck_store(ck, 0, ti, s);
+        const int rest = 3 * n - __reduce_min_sync(kFull, sa);
+#pragma unroll 1
+        for (int q = 0; q < K; ++q) {
+            if (q > 0) {
+                lab = lab_next(lab, n);
+                lab_tasks(lab, N, M, n, cnt, last, order, dseq);
+                ck_load(ck, 0, ti, s, M);
+                s.set_seq(order);
+                s.dseq = PRE ? (dseq << 4) : dseq;
+            } else {
+                ck_load(ck, 0, ti, s, M);
+            }
+            s.run_phased(rest, sigma, rsig);
+            const uint64_t r = r0 + (uint64_t)q;
+            if (valid && r < r1) {
+                if (!s.drained()) atomicExch(err, OSIM_ESTALL);
+                part_add<true>(acc, s.now, r, thr);
+                if (ms_out) ms_out[r - lo] = s.now;
+            }
+        }
+    }
+    acc = block_reduce(acc, sh);
+    if (threadIdx.x == 0) parts[blockIdx.x] = acc;
+}
+
+// 1-DMA runs.  The wave split of a sequence is fixed on the common prefix
+// except for where its last wave ends (that depends on the label at M), so
+// the checkpoint keeps the clock, the K lane and the XFER slot count, and
+// each sequence recomputes its waves and, from them, the XFER item that
+// follows HtD(M - 1): HtD(M) when M is inside that wave, else the wave's
+// DtH block.
+__device__ __forceinline__ void lab_waves(uint64_t lab, int n, uint64_t& wsq, uint64_t& weq) {
+    unsigned starts = 0;
+    uint64_t last = 0;  // 1 + last position per worker
+    int w0 = 0;
+    for (int p = 0; p < n; ++p) {
+        const int sh = 4 * lab_at(lab, p);
+        const int lp = (int)((last >> sh) & 0xF) - 1;
+        if (p == 0 || lp >= w0) { starts |= 1u << p; w0 = p; }
+        last = (last & ~(0xFull << sh)) | ((uint64_t)((p + 1) & 0xF) << sh);
+    }
+    wsq = weq = 0;
+    int ws = 0;
+    for (int p = 0; p < n; ++p) {
+        if ((starts >> p) & 1u) ws = p;
+        const unsigned after = starts & ~((2u << p) - 1u);
+        const int we = after ? __ffs(after) - 1 : n;
+        wsq |= (uint64_t)ws << (4 * p);
+        weq |= (uint64_t)(we - 1) << (4 * p);
+    }
+}
+
+template <bool PRE>
+__global__ void __launch_bounds__(kBlock) k_interleave_pfx1(const double* __restrict__ durs, int T, int N,
+                                                            uint64_t lo, uint64_t hi, uint64_t mtotal, int K,
+                                                            double thr, Part* __restrict__ parts,
+                                                            double* __restrict__ ms_out, int* __restrict__ err) {
+    __shared__ double2 sdr[3 * kStride];
+    __shared__ Part sh[32];
+    __shared__ double cv[4][kBlock];  // now, r2, d2, c2
+    __shared__ int cx[2][kBlock];     // x, s2
+    const int n = T * N;
+    stage_dr(durs, n, sdr);
+    __syncthreads();
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
+    const int ti = threadIdx.x;
+    Part acc;
+    part_init(acc);
+    const uint64_t runs = (hi - lo + (uint64_t)K - 1) / (uint64_t)K;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < runs; b0 += stride) {
+        const uint64_t run = b0 + ti;
+        const bool valid = run < runs;
+        const uint64_t r0 = lo + (valid ? run : 0) * (uint64_t)K;
+        const uint64_t r1 = (r0 + (uint64_t)K < hi) ? r0 + (uint64_t)K : hi;
+        uint64_t lab = unrank_lab(r0, T, N, mtotal);
+        const uint64_t x = lab ^ unrank_lab(r1 - 1, T, N, mtotal);
+        const int M = x ? (__ffsll((long long)x) - 1) >> 2 : n;
+        uint64_t cnt = 0, last = 0, order = 0, dseq = 0;
+        lab_tasks(lab, N, 0, n, 0, 0, order, dseq);
+        for (int p = 0; p < M; ++p) {
+            const int sh4 = 4 * lab_at(lab, p);
+            cnt += 1ull << sh4;
+            last = (last & ~(0xFull << sh4)) | ((uint64_t)((p + 1) & 0xF) << sh4);
+        }
         uint64_t wsq, weq;
-        const uint64_t order = unrank_labels_waves(valid ? r : lo, T, N, mtotal, wsq, weq);
+        lab_waves(lab, n, wsq, weq);
         WaveSim<PRE> s;
         s.init(base, order, n, wsq, weq);
+        // phase A: to the finalize of HtD(M - 1) = XFER slot M - 1 + ws(M - 1)
+        const int xt = (M > 0) ? 4 * (M + s.wsof(M - 1)) : 0;
+        int sa = 0;
 #pragma unroll 1
-        for (int st = 0; st < 3 * n; st += 2) {
-            s.step();
-            s.step();
+        while (__any_sync(kFull, s.x < xt && sa < 3 * kMaxN)) {
+            if (s.x < xt && sa < 3 * kMaxN) {
+                s.step();
+                ++sa;
+            }
         }
-        if (valid) {
-            if (!s.drained()) atomicExch(err, OSIM_ESTALL);
-            part_add<true>(acc, s.now, r, thr);
-            if (ms_out) ms_out[r - lo] = s.now;
+        cv[0][ti] = s.now; cv[1][ti] = s.r2; cv[2][ti] = s.d2; cv[3][ti] = s.c2;
+        cx[0][ti] = s.x; cx[1][ti] = s.s2;
+        const int rest = 3 * n - __reduce_min_sync(kFull, sa);
+#pragma unroll 1
+        for (int q = 0; q < K; ++q) {
+            if (q > 0) {
+                lab = lab_next(lab, n);
+                lab_tasks(lab, N, M, n, cnt, last, order, dseq);
+                lab_waves(lab, n, wsq, weq);
+            }
+            s.init(base, order, n, wsq, weq);
+            s.now = cv[0][ti]; s.r2 = cv[1][ti]; s.d2 = cv[2][ti]; s.c2 = cv[3][ti];
+            s.x = cx[0][ti]; s.s2 = cx[1][ti];
+            if (M > 0) {  // the XFER item after HtD(M - 1)
+                if (M < s.weof(M - 1)) { s.p0 = M; s.h0 = 0; }
+                else { s.p0 = s.wsof(M - 1); s.h0 = 1; }
+            }
+#pragma unroll 1
+            for (int st = 0; st < rest; st += 2) {
+                s.step();
+                s.step();
+            }
+            const uint64_t r = r0 + (uint64_t)q;
+            if (valid && r < r1) {
+                if (!s.drained()) atomicExch(err, OSIM_ESTALL);
+                part_add<true>(acc, s.now, r, thr);
+                if (ms_out) ms_out[r - lo] = s.now;
+            }
         }
     }
     acc = block_reduce(acc, sh);

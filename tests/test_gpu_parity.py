@@ -447,12 +447,34 @@ def test_noreorder_fast_path_4x4_vs_oracle():
     lo, hi = 31_000_000, 31_300_000
     cpus = os.cpu_count() or 4
     for dma, sigma in ((2, 0.5), (2, 0.375), (1, 1.0)):
-        # 1-DMA: the wave-split fast kernel (k_interleave_fast1)
+        # 1-DMA: the wave-split fast kernel (k_interleave_pfx1)
         s, below, ms = _capi.interleavings(d, 4, 4, dma, sigma, lo, hi, threshold=90.0, want_makespans=True)
         o, oms = O.interleavings(d, 4, 4, dma, sigma, lo, hi, threads=cpus, makespans=True)
         assert np.array_equal(ms, oms)
         assert_summary_vs_oracle(s, o)
         assert below == int((oms < 90.0).sum())
+
+
+@pytest.mark.parametrize("T,N,lo,hi", [
+    (3, 5, 0, 756756),          # n = 15: pre-shifted packing, the whole space
+    (2, 8, 5, 12870 - 3),       # ragged ends
+    (1, 16, 0, 1),              # one sequence: the run is the whole ordering
+    (16, 1, 1_000_000_007, 1_000_000_007 + 20_011),  # 16! / 1 labels, prime-length window
+    (4, 4, 62_000_001, 62_100_000),
+    (4, 4, 7, 8),               # a single rank inside a run
+])
+def test_noreorder_prefix_runs_vs_oracle(T, N, lo, hi):
+    # k_interleave_pfx / k_interleave_pfx1 (1-DMA waves): runs of consecutive
+    # ranks share their label prefix; windows cut runs anywhere, shapes cover
+    # both packings and T or N = 1
+    d = synth.real_group("K20", T * N, 7 + T)[1]
+    cpus = os.cpu_count() or 4
+    for dma, sigma in ((2, 0.5), (2, 0.375), (1, 1.0)):
+        s, below, ms = _capi.interleavings(d, T, N, dma, sigma, lo, hi, threshold=60.0, want_makespans=True)
+        o, oms = O.interleavings(d, T, N, dma, sigma, lo, hi, threads=cpus, makespans=True)
+        assert np.array_equal(ms, oms)
+        assert_summary_vs_oracle(s, o)
+        assert below == int((oms < 60.0).sum())
 
 
 def test_simulate_with_deps_dropin():

@@ -30,9 +30,9 @@ def main():
     print(f"heuristic, fast kernel (same batch): {1e5 / t / 1e6:.1f} M decisions/s")
     d1 = synth.real_group("K20", 12, 41)[1]
     t = best(lambda: _capi.interleavings(d1, 4, 3, 1, 1.0, 0, 369600))
-    print(f"f1 1-DMA waves (k_interleave_fast1): {369600 / t / 1e9:.3f} G interleavings/s")
+    print(f"f1 1-DMA waves (k_interleave_pfx1): {369600 / t / 1e9:.3f} G interleavings/s")
     t = best(lambda: _capi.interleavings(d1, 4, 3, 2, 0.5, 0, 369600))
-    print(f"f1 2-DMA (fast): {369600 / t / 1e9:.3f} G interleavings/s")
+    print(f"f1 2-DMA (k_interleave_pfx): {369600 / t / 1e9:.3f} G interleavings/s")
     d4 = synth.c4_group()
     perms = np.stack([np.random.default_rng(i).permutation(12) for i in range(200_000)]).astype(np.uint8)
     t = best(lambda: _capi.eval_perms(d4, 2, 0.5, perms))
