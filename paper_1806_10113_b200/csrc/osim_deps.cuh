@@ -367,14 +367,87 @@ __device__ __forceinline__ void lab_tasks(uint64_t lab, int N, int M, int n, uin
     }
 }
 
+// Runs are sorted by phase-A step count within the CTA before the replays
+// (a deterministic counting sort, as pfx_sort): a warp's replays run for
+// 3n - min(sa) steps, and unsorted runs mix common prefixes of very
+// different lengths.
+#ifndef OSIM_F1_MINB
+#define OSIM_F1_MINB 3
+#endif
+struct RunSort {
+    int cnt[kNW][kSaBins];
+    int base[kSaBins];
+    short order[kBlock];
+    uint64_t lab[kBlock], r0[kBlock];
+    int m[kBlock], sa[kBlock];  // m: M | valid << 8
+};
+
+__device__ __forceinline__ int run_sort(RunSort& S, int key) {
+    const int ti = threadIdx.x, lane = ti & 31, w = ti >> 5;
+    for (int i = lane; i < kSaBins; i += 32) S.cnt[w][i] = 0;
+    __syncwarp();
+    const unsigned m = __match_any_sync(kFull, key);
+    if (lane == __ffs(m) - 1) S.cnt[w][key] = __popc(m);
+    __syncthreads();
+    if (w == 0) {
+        int carry = 0;
+#pragma unroll
+        for (int b0 = 0; b0 < kSaBins; b0 += 32) {
+            const int b = b0 + lane;
+            int t = 0;
+#pragma unroll
+            for (int ww = 0; ww < kNW; ++ww) t += S.cnt[ww][b];
+            int x = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(kFull, x, o);
+                if (lane >= o) x += y;
+            }
+            S.base[b] = carry + x - t;
+            carry += __shfl_sync(kFull, x, 31);
+        }
+    }
+    __syncthreads();
+    int r = S.base[key] + __popc(m & ((1u << lane) - 1u));
+    for (int ww = 0; ww < w; ++ww) r += S.cnt[ww][key];
+    S.order[r] = (short)ti;
+    __syncthreads();
+    return S.order[ti];
+}
+
+// first and last rank of this thread's run, its labels and common prefix
+__device__ __forceinline__ void run_open(uint64_t run, uint64_t runs, uint64_t lo, uint64_t hi, int K, int T, int N,
+                                         uint64_t mtotal, uint64_t& r0, uint64_t& lab, int& M) {
+    const int n = T * N;
+    r0 = lo + (run < runs ? run : 0) * (uint64_t)K;
+    const uint64_t r1 = (r0 + (uint64_t)K < hi) ? r0 + (uint64_t)K : hi;
+    lab = unrank_lab(r0, T, N, mtotal);
+    const uint64_t x = lab ^ unrank_lab(r1 - 1, T, N, mtotal);
+    M = x ? (__ffsll((long long)x) - 1) >> 2 : n;
+}
+
+// task order, prerequisites and the prefix counters (occurrences, 1 + last
+// position per worker) of a run's first sequence
+__device__ __forceinline__ void run_tasks(uint64_t lab, int N, int M, int n, uint64_t& cnt, uint64_t& last,
+                                          uint64_t& order, uint64_t& dseq) {
+    cnt = last = order = dseq = 0;
+    lab_tasks(lab, N, 0, n, 0, 0, order, dseq);
+    for (int p = 0; p < M; ++p) {
+        const int sh4 = 4 * lab_at(lab, p);
+        cnt += 1ull << sh4;
+        last = (last & ~(0xFull << sh4)) | ((uint64_t)((p + 1) & 0xF) << sh4);
+    }
+}
+
 template <bool SIGP2, bool PRE>
-__global__ void __launch_bounds__(kBlock) k_interleave_pfx(const double* __restrict__ durs, int T, int N,
+__global__ void __launch_bounds__(kBlock, OSIM_F1_MINB) k_interleave_pfx(const double* __restrict__ durs, int T, int N,
                                                            double sigma, uint64_t lo, uint64_t hi, uint64_t mtotal,
                                                            int K, double thr, Part* __restrict__ parts,
                                                            double* __restrict__ ms_out, int* __restrict__ err) {
     __shared__ double2 sdr[3 * kStride];
     __shared__ Part sh[32];
     __shared__ CkSlots<1> ck;
+    __shared__ RunSort S;
     const int n = T * N;
     stage_dr(durs, n, sdr);
     __syncthreads();
@@ -386,38 +459,46 @@ __global__ void __launch_bounds__(kBlock) k_interleave_pfx(const double* __restr
     const uint64_t runs = (hi - lo + (uint64_t)K - 1) / (uint64_t)K;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < runs; b0 += stride) {
-        const uint64_t run = b0 + ti;
-        const bool valid = run < runs;
-        const uint64_t r0 = lo + (valid ? run : 0) * (uint64_t)K;
-        const uint64_t r1 = (r0 + (uint64_t)K < hi) ? r0 + (uint64_t)K : hi;
-        uint64_t lab = unrank_lab(r0, T, N, mtotal);
-        const uint64_t x = lab ^ unrank_lab(r1 - 1, T, N, mtotal);
-        const int M = x ? (__ffsll((long long)x) - 1) >> 2 : n;
-        // prefix counters: occurrences and 1 + last position per worker
-        uint64_t cnt = 0, last = 0, order = 0, dseq = 0;
-        lab_tasks(lab, N, 0, n, 0, 0, order, dseq);
-        for (int p = 0; p < M; ++p) {
-            const int sh4 = 4 * lab_at(lab, p);
-            cnt += 1ull << sh4;
-            last = (last & ~(0xFull << sh4)) | ((uint64_t)((p + 1) & 0xF) << sh4);
+        __syncthreads();  // the previous round's slots have been read
+        // ---- phase A: this thread's run to its common-prefix checkpoint
+        {
+            const uint64_t run = b0 + ti;
+            uint64_t r0, lab, cnt, last, order, dseq;
+            int M;
+            run_open(run, runs, lo, hi, K, T, N, mtotal, r0, lab, M);
+            run_tasks(lab, N, M, n, cnt, last, order, dseq);
+            FastSim<2, SIGP2, false, PRE, true> s;
+            s.init(base, order, n);
+            s.dseq = PRE ? (dseq << 4) : dseq;
+            const int sa = advance_to(s, M, sigma, rsig);
+            ck_store(ck, 0, ti, s);
+            const bool valid = run < runs;
+            S.lab[ti] = lab;
+            S.r0[ti] = r0;
+            S.m[ti] = M | (valid ? 256 : 0);
+            S.sa[ti] = valid ? sa : kSaBins - 1;
         }
+        // ---- reassign by sa, then replay the taken run's sequences
+        const int e = run_sort(S, S.sa[ti]);
+        const uint64_t r0 = S.r0[e];
+        uint64_t lab = S.lab[e];
+        const int M = S.m[e] & 255;
+        const bool valid = (S.m[e] >> 8) != 0;
+        const uint64_t r1 = (r0 + (uint64_t)K < hi) ? r0 + (uint64_t)K : hi;
+        uint64_t cnt, last, order, dseq;
+        run_tasks(lab, N, M, n, cnt, last, order, dseq);
+        const int rest = 3 * n - __reduce_min_sync(kFull, valid ? S.sa[e] : 3 * n);
         FastSim<2, SIGP2, false, PRE, true> s;
         s.init(base, order, n);
-        s.dseq = PRE ? (dseq << 4) : dseq;
-        const int sa = advance_to(s, M, sigma, rsig);
-        ck_store(ck, 0, ti, s);
-        const int rest = 3 * n - __reduce_min_sync(kFull, sa);
 #pragma unroll 1
         for (int q = 0; q < K; ++q) {
             if (q > 0) {
                 lab = lab_next(lab, n);
                 lab_tasks(lab, N, M, n, cnt, last, order, dseq);
-                ck_load(ck, 0, ti, s, M);
-                s.set_seq(order);
-                s.dseq = PRE ? (dseq << 4) : dseq;
-            } else {
-                ck_load(ck, 0, ti, s, M);
             }
+            ck_load(ck, 0, e, s, M);
+            s.set_seq(order);
+            s.dseq = PRE ? (dseq << 4) : dseq;
             s.run_phased(rest, sigma, rsig);
             const uint64_t r = r0 + (uint64_t)q;
             if (valid && r < r1) {
@@ -459,7 +540,7 @@ __device__ __forceinline__ void lab_waves(uint64_t lab, int n, uint64_t& wsq, ui
 }
 
 template <bool PRE>
-__global__ void __launch_bounds__(kBlock) k_interleave_pfx1(const double* __restrict__ durs, int T, int N,
+__global__ void __launch_bounds__(kBlock, OSIM_F1_MINB) k_interleave_pfx1(const double* __restrict__ durs, int T, int N,
                                                             uint64_t lo, uint64_t hi, uint64_t mtotal, int K,
                                                             double thr, Part* __restrict__ parts,
                                                             double* __restrict__ ms_out, int* __restrict__ err) {
@@ -467,6 +548,7 @@ __global__ void __launch_bounds__(kBlock) k_interleave_pfx1(const double* __rest
     __shared__ Part sh[32];
     __shared__ double cv[4][kBlock];  // now, r2, d2, c2
     __shared__ int cx[2][kBlock];     // x, s2
+    __shared__ RunSort S;
     const int n = T * N;
     stage_dr(durs, n, sdr);
     __syncthreads();
@@ -477,47 +559,54 @@ __global__ void __launch_bounds__(kBlock) k_interleave_pfx1(const double* __rest
     const uint64_t runs = (hi - lo + (uint64_t)K - 1) / (uint64_t)K;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < runs; b0 += stride) {
-        const uint64_t run = b0 + ti;
-        const bool valid = run < runs;
-        const uint64_t r0 = lo + (valid ? run : 0) * (uint64_t)K;
-        const uint64_t r1 = (r0 + (uint64_t)K < hi) ? r0 + (uint64_t)K : hi;
-        uint64_t lab = unrank_lab(r0, T, N, mtotal);
-        const uint64_t x = lab ^ unrank_lab(r1 - 1, T, N, mtotal);
-        const int M = x ? (__ffsll((long long)x) - 1) >> 2 : n;
-        uint64_t cnt = 0, last = 0, order = 0, dseq = 0;
-        lab_tasks(lab, N, 0, n, 0, 0, order, dseq);
-        for (int p = 0; p < M; ++p) {
-            const int sh4 = 4 * lab_at(lab, p);
-            cnt += 1ull << sh4;
-            last = (last & ~(0xFull << sh4)) | ((uint64_t)((p + 1) & 0xF) << sh4);
-        }
-        uint64_t wsq, weq;
-        lab_waves(lab, n, wsq, weq);
-        WaveSim<PRE> s;
-        s.init(base, order, n, wsq, weq);
-        // phase A: to the finalize of HtD(M - 1) = XFER slot M - 1 + ws(M - 1)
-        const int xt = (M > 0) ? 4 * (M + s.wsof(M - 1)) : 0;
-        int sa = 0;
+        __syncthreads();  // the previous round's slots have been read
+        {
+            const uint64_t run = b0 + ti;
+            uint64_t r0, lab, cnt, last, order, dseq, wsq, weq;
+            int M;
+            run_open(run, runs, lo, hi, K, T, N, mtotal, r0, lab, M);
+            run_tasks(lab, N, M, n, cnt, last, order, dseq);
+            lab_waves(lab, n, wsq, weq);
+            WaveSim<PRE> s;
+            s.init(base, order, n, wsq, weq);
+            // phase A: to the finalize of HtD(M - 1) = XFER slot M - 1 + ws(M - 1)
+            const int xt = (M > 0) ? 4 * (M + s.wsof(M - 1)) : 0;
+            int sa = 0;
 #pragma unroll 1
-        while (__any_sync(kFull, s.x < xt && sa < 3 * kMaxN)) {
-            if (s.x < xt && sa < 3 * kMaxN) {
-                s.step();
-                ++sa;
+            while (__any_sync(kFull, s.x < xt && sa < 3 * kMaxN)) {
+                if (s.x < xt && sa < 3 * kMaxN) {
+                    s.step();
+                    ++sa;
+                }
             }
+            cv[0][ti] = s.now; cv[1][ti] = s.r2; cv[2][ti] = s.d2; cv[3][ti] = s.c2;
+            cx[0][ti] = s.x; cx[1][ti] = s.s2;
+            const bool valid = run < runs;
+            S.lab[ti] = lab;
+            S.r0[ti] = r0;
+            S.m[ti] = M | (valid ? 256 : 0);
+            S.sa[ti] = valid ? sa : kSaBins - 1;
         }
-        cv[0][ti] = s.now; cv[1][ti] = s.r2; cv[2][ti] = s.d2; cv[3][ti] = s.c2;
-        cx[0][ti] = s.x; cx[1][ti] = s.s2;
-        const int rest = 3 * n - __reduce_min_sync(kFull, sa);
+        const int e = run_sort(S, S.sa[ti]);
+        const uint64_t r0 = S.r0[e];
+        uint64_t lab = S.lab[e];
+        const int M = S.m[e] & 255;
+        const bool valid = (S.m[e] >> 8) != 0;
+        const uint64_t r1 = (r0 + (uint64_t)K < hi) ? r0 + (uint64_t)K : hi;
+        uint64_t cnt, last, order, dseq, wsq, weq;
+        run_tasks(lab, N, M, n, cnt, last, order, dseq);
+        const int rest = 3 * n - __reduce_min_sync(kFull, valid ? S.sa[e] : 3 * n);
+        WaveSim<PRE> s;
 #pragma unroll 1
         for (int q = 0; q < K; ++q) {
             if (q > 0) {
                 lab = lab_next(lab, n);
                 lab_tasks(lab, N, M, n, cnt, last, order, dseq);
-                lab_waves(lab, n, wsq, weq);
             }
+            lab_waves(lab, n, wsq, weq);
             s.init(base, order, n, wsq, weq);
-            s.now = cv[0][ti]; s.r2 = cv[1][ti]; s.d2 = cv[2][ti]; s.c2 = cv[3][ti];
-            s.x = cx[0][ti]; s.s2 = cx[1][ti];
+            s.now = cv[0][e]; s.r2 = cv[1][e]; s.d2 = cv[2][e]; s.c2 = cv[3][e];
+            s.x = cx[0][e]; s.s2 = cx[1][e];
             if (M > 0) {  // the XFER item after HtD(M - 1)
                 if (M < s.weof(M - 1)) { s.p0 = M; s.h0 = 0; }
                 else { s.p0 = s.wsof(M - 1); s.h0 = 1; }

@@ -1,6 +1,6 @@
 """Short single-GPU workloads for ncu captures (one launch of each kernel).
 
-    python tools/profile_run.py c4|c3|c2|c5|all
+    python tools/profile_run.py c4|c3|c2|c5|f1|all
 """
 import os
 import sys
@@ -26,6 +26,11 @@ def main(which):
         d, r = synth.c5_batch_fast("nvidia", 200_000)
         o, m, n = _capi.heuristic_batch(d, r, 2, 0.5, 1)
         print("c5", o[0], m[0], n[0])
+    if which in ("f1", "all"):
+        d = synth.real_group("K20", 16, 41)[1]
+        for dma, sigma in ((2, 0.5), (1, 1.0)):
+            s, _, _ = _capi.interleavings(d, 4, 4, dma, sigma, 0, 63_063_000)
+            print("f1", dma, s)
 
 
 if __name__ == "__main__":
