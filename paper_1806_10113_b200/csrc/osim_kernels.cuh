@@ -959,11 +959,16 @@ struct HeurWarpShared {
     double ka[kWG * kKeyN];  // per-candidate keys (m <= 15 per round)
     double kb[kWG * kKeyN];
     uint64_t ot[kWG];
-    unsigned rmask[kWG];
+    uint64_t cand[kWG];  // rt: remaining task ids in input order, 4 bits each
     uint8_t idr[kWG * kMaxN];
-    uint8_t cand[kWG * kMaxN];
     uint8_t pa[kWG], pb[kWG];
 };
+
+// packed rt list: entry j, and the list without entry j (order kept)
+__device__ __forceinline__ int rt_at(uint64_t l, int j) { return (int)((l >> (4 * j)) & 0xF); }
+__device__ __forceinline__ uint64_t rt_drop(uint64_t l, int j) {
+    return (l & ((1ull << (4 * j)) - 1ull)) | ((l >> (4 * j + 4)) << (4 * j));
+}
 
 // (estimate, idle_K, id rank) key of select_next_task (heuristic.py:74-76)
 __device__ __forceinline__ bool key_less(double e, double d, int r, double be, double bd, int br) {
@@ -1010,6 +1015,7 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
     if (lane < Gv) {
         const int g = lane;
         const unsigned all = (1u << n) - 1u;
+        unsigned rm;
         FS s;
         if (n >= 3) {
             int best = -1;
@@ -1027,18 +1033,19 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
                 if (less) { best = t; b1 = k1; b2 = k2; }
             }
             S.ot[g] = (uint64_t)best;
-            S.rmask[g] = all & ~(1u << best);
+            rm = all & ~(1u << best);
             s.init(gbase(g), S.ot[g], 1);
             for (int q = 0; q < 3 * kMaxN && s.htd_done() < 1; ++q) s.step(sigma, rsig);
         } else {
             S.ot[g] = 0;
-            S.rmask[g] = all;
+            rm = all;
             s.init(gbase(g), 0, 1);  // empty prefix: the initial state
         }
         s.save(S.ck[g]);
-        int c = 0;
-        for (int t = 0; t < n; ++t)
-            if ((S.rmask[g] >> t) & 1u) S.cand[g * kMaxN + c++] = (uint8_t)t;
+        uint64_t cl = 0;
+        for (int t = n - 1; t >= 0; --t)
+            if ((rm >> t) & 1u) cl = (cl << 4) | (uint64_t)t;
+        S.cand[g] = cl;
     }
     __syncwarp();
 
@@ -1051,7 +1058,8 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
             const bool valid = i < items;
             const int g = valid ? i / m : 0;
             const int j = valid ? i % m : 0;
-            const int c = S.cand[g * kMaxN + j];
+            const uint64_t cl0 = S.cand[g];
+            const int c = rt_at(cl0, j);
             FS s;
             s.init(gbase(g), S.ot[g] | ((uint64_t)c << (4 * k)), k + 1);
             s.load(S.ck[g]);
@@ -1061,10 +1069,10 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
             // rest's t_k in rt order (cand[] is rt in input order, rest skips
             // position j), min t_dth.  Warp-uniform loop over the m-1 rest.
             double f = 0.0, cmp = 0.0, tail = kBig;
-            const uint8_t* cl = &S.cand[g * kMaxN];
+            uint64_t rl = rt_drop(cl0, j);
 #pragma unroll 1
-            for (int i = 0; i < m - 1; ++i) {
-                const int t = cl[i + (i >= j ? 1 : 0)];
+            for (int i = 0; i < m - 1; ++i, rl >>= 4) {
+                const int t = (int)(rl & 0xF);
                 const double2 kd = make_double2(DV(g, 1, t), DV(g, 2, t));
                 const double x = kd.x;
                 const double tt = __dadd_rn(f, x);
@@ -1100,7 +1108,7 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
             if (g < Gv) {
                 for (int j = part; j < m; j += kLPG) {
                     const double e = S.ka[g * kKeyN + j], d = S.kb[g * kKeyN + j];
-                    const int r = S.idr[g * kMaxN + S.cand[g * kMaxN + j]];
+                    const int r = S.idr[g * kMaxN + rt_at(S.cand[g], j)];
                     if (lj < 0 || key_less(e, d, r, le, ld, lr)) { lj = j; le = e; ld = d; lr = r; }
                 }
             }
@@ -1115,12 +1123,9 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
         }
         if (lane < Gv) {
             const int g = lane;
-            const int c = S.cand[g * kMaxN + bj];
+            const int c = rt_at(S.cand[g], bj);
             S.ot[g] |= (uint64_t)c << (4 * k);
-            S.rmask[g] &= ~(1u << c);
-            int cc = 0;
-            for (int t = 0; t < n; ++t)
-                if ((S.rmask[g] >> t) & 1u) S.cand[g * kMaxN + cc++] = (uint8_t)t;
+            S.cand[g] = rt_drop(S.cand[g], bj);
             // advance the checkpoint by the chosen task (prefix length k+1)
             FS s;
             s.init(gbase(g), S.ot[g], k + 1);
@@ -1136,7 +1141,7 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
     if (n >= 2) {
         if (lane < Gv) {
             const int g = lane;
-            int a = S.cand[g * kMaxN + 0], b = S.cand[g * kMaxN + 1];
+            int a = rt_at(S.cand[g], 0), b = rt_at(S.cand[g], 1);
             if (S.idr[g * kMaxN + b] < S.idr[g * kMaxN + a]) { int x = a; a = b; b = x; }
             S.pa[g] = (uint8_t)a;
             S.pb[g] = (uint8_t)b;
