@@ -1053,11 +1053,15 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
     for (int k = k0; n - k > 2; ++k) {  // heuristic.py:120-123
         const int m = n - k;
         const int items = Gv * m;
+        // i / m for i < 2^7 by a 16-bit reciprocal: (i * (2^16/m + 1)) >> 16
+        // is exact (the excess i/2^16 < 2^-9 stays below 1/m)
+        const unsigned minv = 65536u / (unsigned)m + 1u;
         for (int i0 = 0; i0 < items; i0 += 32) {
             const int i = i0 + lane;
             const bool valid = i < items;
-            const int g = valid ? i / m : 0;
-            const int j = valid ? i % m : 0;
+            const int gq = (int)(((unsigned)i * minv) >> 16);
+            const int g = valid ? gq : 0;
+            const int j = valid ? i - gq * m : 0;
             const uint64_t cl0 = S.cand[g];
             const int c = rt_at(cl0, j);
             FS s;
