@@ -1074,7 +1074,7 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
             // position j), min t_dth.  Warp-uniform loop over the m-1 rest.
             double f = 0.0, cmp = 0.0, tail = kBig;
             uint64_t rl = rt_drop(cl0, j);
-#pragma unroll 1
+#pragma unroll 2
             for (int i = 0; i < m - 1; ++i, rl >>= 4) {
                 const int t = (int)(rl & 0xF);
                 const double2 kd = make_double2(DV(g, 1, t), DV(g, 2, t));
