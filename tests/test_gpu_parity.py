@@ -728,6 +728,46 @@ def test_two_rank_shards_through_the_library_combine_exactly():
         assert close(mean, whole.mean, REL) and close(geo, whole.geomean, REL)
 
 
+def _nccl_worker(port, q):
+    import torch
+    import torch.distributed as tdist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_1806_10113_b200.dist import exhaustive_summary_distributed
+
+        s = exhaustive_summary_distributed(synth.c3_group(), 2, 0.5)  # NCCL all_gather of device tensors
+        q.put((s.best, s.best_ordering, s.worst, s.mean, s.count))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_nccl_exchange_single_rank():
+    # the NCCL branch of the sharded combine (device tensors, all_gather over
+    # NCCL) at world size 1 -- the bench's N>1 code path on the one GPU here
+    import socket
+
+    import torch.multiprocessing as mp
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(port, q))
+    p.start()
+    best, order, worst, mean, count = q.get(timeout=300)
+    p.join(timeout=120)
+    assert p.exitcode == 0
+    whole = osim.exhaustive_summary_durs(synth.c3_group(), 2, 0.5)
+    assert best == whole.best and tuple(order) == tuple(whole.best_ordering) and worst == whole.worst
+    assert count == 3628800 and mean == whole.mean
+
+
 def test_sigma_at_the_fast_range_boundary():
     # sigma = 2^-60 is the smallest fast-path sigma; just below it the
     # general (IEEE division) path runs; both bit-exact with the oracle
