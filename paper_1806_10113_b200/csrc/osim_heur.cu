@@ -33,3 +33,11 @@ void heuristic_launch(int dma, int mode, const LaunchCfg& cfg, const double* d_d
 }
 
 }  // namespace osim
+
+#ifdef OSIM_HSTATS
+extern "C" int osim_hstats(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, osim::g_hstats, sizeof(osim::g_hstats));
+    if (reset) { unsigned long long z[8] = {0}; cudaMemcpyToSymbol(osim::g_hstats, z, sizeof(z)); }
+    return 0;
+}
+#endif

@@ -951,6 +951,9 @@ constexpr int kHGF = kWG * kWPB;       // groups per CTA (fast kernel)
 constexpr int kHTF = 32 * kWPB;        // threads per CTA (fast kernel)
 static_assert(kLPG * kWG == 32 && kWG <= 16, "groups per warp");
 
+#ifdef OSIM_HSTATS
+__device__ unsigned long long g_hstats[8];
+#endif
 template <int DMA, bool SP2>
 struct HeurWarpShared {
     using FS = FastSim<DMA, SP2, true, false>;
@@ -1068,6 +1071,31 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
             s.init(gbase(g), S.ot[g] | ((uint64_t)c << (4 * k)), k + 1);
             s.load(S.ck[g]);
             const int rest = __reduce_max_sync(kFull, 3 * (k + 1) - s.finalized());
+#ifdef OSIM_HSTATS
+            {
+                FS t = s;
+                int h1 = 0, own = 0;
+                for (int q = 0; q < rest; ++q) {
+                    if (t.s0 < t.n4) ++h1;
+                    if (!t.drained()) ++own;
+                    t.step(sigma, rsig);
+                }
+                const int mh1 = __reduce_max_sync(kFull, h1);
+                const unsigned vb = __ballot_sync(kFull, valid);
+                const int sown = __reduce_add_sync(kFull, valid ? own : 0);
+                const int sh1 = __reduce_add_sync(kFull, valid ? h1 : 0);
+                if (lane == 0) {
+                    atomicAdd(&g_hstats[0], (unsigned long long)(32 * rest));
+                    atomicAdd(&g_hstats[1], (unsigned long long)sown);
+                    atomicAdd(&g_hstats[2], (unsigned long long)(32 * mh1));
+                    atomicAdd(&g_hstats[3], (unsigned long long)sh1);
+                    atomicAdd(&g_hstats[4], (unsigned long long)((32 - __popc(vb)) * rest));
+                    atomicAdd(&g_hstats[5], 1ull);
+                    atomicAdd(&g_hstats[6], (unsigned long long)rest);
+                    atomicAdd(&g_hstats[7], (unsigned long long)mh1);
+                }
+            }
+#endif
             s.run_phased(rest, sigma, rsig);
             // _completion_estimate (heuristic.py:34-49): builtin sum of the
             // rest's t_k in rt order (cand[] is rt in input order, rest skips
