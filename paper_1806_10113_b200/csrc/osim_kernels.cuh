@@ -270,6 +270,37 @@ __device__ __forceinline__ void stage_dr(const double* __restrict__ g, int n, do
     }
 }
 
+#ifdef OSIM_HSTATS
+// lane-slot counters of lock-step replays (tools/heur_lanes.py, tools/pfx_lanes.py):
+// 32 x warp replay length, steps each lane needs, the same for the full-step
+// phase, empty-lane slots, replays, sum of warp replay lengths and full phases
+__device__ unsigned long long g_hstats[8];
+template <class FS>
+__device__ __forceinline__ void hstats_replay(const FS& s, int rest, bool valid, double sigma, double rsig) {
+    FS t = s;
+    int h1 = 0, own = 0;
+    for (int q = 0; q < rest; ++q) {
+        if (t.s0 < t.n4) ++h1;
+        if (!t.drained()) ++own;
+        t.step(sigma, rsig);
+    }
+    const int mh1 = __reduce_max_sync(kFull, h1);
+    const unsigned vb = __ballot_sync(kFull, valid);
+    const int sown = __reduce_add_sync(kFull, valid ? own : 0);
+    const int sh1 = __reduce_add_sync(kFull, valid ? h1 : 0);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&g_hstats[0], (unsigned long long)(32 * rest));
+        atomicAdd(&g_hstats[1], (unsigned long long)sown);
+        atomicAdd(&g_hstats[2], (unsigned long long)(32 * mh1));
+        atomicAdd(&g_hstats[3], (unsigned long long)sh1);
+        atomicAdd(&g_hstats[4], (unsigned long long)((32 - __popc(vb)) * rest));
+        atomicAdd(&g_hstats[5], 1ull);
+        atomicAdd(&g_hstats[6], (unsigned long long)rest);
+        atomicAdd(&g_hstats[7], (unsigned long long)mh1);
+    }
+}
+#endif
+
 // Per-thread checkpoint slots in shared memory, structure-of-arrays so that
 // the 32 lanes of a warp touch 32 consecutive 8-byte words (conflict-free);
 // keeping them out of registers lifts occupancy.  At a checkpoint the HtD lane
@@ -479,6 +510,9 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
             s.set_seq(pre | suf);
             // full steps while any lane of the warp still has an HtD to run, then
             // K+DtH steps, then DtH-only steps (FastSim::run_phased)
+#ifdef OSIM_HSTATS
+            hstats_replay(s, rest, validP, sigma, rsig);
+#endif
             s.run_phased(rest, sigma, rsig);
             const uint64_t r = r0 + (uint64_t)j;
             if (all_in || (any_in && r >= lo && r < hi)) {
@@ -951,9 +985,6 @@ constexpr int kHGF = kWG * kWPB;       // groups per CTA (fast kernel)
 constexpr int kHTF = 32 * kWPB;        // threads per CTA (fast kernel)
 static_assert(kLPG * kWG == 32 && kWG <= 16, "groups per warp");
 
-#ifdef OSIM_HSTATS
-__device__ unsigned long long g_hstats[8];
-#endif
 template <int DMA, bool SP2>
 struct HeurWarpShared {
     using FS = FastSim<DMA, SP2, true, false>;
@@ -1072,31 +1103,14 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
             s.load(S.ck[g]);
             const int rest = __reduce_max_sync(kFull, 3 * (k + 1) - s.finalized());
 #ifdef OSIM_HSTATS
-            {
-                FS t = s;
-                int h1 = 0, own = 0;
-                for (int q = 0; q < rest; ++q) {
-                    if (t.s0 < t.n4) ++h1;
-                    if (!t.drained()) ++own;
-                    t.step(sigma, rsig);
-                }
-                const int mh1 = __reduce_max_sync(kFull, h1);
-                const unsigned vb = __ballot_sync(kFull, valid);
-                const int sown = __reduce_add_sync(kFull, valid ? own : 0);
-                const int sh1 = __reduce_add_sync(kFull, valid ? h1 : 0);
-                if (lane == 0) {
-                    atomicAdd(&g_hstats[0], (unsigned long long)(32 * rest));
-                    atomicAdd(&g_hstats[1], (unsigned long long)sown);
-                    atomicAdd(&g_hstats[2], (unsigned long long)(32 * mh1));
-                    atomicAdd(&g_hstats[3], (unsigned long long)sh1);
-                    atomicAdd(&g_hstats[4], (unsigned long long)((32 - __popc(vb)) * rest));
-                    atomicAdd(&g_hstats[5], 1ull);
-                    atomicAdd(&g_hstats[6], (unsigned long long)rest);
-                    atomicAdd(&g_hstats[7], (unsigned long long)mh1);
-                }
-            }
+            hstats_replay(s, rest, valid, sigma, rsig);
 #endif
-            s.run_phased(rest, sigma, rsig);
+            if constexpr (DMA == 2) {
+                s.start_htd();  // the candidate's HtD, the only one left
+                s.run_phased<false>(rest, sigma, rsig);
+            } else {
+                s.run_phased(rest, sigma, rsig);
+            }
             // _completion_estimate (heuristic.py:34-49): builtin sum of the
             // rest's t_k in rt order (cand[] is rt in input order, rest skips
             // position j), min t_dth.  Warp-uniform loop over the m-1 rest.
@@ -1163,7 +1177,12 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
             s.init(gbase(g), S.ot[g], k + 1);
             s.load(S.ck[g]);
             // bounded: the optimistic host pass may run this on ineligible input
-            for (int q = 0; q < 3 * kMaxN && s.htd_done() < k + 1; ++q) s.step(sigma, rsig);
+            if constexpr (DMA == 2) {
+                s.start_htd();  // the chosen task's HtD, the queue's last
+                for (int q = 0; q < 3 * kMaxN && s.htd_done() < k + 1; ++q) s.step<false>(sigma, rsig);
+            } else {
+                for (int q = 0; q < 3 * kMaxN && s.htd_done() < k + 1; ++q) s.step(sigma, rsig);
+            }
             s.save(S.ck[g]);
         }
         __syncwarp();

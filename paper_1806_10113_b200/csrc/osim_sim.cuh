@@ -401,6 +401,9 @@ struct FastSim {
         idleK = 0.0;
     }
     __device__ __forceinline__ void set_seq(uint64_t sq) { seq = PRE ? (sq << 4) : sq; }
+    // start the HtD at the queue head now (the HtD lane is idle and an HtD
+    // is always ready): what the next step's start phase would do
+    __device__ __forceinline__ void start_htd() { start_if(true, base + task_off<PRE>(seq, s0), d0, c0, r0); }
     __device__ __forceinline__ int finalized() const { return (s0 + s1 + s2) >> 2; }
 
     // checkpoint image (prefix sharing across calls, e.g. in shared memory)
@@ -507,14 +510,17 @@ struct FastSim {
 
     // `rest` steps in warp lock-step, switching to the specialized steps as
     // soon as the whole warp has drained its HtD (then K) lanes
+    // H0 = false: see step(); the heuristic's candidate replays start the
+    // candidate's HtD (the queue's last) before the first step
+    template <bool H0 = true>
     __device__ __forceinline__ void run_phased(int rest, double sigma, double rsig) {
         int st = 0;
         if constexpr (DMA == 2) {
 #pragma unroll 1
             for (; st < rest; st += 2) {
                 if (__all_sync(0xffffffffu, s0 >= n4)) break;
-                step(sigma, rsig);
-                step(sigma, rsig);
+                step<H0>(sigma, rsig);
+                step<H0>(sigma, rsig);
             }
 #pragma unroll 1
             for (; st < rest; st += 2) {
@@ -550,16 +556,20 @@ struct FastSim {
         }
     }
 
+    // H0 = false (2-DMA): the caller has already started the last HtD of the
+    // queue, so no HtD can start in this step and its test and load are
+    // skipped (st0 would be false)
+    template <bool H0 = true>
     __device__ __forceinline__ void step(double sigma, double rsig) {
         // ---- start phase (engine.py:188-194); readiness in the all-non-null
         // case: K(p) needs HtD(p) finalized, DtH(p) needs K(p) finalized
         if constexpr (DMA == 2) {
-            bool st0 = idle(r0) && s0 < n4;
+            bool st0 = H0 && idle(r0) && s0 < n4;
             if constexpr (DEPS) st0 = st0 && s1 >= (int)(task_off<PRE>(dseq, s0) >> 2);
             const bool st2 = idle(r2) && s2 < s0;
             const bool st1 = idle(r1) && s1 < s2;
             k_idle_gap(st2);
-            start_if(st0, base + task_off<PRE>(seq, s0), d0, c0, r0);
+            if constexpr (H0) start_if(st0, base + task_off<PRE>(seq, s0), d0, c0, r0);
             start_if(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
             start_if(st1, base + 512 + task_off<PRE>(seq, s1), d1, c1, r1);
         } else {
