@@ -104,9 +104,9 @@ int scratch(DevCtx* c, size_t bytes, void** p) {
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 // ---- validation (model.py:63-71, 91-100; engine.py:129-130, 258-259) -----
-int check_common(int n, int dma, double sigma) {
+int check_common(int n, int dma, double sigma, int maxn = kMaxN) {
     if (n < 1) return fail(OSIM_EINVAL, "task group must be non-empty");
-    if (n > kMaxN) return fail(OSIM_EINVAL, "n=%d exceeds the supported maximum of %d tasks", n, kMaxN);
+    if (n > maxn) return fail(OSIM_EINVAL, "n=%d exceeds the supported maximum of %d tasks", n, maxn);
     if (dma != 1 && dma != 2) return fail(OSIM_EINVAL, "dma_engines must be 1 or 2, got %d", dma);
     if (!(sigma > 0.0 && sigma <= 1.0)) return fail(OSIM_EINVAL, "overlap_sigma must be in (0, 1]");
     return 0;
@@ -181,11 +181,11 @@ int check_id_ranks(const uint8_t* id_rank, uint64_t B, int n) {
     std::vector<uint64_t> bad(nt, ~0ull);
     auto work = [&](unsigned i) {
         for (uint64_t b = B * i / nt; b < B * (i + 1) / nt; ++b) {
-            unsigned seen = 0;
+            uint64_t seen = 0;
             for (int j = 0; j < n; ++j) {
                 const unsigned v = id_rank[b * n + j];
-                if (v >= (unsigned)n || ((seen >> v) & 1u)) { bad[i] = b; return; }
-                seen |= 1u << v;
+                if (v >= (unsigned)n || ((seen >> v) & 1ull)) { bad[i] = b; return; }
+                seen |= 1ull << v;
             }
         }
     };
@@ -433,6 +433,51 @@ int select_kth(std::vector<DevCtx*>& devs, std::vector<const double*>& vals, std
 }
 }  // namespace
 
+// Groups of 17..64 tasks (osim_wide.cuh): validated on the host, one
+// group per thread on the general path, sharded over devices by group range.
+int heuristic_wide(const double* durs, const uint8_t* id_rank, uint64_t B, int n, int dma, double sigma,
+                   int sum_mode, int n_dev, uint8_t* order, double* makespan, uint32_t* n_sims) {
+    int rc = check_common(n, dma, sigma, kWideMaxN);
+    if (rc) return rc;
+    if (B && (!durs || !id_rank || !order || !makespan)) return fail(OSIM_EINVAL, "NULL buffer");
+    if ((rc = check_durs(durs, B * (uint64_t)n))) return rc;
+    if ((rc = check_id_ranks(id_rank, B, n))) return rc;
+    DevList dl;
+    if ((rc = pick_devs(n_dev, dl))) return rc;
+    const int G = (int)dl.v.size();
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        locks.emplace_back(c->mu);
+        CK(cudaSetDevice(c->dev));
+        const uint64_t lo = B * (uint64_t)gi / (uint64_t)G, hi = B * (uint64_t)(gi + 1) / (uint64_t)G;
+        const uint64_t m = hi - lo;
+        if (!m) continue;
+        const size_t off_idr = align_up(m * 3 * n * sizeof(double));
+        const size_t off_ord = off_idr + align_up(m * n);
+        const size_t off_ms = off_ord + align_up(m * n);
+        const size_t off_ns = off_ms + align_up(m * sizeof(double));
+        void* base;
+        if ((rc = scratch(c, off_ns + align_up(m * sizeof(uint32_t)), &base))) return rc;
+        char* b = (char*)base;
+        CK(cudaMemcpyAsync(b, durs + lo * 3 * n, m * 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(b + off_idr, id_rank + lo * n, m * n, cudaMemcpyHostToDevice, c->stream));
+        wide_heuristic_launch(dma, LaunchCfg{c->sms, c->stream}, (double*)b, (uint8_t*)(b + off_idr), m, n, sigma,
+                              sum_mode, (uint8_t*)(b + off_ord), (double*)(b + off_ms), (uint32_t*)(b + off_ns),
+                              c->d_err);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(order + lo * n, b + off_ord, m * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(makespan + lo, b + off_ms, m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        if (n_sims) CK(cudaMemcpyAsync(n_sims + lo, b + off_ns, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    }
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        CK(cudaSetDevice(c->dev));
+        if ((rc = finish(c, c->stream))) return rc;
+    }
+    return 0;
+}
+
 extern "C" {
 
 const char* osim_version(void) { return "offsim-b200 0.1.0 (sm_100a)"; }
@@ -667,18 +712,18 @@ int osim_exhaustive_ex_dev(const double* d_durs, int n, int dma, double sigma, u
 
 int osim_eval_perms(const double* durs, int n, int dma, double sigma, const uint8_t* perms,
                     uint64_t cnt, int n_dev, double* makespans, osim_summary* out) {
-    int rc = check_common(n, dma, sigma);
+    int rc = check_common(n, dma, sigma, kWideMaxN);
     if (rc) return rc;
     if ((rc = check_durs(durs, (uint64_t)n))) return rc;
     if (!perms && cnt) return fail(OSIM_EINVAL, "perms is NULL");
     if (!makespans && cnt) return fail(OSIM_EINVAL, "makespans is NULL");
     for (uint64_t i = 0; i < cnt; ++i) {  // each row must be a permutation of range(n)
-        unsigned seen = 0;
+        uint64_t seen = 0;
         for (int j = 0; j < n; ++j) {
             const unsigned v = perms[i * n + j];
-            if (v >= (unsigned)n || ((seen >> v) & 1u))
+            if (v >= (unsigned)n || ((seen >> v) & 1ull))
                 return fail(OSIM_EINVAL, "row %llu is not a permutation of range(%d)", (unsigned long long)i, n);
-            seen |= 1u << v;
+            seen |= 1ull << v;
         }
     }
     DevList dl;
@@ -694,7 +739,7 @@ int osim_eval_perms(const double* durs, int n, int dma, double sigma, const uint
         const uint64_t lo = cnt * (uint64_t)gi / (uint64_t)G, hi = cnt * (uint64_t)(gi + 1) / (uint64_t)G;
         const uint64_t m = hi - lo;
         const int mp = max_parts_for(c);
-        size_t off_parts = align_up(3 * kMaxN * sizeof(double));
+        size_t off_parts = align_up(3 * kWideMaxN * sizeof(double));
         size_t off_sum = off_parts + align_up(mp * sizeof(Part));
         size_t off_ms = off_sum + align_up(sizeof(osim_summary));
         size_t off_p = off_ms + align_up(m * sizeof(double) + 8);
@@ -706,7 +751,11 @@ int osim_eval_perms(const double* durs, int n, int dma, double sigma, const uint
         if (m) CK(cudaMemcpyAsync(b + off_p, perms + lo * n, m * n, cudaMemcpyHostToDevice, c->stream));
         Part* parts = (Part*)(b + off_parts);
         int g = 0;
-        if (m) {
+        if (m && n > kMaxN) {  // 17..64 tasks: the byte-FIFO general path
+            const LaunchCfg cfg{c->sms, c->stream};
+            g = wide_eval_perms_launch(dma, cfg, (double*)b, n, sigma, (uint8_t*)(b + off_p), m,
+                                       (double*)(b + off_ms), parts, mp, c->d_err);
+        } else if (m) {
             const uint64_t blocks = (m + kBlock - 1) / kBlock;
 #define OSIM_EP(D, F)                                                                            \
     do {                                                                                         \
@@ -792,6 +841,7 @@ int osim_exhaustive_batch_dev(const double* d_durs, uint64_t B, int n, int dma, 
 int osim_heuristic_batch(const double* durs, const uint8_t* id_rank, uint64_t B, int n, int dma,
                          double sigma, int sum_mode, int n_dev, uint8_t* order, double* makespan,
                          uint32_t* n_sims) {
+    if (n > kMaxN) return heuristic_wide(durs, id_rank, B, n, dma, sigma, sum_mode, n_dev, order, makespan, n_sims);
     int rc = check_common(n, dma, sigma);
     if (rc) return rc;
     if (B && (!durs || !id_rank || !order || !makespan)) return fail(OSIM_EINVAL, "NULL buffer");
@@ -916,6 +966,7 @@ int osim_heuristic_batch_dev(const double* d_durs, const uint8_t* d_id_rank, uin
 
 int osim_timeline(const double* durs, int n, int dma, double sigma, const uint8_t* order,
                   double* start, double* end, double* makespan, double* idle) {
+    if (n > kMaxN) return osim_timeline_deps(durs, n, dma, sigma, order, nullptr, 0, start, end, makespan, idle);
     int rc = check_common(n, dma, sigma);
     if (rc) return rc;
     if ((rc = check_durs(durs, (uint64_t)n))) return rc;
@@ -1064,14 +1115,14 @@ int osim_interleavings(const double* durs, int T, int N, int dma, double sigma, 
 
 int osim_eval_sequences(const double* durs, int T, int N, int dma, double sigma, const uint8_t* labels,
                         uint64_t cnt, int n_dev, double* makespans, osim_summary* out) {
-    if (T < 1 || N < 1 || T * N > kMaxN) return fail(OSIM_EINVAL, "T*N must be in [1, %d]", kMaxN);
-    int rc = check_common(T * N, dma, sigma);
+    if (T < 1 || N < 1 || T * N > kWideMaxN) return fail(OSIM_EINVAL, "T*N must be in [1, %d]", kWideMaxN);
+    int rc = check_common(T * N, dma, sigma, kWideMaxN);
     if (rc) return rc;
     if ((rc = check_durs(durs, (uint64_t)(T * N)))) return rc;
     if (cnt && (!labels || !makespans)) return fail(OSIM_EINVAL, "NULL buffer");
     const int n = T * N;
     for (uint64_t i = 0; i < cnt; ++i) {  // each row: every worker exactly N times
-        int c[kMaxN] = {0};
+        int c[kWideMaxN] = {0};
         for (int p = 0; p < n; ++p) {
             const int w = labels[i * n + p];
             if (w >= T || ++c[w] > N)
@@ -1091,7 +1142,7 @@ int osim_eval_sequences(const double* durs, int T, int N, int dma, double sigma,
         const uint64_t lo = cnt * (uint64_t)gi / (uint64_t)G, hi = cnt * (uint64_t)(gi + 1) / (uint64_t)G;
         const uint64_t m = hi - lo;
         const int mp = max_parts_for(c);
-        size_t off_parts = align_up(3 * kMaxN * sizeof(double));
+        size_t off_parts = align_up(3 * kWideMaxN * sizeof(double));
         size_t off_sum = off_parts + align_up(mp * sizeof(Part));
         size_t off_ms = off_sum + align_up(sizeof(osim_summary));
         size_t off_l = off_ms + align_up(m * sizeof(double) + 8);
@@ -1104,7 +1155,11 @@ int osim_eval_sequences(const double* durs, int T, int N, int dma, double sigma,
         if (m) {
             CK(cudaMemcpyAsync(b + off_l, labels + lo * n, m * n, cudaMemcpyHostToDevice, c->stream));
             const uint64_t blocks = (m + kBlock - 1) / kBlock;
-            if (dma == 2) {
+            if (n > kMaxN) {  // 17..64 tasks: the byte-FIFO general path
+                const LaunchCfg cfg{c->sms, c->stream};
+                g = wide_eval_labels_launch(dma, cfg, (double*)b, T, N, sigma, (uint8_t*)(b + off_l), m,
+                                            (double*)(b + off_ms), (Part*)(b + off_parts), mp, c->d_err);
+            } else if (dma == 2) {
                 g = grid_for(k_eval_labels<2>, kBlock, 0, c, blocks);
                 if (g > mp) g = mp;
                 k_eval_labels<2><<<g, kBlock, 0, c->stream>>>((double*)b, T, N, sigma, (uint8_t*)(b + off_l), m,
@@ -1136,14 +1191,14 @@ int osim_eval_sequences(const double* durs, int T, int N, int dma, double sigma,
 
 int osim_timeline_deps(const double* durs, int n, int dma, double sigma, const uint8_t* order, const int8_t* dep,
                        int waves, double* start, double* end, double* makespan, double* idle) {
-    int rc = check_common(n, dma, sigma);
+    int rc = check_common(n, dma, sigma, kWideMaxN);
     if (rc) return rc;
     if ((rc = check_durs(durs, (uint64_t)n))) return rc;
     if (!order || !start || !end) return fail(OSIM_EINVAL, "NULL buffer");
-    unsigned seen = 0;
+    uint64_t seen = 0;
     for (int j = 0; j < n; ++j) {
-        if (order[j] >= n || ((seen >> order[j]) & 1u)) return fail(OSIM_EINVAL, "order is not a permutation");
-        seen |= 1u << order[j];
+        if (order[j] >= n || ((seen >> order[j]) & 1ull)) return fail(OSIM_EINVAL, "order is not a permutation");
+        seen |= 1ull << order[j];
     }
     if (dep)
         for (int t = 0; t < n; ++t)
@@ -1153,11 +1208,11 @@ int osim_timeline_deps(const double* durs, int n, int dma, double sigma, const u
     DevCtx* c = dl.v[0];
     std::lock_guard<std::mutex> lk(c->mu);
     CK(cudaSetDevice(c->dev));
-    size_t off_o = align_up(3 * kMaxN * sizeof(double));
+    size_t off_o = align_up(3 * kWideMaxN * sizeof(double));
     size_t off_dp = off_o + 256;
     size_t off_s = off_dp + 256;
-    size_t off_e = off_s + align_up(3 * kMaxN * sizeof(double));
-    size_t off_r = off_e + align_up(3 * kMaxN * sizeof(double));
+    size_t off_e = off_s + align_up(3 * kWideMaxN * sizeof(double));
+    size_t off_r = off_e + align_up(3 * kWideMaxN * sizeof(double));
     void* base;
     if ((rc = scratch(c, off_r + 256, &base))) return rc;
     char* b = (char*)base;
@@ -1165,7 +1220,10 @@ int osim_timeline_deps(const double* durs, int n, int dma, double sigma, const u
     CK(cudaMemcpyAsync(b + off_o, order, n, cudaMemcpyHostToDevice, c->stream));
     if (dep) CK(cudaMemcpyAsync(b + off_dp, dep, n, cudaMemcpyHostToDevice, c->stream));
     const int8_t* d_dep = dep ? (const int8_t*)(b + off_dp) : nullptr;
-    if (dma == 2)
+    if (n > kMaxN)  // 17..64 tasks: the byte-FIFO general path
+        wide_timeline_launch(dma, c->stream, (double*)b, n, sigma, (uint8_t*)(b + off_o), d_dep, waves,
+                             (double*)(b + off_s), (double*)(b + off_e), (double*)(b + off_r), c->d_err);
+    else if (dma == 2)
         k_timeline_dep<2><<<1, 64, 0, c->stream>>>((double*)b, n, sigma, (uint8_t*)(b + off_o), d_dep, waves,
                                                    (double*)(b + off_s), (double*)(b + off_e), (double*)(b + off_r),
                                                    c->d_err);

@@ -73,4 +73,18 @@ void heuristic_launch(int dma, int mode /* 0 general, 1 fast, 2 null stages */, 
                       uint64_t B, int n, double sigma, int sum_mode, uint8_t* d_order, double* d_ms,
                       uint32_t* d_ns, int* d_err);
 
+// groups of 17..64 tasks, general path (osim_wide.cu); the eval launchers
+// return the grid (= number of per-block partials in `parts`)
+constexpr int kWideMaxN = 64;
+void wide_timeline_launch(int dma, cudaStream_t st, const double* d_durs, int n, double sigma, const uint8_t* d_order,
+                          const int8_t* d_dep, int waves, double* d_start, double* d_end, double* d_res, int* d_err);
+int wide_eval_perms_launch(int dma, const LaunchCfg& cfg, const double* d_durs, int n, double sigma,
+                           const uint8_t* d_perms, uint64_t cnt, double* d_ms, Part* parts, int max_parts, int* d_err);
+int wide_eval_labels_launch(int dma, const LaunchCfg& cfg, const double* d_durs, int T, int N, double sigma,
+                            const uint8_t* d_labels, uint64_t cnt, double* d_ms, Part* parts, int max_parts,
+                            int* d_err);
+void wide_heuristic_launch(int dma, const LaunchCfg& cfg, const double* d_durs, const uint8_t* d_idr, uint64_t B,
+                           int n, double sigma, int sum_mode, uint8_t* d_order, double* d_ms, uint32_t* d_ns,
+                           int* d_err);
+
 }  // namespace osim

@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _capi, synth
 from .engine import KINDS, Command, Timeline, idle_report
-from .model import MAX_TASKS, DeviceProfile, TaskSpec, resolve_group
+from .model import MAX_ENUM_TASKS, DeviceProfile, TaskSpec, resolve_group
 
 DEFAULT_DT = 0.001  # ms, oracle.py:23
 
@@ -26,8 +26,8 @@ def micro_simulate(tasks: Sequence[TaskSpec], profile: DeviceProfile, dt: float 
     """Fixed-step reference timeline (command times quantized to dt)."""
     if dt <= 0:
         raise ValueError("dt must be positive")
-    if len(tasks) > MAX_TASKS:
-        raise NotImplementedError(f"groups of more than {MAX_TASKS} tasks are not supported on the B200 path")
+    if len(tasks) > MAX_ENUM_TASKS:
+        raise NotImplementedError(f"groups of more than {MAX_ENUM_TASKS} tasks are not supported on the B200 path")
     durs = resolve_group(tasks, profile)
     n = len(tasks)
     st, en, ms = _capi.micro_timeline(durs, profile.dma_engines, profile.overlap_sigma, dt, list(range(n)))

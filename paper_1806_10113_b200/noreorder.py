@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _capi
 from .engine import Timeline, _simulate
-from .model import MAX_TASKS, DeviceProfile, TaskSpec, resolve_group
+from .model import MAX_ENUM_TASKS, MAX_TASKS, DeviceProfile, TaskSpec, resolve_group
 from .search import PermutationReport
 
 
@@ -81,6 +81,8 @@ def distribution_durs(durs, dma: int, sigma: float, cap: int = 10_000, seed: int
     total = interleaving_count(T, N)
     flat = d.reshape(-1, 3)
     if total <= cap:
+        if T * N > MAX_ENUM_TASKS:
+            raise NotImplementedError(f"enumerating the interleavings of more than {MAX_ENUM_TASKS} tasks")
         summ, _, ms = _capi.interleavings(flat, T, N, dma, sigma, 0, total, want_makespans=True)
         labels = None
         exhaustive = True

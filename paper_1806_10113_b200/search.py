@@ -25,7 +25,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _capi
-from .model import MAX_TASKS, DeviceProfile, TaskSpec, resolve_group
+from .model import MAX_ENUM_TASKS, MAX_TASKS, DeviceProfile, TaskSpec, resolve_group
 
 DEFAULT_CAP = 10_000  # oracle.py:24
 DEFAULT_DT = 0.001
@@ -93,6 +93,8 @@ def exhaustive_search(tasks: Sequence[TaskSpec], profile: DeviceProfile, cap: in
     total = math.factorial(n)
     dma, sigma = profile.dma_engines, profile.overlap_sigma
     if total <= cap:
+        if n > MAX_ENUM_TASKS:  # n! >= 3.6e14 orderings: infeasible for the reference as well
+            raise NotImplementedError(f"enumerating all orderings of more than {MAX_ENUM_TASKS} tasks")
         summ, ms = _capi.exhaustive(durs, dma, sigma, 0, total, want_makespans=True)
         orderings = [tuple(ids[i] for i in p) for p in permutations(range(n))]
         exhaustive = True

@@ -18,6 +18,8 @@ Fixtures (all under tests/golden/):
   c5_sample.json      config-5 inputs (16 tasks) x 3 profiles through reorder_batch
   sampled.json        exhaustive_search in sampled (cap) mode
   c3_full.json        (--c3, ~3 min on 8 cores) config-3 full 10! sweep
+  wide.json           groups of 17..64 tasks: timelines (plain, deps, 1-DMA waves),
+                      reorder_batch, sampled exhaustive_search, sampled NoReorder
 """
 
 from __future__ import annotations
@@ -543,6 +545,104 @@ def gen_c3(procs=8):
     })
 
 
+# ---------------------------------------------- groups of 17..64 tasks
+def gen_wide():
+    from offsim import workload
+    from offsim.workload import Scenario
+
+    rng = np.random.default_rng(64_17)
+    timelines = []
+    for c in range(60):
+        n = int(rng.choice([17, 20, 24, 31, 33, 40, 48, 57, 64]))
+        mode = ["int", "mixed", "real"][c % 3]
+        dma = 1 + (c // 3) % 2
+        sigma = [0.375, 0.5, 0.8, 1.0][(c // 6) % 4]
+        d = rand_task_durs(rng, n, mode)
+        tasks = [TaskSpec(id=f"t{i}", fixed_durations=tuple(d[i])) for i in range(n)]
+        order = [int(x) for x in rng.permutation(n)]
+        doc = timeline_doc(tasks, order, prof(dma, sigma))
+        doc.update({"n": n, "dma": dma, "sigma": H(sigma), "durs": [[H(x) for x in r] for r in d], "order": order})
+        timelines.append(doc)
+    # simulate_sequence with NoReorder chains (deps; 1-DMA waves)
+    seqs = []
+    for c in range(40):
+        T = int(rng.integers(2, 7)); N = int(rng.integers(3, 10))
+        while T * N <= 16 or T * N > 64:
+            T = int(rng.integers(2, 7)); N = int(rng.integers(3, 10))
+        dma = 1 + c % 2
+        sigma = [0.5, 0.375, 1.0][c % 3]
+        p = prof(dma, sigma)
+        d = rand_task_durs(rng, T * N, ["int", "mixed", "real"][c % 3])
+        tasks = [[TaskSpec(id=f"w{w}.{j}", fixed_durations=tuple(d[w * N + j])) for j in range(N)] for w in range(T)]
+        labels = [int(x) for x in rng.permutation([w for w in range(T) for _ in range(N)])]
+        cnt = [0] * T
+        seq = []
+        for w in labels:
+            seq.append(tasks[w][cnt[w]]); cnt[w] += 1
+        deps = {tasks[w][j].id: tasks[w][j - 1].id for w in range(T) for j in range(1, N)}
+        tl = workload.simulate_sequence(seq, p, deps)
+        flat = [t for row in tasks for t in row]
+        ix = {t.id: i for i, t in enumerate(flat)}
+        kinds = {engine.KIND_HTD: 0, engine.KIND_K: 1, engine.KIND_DTH: 2}
+        start = [[None] * 3 for _ in flat]
+        end = [[None] * 3 for _ in flat]
+        for cmd in tl.commands:
+            start[ix[cmd.task_id]][kinds[cmd.kind]] = H(cmd.start)
+            end[ix[cmd.task_id]][kinds[cmd.kind]] = H(cmd.end)
+        seqs.append({"T": T, "N": N, "dma": dma, "sigma": H(sigma), "labels": labels,
+                     "durs": [[H(x) for x in r] for r in d], "makespan": H(tl.makespan),
+                     "idle": [H(tl.idle[k]) for k in engine.KINDS], "start": start, "end": end})
+    # reorder_batch on real-task groups and on tie-heavy integer groups
+    heur = []
+    for pname, (dev, dma, sigma) in DEVICE_PROFILES.items():
+        p = prof(dma, sigma)
+        for n, seed in ((17, 1), (20, 2), (24, 3), (32, 4)):
+            tasks = sample_real_tasks(dev, n, seed=seed)
+            doc = heuristic_doc(tasks, p)
+            doc.update({"profile": pname, "dma": dma, "sigma": H(sigma), "n": n, "seed": seed,
+                        "ids": [t.id for t in tasks], "durs": durs_of(tasks), "id_rank": id_rank(tasks)})
+            heur.append(doc)
+    for c in range(12):
+        n = int(rng.choice([17, 19, 22, 26]))
+        dma = 1 + c % 2
+        sigma = [0.5, 0.375, 1.0, 0.8][c % 4]
+        d = rand_task_durs(rng, n, "int" if c % 2 else "mixed")
+        ids = [f"x{int(v)}" for v in rng.permutation(100)[:n]]
+        tasks = [TaskSpec(id=ids[i], fixed_durations=tuple(d[i])) for i in range(n)]
+        doc = heuristic_doc(tasks, prof(dma, sigma))
+        doc.update({"profile": "rand", "dma": dma, "sigma": H(sigma), "n": n, "seed": c,
+                    "ids": ids, "durs": durs_of(tasks), "id_rank": id_rank(tasks)})
+        heur.append(doc)
+    # exhaustive_search in sampled mode (n! > cap)
+    sampled = []
+    for n, dev, pname, cap, seed in ((18, "K20", "2dma", 500, 5), (25, "AMD", "1dma", 300, 6)):
+        p = load_profile_arg(pname)
+        tasks = sample_real_tasks(dev, n, seed=seed)
+        sampled.append({"n": n, "profile": pname, "dma": p.dma_engines, "sigma": H(p.overlap_sigma),
+                        "cap": cap, "seed": seed, "durs": durs_of(tasks, p), **report_doc(tasks, p, cap, seed)})
+    # NoReorder distribution in sampled mode (more than 16 tasks)
+    noreorder = []
+    for (T, N, bk, seed, pname, cap) in [(4, 5, "BK50", 11, "2dma", 400), (3, 7, "BK25", 12, "1dma", 300)]:
+        p = load_profile_arg(pname)
+        sc = Scenario(workers=T, batch_depth=N, pool=load_bk_benchmark(bk), seed=seed, profile=p)
+        wt = workload._draw_worker_tasks(sc)
+        rep = workload.noreorder_distribution(sc, wt, cap)
+        ms = np.asarray(rep.makespans)
+        idx = {wt[w][j].id: (w, j) for w in range(T) for j in range(N)}
+        labels = [[idx[i][0] for i in o] for o in rep.orderings]
+        noreorder.append({
+            "T": T, "N": N, "bk": bk, "seed": seed, "profile": pname, "cap": cap,
+            "dma": p.dma_engines, "sigma": H(p.overlap_sigma),
+            "durs": [[[H(float(x)) for x in offsim.stage_times(wt[w][j], p)] for j in range(N)] for w in range(T)],
+            "count": len(ms), "exhaustive": rep.exhaustive,
+            "labels_sha256": hashlib.sha256(np.asarray(labels, dtype=np.uint8).tobytes()).hexdigest(),
+            "makespans_sha256": hashlib.sha256(ms.astype("<f8").tobytes()).hexdigest(),
+            "best": H(rep.best), "argmin": int(np.argmin(ms)), "worst": H(rep.worst), "median": H(rep.median),
+        })
+    dump("wide.json", {"timelines": timelines, "sequences": seqs, "heuristic": heur, "sampled": sampled,
+                       "noreorder": noreorder})
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--c3", action="store_true")
@@ -553,7 +653,7 @@ if __name__ == "__main__":
         sys.exit(0)
     gens = {"c1": gen_c1, "sim": gen_sim_random, "heur": gen_heuristic_random, "c2": gen_c2,
             "c4": gen_c4, "c5": gen_c5, "sampled": gen_sampled, "noreorder": gen_noreorder,
-            "micro": gen_micro, "harness": gen_harness}
+            "micro": gen_micro, "harness": gen_harness, "wide": gen_wide}
     for k, g in gens.items():
         if not a.only or k in a.only.split(","):
             g()

@@ -34,7 +34,8 @@ def test_group_and_profile_rules(call):
         return _capi.micro(d, dma, sigma, 0.01, 0, 1)
 
     raises(lambda: run(np.zeros((0, 3))), "non-empty")
-    raises(lambda: run(np.ones((17, 3))), "exceeds the supported maximum")
+    # enumerated spaces stop at 16 tasks, single orderings at 64 (osim_wide.cuh)
+    raises(lambda: run(np.ones((65 if call == "timeline" else 17, 3))), "exceeds the supported maximum")
     raises(lambda: run(GOOD, dma=3), "dma_engines must be 1 or 2")
     for s in (0.0, 1.5, float("nan")):
         raises(lambda s=s: run(GOOD, sigma=s), r"overlap_sigma must be in \(0, 1\]")
@@ -68,6 +69,18 @@ def test_batch_limits_and_buffers():
     assert L.osim_heuristic_batch(_capi.ptr(d, _capi.C.c_double), None, 2, 3, 2, 0.5, 1, 1, None, None,
                                   None) == _capi.OSIM_EINVAL
     assert b"NULL buffer" in L.osim_last_error()
+
+
+def test_wide_limits():
+    big = np.ones((65, 3))
+    raises(lambda: _capi.eval_perms(big, 2, 0.5, np.arange(65, dtype=np.uint8)[None]), "exceeds the supported maximum")
+    raises(lambda: _capi.heuristic_batch(big[None], np.arange(65, dtype=np.uint8)[None], 2, 0.5, 1),
+           "exceeds the supported maximum")
+    raises(lambda: _capi.eval_sequences(big, 65, 1, 2, 0.5, np.arange(65, dtype=np.uint8)[None]),
+           r"T\*N must be in")
+    d = np.ones((20, 3))
+    raises(lambda: _capi.heuristic_batch(d[None], np.zeros((1, 20), np.uint8), 2, 0.5, 1), "id ranks must be")
+    raises(lambda: _capi.eval_perms(d, 2, 0.5, np.zeros((1, 20), np.uint8)), "row 0 is not a permutation")
 
 
 def test_row_limits():

@@ -858,3 +858,109 @@ def test_heuristic_null_stages_vs_oracle(profile):
     order, ms, sims = _capi.heuristic_batch(d, r, dma, sigma, osim.SUM_MODE)
     o_order, o_ms, o_sims = O.reorder_batch(d, r, dma, sigma, osim.SUM_MODE, threads=os.cpu_count() or 4)
     assert np.array_equal(order, o_order) and np.array_equal(ms, o_ms) and np.array_equal(sims, o_sims)
+
+
+# ---- groups of 17..64 tasks (csrc/osim_wide.cuh; tests/golden/wide.json) -----
+
+def _wide_check_timeline(st, en, c, n):
+    for t in range(n):
+        for k in range(3):
+            s = c["start"][t][k]
+            if s is None:
+                assert st[t, k] == -1.0
+            else:
+                assert st[t, k] == F(s) and en[t, k] == F(c["end"][t][k])
+
+
+def test_wide_timelines_bit_exact():
+    g = load("wide.json")
+    for c in g["timelines"]:
+        st, en, ms, idle = _capi.timeline(durs(c["durs"]), c["dma"], F(c["sigma"]), c["order"])
+        assert ms == F(c["makespan"]) and idle.tolist() == fl(c["idle"])
+        _wide_check_timeline(st, en, c, c["n"])
+    for c in g["sequences"]:
+        T, N = c["T"], c["N"]
+        cnt = [0] * T
+        order = []
+        for w in c["labels"]:
+            order.append(w * N + cnt[w])
+            cnt[w] += 1
+        dep = [(w * N + j - 1 if j else -1) for w in range(T) for j in range(N)]
+        st, en, ms, idle = _capi.timeline_deps(durs(c["durs"]), c["dma"], F(c["sigma"]), order, dep,
+                                               waves=(c["dma"] == 1))
+        assert ms == F(c["makespan"]) and idle.tolist() == fl(c["idle"])
+        _wide_check_timeline(st, en, c, T * N)
+
+
+def test_wide_simulate_dropin():
+    # engine.simulate on a 48-task group through the drop-in API
+    c = [x for x in load("wide.json")["timelines"] if x["n"] >= 40][0]
+    p = osim.DeviceProfile("g", c["dma"], 0.0, 1.0, 0.0, 1.0, overlap_sigma=F(c["sigma"]))
+    d = durs(c["durs"])
+    tasks = [osim.TaskSpec(f"t{i}", fixed_durations=tuple(d[i])) for i in c["order"]]
+    tl = osim.simulate(tasks, p)
+    assert tl.makespan == F(c["makespan"]) and [tl.idle[k] for k in osim.KINDS] == fl(c["idle"])
+    assert [osim.KINDS.index(x.kind) for x in tl.commands] == c["sorted_kinds"]
+    assert [int(x.task_id[1:]) for x in tl.commands] == c["sorted_tasks"]
+
+
+def test_wide_heuristic_goldens_and_batch_vs_oracle():
+    g = load("wide.json")
+    mode = g["meta"]["sum_mode"]
+    assert mode == osim.SUM_MODE
+    for c in g["heuristic"]:
+        order, ms, sims = _capi.heuristic_batch(durs(c["durs"])[None], np.array(c["id_rank"], np.uint8)[None],
+                                                c["dma"], F(c["sigma"]), mode)
+        assert order[0].tolist() == c["order"] and ms[0] == F(c["makespan"]) and sims[0] == c["n_sims"]
+    # batches of real-task groups (17..24 tasks) against the oracle
+    cpus = os.cpu_count() or 4
+    for prof, n, B in (("nvidia", 20, 384), ("amd", 17, 256), ("phi", 24, 192)):
+        _, dma, sigma = synth.PROFILES[prof]
+        dev = {"nvidia": "K20", "amd": "AMD", "phi": "PHI"}[prof]
+        d = np.stack([synth.real_group(dev, n, 500 + b)[1] for b in range(B)])
+        r = np.stack([np.random.default_rng(b).permutation(n) for b in range(B)]).astype(np.uint8)
+        order, ms, sims = _capi.heuristic_batch(d, r, dma, sigma, mode)
+        oo, om, osims = O.reorder_batch(d, r, dma, sigma, mode, threads=cpus)
+        assert np.array_equal(order, oo) and np.array_equal(ms, om) and np.array_equal(sims, osims)
+
+
+def test_wide_sampled_search_and_noreorder():
+    import hashlib
+
+    from paper_1806_10113_b200 import noreorder as nr
+    from paper_1806_10113_b200.search import sample_permutations
+
+    g = load("wide.json")
+    for c in g["sampled"]:
+        d = durs(c["durs"])
+        p = osim.DeviceProfile("g", c["dma"], 0.0, 1.0, 0.0, 1.0, overlap_sigma=F(c["sigma"]))
+        tasks = [osim.TaskSpec(f"t{i}", fixed_durations=tuple(d[i])) for i in range(c["n"])]
+        rep = osim.exhaustive_search(tasks, p, cap=c["cap"], seed=c["seed"])  # sampled mode (n! > cap)
+        assert rep.exhaustive is False
+        assert sha(np.array(rep.makespans)) == c["makespans_sha256"]
+        assert [int(x[1:]) for x in rep.best_ordering] == c["best_ordering"]
+        assert rep.best == F(c["best"]) and rep.median == F(c["median"]) and rep.worst == F(c["worst"])
+        perms = sample_permutations(c["n"], c["cap"], c["seed"])
+        s, ms = _capi.eval_perms(d, c["dma"], F(c["sigma"]), perms)
+        assert s["best_rank"] == c["argmin"] and sha(ms) == c["makespans_sha256"]
+    for c in g["noreorder"]:
+        d = np.array([[[F(x) for x in r] for r in row] for row in c["durs"]])
+        labels, ms, summ, exhaustive = nr.distribution_durs(d, c["dma"], F(c["sigma"]), c["cap"], c["seed"])
+        assert exhaustive is False and len(ms) == c["count"]
+        assert hashlib.sha256(ms.astype("<f8").tobytes()).hexdigest() == c["makespans_sha256"]
+        assert summ["best_rank"] == c["argmin"] and summ["best"] == F(c["best"]) and summ["worst"] == F(c["worst"])
+        assert float(np.median(ms)) == F(c["median"])
+
+
+def test_wide_eval_perms_64_tasks_vs_oracle():
+    # the largest groups (64 tasks), null stages, both DMA modes
+    rng = np.random.default_rng(64)
+    d = rng.uniform(0.1, 4.0, (64, 3))
+    d[rng.random((64, 3)) < 0.1] = 0.0
+    d[:, 1] = np.maximum(d[:, 1], 0.05)  # every task keeps a command
+    perms = np.stack([rng.permutation(64) for _ in range(4000)]).astype(np.uint8)
+    for dma, sigma in ((2, 0.375), (1, 1.0)):
+        s, ms = _capi.eval_perms(d, dma, sigma, perms)
+        o, oms = O.eval_perms(d, dma, sigma, perms, threads=os.cpu_count() or 4)
+        assert np.array_equal(ms, oms)
+        assert_summary_vs_oracle(s, o)
