@@ -26,10 +26,11 @@
  * a stage <= 0 is null (no command, engine.py:129-151).  `dma` is
  * DeviceProfile.dma_engines (1 or 2), `sigma` its overlap_sigma in (0, 1].
  * Orderings are task indices 0..n-1.  Group size: n <= 16 for the enumerated
- * spaces (osim_exhaustive*, osim_interleavings, osim_micro*, osim_harness_batch,
- * and every _dev variant); n <= 64 for single orderings and explicit lists
+ * spaces (osim_exhaustive*, osim_interleavings, osim_micro*, and every _dev
+ * variant); n <= 64 for single orderings, explicit lists and scenarios
  * (osim_timeline, osim_timeline_deps, osim_eval_perms, osim_eval_sequences,
- * osim_heuristic_batch), which above 16 tasks run on the byte-FIFO general path.
+ * osim_heuristic_batch, osim_harness_batch), which above 16 tasks run on the
+ * byte-FIFO general path.
  *
  * Conventions: every function returns 0 on success or a negative OSIM_E*
  * code; osim_last_error() gives a thread-local message.  Host buffers are

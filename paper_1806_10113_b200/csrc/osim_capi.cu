@@ -1349,9 +1349,9 @@ int osim_micro_timeline(const double* durs, int n, int dma, double sigma, double
 int osim_harness_batch(const double* durs, const uint8_t* id_rank, uint64_t S, int T, int N, int dma, double sigma,
                        int sum_mode, int n_dev, double* makespan, uint8_t* n_groups, uint8_t* tg_sizes,
                        double* start, double* end) {
-    if (T < 1 || N < 1 || T * N > kMaxN) return fail(OSIM_EINVAL, "T*N must be in [1, %d]", kMaxN);
+    if (T < 1 || N < 1 || T * N > kWideMaxN) return fail(OSIM_EINVAL, "T*N must be in [1, %d]", kWideMaxN);
     const int n = T * N;
-    int rc = check_common(n, dma, sigma);
+    int rc = check_common(n, dma, sigma, kWideMaxN);
     if (rc) return rc;
     if ((rc = check_durs(durs, S * (uint64_t)n))) return rc;
     if (S && (!id_rank || !makespan || !n_groups)) return fail(OSIM_EINVAL, "NULL buffer");
@@ -1383,7 +1383,11 @@ int osim_harness_batch(const double* durs, const uint8_t* id_rank, uint64_t S, i
         const unsigned blocks = (unsigned)((m + 127) / 128);
         double* d_st = tl ? (double*)(b + off_st) : nullptr;
         double* d_en = tl ? (double*)(b + off_en) : nullptr;
-        if (dma == 2)
+        if (n > kMaxN)  // more than 16 tasks: WideSim FIFOs (osim_wide.cuh)
+            wide_harness_launch(dma, c->stream, (double*)b, (uint8_t*)(b + off_r), m, T, N, sigma, sum_mode,
+                                (double*)(b + off_ms), (uint8_t*)(b + off_ng), (uint8_t*)(b + off_sz), d_st, d_en,
+                                c->d_err);
+        else if (dma == 2)
             k_harness<2><<<blocks, 128, 0, c->stream>>>((double*)b, (uint8_t*)(b + off_r), m, T, N, sigma, sum_mode,
                                                         (double*)(b + off_ms), (uint8_t*)(b + off_ng),
                                                         (uint8_t*)(b + off_sz), d_st, d_en, c->d_err);

@@ -86,5 +86,8 @@ int wide_eval_labels_launch(int dma, const LaunchCfg& cfg, const double* d_durs,
 void wide_heuristic_launch(int dma, const LaunchCfg& cfg, const double* d_durs, const uint8_t* d_idr, uint64_t B,
                            int n, double sigma, int sum_mode, uint8_t* d_order, double* d_ms, uint32_t* d_ns,
                            int* d_err);
+void wide_harness_launch(int dma, cudaStream_t st, const double* d_durs, const uint8_t* d_idr, uint64_t S, int T,
+                         int N, double sigma, int sum_mode, double* d_ms, uint8_t* d_ng, uint8_t* d_sizes,
+                         double* d_start, double* d_end, int* d_err);
 
 }  // namespace osim

@@ -59,4 +59,17 @@ void wide_heuristic_launch(int dma, const LaunchCfg& cfg, const double* d_durs, 
                                                              d_ns, d_err);
 }
 
+void wide_harness_launch(int dma, cudaStream_t st, const double* d_durs, const uint8_t* d_idr, uint64_t S, int T,
+                         int N, double sigma, int sum_mode, double* d_ms, uint8_t* d_ng, uint8_t* d_sizes,
+                         double* d_start, double* d_end, int* d_err) {
+    const unsigned grid = (unsigned)((S + kWideBlock - 1) / kWideBlock);
+    if (!grid) return;
+    if (dma == 2)
+        k_wide_harness<2><<<grid, kWideBlock, 0, st>>>(d_durs, d_idr, S, T, N, sigma, sum_mode, d_ms, d_ng, d_sizes,
+                                                       d_start, d_end, d_err);
+    else
+        k_wide_harness<1><<<grid, kWideBlock, 0, st>>>(d_durs, d_idr, S, T, N, sigma, sum_mode, d_ms, d_ng, d_sizes,
+                                                       d_start, d_end, d_err);
+}
+
 }  // namespace osim

@@ -253,26 +253,17 @@ __global__ void __launch_bounds__(kWideBlock) k_wide_eval_labels(const double* _
     if (threadIdx.x == 0) parts[blockIdx.x] = acc;
 }
 
-// Algorithm 1 (heuristic.py:105-125), one group per thread, every candidate
-// simulated from time 0 (select_next_task :52-78, select_last_tasks :81-102,
-// select_first_task :22-31, _completion_estimate :34-49 with CPython's sum).
+// Algorithm 1 (heuristic.py:105-125) in one thread, every candidate
+// simulated from time 0 (select_first_task :22-31, select_next_task :52-78,
+// _completion_estimate :34-49 with CPython's sum, select_last_tasks :81-102).
+// gd: the group's durations [n][3]; idr: id ranks; ot: the order out.
+// Returns the makespan of the chosen order (simulate(order)).
 template <int DMA>
-__global__ void __launch_bounds__(kWideBlock) k_wide_heuristic(const double* __restrict__ durs,
-                                                               const uint8_t* __restrict__ id_rank, uint64_t B, int n,
-                                                               double sigma, int sum_mode,
-                                                               uint8_t* __restrict__ order_out,
-                                                               double* __restrict__ ms_out,
-                                                               uint32_t* __restrict__ nsims_out,
-                                                               int* __restrict__ err) {
-    const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= B) return;
-    const double* gd = durs + g * 3 * (uint64_t)n;
-    const uint8_t* idr = id_rank + g * (uint64_t)n;
+__device__ double wide_reorder(const double* gd, const uint8_t* idr, int n, double sigma, int sum_mode, uint8_t* ot,
+                               bool& ok) {
     auto dur = [&](int k, int t) { return gd[3 * t + k]; };
-    uint8_t ot[kWideMax];
     int k = 0;
     uint64_t rt = (n >= 64) ? ~0ull : ((1ull << n) - 1ull);
-    bool ok = true;
     if (n >= 3) {  // select_first_task: min of (-(t_k - t_htd), -t_dth, id)
         int best = -1;
         double b1 = 0, b2 = 0;
@@ -326,7 +317,6 @@ __global__ void __launch_bounds__(kWideBlock) k_wide_heuristic(const double* __r
         ot[k++] = (uint8_t)bc;
         rt &= ~(1ull << bc);
     }
-    double ms;
     if (n >= 2) {  // select_last_tasks: the pair in id order, both orders simulated
         int a = __ffsll((long long)rt) - 1;
         int b = __ffsll((long long)(rt & (rt - 1))) - 1;
@@ -346,18 +336,120 @@ __global__ void __launch_bounds__(kWideBlock) k_wide_heuristic(const double* __r
         else ab = !(dur(2, a) <= dur(2, b));  // tie: shorter DtH last
         ot[k] = (uint8_t)(ab ? a : b);
         ot[k + 1] = (uint8_t)(ab ? b : a);
-        ms = ab ? m2[0] : m2[1];
-    } else {  // reorder_batch returns [tg[0]] without simulating
-        ot[0] = 0;
-        WideSim<DMA, false> s;
-        s.init(gd, n, sigma, ot, 1, nullptr, false);
-        ok = s.run_all() && ok;
-        ms = s.now;
+        return ab ? m2[0] : m2[1];
     }
+    ot[0] = 0;  // reorder_batch returns [tg[0]] without simulating
+    WideSim<DMA, false> s;
+    s.init(gd, n, sigma, ot, 1, nullptr, false);
+    ok = s.run_all() && ok;
+    return s.now;
+}
+
+// reorder_batch over many groups, one group per thread
+template <int DMA>
+__global__ void __launch_bounds__(kWideBlock) k_wide_heuristic(const double* __restrict__ durs,
+                                                               const uint8_t* __restrict__ id_rank, uint64_t B, int n,
+                                                               double sigma, int sum_mode,
+                                                               uint8_t* __restrict__ order_out,
+                                                               double* __restrict__ ms_out,
+                                                               uint32_t* __restrict__ nsims_out,
+                                                               int* __restrict__ err) {
+    const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= B) return;
+    uint8_t ot[kWideMax];
+    bool ok = true;
+    const double ms = wide_reorder<DMA>(durs + g * 3 * (uint64_t)n, id_rank + g * (uint64_t)n, n, sigma, sum_mode,
+                                        ot, ok);
     if (!ok) atomicExch(err, OSIM_ESTALL);
     for (int p = 0; p < n; ++p) order_out[g * (uint64_t)n + p] = ot[p];
     ms_out[g] = ms;
     if (nsims_out) nsims_out[g] = (n >= 3) ? (uint32_t)(n * (n - 1) / 2 - 1) : (n == 2 ? 2u : 0u);
+}
+
+// The proxy-thread harness (workload.py:197-256) for
+// scenarios of more than 16 tasks (the paper's T = 6, 8 workers x N = 4):
+// k_harness (osim_harness.cuh) with WideSim FIFOs and 64-bit worker masks.
+template <int DMA>
+__global__ void __launch_bounds__(kWideBlock) k_wide_harness(const double* __restrict__ durs,
+                                                             const uint8_t* __restrict__ id_rank, uint64_t S, int T,
+                                                             int N, double sigma, int sum_mode,
+                                                             double* __restrict__ ms_out, uint8_t* __restrict__ ng_out,
+                                                             uint8_t* __restrict__ sizes_out,
+                                                             double* __restrict__ start_out,
+                                                             double* __restrict__ end_out, int* __restrict__ err) {
+    const uint64_t sc = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (sc >= S) return;
+    const int n = T * N;
+    const double* gd = durs + sc * 3 * (uint64_t)n;
+    const uint8_t* gr = id_rank + sc * (uint64_t)n;
+    WideSim<DMA, false> s;
+    s.init(gd, n, sigma, nullptr, 0, nullptr, false);  // empty FIFOs, null stages marked done
+    int next_idx[kWideMax];
+    for (int w = 0; w < T; ++w) next_idx[w] = 0;
+    uint64_t avail = (T >= 64) ? ~0ull : ((1ull << T) - 1ull);
+    bool polling = true;
+    int watched = -1;  // XFER/HtD FIFO slot of the group's last HtD
+    int ng = 0;
+    bool ok = true;
+    auto submit_group = [&]() {  // workload.py:219-233
+        uint8_t tg[kWideMax];
+        int m = 0;
+        for (int w = 0; w < T; ++w)
+            if ((avail >> w) & 1ull) tg[m++] = (uint8_t)(w * N + next_idx[w]++);
+        avail = 0;
+        double td[3 * kWideMax];
+        uint8_t tr[kWideMax], ord[kWideMax];
+        for (int i = 0; i < m; ++i) {
+            for (int k = 0; k < 3; ++k) td[3 * i + k] = gd[3 * tg[i] + k];
+            int r = 0;
+            for (int j = 0; j < m; ++j) r += gr[tg[j]] < gr[tg[i]];
+            tr[i] = (uint8_t)r;
+        }
+        wide_reorder<DMA>(td, tr, m, sigma, sum_mode, ord, ok);
+        watched = -1;
+        for (int i = 0; i < m; ++i) {  // DeviceSim.submit (engine.py:125-156)
+            const int u = tg[ord[i]];
+            if (s.nonnull(0, u)) { watched = s.len[0]; s.push(0, u, 0); ++s.ncmd; }
+            if (s.nonnull(1, u)) { s.push(2, u, 0); ++s.ncmd; }
+            if (DMA == 2 && s.nonnull(2, u)) { s.push(1, u, 0); ++s.ncmd; }
+        }
+        if (DMA == 1)
+            for (int i = 0; i < m; ++i) {
+                const int u = tg[ord[i]];
+                if (s.nonnull(2, u)) { s.push(0, u, 1); ++s.ncmd; }
+            }
+        if (sizes_out) sizes_out[sc * n + ng] = (uint8_t)m;
+        ++ng;
+        polling = watched < 0;
+    };
+    TimelineOut tlo{start_out ? start_out + sc * 3 * n : nullptr, end_out ? end_out + sc * 3 * n : nullptr};
+    TimelineOut* tl = start_out && end_out ? &tlo : nullptr;
+    if (tl)
+        for (int i = 0; i < 3 * n; ++i) { tl->start[i] = -1.0; tl->end[i] = -1.0; }
+    submit_group();
+    for (int guard = 0; guard < (3 * n + 1) * kSlowSteps + n + 1; ++guard) {
+        if (polling && avail) submit_group();
+        int hb[3];
+        for (int l = 0; l < 3; ++l) hb[l] = s.h[l];
+        if (!s.step(tl)) {
+            bool remaining = false;
+            for (int w = 0; w < T; ++w) remaining |= next_idx[w] < N;
+            ok = ok && !remaining && s.drained();
+            break;
+        }
+        for (int l = 0; l < 3; ++l) {  // the step's finalized commands
+            if (s.h[l] == hb[l]) continue;
+            if (l == 0 && hb[0] == watched) polling = true;
+            const int t = s.ct[l];
+            if (s.finished(t)) {
+                const int w = t / N, j = t % N;
+                if (j + 1 < N) avail |= 1ull << w;
+            }
+        }
+    }
+    if (!ok) atomicExch(err, OSIM_ESTALL);
+    ms_out[sc] = s.now;
+    ng_out[sc] = (uint8_t)ng;
 }
 
 }  // namespace osim

@@ -639,8 +639,29 @@ def gen_wide():
             "makespans_sha256": hashlib.sha256(ms.astype("<f8").tobytes()).hexdigest(),
             "best": H(rep.best), "argmin": int(np.argmin(ms)), "worst": H(rep.worst), "median": H(rep.median),
         })
+    # the proxy-thread harness at the paper's scenario sizes (T = 6, 8 workers x N = 4)
+    harness = []
+    for c, (T, N) in enumerate([(6, 4), (8, 4), (5, 4), (4, 8), (8, 3), (6, 6), (8, 4), (6, 4),
+                                (3, 7), (9, 2), (16, 2), (8, 8)]):
+        if c < 8:
+            bk = BK_NAMES[c % 5]
+            pool = load_bk_benchmark(bk)
+        else:
+            bk = "real"
+            pool = workload.make_benchmark("real", sample_real_tasks(["K20", "AMD", "PHI"][c % 3], 8, seed=c))
+        p = [load_profile_arg("2dma"), load_profile_arg("1dma"), prof(2, 0.375)][c % 3]
+        seed = 100 + c
+        sc = Scenario(workers=T, batch_depth=N, pool=pool, seed=seed, profile=p)
+        wt = workload._draw_worker_tasks(sc)
+        res = workload.run_scenario(sc, evaluate_noreorder=False)
+        flat = [t for row in wt for t in row]
+        harness.append({"T": T, "N": N, "bk": bk, "seed": seed, "dma": p.dma_engines, "sigma": H(p.overlap_sigma),
+                        "ids": [t.id for t in flat], "id_rank": id_rank(flat),
+                        "durs": [[H(float(x)) for x in offsim.stage_times(t, p)] for t in flat],
+                        "makespan": H(res.heuristic_makespan), "tg_sizes": res.tg_sizes,
+                        "idle": [H(res.timeline.idle[k]) for k in engine.KINDS]})
     dump("wide.json", {"timelines": timelines, "sequences": seqs, "heuristic": heur, "sampled": sampled,
-                       "noreorder": noreorder})
+                       "noreorder": noreorder, "harness": harness})
 
 
 if __name__ == "__main__":

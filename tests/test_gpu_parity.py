@@ -964,3 +964,24 @@ def test_wide_eval_perms_64_tasks_vs_oracle():
         o, oms = O.eval_perms(d, dma, sigma, perms, threads=os.cpu_count() or 4)
         assert np.array_equal(ms, oms)
         assert_summary_vs_oracle(s, o)
+
+
+def test_wide_harness_bit_exact_and_dropin():
+    # the paper's scenario sizes (T = 6, 8 workers x N = 4 dependent tasks)
+    g = load("wide.json")
+    mode = g["meta"]["sum_mode"]
+    for c in g["harness"]:
+        d = durs(c["durs"])[None]
+        r = np.array(c["id_rank"], dtype=np.uint8)[None]
+        ms, ng, sz, st, en = _capi.harness_batch(d, r, c["T"], c["N"], c["dma"], F(c["sigma"]), mode, timeline=True)
+        assert ms[0] == F(c["makespan"]) and sz[0, : ng[0]].tolist() == c["tg_sizes"], (c["T"], c["N"], c["bk"])
+    from paper_1806_10113_b200 import workload as wl
+
+    c = [x for x in g["harness"] if x["T"] == 8 and x["N"] == 4 and x["bk"] != "real"][0]
+    p = osim.DeviceProfile("p", c["dma"], 0.0, 1.0, 0.0, 1.0, overlap_sigma=F(c["sigma"]))
+    sc = wl.Scenario(8, 4, wl.load_bk_benchmark(c["bk"]), c["seed"], p)
+    res = wl.run_scenario(sc, evaluate_noreorder=True, cap=500)  # NoReorder sampled over 32-task sequences
+    assert res.heuristic_makespan == F(c["makespan"]) and res.tg_sizes == c["tg_sizes"]
+    assert [res.timeline.idle[k] for k in osim.KINDS] == fl(c["idle"])
+    assert res.noreorder is not None and len(res.noreorder.makespans) == 500
+    assert res.speedup_best >= res.speedup_median

@@ -299,3 +299,20 @@ def test_wide_heuristic_sampled_noreorder_oracle_pinned():
         s, ms = O.eval_sequences(d, T, N, c["dma"], F(c["sigma"]), lab)
         assert hashlib.sha256(ms.astype("<f8").tobytes()).hexdigest() == c["makespans_sha256"]
         assert s["best_rank"] == c["argmin"] and float(np.median(ms)) == F(c["median"])
+
+
+def test_wide_harness_oracle_pinned():
+    import ctypes as C
+
+    L = O.lib()
+    L.oracle_harness.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_int,
+                                 C.c_double, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    g = load("wide.json")
+    for c in g["harness"]:
+        d = np.ascontiguousarray(durs(c["durs"]))
+        r = np.array(c["id_rank"], dtype=np.uint8)
+        ms, ng, sizes = C.c_double(), C.c_int(), np.zeros(64, dtype=np.int32)
+        rc = L.oracle_harness(d.ctypes.data_as(C.POINTER(C.c_double)), r.ctypes.data_as(C.POINTER(C.c_uint8)),
+                              c["T"], c["N"], c["dma"], F(c["sigma"]), sum_mode_of(g), C.byref(ms), C.byref(ng),
+                              sizes.ctypes.data_as(C.POINTER(C.c_int)))
+        assert rc == 0 and ms.value == F(c["makespan"]) and sizes[: ng.value].tolist() == c["tg_sizes"], (c["T"], c["N"])
