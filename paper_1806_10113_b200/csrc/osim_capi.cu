@@ -391,29 +391,58 @@ int pick_devs(int n_dev, DevList& out) {
 // k-th smallest (0-based) of the positive doubles held by several devices
 // (each device: d_vals[i] with counts[i] values); histograms of every pass
 // are summed over devices on the host.  Exact: the result is a bit pattern.
+// k-th smallest (0-based) of the values spread over the devices, by MSB-first
+// radix selection on the bit patterns (positive doubles order like their
+// bits).  The walk starts below the bits shared by the smallest and largest
+// value (vmin, vmax: the summary's best / worst), and once the candidates
+// fit the per-device compaction buffers (cbuf, ccap values each) the next
+// pass also copies them out, so the remaining passes read only those.
+// *same_next: whether the (k+1)-th value equals the k-th.
 int select_kth(std::vector<DevCtx*>& devs, std::vector<const double*>& vals, std::vector<uint64_t>& counts,
-               std::vector<unsigned*>& d_hist, uint64_t k, double* out) {
-    unsigned long long prefix = 0;
+               std::vector<unsigned*>& d_hist, uint64_t k, double vmin, double vmax,
+               std::vector<unsigned long long*>& cbuf, uint64_t ccap, double* out, bool* same_next) {
+    unsigned long long prefix = 0, a, b;
+    memcpy(&a, &vmin, sizeof(a));
+    memcpy(&b, &vmax, sizeof(b));
     int pbits = 0;
+    if (vmin > 0.0 && vmax >= vmin)  // common leading bits of every value in [vmin, vmax]
+        while (pbits < 63 && ((a ^ b) >> (63 - pbits)) == 0) ++pbits;
+    prefix = pbits ? (a >> (64 - pbits)) : 0ull;
+    std::vector<const unsigned long long*> cur(devs.size());
+    std::vector<uint64_t> cnt(counts);
+    for (size_t i = 0; i < devs.size(); ++i) cur[i] = (const unsigned long long*)vals[i];
+    uint64_t matching = 0;  // values carrying the current prefix, over all devices
+    for (size_t i = 0; i < devs.size(); ++i) matching += cnt[i];
+    bool compacted = false;
     std::vector<unsigned> h(1 << kRadixBits), tot(1 << kRadixBits);
+    uint64_t last_bin_count = 0;
     while (pbits < 64) {
         const int d = (64 - pbits) < kRadixBits ? (64 - pbits) : kRadixBits;
         const int nb = 1 << d;
+        const bool append = !compacted && pbits > 0 && matching <= ccap && !cbuf.empty();
         std::fill(tot.begin(), tot.begin() + nb, 0u);
+        std::vector<unsigned long long> got(devs.size(), 0);
         for (size_t i = 0; i < devs.size(); ++i) {
             DevCtx* c = devs[i];
             CK(cudaSetDevice(c->dev));
             CK(cudaMemsetAsync(d_hist[i], 0, nb * sizeof(unsigned), c->stream));
-            if (counts[i]) {
-                const uint64_t blocks = (counts[i] + 255) / 256;
+            unsigned long long* d_cnt = (unsigned long long*)((char*)d_hist[i] + (1u << kRadixBits) * sizeof(unsigned));
+            if (append) CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), c->stream));
+            if (cnt[i]) {
+                const uint64_t blocks = (cnt[i] + 255) / 256;
                 const int g = (int)(blocks < (uint64_t)c->sms * 8 ? blocks : (uint64_t)c->sms * 8);
-                k_radix_hist<<<g, 256, 0, c->stream>>>((const unsigned long long*)vals[i], counts[i], prefix, pbits,
-                                                       d, d_hist[i]);
+                k_radix_hist<<<g, 256, 0, c->stream>>>(cur[i], cnt[i], prefix, pbits, d, d_hist[i],
+                                                       append ? cbuf[i] : nullptr, append ? d_cnt : nullptr);
                 CK(cudaGetLastError());
             }
             CK(cudaMemcpyAsync(h.data(), d_hist[i], nb * sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+            if (append) CK(cudaMemcpyAsync(&got[i], d_cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
             CK(cudaStreamSynchronize(c->stream));
-            for (int b = 0; b < nb; ++b) tot[b] += h[b];
+            for (int bb = 0; bb < nb; ++bb) tot[bb] += h[bb];
+        }
+        if (append) {
+            for (size_t i = 0; i < devs.size(); ++i) { cur[i] = cbuf[i]; cnt[i] = got[i]; }
+            compacted = true;
         }
         uint64_t cum = 0;
         int bin = 0;
@@ -423,12 +452,15 @@ int select_kth(std::vector<DevCtx*>& devs, std::vector<const double*>& vals, std
         }
         if (bin == nb) return fail(OSIM_EINVAL, "rank %llu outside the value set", (unsigned long long)k);
         k -= cum;
+        matching = tot[bin];
+        last_bin_count = tot[bin];
         prefix = (prefix << d) | (unsigned long long)bin;
         pbits += d;
     }
     double v;
     memcpy(&v, &prefix, sizeof(v));
     *out = v;
+    if (same_next) *same_next = k + 1 < last_bin_count;  // v occurs again at rank k + 1
     return 0;
 }
 }  // namespace
@@ -613,6 +645,8 @@ int osim_exhaustive_stats(const double* durs, int n, int dma, double sigma, uint
     std::vector<const double*> vals(G);
     std::vector<uint64_t> counts(G);
     std::vector<unsigned*> hists(G);
+    std::vector<unsigned long long*> cbufs(G);
+    uint64_t ccap = 0;  // per-device compaction capacity (values)
     std::vector<std::unique_lock<std::mutex>> locks;
     for (int gi = 0; gi < G; ++gi) {
         DevCtx* c = dl.v[gi];
@@ -625,8 +659,9 @@ int osim_exhaustive_stats(const double* durs, int n, int dma, double sigma, uint
         size_t off_sum = off_parts + align_up(mp * sizeof(Part));
         size_t off_bel = off_sum + align_up(sizeof(osim_summary));
         size_t off_hist = off_bel + 256;
-        size_t off_ms = off_hist + align_up((1u << kRadixBits) * sizeof(unsigned));
-        size_t bytes = off_ms + align_up((hi - lo) * sizeof(double) + 8);
+        size_t off_ms = off_hist + align_up((1u << kRadixBits) * sizeof(unsigned) + 256);
+        size_t off_cb = off_ms + align_up((hi - lo) * sizeof(double) + 8);
+        size_t bytes = off_cb + (median ? align_up(((hi - lo) / 8 + 1) * sizeof(double)) : 0);
         void* base;
         if ((rc = scratch(c, bytes, &base))) return rc;
         char* b = (char*)base;
@@ -640,6 +675,8 @@ int osim_exhaustive_stats(const double* durs, int n, int dma, double sigma, uint
         vals[gi] = (const double*)(b + off_ms);
         counts[gi] = hi - lo;
         hists[gi] = (unsigned*)(b + off_hist);
+        cbufs[gi] = (unsigned long long*)(b + off_cb);
+        ccap = (gi == 0 || (hi - lo) / 8 + 1 < ccap) ? (hi - lo) / 8 + 1 : ccap;
     }
     osim_summary acc;
     memset(&acc, 0, sizeof(acc));
@@ -660,11 +697,19 @@ int osim_exhaustive_stats(const double* durs, int n, int dma, double sigma, uint
         if (cnt == 0) {
             *median = NAN;
         } else if (cnt & 1) {
-            if ((rc = select_kth(dl.v, vals, counts, hists, cnt / 2, median))) return rc;
+            if ((rc = select_kth(dl.v, vals, counts, hists, cnt / 2, acc.best, acc.worst, cbufs, ccap, median,
+                                 nullptr)))
+                return rc;
         } else {
             double a, bb;
-            if ((rc = select_kth(dl.v, vals, counts, hists, cnt / 2 - 1, &a))) return rc;
-            if ((rc = select_kth(dl.v, vals, counts, hists, cnt / 2, &bb))) return rc;
+            bool same = false;
+            if ((rc = select_kth(dl.v, vals, counts, hists, cnt / 2 - 1, acc.best, acc.worst, cbufs, ccap, &a,
+                                 &same)))
+                return rc;
+            if (same) bb = a;  // the two middle values are equal
+            else if ((rc = select_kth(dl.v, vals, counts, hists, cnt / 2, acc.best, acc.worst, cbufs, ccap, &bb,
+                                      nullptr)))
+                return rc;
             volatile double s = a + bb;  // two IEEE roundings, as numpy's mean
             *median = s / 2.0;
         }

@@ -1288,9 +1288,15 @@ static __global__ void k_check_batch(const double* __restrict__ durs, const uint
 // ---------------------------------------------------------------------------
 constexpr int kRadixBits = 11;
 
+// Histogram of the dbits-bit digit below a pbits-bit prefix over the values
+// carrying that prefix (bit patterns of positive doubles order like the
+// values).  With `out`, the matching values are also appended to out
+// (warp-aggregated, order unspecified), so later passes can run on them.
 static __global__ void __launch_bounds__(256) k_radix_hist(const unsigned long long* __restrict__ vals,
                                                            uint64_t count, unsigned long long prefix, int pbits,
-                                                           int dbits, unsigned* __restrict__ hist) {
+                                                           int dbits, unsigned* __restrict__ hist,
+                                                           unsigned long long* __restrict__ out = nullptr,
+                                                           unsigned long long* __restrict__ out_count = nullptr) {
     __shared__ unsigned sh[1 << kRadixBits];
     const int nb = 1 << dbits;
     for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
@@ -1308,6 +1314,15 @@ static __global__ void __launch_bounds__(256) k_radix_hist(const unsigned long l
         const unsigned key = match ? digit : 0xFFFFFFFFu;
         const unsigned peers = __match_any_sync(kFull, key);
         if (match && lane == __ffs(peers) - 1) atomicAdd(&sh[digit], (unsigned)__popc(peers));
+        if (out) {
+            const unsigned mm = __ballot_sync(kFull, match);
+            if (mm) {
+                unsigned long long base = 0;
+                if (lane == __ffs(mm) - 1) base = atomicAdd(out_count, (unsigned long long)__popc(mm));
+                base = __shfl_sync(kFull, base, __ffs(mm) - 1);
+                if (match) out[base + __popc(mm & ((1u << lane) - 1u))] = u;
+            }
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < nb; i += blockDim.x)

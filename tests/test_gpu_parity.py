@@ -334,6 +334,18 @@ def test_c4_window_median_odd_and_even_vs_numpy():
         assert s["count"] == cnt
 
 
+def test_median_with_heavy_ties_vs_numpy():
+    # integer stage times: makespans repeat massively (duplicate middle
+    # values, narrow common prefix), odd and even windows, both DMA modes
+    rng = np.random.default_rng(11)
+    d = rng.integers(1, 6, (9, 3)).astype(np.float64)
+    for dma, sigma in ((2, 0.5), (1, 1.0)):
+        for lo, hi in ((0, 362880), (1000, 362880 - 7)):
+            _, oms = O.exhaustive(d, dma, sigma, lo, hi, threads=8, makespans=True)
+            _, below, med = _capi.exhaustive_stats(d, dma, sigma, lo, hi, threshold=float(np.median(oms)))
+            assert med == float(np.median(oms)) and below == int((oms < np.median(oms)).sum())
+
+
 def test_c4_full_space_median_is_an_order_statistic():
     d = synth.c4_group()
     total = math.factorial(12)
