@@ -103,13 +103,31 @@ def _bits_to_double(b: int) -> float:
     return float(np.array([b], dtype=np.uint64).view(np.float64)[0])
 
 
-def select_kth_distributed(local_hist: Callable, k: int, group=None, device=None) -> float:
+def _double_bits(x: float) -> int:
+    return int(np.array([x], dtype=np.float64).view(np.uint64)[0])
+
+
+def common_prefix(vmin: float, vmax: float) -> Tuple[int, int]:
+    """(prefix, bits): the leading bit-pattern bits shared by every positive
+    double in [vmin, vmax] (the selection walk starts below them)."""
+    if not (vmin > 0.0 and vmax >= vmin):
+        return 0, 0
+    a, b = _double_bits(vmin), _double_bits(vmax)
+    bits = 64 - (a ^ b).bit_length()
+    bits = min(bits, 63)
+    return a >> (64 - bits) if bits else 0, bits
+
+
+def select_kth_distributed(local_hist: Callable, k: int, group=None, device=None,
+                           vmin: float = 0.0, vmax: float = 0.0) -> float:
     """k-th smallest (0-based) positive double of a set sharded over ranks.
 
     local_hist(prefix, prefix_bits, digit_bits) -> int64 histogram of this
     rank's values (2**digit_bits bins, MSB-first digits of the bit pattern,
     values whose top prefix_bits bits equal prefix).  One all_reduce(SUM)
     per pass combines the ranks (NCCL on GPUs); every rank gets the answer.
+    vmin / vmax (the set's min and max, e.g. best / worst) skip the leading
+    bits all values share.
     """
     import torch
     import torch.distributed as tdist
@@ -117,7 +135,7 @@ def select_kth_distributed(local_hist: Callable, k: int, group=None, device=None
     backend = tdist.get_backend(group)
     dev = device if device is not None else (torch.device("cuda", torch.cuda.current_device())
                                              if backend == "nccl" else torch.device("cpu"))
-    prefix, pbits = 0, 0
+    prefix, pbits = common_prefix(vmin, vmax)
     while pbits < 64:
         d = min(RADIX_BITS, 64 - pbits)
         h = torch.from_numpy(np.ascontiguousarray(local_hist(prefix, pbits, d), dtype=np.int64)).to(dev)
@@ -145,12 +163,13 @@ def numpy_hist(vals: np.ndarray):
     return hist
 
 
-def median_distributed(local_hist: Callable, count: int, group=None, device=None) -> float:
+def median_distributed(local_hist: Callable, count: int, group=None, device=None,
+                       vmin: float = 0.0, vmax: float = 0.0) -> float:
     """np.median of the sharded set: the middle value, or (a + b) / 2."""
     if count % 2:
-        return select_kth_distributed(local_hist, count // 2, group, device)
-    a = select_kth_distributed(local_hist, count // 2 - 1, group, device)
-    b = select_kth_distributed(local_hist, count // 2, group, device)
+        return select_kth_distributed(local_hist, count // 2, group, device, vmin, vmax)
+    a = select_kth_distributed(local_hist, count // 2 - 1, group, device, vmin, vmax)
+    b = select_kth_distributed(local_hist, count // 2, group, device, vmin, vmax)
     return float(np.float64(a) + np.float64(b)) / 2.0
 
 
@@ -206,5 +225,5 @@ def _stats_on_stream(L, C, torch, tdist, _capi, d, n, dma, sigma, threshold, gro
                                           C.c_void_p(hist.data_ptr()), sp))
         return hist[: 1 << dbits].to(torch.int64).cpu().numpy()
 
-    med = median_distributed(local_hist, summ.count, group)
+    med = median_distributed(local_hist, summ.count, group, vmin=summ.best, vmax=summ.worst)
     return summ, int(below.item()), med

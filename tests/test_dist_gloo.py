@@ -76,8 +76,10 @@ def _median_worker(rank, world, port, vals, q):
         mine = vals[lo:hi]
         h = numpy_hist(mine)
         med = median_distributed(h, len(vals))
-        k7 = select_kth_distributed(h, 7)
-        q.put((rank, med, k7))
+        # starting below the common prefix of the set's min and max
+        med2 = median_distributed(h, len(vals), vmin=float(vals.min()), vmax=float(vals.max()))
+        k7 = select_kth_distributed(h, 7, vmin=float(vals.min()), vmax=float(vals.max()))
+        q.put((rank, med, k7, med2))
     finally:
         tdist.destroy_process_group()
 
@@ -100,6 +102,6 @@ def test_gloo_sharded_median_selection(count):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for _, med, k7 in res:
-        assert med == float(np.median(vals))
+    for _, med, k7, med2 in res:
+        assert med == med2 == float(np.median(vals))
         assert k7 == float(np.sort(vals)[7])

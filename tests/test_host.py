@@ -179,3 +179,18 @@ def test_worker_task_draws_match_reference():
         flat = [t for row in wl.draw_worker_tasks(sc) for t in row]
         assert [t.id for t in flat] == c["ids"]
         assert [list(t.fixed_durations) for t in flat] == durs(c["durs"]).tolist()
+
+
+def test_common_prefix_of_value_range():
+    import numpy as np
+
+    from paper_1806_10113_b200.dist import common_prefix
+
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        v = np.sort(rng.uniform(0.1, 100.0, 50) * 2.0 ** rng.integers(-3, 4))
+        p, bits = common_prefix(float(v[0]), float(v[-1]))
+        u = v.view(np.uint64)
+        assert bits == 0 or all(int(x) >> (64 - bits) == p for x in u)
+    assert common_prefix(2.0, 2.0)[1] == 63
+    assert common_prefix(0.0, 1.0) == (0, 0)
