@@ -933,7 +933,12 @@ int osim_heuristic_batch(const double* durs, const uint8_t* id_rank, uint64_t B,
         // large batches: chunks alternate between two streams so the H2D of
         // chunk i+1 and the D2H of chunk i-1 overlap the kernel of chunk i
         // (effective when the caller's buffers are pinned)
-        const uint64_t nchunk = m >= (1ull << 17) ? 8 : 1;
+        static const uint64_t kChunks = [] {  // OSIM_HCHUNKS overrides (tuning only)
+            const char* e = std::getenv("OSIM_HCHUNKS");
+            const int x = e ? std::atoi(e) : 0;
+            return (uint64_t)((x >= 1 && x <= 256) ? x : 8);
+        }();
+        const uint64_t nchunk = m >= (1ull << 17) ? kChunks : 1;
         for (uint64_t ci = 0; ci < nchunk; ++ci) {
             const uint64_t a = m * ci / nchunk, e = m * (ci + 1) / nchunk, mm = e - a;
             if (!mm) continue;
