@@ -2,6 +2,7 @@
 #include <cmath>
 
 #include "osim_launch.cuh"
+#include "osim_heur_null.cuh"
 
 namespace osim {
 
@@ -24,8 +25,16 @@ void heuristic_launch(int dma, int mode, const LaunchCfg& cfg, const double* d_d
     }
 #define OSIM_HL(D, M) \
     k_heuristic<D, M><<<grid, kHT, sm, cfg.st>>>(d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms, d_ns, d_err)
-    if (mode == 2) {  // null stages in the fast range: NullSim per candidate
-        if (dma == 2) OSIM_HL(2, 2); else OSIM_HL(1, 2);
+    if (mode == 2) {  // null stages in the fast range: NullSim with prefix-world checkpoints
+        const unsigned gridf = (unsigned)((B + kHGF - 1) / kHGF);
+        int e;
+        const bool sp2 = std::frexp(sigma, &e) == 0.5;
+#define OSIM_HN(D, P)                                                                                         \
+    k_heuristic_nullck<D, P><<<gridf, kHTF, kWPB * sizeof(NullHeurWarpShared<D, P>), cfg.st>>>(              \
+        d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms, d_ns, d_err)
+        if (dma == 2) { if (sp2) OSIM_HN(2, true); else OSIM_HN(2, false); }
+        else OSIM_HN(1, false);
+#undef OSIM_HN
     } else {
         if (dma == 2) OSIM_HL(2, 0); else OSIM_HL(1, 0);
     }

@@ -1107,7 +1107,7 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
 #endif
             if constexpr (DMA == 2) {
                 s.start_htd();  // the candidate's HtD, the only one left
-                s.run_phased<false>(rest, sigma, rsig);
+                s.template run_phased<false>(rest, sigma, rsig);
             } else {
                 s.run_phased(rest, sigma, rsig);
             }
@@ -1179,7 +1179,7 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
             // bounded: the optimistic host pass may run this on ineligible input
             if constexpr (DMA == 2) {
                 s.start_htd();  // the chosen task's HtD, the queue's last
-                for (int q = 0; q < 3 * kMaxN && s.htd_done() < k + 1; ++q) s.step<false>(sigma, rsig);
+                for (int q = 0; q < 3 * kMaxN && s.htd_done() < k + 1; ++q) s.template step<false>(sigma, rsig);
             } else {
                 for (int q = 0; q < 3 * kMaxN && s.htd_done() < k + 1; ++q) s.step(sigma, rsig);
             }

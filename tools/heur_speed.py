@@ -18,9 +18,12 @@ def main():
     st = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(st)
     B = 1_000_000
+    null = "--null" in sys.argv  # one null DtH per group: the NullSim checkpoint kernel
     for prof in ("nvidia", "amd", "phi"):
         _, dma, sigma = synth.PROFILES[prof]
         d, r = synth.c5_batch_fast(prof, B)
+        if null:
+            d[:, 5, 2] = 0.0
         dd, rr = torch.from_numpy(d).to(dev), torch.from_numpy(r).to(dev)
         oo = torch.empty((B, 16), dtype=torch.uint8, device=dev)
         mm = torch.empty(B, dtype=torch.float64, device=dev)
@@ -28,7 +31,8 @@ def main():
 
         def run():
             _capi.check(L.osim_heuristic_batch_dev(C.c_void_p(dd.data_ptr()), C.c_void_p(rr.data_ptr()), B, 16, dma,
-                                                   sigma, 1, 1, C.c_void_p(oo.data_ptr()), C.c_void_p(mm.data_ptr()),
+                                                   sigma, 1, 2 if null else 1, C.c_void_p(oo.data_ptr()),
+                                                   C.c_void_p(mm.data_ptr()),
                                                    C.c_void_p(ns.data_ptr()), C.c_void_p(st.cuda_stream)))
         run()
         torch.cuda.synchronize()
@@ -38,7 +42,7 @@ def main():
             run()
         e1.record()
         torch.cuda.synchronize()
-        print(f"{prof}: {5 * B / (e0.elapsed_time(e1) / 1e3) / 1e6:.1f} M decisions/s", flush=True)
+        print(f"{prof}{' (null stages)' if null else ''}: {5 * B / (e0.elapsed_time(e1) / 1e3) / 1e6:.1f} M decisions/s", flush=True)
 
 
 if __name__ == "__main__":
