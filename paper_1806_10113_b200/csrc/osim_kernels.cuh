@@ -1105,12 +1105,8 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
 #ifdef OSIM_HSTATS
             hstats_replay(s, rest, valid, sigma, rsig);
 #endif
-            if constexpr (DMA == 2) {
-                s.start_htd();  // the candidate's HtD, the only one left
-                s.template run_phased<false>(rest, sigma, rsig);
-            } else {
-                s.run_phased(rest, sigma, rsig);
-            }
+            s.start_htd();  // the candidate's HtD, the only one left
+            s.template run_phased<false>(rest, sigma, rsig);
             // _completion_estimate (heuristic.py:34-49): builtin sum of the
             // rest's t_k in rt order (cand[] is rt in input order, rest skips
             // position j), min t_dth.  Warp-uniform loop over the m-1 rest.
@@ -1177,11 +1173,11 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
             s.init(gbase(g), S.ot[g], k + 1);
             s.load(S.ck[g]);
             // bounded: the optimistic host pass may run this on ineligible input
+            s.start_htd();  // the chosen task's HtD, the queue's last
             if constexpr (DMA == 2) {
-                s.start_htd();  // the chosen task's HtD, the queue's last
                 for (int q = 0; q < 3 * kMaxN && s.htd_done() < k + 1; ++q) s.template step<false>(sigma, rsig);
             } else {
-                for (int q = 0; q < 3 * kMaxN && s.htd_done() < k + 1; ++q) s.step(sigma, rsig);
+                for (int q = 0; q < 3 * kMaxN && s.htd_done() < k + 1; ++q) s.step_1dk();
             }
             s.save(S.ck[g]);
         }

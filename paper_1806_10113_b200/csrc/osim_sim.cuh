@@ -496,6 +496,30 @@ struct FastSim {
             if constexpr (TRACK) kEnd = now;
         }
     }
+    // 1-DMA with the queue's last HtD already started (start_htd): the XFER
+    // lane can only start DtHs (every HtD is finalized whenever it is idle), so
+    // step() reduces to step_1d() plus the K readiness test on the HtD head
+    __device__ __forceinline__ void step_1dk() {
+        static_assert(DMA == 1, "1-DMA only");
+        const int ps = s0 - n4;
+        const bool st0 = idle(r0) && s0 < 2 * n4 && s2 > ps;
+        const bool st2 = idle(r2) && s2 < n4 && s2 < s0;
+        k_idle_gap(st2);
+        start_if(st0, base + 512u + task_off<PRE>(seq, ps), d0, c0, r0);
+        start_if(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
+        const double dt = dmin(r0, r2);
+        now = __dadd_rn(now, dt);
+        r0 = upd(r0, dt, d0, c0);
+        r2 = upd(r2, dt, d2, c2);
+        const bool f0 = r0 <= kEndEps;
+        r0 = retire_or_drain(f0, r0, s0 + 4 >= 2 * n4);
+        s0 += f0 ? 4 : 0;
+        if (r2 <= kEndEps) {
+            r2 = retire(r2);
+            s2 += 4;
+            if constexpr (TRACK) kEnd = now;
+        }
+    }
     __device__ __forceinline__ void step_1dd() {
         static_assert(DMA == 1, "1-DMA only");
         const bool st0 = idle(r0) && s0 < 2 * n4;
@@ -530,7 +554,7 @@ struct FastSim {
             }
 #pragma unroll 2
             for (; st < rest; ++st) step_d();
-        } else {
+        } else if constexpr (H0) {
 #pragma unroll 1
             for (; st < rest; st += 2) {
                 if (__all_sync(0xffffffffu, s0 >= n4)) break;
@@ -542,6 +566,15 @@ struct FastSim {
                 if (__all_sync(0xffffffffu, s2 >= n4)) break;
                 step_1d();
                 step_1d();
+            }
+#pragma unroll 2
+            for (; st < rest; ++st) step_1dd();
+        } else {  // the last HtD already started: K+XFER-DtH steps, then XFER only
+#pragma unroll 1
+            for (; st < rest; st += 2) {
+                if (__all_sync(0xffffffffu, s2 >= n4)) break;
+                step_1dk();
+                step_1dk();
             }
 #pragma unroll 2
             for (; st < rest; ++st) step_1dd();
