@@ -539,6 +539,47 @@ __device__ __forceinline__ void lab_waves(uint64_t lab, int n, uint64_t& wsq, ui
     }
 }
 
+// Waves of the run's later sequences: the wave starts below M are the run's
+// (prefix-determined), so only positions >= M extend the start set and only
+// the ws / we nibbles from the wave holding position M - 1 on change.
+// startsM / w0M / lastM: start bits below M, start of the wave holding M - 1,
+// 1 + last position per worker over the prefix (lab_wave_prefix).
+__device__ __forceinline__ void lab_wave_prefix(uint64_t lab, int M, unsigned& starts, int& w0, uint64_t& last) {
+    starts = 0;
+    w0 = 0;
+    last = 0;
+    for (int p = 0; p < M; ++p) {
+        const int sh = 4 * lab_at(lab, p);
+        const int lp = (int)((last >> sh) & 0xF) - 1;
+        if (p == 0 || lp >= w0) { starts |= 1u << p; w0 = p; }
+        last = (last & ~(0xFull << sh)) | ((uint64_t)((p + 1) & 0xF) << sh);
+    }
+}
+
+__device__ __forceinline__ void lab_waves_from(uint64_t lab, int n, int M, unsigned startsM, int w0M, uint64_t lastM,
+                                               uint64_t& wsq, uint64_t& weq) {
+    unsigned starts = startsM;
+    int w0 = w0M;
+    uint64_t last = lastM;
+    for (int p = M; p < n; ++p) {
+        const int sh = 4 * lab_at(lab, p);
+        const int lp = (int)((last >> sh) & 0xF) - 1;
+        if (p == 0 || lp >= w0) { starts |= 1u << p; w0 = p; }
+        last = (last & ~(0xFull << sh)) | ((uint64_t)((p + 1) & 0xF) << sh);
+    }
+    const uint64_t keep = (w0M >= 16) ? ~0ull : ((1ull << (4 * w0M)) - 1ull);
+    wsq &= keep;
+    weq &= keep;
+    int ws = w0M;
+    for (int p = w0M; p < n; ++p) {
+        if ((starts >> p) & 1u) ws = p;
+        const unsigned after = starts & ~((2u << p) - 1u);
+        const int we = after ? __ffs(after) - 1 : n;
+        wsq |= (uint64_t)ws << (4 * p);
+        weq |= (uint64_t)(we - 1) << (4 * p);
+    }
+}
+
 template <bool PRE>
 __global__ void __launch_bounds__(kBlock, OSIM_F1_MINB) k_interleave_pfx1(const double* __restrict__ durs, int T, int N,
                                                             uint64_t lo, uint64_t hi, uint64_t mtotal, int K,
@@ -593,8 +634,12 @@ __global__ void __launch_bounds__(kBlock, OSIM_F1_MINB) k_interleave_pfx1(const 
         const int M = S.m[e] & 255;
         const bool valid = (S.m[e] >> 8) != 0;
         const uint64_t r1 = (r0 + (uint64_t)K < hi) ? r0 + (uint64_t)K : hi;
-        uint64_t cnt, last, order, dseq, wsq, weq;
+        uint64_t cnt, last, order, dseq, wsq, weq, wlast;
         run_tasks(lab, N, M, n, cnt, last, order, dseq);
+        unsigned wstarts;
+        int w0M;
+        lab_wave_prefix(lab, M, wstarts, w0M, wlast);
+        lab_waves(lab, n, wsq, weq);
         const int rest = 3 * n - __reduce_min_sync(kFull, valid ? S.sa[e] : 3 * n);
         WaveSim<PRE> s;
 #pragma unroll 1
@@ -602,8 +647,8 @@ __global__ void __launch_bounds__(kBlock, OSIM_F1_MINB) k_interleave_pfx1(const 
             if (q > 0) {
                 lab = lab_next(lab, n);
                 lab_tasks(lab, N, M, n, cnt, last, order, dseq);
+                lab_waves_from(lab, n, M, wstarts, w0M, wlast, wsq, weq);
             }
-            lab_waves(lab, n, wsq, weq);
             s.init(base, order, n, wsq, weq);
             s.now = cv[0][e]; s.r2 = cv[1][e]; s.d2 = cv[2][e]; s.c2 = cv[3][e];
             s.x = cx[0][e]; s.s2 = cx[1][e];
