@@ -53,6 +53,7 @@ struct DevCtx {
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
     int* d_err = nullptr;
+    unsigned* d_done = nullptr;  // last-CTA counter of the fused final reductions (kept at 0)
     std::mutex mu;
 };
 
@@ -76,6 +77,8 @@ int ensure_init() {
         CK(cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming));
         CK(cudaMalloc(&c->d_err, sizeof(int)));
         CK(cudaMemset(c->d_err, 0, sizeof(int)));
+        CK(cudaMalloc(&c->d_done, sizeof(unsigned)));
+        CK(cudaMemset(c->d_done, 0, sizeof(unsigned)));
         g_devs.push_back(c);
     }
     return 0;
@@ -232,16 +235,20 @@ bool sigma_pow2(double sigma) {
 
 int launch_exh_fast_dispatch(int dma, int n, DevCtx* c, cudaStream_t st, const double* d_durs, double sigma,
                              uint64_t lo, uint64_t hi, double thr, Part* parts, int max_parts, double* d_ms,
-                             int* g) {
+                             int* g, osim_summary* d_out, unsigned long long* d_below) {
     const LaunchCfg cfg{c->sms, st};
     const int L = pfx_l_for(n);
+    unsigned* dn = c->d_done;
     int rc;
     if (dma == 2)
         rc = sigma_pow2(sigma)
-                 ? exh_fast_launch_d2s1(n, L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g)
-                 : exh_fast_launch_d2s0(n, L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g);
+                 ? exh_fast_launch_d2s1(n, L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, d_out,
+                                        d_below, dn)
+                 : exh_fast_launch_d2s0(n, L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, d_out,
+                                        d_below, dn);
     else
-        rc = exh_fast_launch_d1(n, L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g);
+        rc = exh_fast_launch_d1(n, L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, d_out, d_below,
+                                dn);
     if (rc) return fail(OSIM_EINVAL, "unsupported n=%d", n);
     return 0;
 }
@@ -264,8 +271,12 @@ int enqueue_exhaustive(DevCtx* c, cudaStream_t st, const double* d_durs, int n, 
     int g = 1;
     int rc = 0;
     if (hi > lo) {
-        if (fast == 1) {
-            rc = launch_exh_fast_dispatch(dma, n, c, st, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, &g);
+        if (fast == 1) {  // the kernel's last CTA writes d_out (no final-reduce launch)
+            rc = launch_exh_fast_dispatch(dma, n, c, st, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, &g,
+                                          d_out, d_below);
+            if (rc) return rc;
+            CK(cudaGetLastError());
+            return 0;
         } else if (fast == 2) {  // null stages in the fast range: NullSim with prefix sharing
             if (null_pfx_launch(n, dma, sigma_pow2(sigma), LaunchCfg{c->sms, st}, d_durs, sigma, lo, hi, thr, parts,
                                 max_parts, d_ms, c->d_err, &g))

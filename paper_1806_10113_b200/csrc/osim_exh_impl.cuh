@@ -9,7 +9,8 @@ namespace {
 
 template <int N, int L>
 int exh_t(const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo, uint64_t hi, double thr,
-          Part* parts, int max_parts, double* d_ms, int* grid_out) {
+          Part* parts, int max_parts, double* d_ms, int* grid_out, osim_summary* d_out, unsigned long long* d_below,
+          unsigned* d_done) {
     // makespans out or a positive threshold need the stats variant
     auto k = (d_ms || thr > 0.0) ? k_exhaustive_pfx<N, OSIM_DMA, OSIM_SP2, L, true>
                                  : k_exhaustive_pfx<N, OSIM_DMA, OSIM_SP2, L, false>;
@@ -18,29 +19,31 @@ int exh_t(const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo,
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPfxDynSmem);
     int g = grid_for_sms(k, kBlock, kPfxDynSmem, cfg.sms, (prefixes + kPfxQ * kBlock - 1) / (kPfxQ * kBlock));
     if (g > max_parts) g = max_parts;
-    k<<<g, kBlock, kPfxDynSmem, cfg.st>>>(d_durs, sigma, lo, hi, thr, parts, d_ms);
+    k<<<g, kBlock, kPfxDynSmem, cfg.st>>>(d_durs, sigma, lo, hi, thr, parts, d_ms, d_out, d_below, d_done);
     *grid_out = g;
     return 0;
 }
 
 template <int N>
 int exh_n(int L, const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo, uint64_t hi,
-          double thr, Part* parts, int max_parts, double* d_ms, int* g) {
+          double thr, Part* parts, int max_parts, double* d_ms, int* g, osim_summary* o, unsigned long long* b,
+          unsigned* dn) {
     if constexpr (tunable_n(N)) {
-        if (L == 3) return exh_t<N, 3>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g);
-        if (L == 5) return exh_t<N, 5>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g);
-        if (L == 4) return exh_t<N, 4>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g);
+        if (L == 3) return exh_t<N, 3>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, o, b, dn);
+        if (L == 5) return exh_t<N, 5>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, o, b, dn);
+        if (L == 4) return exh_t<N, 4>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, o, b, dn);
     }
-    return exh_t<N, default_pfx_l(N)>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g);
+    return exh_t<N, default_pfx_l(N)>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, o, b, dn);
 }
 
 }  // namespace
 
 int OSIM_EXH_NAME(int n, int L, const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo,
-                  uint64_t hi, double thr, Part* parts, int max_parts, double* d_ms, int* g) {
+                  uint64_t hi, double thr, Part* parts, int max_parts, double* d_ms, int* g, osim_summary* d_out,
+                  unsigned long long* d_below, unsigned* d_done) {
     switch (n) {
 #define OSIM_CASE(NN) \
-    case NN: return exh_n<NN>(L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g);
+    case NN: return exh_n<NN>(L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, d_out, d_below, d_done);
         OSIM_CASE(1) OSIM_CASE(2) OSIM_CASE(3) OSIM_CASE(4) OSIM_CASE(5) OSIM_CASE(6)
         OSIM_CASE(7) OSIM_CASE(8) OSIM_CASE(9) OSIM_CASE(10) OSIM_CASE(11) OSIM_CASE(12)
         OSIM_CASE(13) OSIM_CASE(14) OSIM_CASE(15) OSIM_CASE(16)

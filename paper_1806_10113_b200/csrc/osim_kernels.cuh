@@ -533,13 +533,47 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
     // warp done early runs its next phase A meanwhile.
 }
 
+// The last CTA to finish reduces every CTA's partial (the work of
+// k_final_reduce, same thread mapping and tree, so the same bits) and resets
+// the counter: one launch per search instead of two.  `done` must be 0 on
+// entry; `parts` are read past L1 (written by other CTAs).
+__device__ __forceinline__ void fused_final_reduce(const Part* parts, osim_summary* out, unsigned long long* below,
+                                                   unsigned* done, Part* sh) {
+    __shared__ bool last;
+    __syncthreads();  // this CTA's partial is written (thread 0 wrote it)
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    Part a;
+    part_init(a);
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+        const volatile Part& p = parts[i];
+        Part b;
+        b.best = p.best; b.rank = p.rank; b.worst = p.worst; b.sum = p.sum; b.csum = p.csum;
+        b.lpm = p.lpm; b.lpe = p.lpe; b.count = p.count; b.below = p.below;
+        part_merge(a, b);
+    }
+    a = block_reduce(a, sh);
+    if (threadIdx.x == 0) {
+        *out = part_to_summary(a);
+        if (below) *below = a.below;
+        *done = 0u;
+    }
+}
+
 // dynamic shared memory of the prefix kernels (checkpoint slots + sort)
 constexpr size_t kPfxDynSmem = sizeof(CkSlots<kPfxQ>) + sizeof(PfxSort);
 
 template <int N, int DMA, bool SIGP2, int L, bool STATS>
 __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const double* __restrict__ durs, double sigma,
                                                            uint64_t lo, uint64_t hi, double thr, Part* __restrict__ parts,
-                                                           double* __restrict__ ms_out) {
+                                                           double* __restrict__ ms_out, osim_summary* __restrict__ out,
+                                                           unsigned long long* __restrict__ below,
+                                                           unsigned* __restrict__ done) {
     __shared__ double2 sdr[3 * kStride];
     __shared__ Part sh[32];
     extern __shared__ __align__(16) unsigned char pfx_dsm[];
@@ -563,6 +597,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
         pfx_leaves<N, DMA, SIGP2, L, STATS>(base, sigma, rsig, pb, p_hi, lo, hi, thr, acc, ms_out, lo, K, S);
     acc = block_reduce(acc, sh);
     if (threadIdx.x == 0) parts[blockIdx.x] = acc;
+    if (out) fused_final_reduce(parts, out, below, done, sh);
 }
 
 // Batched groups with prefix sharing: one CTA per group.

@@ -47,10 +47,13 @@ inline int pfx_l_for(int n) {
     return default_pfx_l(n);
 }
 
-// exhaustive, all stages non-null, prefix-sharing (returns -1: unsupported n)
+// exhaustive, all stages non-null, prefix-sharing (returns -1: unsupported n);
+// with d_out the kernel's last CTA also does the final reduction (d_done: a
+// zeroed per-device counter the kernel leaves at zero)
 #define OSIM_EXH_DECL(NAME)                                                                          \
     int NAME(int n, int L, const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo,   \
-             uint64_t hi, double thr, Part* parts, int max_parts, double* d_ms, int* grid_out);
+             uint64_t hi, double thr, Part* parts, int max_parts, double* d_ms, int* grid_out,        \
+             osim_summary* d_out, unsigned long long* d_below, unsigned* d_done);
 OSIM_EXH_DECL(exh_fast_launch_d2s1)
 OSIM_EXH_DECL(exh_fast_launch_d2s0)
 OSIM_EXH_DECL(exh_fast_launch_d1)
