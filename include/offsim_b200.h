@@ -38,7 +38,10 @@
  * Device memory and streams are library-owned.  Calls are reentrant
  * (per-device mutex).  `_dev` variants take device pointers on the calling
  * thread's current library device, enqueue on `stream` (NULL = the
- * library's stream) and do not synchronize.
+ * library's stream) and do not synchronize; they use the device's library
+ * scratch (per-block partials, the last-block counter), so work enqueued by
+ * _dev calls on one device must be ordered (one stream, or events between
+ * streams) -- as in bench.py and dist.py.
  */
 #ifndef OFFSIM_B200_H
 #define OFFSIM_B200_H
