@@ -9,7 +9,9 @@ attaining the minimum" is the global lowest-rank argmin, so best / argmin /
 worst / count are bit-exact and mean / geomean are fixed-order sums.
 
 Batched groups and the heuristic (configs 2/5) shard the group index range
-with no collective at all.
+with no collective in the compute (reorder_durs_distributed,
+exhaustive_summary_batch_distributed; an optional all_gather assembles the
+whole batch on every rank).
 """
 
 from __future__ import annotations
@@ -92,6 +94,88 @@ def exhaustive_summary_distributed(durs, dma: int, sigma: float, group=None,
     tdist.all_gather(bufs, mine, group=group)
     parts = [unpack(b.cpu().numpy()) for b in bufs]
     return summary_from_dict(combine(parts), n)
+
+
+# ---- batches of groups (configs 2 and 5): group-range shards, no collective
+# in the compute; gather=True assembles the whole batch on every rank -------
+
+def _gather_rows(local: np.ndarray, total: int, group, world: int, device) -> np.ndarray:
+    """all_gather of this rank's contiguous rows of a [total][...] array
+    (shards from `shard`, padded to the largest shard for the collective)."""
+    import torch
+    import torch.distributed as tdist
+
+    width = max(shard(total, r, world)[1] - shard(total, r, world)[0] for r in range(world))
+    row = local.shape[1:]
+    raw = np.ascontiguousarray(local).view(np.uint8).reshape(local.shape[0], -1)
+    pad = np.zeros((width, raw.shape[1]), dtype=np.uint8)
+    pad[: raw.shape[0]] = raw
+    t = torch.from_numpy(pad).to(device)
+    bufs = [torch.empty_like(t) for _ in range(world)]
+    tdist.all_gather(bufs, t, group=group)
+    parts = []
+    for r, b in enumerate(bufs):
+        lo, hi = shard(total, r, world)
+        parts.append(b.cpu().numpy()[: hi - lo])
+    out = np.concatenate(parts).view(local.dtype)
+    return out.reshape((total,) + row)
+
+
+def _coll_device(group, device):
+    import torch
+    import torch.distributed as tdist
+
+    if device is not None:
+        return device
+    return torch.device("cuda", torch.cuda.current_device()) if tdist.get_backend(group) == "nccl" else \
+        torch.device("cpu")
+
+
+def reorder_durs_distributed(durs, id_rank, dma: int, sigma: float, sum_mode: Optional[int] = None, group=None,
+                             gather: bool = True, local_fn: Optional[Callable] = None, device=None):
+    """reorder_batch over a batch sharded by group range over the process
+    group (one GPU per rank, no collective in the compute).  Returns
+    (order uint8 [B][n], makespan [B], n_sims [B]) for the whole batch on every
+    rank (gather=True, one all_gather per output) or this rank's rows."""
+    import torch.distributed as tdist
+
+    from . import _capi
+    from .heuristic import SUM_MODE
+
+    d = np.ascontiguousarray(np.asarray(durs, dtype=np.float64))
+    r = np.ascontiguousarray(np.asarray(id_rank, dtype=np.uint8))
+    B = d.shape[0]
+    world, rank = tdist.get_world_size(group), tdist.get_rank(group)
+    lo, hi = shard(B, rank, world)
+    mode = SUM_MODE if sum_mode is None else int(sum_mode)
+    fn = local_fn or (lambda dd, rr: _capi.heuristic_batch(dd, rr, dma, sigma, mode))
+    order, ms, sims = fn(d[lo:hi], r[lo:hi])
+    if not gather:
+        return order, ms, sims
+    dev = _coll_device(group, device)
+    return (_gather_rows(np.asarray(order, dtype=np.uint8), B, group, world, dev),
+            _gather_rows(np.asarray(ms, dtype=np.float64), B, group, world, dev),
+            _gather_rows(np.asarray(sims, dtype=np.uint32), B, group, world, dev))
+
+
+def exhaustive_summary_batch_distributed(durs, dma: int, sigma: float, group=None, gather: bool = True,
+                                         local_fn: Optional[Callable] = None, device=None) -> np.ndarray:
+    """One full-space summary per group of a batch sharded by group range
+    (config 2); _capi.SUMMARY_DTYPE records for the whole batch on every rank
+    (gather=True) or this rank's rows."""
+    import torch.distributed as tdist
+
+    from . import _capi
+
+    d = np.ascontiguousarray(np.asarray(durs, dtype=np.float64))
+    B = d.shape[0]
+    world, rank = tdist.get_world_size(group), tdist.get_rank(group)
+    lo, hi = shard(B, rank, world)
+    fn = local_fn or (lambda dd: _capi.exhaustive_batch(dd, dma, sigma))
+    out = fn(d[lo:hi])
+    if not gather:
+        return out
+    return _gather_rows(out, B, group, world, _coll_device(group, device))
 
 
 # ---- order statistics of a sharded makespan set (row f2) -------------------

@@ -105,3 +105,58 @@ def test_gloo_sharded_median_selection(count):
     for _, med, k7, med2 in res:
         assert med == med2 == float(np.median(vals))
         assert k7 == float(np.sort(vals)[7])
+
+
+def _oracle_reorder(dd, rr):
+    return O.reorder_batch(dd, rr, 2, 0.5, 1, threads=2)
+
+
+def _oracle_batch(dd):
+    from paper_1806_10113_b200 import _capi
+
+    out = np.zeros(dd.shape[0], dtype=_capi.SUMMARY_DTYPE)
+    for i in range(dd.shape[0]):
+        s, _ = O.exhaustive(dd[i], 2, 0.5, threads=1)
+        for k in out.dtype.names:
+            out[i][k] = s[k]
+    return out
+
+
+def _batch_worker(rank, world, port, d, r, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1806_10113_b200.dist import exhaustive_summary_batch_distributed, reorder_durs_distributed
+
+        order, ms, sims = reorder_durs_distributed(d, r, 2, 0.5, 1, local_fn=_oracle_reorder)
+        summ = exhaustive_summary_batch_distributed(d[:, :6], 2, 0.5, local_fn=_oracle_batch)
+        q.put((rank, order, ms, sims, summ))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_gloo_batch_shards_gather_whole_batch():
+    # configs 2/5 over 3 ranks: ragged group-range shards (101 groups), the
+    # gathered arrays equal the single-process batch on every rank
+    from paper_1806_10113_b200 import synth
+
+    B, n = 101, 9
+    d = np.stack([synth.real_group("K20", n, 40 + b)[1] for b in range(B)])
+    r = np.stack([np.random.default_rng(b).permutation(n) for b in range(B)]).astype(np.uint8)
+    want = O.reorder_batch(d, r, 2, 0.5, 1, threads=4)
+    want_s = _oracle_batch(d[:, :6])
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(k, world, port, d, r, q)) for k in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, order, ms, sims, summ in res:
+        assert np.array_equal(order, want[0]) and np.array_equal(ms, want[1]) and np.array_equal(sims, want[2])
+        assert summ.tobytes() == want_s.tobytes()

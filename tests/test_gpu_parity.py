@@ -752,7 +752,12 @@ def _nccl_worker(port, q):
         from paper_1806_10113_b200.dist import exhaustive_summary_distributed
 
         s = exhaustive_summary_distributed(synth.c3_group(), 2, 0.5)  # NCCL all_gather of device tensors
-        q.put((s.best, s.best_ordering, s.worst, s.mean, s.count))
+        from paper_1806_10113_b200.dist import exhaustive_summary_batch_distributed, reorder_durs_distributed
+
+        d5, r5 = synth.c5_batch_fast("nvidia", 5000)
+        order, ms, sims = reorder_durs_distributed(d5, r5, 2, 0.5)
+        summ = exhaustive_summary_batch_distributed(synth.c2_batch(300), 2, 0.5)
+        q.put((s.best, s.best_ordering, s.worst, s.mean, s.count, order, ms, sims, summ))
     finally:
         tdist.destroy_process_group()
 
@@ -772,12 +777,16 @@ def test_nccl_exchange_single_rank():
     q = ctx.Queue()
     p = ctx.Process(target=_nccl_worker, args=(port, q))
     p.start()
-    best, order, worst, mean, count = q.get(timeout=300)
+    best, order, worst, mean, count, o5, m5, s5, summ = q.get(timeout=300)
     p.join(timeout=120)
     assert p.exitcode == 0
     whole = osim.exhaustive_summary_durs(synth.c3_group(), 2, 0.5)
     assert best == whole.best and tuple(order) == tuple(whole.best_ordering) and worst == whole.worst
     assert count == 3628800 and mean == whole.mean
+    d5, r5 = synth.c5_batch_fast("nvidia", 5000)
+    wo, wm, ws = _capi.heuristic_batch(d5, r5, 2, 0.5, osim.SUM_MODE)
+    assert np.array_equal(o5, wo) and np.array_equal(m5, wm) and np.array_equal(s5, ws)
+    assert summ.tobytes() == _capi.exhaustive_batch(synth.c2_batch(300), 2, 0.5).tobytes()
 
 
 def test_sigma_at_the_fast_range_boundary():
