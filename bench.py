@@ -251,6 +251,18 @@ def run_ours(a):
                              if k in ("issue_active_pct", "fp64_pipe_active_pct", "alu_pipe_active_pct",
                                       "warp_exec_efficiency", "achieved_occupancy_pct",
                                       "theoretical_occupancy_pct", "source")}}
+    # the issue roofline (SURVEY 8(d) ii): warp instructions the kernel executes
+    # per launch (the committed ncu capture of the same kernel on the whole
+    # 12! space, scaled to this rank's shard) over 4 issues/clk/SM x SMs x the
+    # SM clock measured during the timed region
+    wi = profile_headline().get("warp_instructions_per_launch")
+    sm_mhz = clk.summary().get("sm_mhz")
+    if wi and sm_mhz:
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        ach = wi * (hi - lo) / TOTAL12 / kern_avg
+        peak_i = 4.0 * sms * sm_mhz * 1e6
+        roof["issue"] = {"achieved_warp_instr_per_s": ach, "peak_warp_instr_per_s": peak_i, "frac": ach / peak_i,
+                         "warp_instr_per_launch": wi * (hi - lo) / TOTAL12, "sms": sms, "sm_mhz": sm_mhz}
 
     # ---- e2e through the public API (host buffers) ---------------------------
     e2e_steps = max(3, a.steps // 2)

@@ -64,6 +64,7 @@ def main(rep, out, label, headline=False):
                    "achieved_occupancy_pct": float(
                        k["sm__warps_active.avg.pct_of_peak_sustained_active"].split()[0]),
                    "theoretical_occupancy_pct": float(k["sm__maximum_warps_per_active_cycle_pct"].split()[0]),
+                   "warp_instructions_per_launch": float(k["smsp__inst_executed.sum"].split()[0]),
                    "source": out}, open("profiles/ncu_headline.json", "w"), indent=1)
     print(json.dumps(kernels, indent=1)[:3000])
 
