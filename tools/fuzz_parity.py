@@ -1,0 +1,119 @@
+"""Randomized GPU-vs-oracle parity sweep over the input space the fixtures do
+not enumerate: group sizes 1..12 (exhaustive, every ordering) and 1..40
+(heuristic, timelines), integer / mixed / real / wide-range durations with
+null stages and ties, sigma in {1, 1/2, 3/8, 0.8, 2^-k}, both DMA modes.
+Every makespan, argmin, order and simulation count must match bit for bit
+(sums within 1e-12).  Runs for --seconds; writes a JSON summary.
+
+    python tools/fuzz_parity.py [--seconds 600] [--seed 1] [--out fuzz.json]
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+
+from oracle import oracle as O  # noqa: E402
+from paper_1806_10113_b200 import _capi  # noqa: E402
+from paper_1806_10113_b200.heuristic import SUM_MODE  # noqa: E402
+
+SIGMAS = (1.0, 0.5, 0.375, 0.8, 0.25, 0.125, 0.9999999999999999)
+
+
+def durations(rng, n):
+    mode = rng.integers(4)
+    if mode == 0:
+        d = rng.integers(0, 5, (n, 3)).astype(np.float64)
+    elif mode == 1:
+        d = np.where(rng.random((n, 3)) < 0.5, rng.integers(1, 4, (n, 3)).astype(np.float64),
+                     rng.uniform(0.1, 5.0, (n, 3)))
+    elif mode == 2:
+        d = rng.uniform(0.01, 10.0, (n, 3))
+    else:
+        d = np.exp(rng.uniform(np.log(1e-6), np.log(1e8), (n, 3)))  # wide range (above 2^22 ms: general path)
+    d[rng.random((n, 3)) < (0.15 if mode else 0.0)] = 0.0
+    empty = d.sum(axis=1) == 0.0
+    d[empty, 1] = 1.0  # every task keeps a command (the reference rejects empty tasks)
+    return d
+
+
+def close(a, b):
+    return abs(a - b) <= 1e-12 * max(abs(a), abs(b), 1e-300)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--seconds", type=float, default=600.0)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--out", default="fuzz_parity.json")
+    a = ap.parse_args()
+    rng = np.random.default_rng(a.seed)
+    threads = os.cpu_count() or 1
+    stats = {"exhaustive_groups": 0, "exhaustive_orderings": 0, "heuristic_groups": 0, "timelines": 0,
+             "mismatches": []}
+    t_end = time.perf_counter() + a.seconds
+    it = 0
+    while time.perf_counter() < t_end:
+        it += 1
+        dma = int(rng.integers(1, 3))
+        sigma = 1.0 if dma == 1 else float(SIGMAS[rng.integers(len(SIGMAS))])
+        # exhaustive summary (every ordering, or a window for n >= 10)
+        n = int(rng.integers(1, 13))
+        d = durations(rng, n)
+        total = math.factorial(n)
+        lo, hi = 0, total
+        if n >= 10:
+            lo = int(rng.integers(0, total - 200_000))
+            hi = lo + 200_000
+        g, gm = _capi.exhaustive(d, dma, sigma, lo, hi, want_makespans=True)
+        o, om = O.exhaustive(d, dma, sigma, lo, hi, threads=threads, makespans=True)
+        ok = (np.array_equal(gm.view(np.uint64), om.view(np.uint64)) and g["best"] == o["best"]
+              and g["best_rank"] == o["best_rank"] and g["worst"] == o["worst"] and g["count"] == o["count"]
+              and close(g["sum"], o["sum"]) and close(g["sum_log"], o["sum_log"]))
+        stats["exhaustive_groups"] += 1
+        stats["exhaustive_orderings"] += hi - lo
+        if not ok:
+            stats["mismatches"].append({"kind": "exhaustive", "n": n, "dma": dma, "sigma": sigma, "lo": lo,
+                                        "durs": d.tolist()})
+        # heuristic batch of 64 groups of one size (up to 40 tasks: the wide path above 16)
+        n = int(rng.integers(1, 41)) if rng.random() < 0.3 else int(rng.integers(1, 17))
+        B = 64
+        dd = np.stack([durations(rng, n) for _ in range(B)])
+        rr = np.stack([rng.permutation(n) for _ in range(B)]).astype(np.uint8)
+        go, gms, gs = _capi.heuristic_batch(dd, rr, dma, sigma, SUM_MODE)
+        oo, oms, osims = O.reorder_batch(dd, rr, dma, sigma, SUM_MODE, threads=threads)
+        stats["heuristic_groups"] += B
+        if not (np.array_equal(go, oo) and np.array_equal(gms.view(np.uint64), oms.view(np.uint64))
+                and np.array_equal(gs, osims)):
+            bad = int(np.nonzero((go != oo).any(axis=1) | (gms != oms) | (gs != osims))[0][0])
+            stats["mismatches"].append({"kind": "heuristic", "n": n, "dma": dma, "sigma": sigma,
+                                        "durs": dd[bad].tolist(), "id_rank": rr[bad].tolist()})
+        # one timeline
+        n = int(rng.integers(1, 65)) if rng.random() < 0.2 else int(rng.integers(1, 17))
+        d = durations(rng, n)
+        order = [int(x) for x in rng.permutation(n)]
+        st, en, ms, idle = _capi.timeline(d, dma, sigma, order)
+        r = O.simulate(d, order, dma, sigma)
+        stats["timelines"] += 1
+        if not (ms == r.makespan and np.array_equal(st, r.start) and np.array_equal(en, r.end)
+                and idle.tolist() == r.idle.tolist()):
+            stats["mismatches"].append({"kind": "timeline", "n": n, "dma": dma, "sigma": sigma, "order": order,
+                                        "durs": d.tolist()})
+        if it % 20 == 0:
+            print(it, {k: v for k, v in stats.items() if k != "mismatches"}, "mismatches", len(stats["mismatches"]),
+                  flush=True)
+    stats["iterations"] = it
+    stats["host_threads"] = threads
+    with open(a.out, "w") as fh:
+        json.dump(stats, fh, indent=1)
+    print("done", {k: v for k, v in stats.items() if k != "mismatches"}, "mismatches", len(stats["mismatches"]))
+    sys.exit(1 if stats["mismatches"] else 0)
+
+
+if __name__ == "__main__":
+    main()
