@@ -46,16 +46,63 @@ def close(a, b):
     return abs(a - b) <= 1e-12 * max(abs(a), abs(b), 1e-300)
 
 
+def rows_step(rng, dma, sigma, threads, stats):
+    """f1: an interleaving window (T*N <= 16) and sampled label sequences (up
+    to 48 tasks); f3: a batch of proxy-thread scenarios (up to 48 tasks)."""
+    import ctypes as C
+
+    T, N = int(rng.integers(1, 5)), int(rng.integers(1, 5))
+    d = durations(rng, T * N)
+    total = math.factorial(T * N) // math.factorial(N) ** T
+    lo = int(rng.integers(0, max(1, total - 50_000)))
+    hi = min(total, lo + 50_000)
+    g, _, gm = _capi.interleavings(d, T, N, dma, sigma, lo, hi, want_makespans=True)
+    o, om = O.interleavings(d, T, N, dma, sigma, lo, hi, threads=threads, makespans=True)
+    stats["interleavings"] += hi - lo
+    if not (np.array_equal(gm.view(np.uint64), om.view(np.uint64)) and g["best_rank"] == o["best_rank"]):
+        stats["mismatches"].append({"kind": "interleavings", "T": T, "N": N, "dma": dma, "sigma": sigma, "lo": lo,
+                                    "durs": d.tolist()})
+    T, N = int(rng.integers(1, 9)), int(rng.integers(1, 7))
+    d = durations(rng, T * N)
+    lab = np.stack([rng.permutation(np.repeat(np.arange(T), N)) for _ in range(256)]).astype(np.uint8)
+    _, gm = _capi.eval_sequences(d, T, N, dma, sigma, lab)
+    _, om = O.eval_sequences(d, T, N, dma, sigma, lab, threads=threads)
+    stats["sequences"] += len(lab)
+    if not np.array_equal(gm.view(np.uint64), om.view(np.uint64)):
+        stats["mismatches"].append({"kind": "sequences", "T": T, "N": N, "dma": dma, "sigma": sigma,
+                                    "durs": d.tolist()})
+    T, N = int(rng.integers(1, 9)), int(rng.integers(1, 7))
+    S = 64
+    dd = np.stack([durations(rng, T * N) for _ in range(S)])
+    rr = np.stack([rng.permutation(T * N) for _ in range(S)]).astype(np.uint8)
+    ms, ng, sz, _, _ = _capi.harness_batch(dd, rr, T, N, dma, sigma, SUM_MODE)
+    L = O.lib()
+    L.oracle_harness.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_int,
+                                 C.c_double, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    for s_ in range(S):
+        om_, ong, osz = C.c_double(), C.c_int(), np.zeros(64, dtype=np.int32)
+        x = np.ascontiguousarray(dd[s_])
+        y = np.ascontiguousarray(rr[s_])
+        rc = L.oracle_harness(x.ctypes.data_as(C.POINTER(C.c_double)), y.ctypes.data_as(C.POINTER(C.c_uint8)), T, N,
+                              dma, sigma, SUM_MODE, C.byref(om_), C.byref(ong), osz.ctypes.data_as(C.POINTER(C.c_int)))
+        stats["scenarios"] += 1
+        if rc != 0 or ms[s_] != om_.value or sz[s_, : ng[s_]].tolist() != osz[: ong.value].tolist():
+            stats["mismatches"].append({"kind": "harness", "T": T, "N": N, "dma": dma, "sigma": sigma,
+                                        "durs": x.tolist(), "id_rank": y.tolist()})
+            break
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=600.0)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--out", default="fuzz_parity.json")
+    ap.add_argument("--rows", action="store_true", help="also the f1 (interleavings, sequences) and f3 (harness) paths")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     threads = os.cpu_count() or 1
     stats = {"exhaustive_groups": 0, "exhaustive_orderings": 0, "heuristic_groups": 0, "timelines": 0,
-             "mismatches": []}
+             "interleavings": 0, "sequences": 0, "scenarios": 0, "mismatches": []}
     t_end = time.perf_counter() + a.seconds
     it = 0
     while time.perf_counter() < t_end:
@@ -104,6 +151,8 @@ def main():
                 and idle.tolist() == r.idle.tolist()):
             stats["mismatches"].append({"kind": "timeline", "n": n, "dma": dma, "sigma": sigma, "order": order,
                                         "durs": d.tolist()})
+        if a.rows:
+            rows_step(rng, dma, sigma, threads, stats)
         if it % 20 == 0:
             print(it, {k: v for k, v in stats.items() if k != "mismatches"}, "mismatches", len(stats["mismatches"]),
                   flush=True)
