@@ -8,11 +8,13 @@ per second at N=10/12, heuristic TG decisions per second).
 Headline workload (BASELINE config 4): one 12-task group (the reference's
 sample_real_tasks("AMD", 12, seed=12), 2-DMA, sigma 0.5); one step = the
 exhaustive search of all 12! = 479,001,600 orderings -> best makespan,
-lowest-rank argmin, worst, mean, geomean.  With N ranks the Lehmer-rank
-space is sharded contiguously and the 48-byte per-rank summaries are
-combined by one NCCL all_gather inside the step (strong scaling).
+lowest-rank argmin, worst, mean, geomean.  With N ranks rank r takes the
+interleaved 512-prefix calls r, r + N, ... of the Lehmer-rank space (every
+rank samples the whole space, so the per-rank work evens out) and the 48-byte
+per-rank summaries are combined by one NCCL all_gather inside the step
+(strong scaling).
 
-`value` times the device-resident path (osim_exhaustive_dev: inputs in HBM,
+`value` times the device-resident path (osim_exhaustive_shard_dev: inputs in HBM,
 CUDA events on the launching stream, L2 flushed between steps and excluded).
 `e2e` times the public host API (exhaustive_summary_durs /
 dist.exhaustive_summary_distributed): host buffers, H2D + kernels + D2H +
@@ -214,12 +216,13 @@ def run_ours(a):
     d_durs = torch.from_numpy(durs).to(dev)
     d_out = torch.zeros(6, dtype=torch.float64, device=dev)
     gathered = [torch.zeros(6, dtype=torch.float64, device=dev) for _ in range(D.world)]
-    lo, hi = odist.shard(TOTAL12, D.rank, D.world)
     launches_per_step = 1 if fast == 1 else 2  # fast path: the kernel's last CTA does the final reduce
 
+    # rank r's shard: the interleaved 512-prefix calls r, r + N, ... of 12!
+    # (osim_exhaustive_shard_dev; at N = 1 the whole space, as osim_exhaustive_dev)
     def step(ev_kernel_done=None):
-        _capi.check(L.osim_exhaustive_dev(C.c_void_p(d_durs.data_ptr()), N12, DMA, SIGMA, lo, hi, fast,
-                                          C.c_void_p(d_out.data_ptr()), None, sp))
+        _capi.check(L.osim_exhaustive_shard_dev(C.c_void_p(d_durs.data_ptr()), N12, DMA, SIGMA, D.rank, D.world,
+                                                fast, C.c_void_p(d_out.data_ptr()), sp))
         if ev_kernel_done is not None:
             ev_kernel_done.record()
         if D.pg:
@@ -236,10 +239,11 @@ def run_ours(a):
     parts = [odist.unpack(g.cpu().numpy()) for g in gathered] if D.pg else [odist.unpack(d_out.cpu().numpy())]
     res = search.summary_from_dict(odist.combine(parts), N12)
     assert res.count == TOTAL12, res
+    mine = odist.unpack(d_out.cpu().numpy())["count"]  # orderings this rank simulated per step
 
     ops_per = ops[f"c4_sigma{SIGMA}"]["ops"]
     kern_avg = t_kern / a.steps
-    achieved = ops_per * (hi - lo) / kern_avg / 1e12
+    achieved = ops_per * mine / kern_avg / 1e12
     roof = {"bound": "fp64", "achieved": achieved, "peak": peak_ops, "unit": "TFLOP/s", "frac": achieved / peak_ops,
             "traffic": profile_traffic(),
             "definition": ("algorithmic FP64 ops per ordering (S+8R+2O = %.1f, tests/golden/op_counts.json, "
@@ -259,10 +263,10 @@ def run_ours(a):
     sm_mhz = clk.summary().get("sm_mhz")
     if wi and sm_mhz:
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        ach = wi * (hi - lo) / TOTAL12 / kern_avg
+        ach = wi * mine / TOTAL12 / kern_avg
         peak_i = 4.0 * sms * sm_mhz * 1e6
         roof["issue"] = {"achieved_warp_instr_per_s": ach, "peak_warp_instr_per_s": peak_i, "frac": ach / peak_i,
-                         "warp_instr_per_launch": wi * (hi - lo) / TOTAL12, "sms": sms, "sm_mhz": sm_mhz}
+                         "warp_instr_per_launch": wi * mine / TOTAL12, "sms": sms, "sm_mhz": sm_mhz}
 
     # ---- e2e through the public API (host buffers) ---------------------------
     e2e_steps = max(3, a.steps // 2)
@@ -303,7 +307,7 @@ def run_ours(a):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": t_max / a.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "orderings_per_step": TOTAL12, "n_tasks": N12,
-                       "parallelism": f"Lehmer-rank shards x{D.world}" + (" + NCCL all_gather of 48-B summaries"
+                       "parallelism": f"interleaved Lehmer-rank shards x{D.world}" + (" + NCCL all_gather of 48-B summaries"
                                                                           if D.pg else ""),
                        "l2": "256 MiB buffer zeroed before every timed step (excluded from timing); inputs 288 B",
                        "fast_path": bool(fast)},
@@ -348,14 +352,13 @@ def run_secondary(a, D, torch, dev, sp, flush, ops, peak_ops, L):
     d3 = torch.from_numpy(synth.c3_group()).to(dev)
     o3 = torch.zeros(6, dtype=torch.float64, device=dev)
     t10 = math.factorial(10)
-    lo, hi = odist.shard(t10, D.rank, D.world)
     g3 = [torch.zeros(6, dtype=torch.float64, device=dev) for _ in range(D.world)]
     reps = 20  # one step = 20 back-to-back searches (a single one is ~0.2 ms)
 
     def s3(ev=None):
         for _ in range(reps):
-            _capi.check(L.osim_exhaustive_dev(C.c_void_p(d3.data_ptr()), 10, 2, 0.5, lo, hi, 1,
-                                              C.c_void_p(o3.data_ptr()), None, sp))
+            _capi.check(L.osim_exhaustive_shard_dev(C.c_void_p(d3.data_ptr()), 10, 2, 0.5, D.rank, D.world, 1,
+                                                    C.c_void_p(o3.data_ptr()), sp))
         if ev is not None:
             ev.record()
         if D.pg:
@@ -365,7 +368,8 @@ def run_secondary(a, D, torch, dev, sp, flush, ops, peak_ops, L):
     t = D.max(t)
     out["c3_orderings_per_s"] = {"value": t10 * reps * K / t, "unit": "orderings/s",
                                  "workload": "C3: K20 seed 10, 10 tasks, 10! orderings x20 per step",
-                                 "frac_fp64": ops["c3"]["ops"] * (hi - lo) * reps * K / tk / 1e12 / peak_ops}
+                                 "frac_fp64": ops["c3"]["ops"] * odist.unpack(o3.cpu().numpy())["count"] * reps * K
+                                 / tk / 1e12 / peak_ops}
 
     # C4 variants: sigma 0.375 (true-divide path) and 1-DMA
     d4v = torch.from_numpy(synth.c4_group()).to(dev)

@@ -173,6 +173,22 @@ int osim_fast_eligible(const double* durs, uint64_t count /* tasks */, double si
 int osim_exhaustive_dev(const double* d_durs, int n, int dma, double sigma, uint64_t rank_lo,
                         uint64_t rank_hi, int fast, osim_summary* d_out, double* d_makespans,
                         void* stream);
+/* Shard `shard` of `shards` of the whole space [0, n!) for multi-GPU strong
+ * scaling (one call per rank; combine the summaries with the osim merge rules:
+ * lowest best, ties to the lower best_rank).  On the fast path (fast = 1) the
+ * shard is the interleaved set of 512-prefix calls shard, shard + shards, ...,
+ * so every shard samples the whole rank space and the per-rank work evens
+ * out; otherwise it is the contiguous range [shard*n!/shards,
+ * (shard+1)*n!/shards).  Every ordering falls in exactly one shard.
+ * Replaces, per rank, the enumeration loop of oracle.exhaustive_search
+ * (/root/reference/pkg/src/offsim/oracle.py:124-135). */
+int osim_exhaustive_shard_dev(const double* d_durs, int n, int dma, double sigma, int shard, int shards,
+                              int fast, osim_summary* d_out, void* stream);
+/* Host-buffer form of osim_exhaustive_shard_dev on the calling thread's
+ * device (osim_set_device); chooses the path like osim_exhaustive.  The call
+ * each rank of dist.exhaustive_summary_distributed makes. */
+int osim_exhaustive_shard(const double* durs, int n, int dma, double sigma, int shard, int shards,
+                          osim_summary* out);
 /* As osim_exhaustive_dev plus the below-threshold count (d_below: one uint64). */
 int osim_exhaustive_ex_dev(const double* d_durs, int n, int dma, double sigma, uint64_t rank_lo,
                            uint64_t rank_hi, int fast, double threshold, osim_summary* d_out,

@@ -28,6 +28,7 @@ EXPORTS = (
     "osim_heuristic_batch_dev", "osim_selftest_div", "osim_fp64_peak", "osim_exhaustive_stats",
     "osim_exhaustive_ex_dev", "osim_radix_hist_dev", "osim_interleavings", "osim_eval_sequences",
     "osim_timeline_deps", "osim_micro", "osim_micro_timeline", "osim_harness_batch",
+    "osim_exhaustive_shard_dev", "osim_exhaustive_shard",
 )
 
 
@@ -92,6 +93,8 @@ def load(path: str = LIB_PATH):
             "osim_timeline": ([dp, i, i, d, u8p, dp, dp, dp, dp], i),
             "osim_fast_eligible": ([dp, u64, d], i),
             "osim_exhaustive_dev": ([vp, i, i, d, u64, u64, i, vp, vp, vp], i),
+            "osim_exhaustive_shard_dev": ([vp, i, i, d, i, i, i, vp, vp], i),
+            "osim_exhaustive_shard": ([dp, i, i, d, i, i, sp], i),
             "osim_exhaustive_batch_dev": ([vp, u64, i, i, d, i, vp, vp], i),
             "osim_heuristic_batch_dev": ([vp, vp, u64, i, i, d, i, i, vp, vp, vp, vp], i),
             "osim_selftest_div": ([u64, u64, C.POINTER(u64)], i),
@@ -161,6 +164,16 @@ def exhaustive(durs, dma, sigma, lo, hi, n_dev=1, want_makespans=False):
     check(load().osim_exhaustive(ptr(d, C.c_double), n, int(dma), float(sigma), int(lo), int(hi), int(n_dev),
                                  C.byref(out), ptr(ms, C.c_double) if ms is not None else None))
     return out.as_dict(), ms
+
+
+def exhaustive_shard(durs, dma, sigma, shard, shards):
+    """Summary dict of shard `shard` of `shards` of all n! orderings
+    (osim_exhaustive_shard: interleaved prefix calls on the fast path)."""
+    d = f64(durs, (-1, 3))
+    out = OsimSummary()
+    check(load().osim_exhaustive_shard(ptr(d, C.c_double), d.shape[0], int(dma), float(sigma), int(shard),
+                                       int(shards), C.byref(out)))
+    return out.as_dict()
 
 
 def exhaustive_stats(durs, dma, sigma, lo, hi, threshold=float("-inf"), n_dev=1, median=True):

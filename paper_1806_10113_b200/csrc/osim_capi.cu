@@ -235,7 +235,8 @@ bool sigma_pow2(double sigma) {
 
 int launch_exh_fast_dispatch(int dma, int n, DevCtx* c, cudaStream_t st, const double* d_durs, double sigma,
                              uint64_t lo, uint64_t hi, double thr, Part* parts, int max_parts, double* d_ms,
-                             int* g, osim_summary* d_out, unsigned long long* d_below) {
+                             int* g, osim_summary* d_out, unsigned long long* d_below, unsigned shard = 0,
+                             unsigned shards = 1) {
     const LaunchCfg cfg{c->sms, st};
     const int L = pfx_l_for(n);
     unsigned* dn = c->d_done;
@@ -243,12 +244,12 @@ int launch_exh_fast_dispatch(int dma, int n, DevCtx* c, cudaStream_t st, const d
     if (dma == 2)
         rc = sigma_pow2(sigma)
                  ? exh_fast_launch_d2s1(n, L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, d_out,
-                                        d_below, dn)
+                                        d_below, dn, shard, shards)
                  : exh_fast_launch_d2s0(n, L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, d_out,
-                                        d_below, dn);
+                                        d_below, dn, shard, shards);
     else
         rc = exh_fast_launch_d1(n, L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, d_out, d_below,
-                                dn);
+                                dn, shard, shards);
     if (rc) return fail(OSIM_EINVAL, "unsupported n=%d", n);
     return 0;
 }
@@ -636,6 +637,66 @@ int osim_exhaustive_dev(const double* d_durs, int n, int dma, double sigma, uint
     if ((rc = scratch(c, align_up(mp * sizeof(Part)), &base))) return rc;
     return enqueue_exhaustive(c, st, d_durs, n, dma, sigma, rank_lo, rank_hi, fast, d_out,
                               d_makespans, (Part*)base, mp);
+}
+
+// one shard of [0, n!) (see offsim_b200.h): interleaved 512-prefix calls on
+// the fast path, the contiguous range otherwise
+int enqueue_shard(DevCtx* c, cudaStream_t st, const double* d_durs, int n, int dma, double sigma, int shard,
+                  int shards, int fast, osim_summary* d_out, Part* parts, int mp) {
+    const uint64_t total = factorial(n);
+    if (fast == 1) {
+        int g = 1;
+        int rc = launch_exh_fast_dispatch(dma, n, c, st, d_durs, sigma, 0, total, -HUGE_VAL, parts, mp, nullptr, &g,
+                                          d_out, nullptr, (unsigned)shard, (unsigned)shards);
+        if (rc) return rc;
+        CK(cudaGetLastError());
+        return 0;
+    }
+    const uint64_t lo = (uint64_t)((unsigned __int128)total * (unsigned)shard / (unsigned)shards);
+    const uint64_t hi = (uint64_t)((unsigned __int128)total * (unsigned)(shard + 1) / (unsigned)shards);
+    return enqueue_exhaustive(c, st, d_durs, n, dma, sigma, lo, hi, fast, d_out, nullptr, parts, mp);
+}
+
+int osim_exhaustive_shard_dev(const double* d_durs, int n, int dma, double sigma, int shard, int shards, int fast,
+                              osim_summary* d_out, void* stream) {
+    int rc = check_common(n, dma, sigma);
+    if (rc) return rc;
+    if (shards < 1 || shard < 0 || shard >= shards) return fail(OSIM_EINVAL, "shard %d of %d", shard, shards);
+    DevList dl;
+    if ((rc = pick_devs(1, dl))) return rc;
+    DevCtx* c = dl.v[0];
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+    const int mp = max_parts_for(c);
+    void* base;
+    if ((rc = scratch(c, align_up(mp * sizeof(Part)), &base))) return rc;
+    return enqueue_shard(c, st, d_durs, n, dma, sigma, shard, shards, fast, d_out, (Part*)base, mp);
+}
+
+int osim_exhaustive_shard(const double* durs, int n, int dma, double sigma, int shard, int shards,
+                          osim_summary* out) {
+    int rc = check_common(n, dma, sigma);
+    if (rc) return rc;
+    if ((rc = check_durs(durs, (uint64_t)n))) return rc;
+    if (!out) return fail(OSIM_EINVAL, "out is NULL");
+    if (shards < 1 || shard < 0 || shard >= shards) return fail(OSIM_EINVAL, "shard %d of %d", shard, shards);
+    DevList dl;
+    if ((rc = pick_devs(1, dl))) return rc;
+    DevCtx* c = dl.v[0];
+    std::lock_guard<std::mutex> lk(c->mu);
+    const int fast = fast_ok(durs, n, sigma) ? 1 : (null_fast_ok(durs, n, sigma) ? 2 : 0);
+    const int mp = max_parts_for(c);
+    const size_t off_parts = align_up(3 * kMaxN * sizeof(double));
+    const size_t off_sum = off_parts + align_up(mp * sizeof(Part));
+    void* base;
+    if ((rc = scratch(c, off_sum + align_up(sizeof(osim_summary)), &base))) return rc;
+    char* b = (char*)base;
+    CK(cudaMemcpyAsync(b, durs, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    if ((rc = enqueue_shard(c, c->stream, (double*)b, n, dma, sigma, shard, shards, fast, (osim_summary*)(b + off_sum),
+                            (Part*)(b + off_parts), mp)))
+        return rc;
+    CK(cudaMemcpyAsync(out, b + off_sum, sizeof(osim_summary), cudaMemcpyDeviceToHost, c->stream));
+    return finish(c, c->stream);
 }
 
 int osim_exhaustive_stats(const double* durs, int n, int dma, double sigma, uint64_t rank_lo, uint64_t rank_hi,

@@ -10,16 +10,19 @@ namespace {
 template <int N, int L>
 int exh_t(const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo, uint64_t hi, double thr,
           Part* parts, int max_parts, double* d_ms, int* grid_out, osim_summary* d_out, unsigned long long* d_below,
-          unsigned* d_done) {
+          unsigned* d_done, unsigned shard, unsigned shards) {
     // makespans out or a positive threshold need the stats variant
     auto k = (d_ms || thr > 0.0) ? k_exhaustive_pfx<N, OSIM_DMA, OSIM_SP2, L, true>
                                  : k_exhaustive_pfx<N, OSIM_DMA, OSIM_SP2, L, false>;
     constexpr uint64_t LF = Fact<L>::v;
     const uint64_t prefixes = (hi + LF - 1) / LF - lo / LF;
+    constexpr uint64_t kPer = (uint64_t)kPfxQ * kBlock;
+    const uint64_t calls = (prefixes + kPer - 1) / kPer;  // this shard's: calls shard, shard + shards, ...
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPfxDynSmem);
-    int g = grid_for_sms(k, kBlock, kPfxDynSmem, cfg.sms, (prefixes + kPfxQ * kBlock - 1) / (kPfxQ * kBlock));
+    int g = grid_for_sms(k, kBlock, kPfxDynSmem, cfg.sms, calls > shard ? (calls - shard + shards - 1) / shards : 1);
     if (g > max_parts) g = max_parts;
-    k<<<g, kBlock, kPfxDynSmem, cfg.st>>>(d_durs, sigma, lo, hi, thr, parts, d_ms, d_out, d_below, d_done);
+    k<<<g, kBlock, kPfxDynSmem, cfg.st>>>(d_durs, sigma, lo, hi, thr, parts, d_ms, d_out, d_below, d_done, shard,
+                                          shards);
     *grid_out = g;
     return 0;
 }
@@ -27,23 +30,24 @@ int exh_t(const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo,
 template <int N>
 int exh_n(int L, const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo, uint64_t hi,
           double thr, Part* parts, int max_parts, double* d_ms, int* g, osim_summary* o, unsigned long long* b,
-          unsigned* dn) {
+          unsigned* dn, unsigned sh, unsigned shs) {
     if constexpr (tunable_n(N)) {
-        if (L == 3) return exh_t<N, 3>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, o, b, dn);
-        if (L == 5) return exh_t<N, 5>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, o, b, dn);
-        if (L == 4) return exh_t<N, 4>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, o, b, dn);
+        if (L == 3) return exh_t<N, 3>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, o, b, dn, sh, shs);
+        if (L == 5) return exh_t<N, 5>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, o, b, dn, sh, shs);
+        if (L == 4) return exh_t<N, 4>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, o, b, dn, sh, shs);
     }
-    return exh_t<N, default_pfx_l(N)>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, o, b, dn);
+    return exh_t<N, default_pfx_l(N)>(cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, o, b, dn, sh, shs);
 }
 
 }  // namespace
 
 int OSIM_EXH_NAME(int n, int L, const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo,
                   uint64_t hi, double thr, Part* parts, int max_parts, double* d_ms, int* g, osim_summary* d_out,
-                  unsigned long long* d_below, unsigned* d_done) {
+                  unsigned long long* d_below, unsigned* d_done, unsigned shard, unsigned shards) {
     switch (n) {
 #define OSIM_CASE(NN) \
-    case NN: return exh_n<NN>(L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, d_out, d_below, d_done);
+    case NN: return exh_n<NN>(L, cfg, d_durs, sigma, lo, hi, thr, parts, max_parts, d_ms, g, d_out, d_below, d_done, \
+                         shard, shards);
         OSIM_CASE(1) OSIM_CASE(2) OSIM_CASE(3) OSIM_CASE(4) OSIM_CASE(5) OSIM_CASE(6)
         OSIM_CASE(7) OSIM_CASE(8) OSIM_CASE(9) OSIM_CASE(10) OSIM_CASE(11) OSIM_CASE(12)
         OSIM_CASE(13) OSIM_CASE(14) OSIM_CASE(15) OSIM_CASE(16)

@@ -573,7 +573,8 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
                                                            uint64_t lo, uint64_t hi, double thr, Part* __restrict__ parts,
                                                            double* __restrict__ ms_out, osim_summary* __restrict__ out,
                                                            unsigned long long* __restrict__ below,
-                                                           unsigned* __restrict__ done) {
+                                                           unsigned* __restrict__ done, unsigned shard,
+                                                           unsigned shards) {
     __shared__ double2 sdr[3 * kStride];
     __shared__ Part sh[32];
     extern __shared__ __align__(16) unsigned char pfx_dsm[];
@@ -591,9 +592,12 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
     // grid-stride over calls of 512 prefixes.  (An even split of the ragged
     // last round over all CTAs measured slower: a CTA left alone on an SM by
     // the partial wave runs ~3x faster than one sharing it, so the grid-stride
-    // tail costs only a fraction of a call.)
-    const uint64_t stride = (uint64_t)gridDim.x * kPer;
-    for (uint64_t pb = p_lo + (uint64_t)blockIdx.x * kPer; pb < p_hi; pb += stride)
+    // tail costs only a fraction of a call.)  Interleaved shards (shards > 1,
+    // osim_exhaustive_shard_dev): this launch takes calls shard, shard +
+    // shards, ... of the range, so every shard samples the whole rank space
+    // and the per-shard work evens out.
+    const uint64_t stride = (uint64_t)gridDim.x * kPer * shards;
+    for (uint64_t pb = p_lo + ((uint64_t)blockIdx.x * shards + shard) * kPer; pb < p_hi; pb += stride)
         pfx_leaves<N, DMA, SIGP2, L, STATS>(base, sigma, rsig, pb, p_hi, lo, hi, thr, acc, ms_out, lo, K, S);
     acc = block_reduce(acc, sh);
     if (threadIdx.x == 0) parts[blockIdx.x] = acc;

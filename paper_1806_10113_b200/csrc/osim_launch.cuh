@@ -53,7 +53,8 @@ inline int pfx_l_for(int n) {
 #define OSIM_EXH_DECL(NAME)                                                                          \
     int NAME(int n, int L, const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo,   \
              uint64_t hi, double thr, Part* parts, int max_parts, double* d_ms, int* grid_out,        \
-             osim_summary* d_out, unsigned long long* d_below, unsigned* d_done);
+             osim_summary* d_out, unsigned long long* d_below, unsigned* d_done, unsigned shard,    \
+             unsigned shards);
 OSIM_EXH_DECL(exh_fast_launch_d2s1)
 OSIM_EXH_DECL(exh_fast_launch_d2s0)
 OSIM_EXH_DECL(exh_fast_launch_d1)

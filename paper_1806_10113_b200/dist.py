@@ -1,12 +1,14 @@
 """Multi-GPU sharding over torch.distributed (one process per GPU).
 
-Exhaustive search of one group (configs 3/4): rank r of W takes the
-contiguous Lehmer-rank range [r*n!/W, (r+1)*n!/W) and reduces it on its
-own GPU; the only exchange is one all_gather of the 48-byte summaries
-(NCCL over NVLink on the GPU box, gloo in the CPU tests), combined on
-every rank in rank order.  Because the ranges are ordered, "first rank
-attaining the minimum" is the global lowest-rank argmin, so best / argmin /
-worst / count are bit-exact and mean / geomean are fixed-order sums.
+Exhaustive search of one group (configs 3/4): rank r of W takes shard r
+of the Lehmer-rank space -- on the GPU fast path the interleaved calls of
+512 prefixes r, r + W, ... (osim_exhaustive_shard), otherwise (and with a
+`local_fn`) the contiguous range [r*n!/W, (r+1)*n!/W) -- and reduces it on
+its own GPU; the only exchange is one all_gather of the 48-byte summaries
+(NCCL over NVLink on the GPU box, gloo in the CPU tests), combined on every
+rank in rank order.  The merge keeps the lowest best and, on ties, the lower
+best_rank, so best / argmin / worst / count are bit-exact for any partition
+and mean / geomean are fixed-order sums.
 
 Batched groups and the heuristic (configs 2/5) shard the group index range
 with no collective in the compute (reorder_durs_distributed,
@@ -66,12 +68,6 @@ def combine(parts: List[dict]) -> dict:
     return acc
 
 
-def _gpu_local(durs, dma, sigma, lo, hi) -> dict:
-    from . import _capi
-    s, _ = _capi.exhaustive(durs, dma, sigma, lo, hi)
-    return s
-
-
 def exhaustive_summary_distributed(durs, dma: int, sigma: float, group=None,
                                    local_fn: Optional[Callable] = None,
                                    device=None) -> OrderingSummary:
@@ -84,8 +80,17 @@ def exhaustive_summary_distributed(durs, dma: int, sigma: float, group=None,
     total = math.factorial(n)
     world = tdist.get_world_size(group)
     rank = tdist.get_rank(group)
-    lo, hi = shard(total, rank, world)
-    local = (local_fn or _gpu_local)(d, dma, sigma, lo, hi)
+    if local_fn is None:
+        # the library's shard: interleaved 512-prefix calls on the fast path
+        # (every rank samples the whole rank space, so per-rank work evens
+        # out), the contiguous range otherwise; combine() is order-free for
+        # best / argmin (ties to the lower rank) / worst / count
+        from . import _capi
+
+        local = _capi.exhaustive_shard(d, dma, sigma, rank, world)
+    else:
+        lo, hi = shard(total, rank, world)
+        local = local_fn(d, dma, sigma, lo, hi)
     backend = tdist.get_backend(group)
     dev = device if device is not None else (torch.device("cuda", torch.cuda.current_device())
                                              if backend == "nccl" else torch.device("cpu"))

@@ -1007,3 +1007,58 @@ def test_wide_harness_bit_exact_and_dropin():
     assert [res.timeline.idle[k] for k in osim.KINDS] == fl(c["idle"])
     assert res.noreorder is not None and len(res.noreorder.makespans) == 500
     assert res.speedup_best >= res.speedup_median
+
+
+def _oracle_union(d, dma, sigma, ranges):
+    from paper_1806_10113_b200 import dist as odist
+
+    return odist.combine([O.exhaustive(d, dma, sigma, lo, hi, threads=8)[0] for lo, hi in ranges])
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_interleaved_shard_partition_vs_oracle(world):
+    # fast path: shard s of W = the 512-prefix calls s, s + W, ... of the
+    # whole space; n = 8 uses suffixes of L = 3 tasks, so one call covers
+    # 512 * 3! = 3072 consecutive ranks (osim_exhaustive_shard, offsim_b200.h)
+    d = synth.c2_batch(1)[0]
+    total, chunk = math.factorial(8), 512 * 6
+    calls = -(-total // chunk)
+    for s in range(world):
+        got = _capi.exhaustive_shard(d, 2, 0.5, s, world)
+        want = _oracle_union(d, 2, 0.5, [(k * chunk, min(total, (k + 1) * chunk)) for k in range(s, calls, world)])
+        assert_summary_vs_oracle(got, want)
+
+
+@pytest.mark.parametrize("case", ["c3", "c4_w8", "c4_sigma0.375", "c4_1dma", "null_stage", "general"])
+def test_shards_combine_to_the_whole_space(case):
+    from paper_1806_10113_b200 import dist as odist
+
+    dma, sigma, world = 2, 0.5, 3
+    if case == "c3":
+        d = synth.c3_group()
+    elif case == "c4_w8":
+        d, world = synth.c4_group(), 8
+    elif case == "c4_sigma0.375":
+        d, sigma, world = synth.c4_group(), 0.375, 4
+    elif case == "c4_1dma":
+        d, dma, sigma, world = synth.c4_group(), 1, 1.0, 2
+    elif case == "null_stage":  # NullSim path: contiguous shards
+        d = synth.c3_group().copy()
+        d[3, 0] = 0.0
+    else:  # general path (a duration outside the fast range): contiguous shards
+        d = synth.c3_group()[:9].copy()
+        d[2, 1] = 2.0 ** 23
+    whole, _ = _capi.exhaustive(d, dma, sigma, 0, math.factorial(d.shape[0]))
+    parts = [_capi.exhaustive_shard(d, dma, sigma, s, world) for s in range(world)]
+    assert sum(p["count"] for p in parts) == whole["count"]
+    got = odist.combine(parts)
+    assert got["best"] == whole["best"] and got["best_rank"] == whole["best_rank"]
+    assert got["worst"] == whole["worst"] and got["count"] == whole["count"]
+    assert close(got["sum"], whole["sum"], REL) and close(got["sum_log"], whole["sum_log"], REL)
+
+
+def test_shard_arguments_are_checked():
+    d = synth.c3_group()
+    for s, w in ((0, 0), (-1, 2), (2, 2)):
+        with pytest.raises(ValueError, match="shard"):  # OSIM_EINVAL, the reference's error type
+            _capi.exhaustive_shard(d, 2, 0.5, s, w)
