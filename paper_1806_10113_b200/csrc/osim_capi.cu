@@ -542,6 +542,7 @@ int osim_shutdown(void) {
         cudaSetDevice(c->dev);
         if (c->scratch) cudaFree(c->scratch);
         if (c->d_err) cudaFree(c->d_err);
+        if (c->d_done) cudaFree(c->d_done);
         if (c->stream) cudaStreamDestroy(c->stream);
         if (c->stream2) cudaStreamDestroy(c->stream2);
         if (c->ev) cudaEventDestroy(c->ev);
