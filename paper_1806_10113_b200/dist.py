@@ -32,6 +32,26 @@ def shard(total: int, rank: int, world: int) -> Tuple[int, int]:
     return total * rank // world, total * (rank + 1) // world
 
 
+def default_suffix_len(n: int) -> int:
+    """Suffix length L of the prefix-sharing kernel (csrc/osim_launch.cuh
+    default_pfx_l): one kernel call covers 512 prefixes x L! leaves."""
+    return 1 if n <= 3 else (2 if n <= 5 else (3 if n <= 10 else 4))
+
+
+def shard_ranges(n: int, rank: int, world: int, fast: bool = True) -> List[Tuple[int, int]]:
+    """The Lehmer-rank ranges osim_exhaustive_shard gives rank `rank` of
+    `world`: on the fast path the interleaved 512-prefix calls rank,
+    rank + world, ... (each 512 * L! consecutive ranks), otherwise the
+    contiguous `shard` range.  Every ordering lies in exactly one rank's
+    ranges."""
+    total = math.factorial(n)
+    if not fast:
+        return [shard(total, rank, world)]
+    chunk = 512 * math.factorial(default_suffix_len(n))
+    calls = -(-total // chunk)
+    return [(k * chunk, min(total, (k + 1) * chunk)) for k in range(rank, calls, world)]
+
+
 def pack(s: dict) -> np.ndarray:
     """Summary dict -> 6 float64 words (integers bit-cast, no rounding)."""
     out = np.empty(6, dtype=np.float64)
@@ -70,14 +90,17 @@ def combine(parts: List[dict]) -> dict:
 
 def exhaustive_summary_distributed(durs, dma: int, sigma: float, group=None,
                                    local_fn: Optional[Callable] = None,
-                                   device=None) -> OrderingSummary:
-    """Whole-space summary of one group sharded over the process group."""
+                                   device=None, interleaved: bool = False) -> OrderingSummary:
+    """Whole-space summary of one group sharded over the process group.
+    Without `local_fn` each rank runs its library shard on its GPU; with
+    `local_fn(durs, dma, sigma, lo, hi) -> summary dict` (e.g. the oracle in
+    the CPU tests) each rank evaluates its contiguous `shard` range, or with
+    `interleaved=True` the library's interleaved ranges (`shard_ranges`)."""
     import torch
     import torch.distributed as tdist
 
     d = np.asarray(durs, dtype=np.float64).reshape(-1, 3)
     n = d.shape[0]
-    total = math.factorial(n)
     world = tdist.get_world_size(group)
     rank = tdist.get_rank(group)
     if local_fn is None:
@@ -89,8 +112,8 @@ def exhaustive_summary_distributed(durs, dma: int, sigma: float, group=None,
 
         local = _capi.exhaustive_shard(d, dma, sigma, rank, world)
     else:
-        lo, hi = shard(total, rank, world)
-        local = local_fn(d, dma, sigma, lo, hi)
+        ranges = shard_ranges(n, rank, world, fast=interleaved)
+        local = combine([local_fn(d, dma, sigma, lo, hi) for lo, hi in ranges])
     backend = tdist.get_backend(group)
     dev = device if device is not None else (torch.device("cuda", torch.cuda.current_device())
                                              if backend == "nccl" else torch.device("cpu"))

@@ -28,21 +28,23 @@ def _oracle_local(d, dma, sigma, lo, hi):
     return s
 
 
-def _worker(rank, world, port, d, dma, sigma, q):
+def _worker(rank, world, port, d, dma, sigma, q, interleaved=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     tdist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1806_10113_b200.dist import exhaustive_summary_distributed
 
-        s = exhaustive_summary_distributed(d, dma, sigma, local_fn=_oracle_local)
+        s = exhaustive_summary_distributed(d, dma, sigma, local_fn=_oracle_local, interleaved=interleaved)
         q.put((rank, s.best, s.best_rank, s.worst, s.count, s.sum, s.sum_log))
     finally:
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_gloo_sharded_exhaustive_matches_whole_space(world):
+@pytest.mark.parametrize("world,interleaved", [(2, False), (3, False), (2, True), (3, True)])
+def test_gloo_sharded_exhaustive_matches_whole_space(world, interleaved):
+    # interleaved: the library's partition (512-prefix calls of 3072 ranks at
+    # n = 7: two calls, so at world 3 one rank has an empty shard)
     c = load("c1_bk.json")["cases"][3]  # BK25 2-DMA: a unique best at rank 19
     d = np.concatenate([durs(c["durs"]), durs(c["durs"])[:3] * 1.25])  # 7 tasks, 5040 orderings
     dma, sigma = c["dma"], F(c["sigma"])
@@ -50,7 +52,7 @@ def test_gloo_sharded_exhaustive_matches_whole_space(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, d, dma, sigma, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, d, dma, sigma, q, interleaved)) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=120) for _ in range(world)]
@@ -160,3 +162,19 @@ def test_gloo_batch_shards_gather_whole_batch():
     for _, order, ms, sims, summ in res:
         assert np.array_equal(order, want[0]) and np.array_equal(ms, want[1]) and np.array_equal(sims, want[2])
         assert summ.tobytes() == want_s.tobytes()
+
+
+@pytest.mark.parametrize("fast", [True, False])
+def test_shard_ranges_partition_every_space(fast):
+    # every ordering of n! in exactly one rank's ranges, for any world size
+    import math
+
+    from paper_1806_10113_b200.dist import shard_ranges
+
+    for n in range(1, 13 if fast else 17):
+        total = math.factorial(n)
+        for world in (1, 2, 3, 5, 8, 13):
+            rs = sorted(r for w in range(world) for r in shard_ranges(n, w, world, fast=fast))
+            rs = [r for r in rs if r[1] > r[0]]
+            assert rs[0][0] == 0 and rs[-1][1] == total
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))

@@ -1015,17 +1015,17 @@ def _oracle_union(d, dma, sigma, ranges):
     return odist.combine([O.exhaustive(d, dma, sigma, lo, hi, threads=8)[0] for lo, hi in ranges])
 
 
-@pytest.mark.parametrize("world", [2, 3, 5])
-def test_interleaved_shard_partition_vs_oracle(world):
+@pytest.mark.parametrize("n,world", [(8, 2), (8, 3), (8, 5), (7, 2), (9, 4)])
+def test_interleaved_shard_partition_vs_oracle(n, world):
     # fast path: shard s of W = the 512-prefix calls s, s + W, ... of the
-    # whole space; n = 8 uses suffixes of L = 3 tasks, so one call covers
-    # 512 * 3! = 3072 consecutive ranks (osim_exhaustive_shard, offsim_b200.h)
-    d = synth.c2_batch(1)[0]
-    total, chunk = math.factorial(8), 512 * 6
-    calls = -(-total // chunk)
+    # whole space, each 512 * L! consecutive ranks (n = 8: L = 3, 3072 ranks;
+    # osim_exhaustive_shard, offsim_b200.h); dist.shard_ranges states it
+    from paper_1806_10113_b200 import dist as odist
+
+    d = synth.c2_batch(1)[0] if n == 8 else synth.c3_group()[:n].copy()
     for s in range(world):
         got = _capi.exhaustive_shard(d, 2, 0.5, s, world)
-        want = _oracle_union(d, 2, 0.5, [(k * chunk, min(total, (k + 1) * chunk)) for k in range(s, calls, world)])
+        want = _oracle_union(d, 2, 0.5, odist.shard_ranges(n, s, world))
         assert_summary_vs_oracle(got, want)
 
 
