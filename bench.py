@@ -130,7 +130,10 @@ class Dist:
         import torch
 
         torch.cuda.set_device(self.local)
-        if self.world > 1:
+        # OSIM_BENCH_FORCE_PG=1: the N>1 code path (NCCL process group, the
+        # per-step all_gather, max-over-ranks) at world size 1, to exercise it
+        # on a single-GPU box under torchrun --nproc-per-node 1
+        if self.world > 1 or os.environ.get("OSIM_BENCH_FORCE_PG") == "1":
             import torch.distributed as tdist
 
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
