@@ -191,6 +191,12 @@ def run_ours(a):
 
     import torch
 
+    # stdout carries exactly the one JSON line: native code that prints on
+    # fd 1 (NCCL's version banner at process-group init) goes to stderr
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+
     from paper_1806_10113_b200 import _capi, dist as odist, search, synth
 
     D = Dist(a.gpus)
@@ -321,7 +327,9 @@ def run_ours(a):
         }
         if cpu:
             line["cpu_baseline"] = cpu
-        print(json.dumps(line), flush=True)
+        buf = (json.dumps(line) + "\n").encode()
+        while buf:
+            buf = buf[os.write(json_fd, buf):]
     if D.pg:
         D.pg.barrier()
         D.pg.destroy_process_group()
