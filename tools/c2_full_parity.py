@@ -9,7 +9,6 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-import numpy as np  # noqa: E402
 
 from oracle import oracle as O  # noqa: E402
 from paper_1806_10113_b200 import _capi, synth  # noqa: E402
