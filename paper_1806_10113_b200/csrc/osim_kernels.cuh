@@ -1016,6 +1016,11 @@ __global__ void __launch_bounds__(kHT) k_heuristic(const double* __restrict__ du
 #ifndef OSIM_HWG
 #define OSIM_HWG 8
 #endif
+// candidate keys: per-lane registers (lane owns group lane % kWG; 7 CTAs/SM)
+// unless -DOSIM_HKSHARED (keys in shared memory, group-major items; 6 CTAs/SM)
+#if !defined(OSIM_HKSHARED) && !defined(OSIM_HKREG)
+#define OSIM_HKREG 1
+#endif
 constexpr int kWG = OSIM_HWG;          // groups per warp
 constexpr int kLPG = 32 / kWG;         // lanes per group in the key argmin
 constexpr int kKeyN = kMaxN - 1;       // candidates per greedy round (n - k, k >= 1)
@@ -1029,8 +1034,12 @@ struct HeurWarpShared {
     using FS = FastSim<DMA, SP2, true, false>;
     double2 dr[kWG * kHS];
     typename FS::Ck ck[kWG];
+#ifndef OSIM_HKREG
     double ka[kWG * kKeyN];  // per-candidate keys (m <= 15 per round)
     double kb[kWG * kKeyN];
+#else
+    double ka[kWG * 2];  // the final pair's makespans only
+#endif
     uint64_t ot[kWG];
     uint64_t cand[kWG];  // rt: remaining task ids in input order, 4 bits each
     uint8_t idr[kWG * kMaxN];
@@ -1083,6 +1092,11 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
     }
     __syncwarp();
     auto DV = [&](int g, int k, int t) { return S.dr[g * kHS + k * kStride + t].x; };
+#ifndef OSIM_HKREG
+    constexpr int KA = kKeyN;
+#else
+    constexpr int KA = 2;
+#endif
 
     // select_first_task (heuristic.py:22-31) and the first checkpoint
     if (lane < Gv) {
@@ -1128,6 +1142,7 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
         const int items = Gv * m;
         // i / m for i < 2^7 by a 16-bit reciprocal: (i * (2^16/m + 1)) >> 16
         // is exact (the excess i/2^16 < 2^-9 stays below 1/m)
+#ifndef OSIM_HKREG
         const unsigned minv = 65536u / (unsigned)m + 1u;
         for (int i0 = 0; i0 < items; i0 += 32) {
             const int i = i0 + lane;
@@ -1135,6 +1150,19 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
             const int gq = (int)(((unsigned)i * minv) >> 16);
             const int g = valid ? gq : 0;
             const int j = valid ? i - gq * m : 0;
+#else
+        // lane owns group lane % kWG and candidates j = lane / kWG + kLPG * it;
+        // its best key is kept in registers across the iterations
+        (void)items;
+        int lj = -1;
+        double le = 0, ld = 0;
+        int lr = 0;
+        for (int j0 = 0; j0 < m; j0 += kLPG) {
+            const int jq = j0 + lane / kWG;
+            const bool valid = (lane % kWG) < Gv && jq < m;
+            const int g = valid ? lane % kWG : 0;
+            const int j = valid ? jq : 0;
+#endif
             const uint64_t cl0 = S.cand[g];
             const int c = rt_at(cl0, j);
             FS s;
@@ -1171,16 +1199,35 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
             if (sum_mode && cmp != 0.0 && isfinite(cmp)) f = __dadd_rn(f, cmp);
             const double bound = __dadd_rn(__dadd_rn(s.kEnd, f), tail);
             const double est = (bound > s.now) ? bound : s.now;
+#ifndef OSIM_HKREG
             if (valid) {
                 S.ka[g * kKeyN + j] = est;
                 S.kb[g * kKeyN + j] = s.idleK;
             }
+#else
+            if (valid) {
+                const int r = S.idr[g * kMaxN + c];
+                if (lj < 0 || key_less(est, s.idleK, r, le, ld, lr)) { lj = j; le = est; ld = s.idleK; lr = r; }
+            }
+#endif
         }
         __syncwarp();
         // argmin of the key over the m candidates: kLPG lanes per group, each
         // scanning every kLPG-th candidate, then a shuffle reduction
         // (the key is a strict total order, so the tree order is immaterial)
         int bj;
+#ifdef OSIM_HKREG
+        {
+#pragma unroll
+            for (int off = kWG; off < 32; off <<= 1) {
+                const int oj = __shfl_xor_sync(kFull, lj, off);
+                const double oe = __shfl_xor_sync(kFull, le, off), od = __shfl_xor_sync(kFull, ld, off);
+                const int orr = __shfl_xor_sync(kFull, lr, off);
+                if (oj >= 0 && (lj < 0 || key_less(oe, od, orr, le, ld, lr))) { lj = oj; le = oe; ld = od; lr = orr; }
+            }
+            bj = lj;  // lane < kWG holds group `lane`'s argmin
+        }
+#else
         {
             const int g = lane / kLPG, part = lane % kLPG;
             int lj = -1;
@@ -1202,6 +1249,7 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
             }
             bj = __shfl_sync(kFull, lj, (lane % kWG) * kLPG);  // group `lane` (< kWG) result
         }
+#endif
         if (lane < Gv) {
             const int g = lane;
             const int c = rt_at(S.cand[g], bj);
@@ -1244,7 +1292,7 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
             s.load(S.ck[g]);
             const int rest = __reduce_max_sync(kFull, 3 * n - s.finalized());
             s.run_phased(rest, sigma, rsig);
-            if (valid) S.ka[g * kKeyN + w] = s.now;
+            if (valid) S.ka[g * KA + w] = s.now;
         }
         __syncwarp();
     }
@@ -1253,7 +1301,7 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
         double ms;
         if (n >= 2) {
             const int a = S.pa[g], b = S.pb[g];
-            const double m_ab = S.ka[g * kKeyN + 0], m_ba = S.ka[g * kKeyN + 1];
+            const double m_ab = S.ka[g * KA + 0], m_ba = S.ka[g * KA + 1];
             bool ab;
             if (m_ab < m_ba) ab = true;
             else if (m_ba < m_ab) ab = false;
