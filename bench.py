@@ -367,18 +367,25 @@ def run_secondary(a, D, torch, dev, sp, flush, ops, peak_ops, L):
     reps = 20  # one step = 20 back-to-back searches (a single one is ~0.2 ms)
 
     def s3(ev=None):
+        # every search is complete: its shard, then its own all_gather of the
+        # 48-B summaries (N > 1), as dist.exhaustive_summary_distributed does
         for _ in range(reps):
             _capi.check(L.osim_exhaustive_shard_dev(C.c_void_p(d3.data_ptr()), 10, 2, 0.5, D.rank, D.world, 1,
                                                     C.c_void_p(o3.data_ptr()), sp))
+            if D.pg:
+                D.pg.all_gather(g3, o3)
         if ev is not None:
             ev.record()
-        if D.pg:
-            D.pg.all_gather(g3, o3)
 
     t, tk = timed_steps(s3, K, W, flush, sync)
     t = D.max(t)
+    parts3 = [odist.unpack(g.cpu().numpy()) for g in g3] if D.pg else [odist.unpack(o3.cpu().numpy())]
+    c3 = odist.combine(parts3)
+    assert c3["count"] == t10 and c3["best_rank"] == 381558, c3  # SURVEY appendix C3 golden
     out["c3_orderings_per_s"] = {"value": t10 * reps * K / t, "unit": "orderings/s",
-                                 "workload": "C3: K20 seed 10, 10 tasks, 10! orderings x20 per step",
+                                 "workload": "C3: K20 seed 10, 10 tasks, 10! orderings x20 per step, one "
+                                             "all_gather per search at N > 1",
+                                 "latency_us_per_search": t / (reps * K) * 1e6,
                                  "frac_fp64": ops["c3"]["ops"] * odist.unpack(o3.cpu().numpy())["count"] * reps * K
                                  / tk / 1e12 / peak_ops}
 
@@ -429,6 +436,8 @@ def run_secondary(a, D, torch, dev, sp, flush, ops, peak_ops, L):
 
     t, tk = timed_steps(s2, K, W, flush, sync)
     t = D.max(t)
+    # the credited device-resident output equals the host API's on the same groups
+    assert o2.cpu().numpy().tobytes() == _capi.exhaustive_batch(synth.c2_batch(B2)[lo2:hi2], 2, 0.5).tobytes()
     out["c2_orderings_per_s"] = {"value": B2 * 40320 * K / t, "unit": "orderings/s",
                                  "workload": "C2: 100000 x 8-task TGs (Table-2 x U(0.5,1.5)), 8! each, 2-DMA 0.5",
                                  "frac_fp64": ops["c2"]["ops"] * (hi2 - lo2) * 40320 * K / tk / 1e12 / peak_ops}
@@ -456,6 +465,11 @@ def run_secondary(a, D, torch, dev, sp, flush, ops, peak_ops, L):
 
         t, tk = timed_steps(s5, K, W, flush, sync)
         t = D.max(t)
+        # the credited device-resident output equals the host API's on the same groups
+        ho, hm, hn = _capi.heuristic_batch(dh[lo5:hi5], rh[lo5:hi5], dma, sigma,
+                                           1 if sys.version_info >= (3, 12) else 0)
+        assert np.array_equal(oo.cpu().numpy(), ho) and mm.cpu().numpy().tobytes() == hm.tobytes()
+        assert np.array_equal(ns.cpu().numpy().view(np.uint32), hn)
         out[f"c5_{prof}_decisions_per_s"] = {
             "value": B5 * K / t, "unit": "TG decisions/s",
             "workload": f"C5: 10^6 x 16-task TGs, {prof}-style ({dma}-DMA, sigma {sigma}), reorder_batch",

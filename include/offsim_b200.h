@@ -147,8 +147,8 @@ int osim_timeline_deps(const double* durs, int n, int dma, double sigma, const u
 /* workload._run_heuristic_schedule (workload.py:197-256) for S independent
  * scenarios of T workers x N tasks: durs[S][T*N][3] (task (w, j) at w*N+j),
  * id_rank[S][T*N] = sorted() order of each scenario's task ids.  Outputs
- * makespan[S], n_groups[S], tg_sizes[S][T*N] (nullable; first n_groups
- * entries), start/end[S][T*N][3] (nullable; -1 = null stage). */
+ * makespan[S], n_groups[S], tg_sizes[S][T*N] (nullable; first n_groups entries, the rest 0;
+ * start/end[S][T*N][3] (nullable; -1 = null stage). */
 int osim_harness_batch(const double* durs, const uint8_t* id_rank, uint64_t S, int T, int N, int dma,
                        double sigma, int sum_mode, int n_dev, double* makespan, uint8_t* n_groups,
                        uint8_t* tg_sizes, double* start, double* end);
@@ -169,6 +169,12 @@ int osim_micro_timeline(const double* durs, int n, int dma, double sigma, double
  * (0) stages allowed (the null-stage fast simulator); 0 selects the general
  * path.  The host entry points choose the mode themselves. */
 int osim_fast_eligible(const double* durs, uint64_t count /* tasks */, double sigma);
+/* Suffix length L of the prefix-sharing kernels for n tasks (1..16): one
+ * kernel call covers 512 prefixes x L! consecutive Lehmer ranks, and
+ * osim_exhaustive_shard on the fast path gives shard r of W the calls
+ * r, r + W, ...  (dist.shard_ranges mirrors it; OSIM_PFX_L may override it
+ * for n in {8, 10, 12}, read once per process.) */
+int osim_pfx_suffix_len(int n);
 
 int osim_exhaustive_dev(const double* d_durs, int n, int dma, double sigma, uint64_t rank_lo,
                         uint64_t rank_hi, int fast, osim_summary* d_out, double* d_makespans,
@@ -195,11 +201,16 @@ int osim_exhaustive_ex_dev(const double* d_durs, int n, int dma, double sigma, u
                            uint64_t* d_below, double* d_makespans, void* stream);
 /* One radix-selection pass over positive doubles in HBM: d_hist[2^digit_bits]
  * = histogram of the next digit_bits bits (MSB first) of the values whose top
- * prefix_bits bits equal `prefix` (digit_bits <= 11).  Ranks sum these
+ * prefix_bits bits equal `prefix` (digit_bits <= 11); 64-bit counts.  Ranks sum these
  * histograms (e.g. NCCL all_reduce) to select an order statistic of a
  * sharded makespan set. */
 int osim_radix_hist_dev(const double* d_vals, uint64_t count, uint64_t prefix, int prefix_bits,
-                        int digit_bits, uint32_t* d_hist, void* stream);
+                        int digit_bits, uint64_t* d_hist, void* stream);
+/* k-th smallest (0-based) of `count` non-negative doubles in HBM (no NaN, no
+ * -0.0), by the same MSB-first radix selection with 64-bit bin counts that
+ * osim_exhaustive_stats uses for np.median (oracle.py:54).  Waits for
+ * `stream` (the producer of d_vals) first; synchronous. */
+int osim_select_kth_dev(const double* d_vals, uint64_t count, uint64_t k, double* kth, void* stream);
 int osim_exhaustive_batch_dev(const double* d_durs, uint64_t B, int n, int dma, double sigma,
                               int fast, osim_summary* d_out, void* stream);
 int osim_heuristic_batch_dev(const double* d_durs, const uint8_t* d_id_rank, uint64_t B, int n,

@@ -28,7 +28,8 @@ EXPORTS = (
     "osim_heuristic_batch_dev", "osim_selftest_div", "osim_fp64_peak", "osim_exhaustive_stats",
     "osim_exhaustive_ex_dev", "osim_radix_hist_dev", "osim_interleavings", "osim_eval_sequences",
     "osim_timeline_deps", "osim_micro", "osim_micro_timeline", "osim_harness_batch",
-    "osim_exhaustive_shard_dev", "osim_exhaustive_shard",
+    "osim_exhaustive_shard_dev", "osim_exhaustive_shard", "osim_select_kth_dev",
+    "osim_pfx_suffix_len",
 )
 
 
@@ -101,6 +102,8 @@ def load(path: str = LIB_PATH):
             "osim_exhaustive_stats": ([dp, i, i, d, u64, u64, d, i, sp, C.POINTER(u64), dp], i),
             "osim_exhaustive_ex_dev": ([vp, i, i, d, u64, u64, i, d, vp, vp, vp, vp], i),
             "osim_radix_hist_dev": ([vp, u64, u64, i, i, vp, vp], i),
+            "osim_select_kth_dev": ([vp, u64, u64, dp, vp], i),
+            "osim_pfx_suffix_len": ([i], i),
             "osim_interleavings": ([dp, i, i, i, d, u64, u64, d, i, sp, C.POINTER(u64), dp], i),
             "osim_eval_sequences": ([dp, i, i, i, d, u8p, u64, i, dp, sp], i),
             "osim_micro": ([dp, i, i, d, d, u64, u64, i, dp], i),
@@ -187,6 +190,15 @@ def exhaustive_stats(durs, dma, sigma, lo, hi, threshold=float("-inf"), n_dev=1,
                                        float(threshold), int(n_dev), C.byref(out), C.byref(below),
                                        C.byref(med) if median else None))
     return out.as_dict(), below.value, (med.value if median else None)
+
+
+def select_kth_dev(d_vals_ptr: int, count: int, k: int, stream: int = 0) -> float:
+    """k-th smallest (0-based) of `count` non-negative doubles at device
+    address d_vals_ptr (osim_select_kth_dev; waits for `stream` first)."""
+    out = C.c_double()
+    check(load().osim_select_kth_dev(C.c_void_p(d_vals_ptr), int(count), int(k), C.byref(out),
+                                     C.c_void_p(stream) if stream else None))
+    return out.value
 
 
 def eval_perms(durs, dma, sigma, perms, n_dev=1):

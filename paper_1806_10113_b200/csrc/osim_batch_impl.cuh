@@ -8,7 +8,6 @@ namespace {
 template <int N, bool SP2, int L>
 int batch_t(const LaunchCfg& cfg, const double* d_durs, uint64_t B, double sigma, osim_summary* d_out) {
     auto k = k_exhaustive_batch_pfx<N, OSIM_DMA, SP2, L>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPfxDynSmem);
     const int g = grid_for_sms(k, kBlock, kPfxDynSmem, cfg.sms, B);
     k<<<g, kBlock, kPfxDynSmem, cfg.st>>>(d_durs, B, sigma, d_out);
     return 0;

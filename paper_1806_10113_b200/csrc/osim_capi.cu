@@ -12,6 +12,7 @@
 #include <mutex>
 #include <thread>
 #include <string>
+#include <array>
 #include <vector>
 
 #include "osim_deps.cuh"
@@ -67,7 +68,17 @@ int ensure_init() {
     cudaError_t e = cudaGetDeviceCount(&count);
     if (e != cudaSuccess || count <= 0)
         return fail(OSIM_ENODEV, "no CUDA device available (%s)", cudaGetErrorString(e));
-    for (int d = 0; d < count; ++d) {
+    // OSIM_VIRTUAL_DEVICES=<k> (testing only): k library devices, device i on
+    // physical GPU i % count, each with its own streams, scratch, error flag
+    // and lock -- so the n_dev > 1 host paths (sharding, per-device
+    // validation, host-side merges) run, and are tested, on a one-GPU box
+    int nctx = count;
+    if (const char* e = std::getenv("OSIM_VIRTUAL_DEVICES")) {
+        const int k = std::atoi(e);
+        if (k > count && k <= 64) nctx = k;
+    }
+    for (int i = 0; i < nctx; ++i) {
+        const int d = i % count;
         DevCtx* c = new DevCtx();
         c->dev = d;
         CK(cudaSetDevice(d));
@@ -410,8 +421,19 @@ int pick_devs(int n_dev, DevList& out) {
 // fit the per-device compaction buffers (cbuf, ccap values each) the next
 // pass also copies them out, so the remaining passes read only those.
 // *same_next: whether the (k+1)-th value equals the k-th.
+// Grid of k_radix_hist over `count` values: 8 CTAs per SM, more if a CTA
+// would otherwise visit 2^32 values or more (its shared counts are 32-bit).
+int radix_grid(uint64_t count, int sms) {
+    const uint64_t blocks = (count + 255) / 256;
+    uint64_t g = blocks < (uint64_t)sms * 8 ? blocks : (uint64_t)sms * 8;
+    const uint64_t per_cta_max = (1ull << 32) - 256;  // values one CTA may visit
+    while (g < blocks && ((count + g * 256 - 1) / (g * 256)) * 256 > per_cta_max) g *= 2;
+    if (g > blocks) g = blocks;
+    return (int)(g < 1 ? 1 : g);
+}
+
 int select_kth(std::vector<DevCtx*>& devs, std::vector<const double*>& vals, std::vector<uint64_t>& counts,
-               std::vector<unsigned*>& d_hist, uint64_t k, double vmin, double vmax,
+               std::vector<unsigned long long*>& d_hist, uint64_t k, double vmin, double vmax,
                std::vector<unsigned long long*>& cbuf, uint64_t ccap, double* out, bool* same_next) {
     unsigned long long prefix = 0, a, b;
     memcpy(&a, &vmin, sizeof(a));
@@ -426,28 +448,28 @@ int select_kth(std::vector<DevCtx*>& devs, std::vector<const double*>& vals, std
     uint64_t matching = 0;  // values carrying the current prefix, over all devices
     for (size_t i = 0; i < devs.size(); ++i) matching += cnt[i];
     bool compacted = false;
-    std::vector<unsigned> h(1 << kRadixBits), tot(1 << kRadixBits);
+    std::vector<unsigned long long> h(1 << kRadixBits), tot(1 << kRadixBits);  // 64-bit: bins can exceed 2^32
     uint64_t last_bin_count = 0;
     while (pbits < 64) {
         const int d = (64 - pbits) < kRadixBits ? (64 - pbits) : kRadixBits;
         const int nb = 1 << d;
         const bool append = !compacted && pbits > 0 && matching <= ccap && !cbuf.empty();
-        std::fill(tot.begin(), tot.begin() + nb, 0u);
+        std::fill(tot.begin(), tot.begin() + nb, 0ull);
         std::vector<unsigned long long> got(devs.size(), 0);
         for (size_t i = 0; i < devs.size(); ++i) {
             DevCtx* c = devs[i];
             CK(cudaSetDevice(c->dev));
-            CK(cudaMemsetAsync(d_hist[i], 0, nb * sizeof(unsigned), c->stream));
-            unsigned long long* d_cnt = (unsigned long long*)((char*)d_hist[i] + (1u << kRadixBits) * sizeof(unsigned));
+            CK(cudaMemsetAsync(d_hist[i], 0, nb * sizeof(unsigned long long), c->stream));
+            unsigned long long* d_cnt = d_hist[i] + (1u << kRadixBits);
             if (append) CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), c->stream));
             if (cnt[i]) {
-                const uint64_t blocks = (cnt[i] + 255) / 256;
-                const int g = (int)(blocks < (uint64_t)c->sms * 8 ? blocks : (uint64_t)c->sms * 8);
+                const int g = radix_grid(cnt[i], c->sms);
                 k_radix_hist<<<g, 256, 0, c->stream>>>(cur[i], cnt[i], prefix, pbits, d, d_hist[i],
                                                        append ? cbuf[i] : nullptr, append ? d_cnt : nullptr);
                 CK(cudaGetLastError());
             }
-            CK(cudaMemcpyAsync(h.data(), d_hist[i], nb * sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(h.data(), d_hist[i], nb * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               c->stream));
             if (append) CK(cudaMemcpyAsync(&got[i], d_cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
             CK(cudaStreamSynchronize(c->stream));
             for (int bb = 0; bb < nb; ++bb) tot[bb] += h[bb];
@@ -558,13 +580,18 @@ int osim_set_device(int device) {
     if (device < 0 || device >= (int)g_devs.size())
         return fail(OSIM_ENODEV, "device %d not available (%d visible)", device, (int)g_devs.size());
     g_thread_dev = device;
-    CK(cudaSetDevice(device));
+    CK(cudaSetDevice(g_devs[device]->dev));
     return 0;
 }
 
 int osim_fast_eligible(const double* durs, uint64_t count, double sigma) {
     if (!durs) return 0;
     return fast_ok(durs, count, sigma) ? 1 : 0;
+}
+
+int osim_pfx_suffix_len(int n) {
+    if (n < 1 || n > kMaxN) return fail(OSIM_EINVAL, "n=%d outside [1, %d]", n, kMaxN);
+    return pfx_l_for(n);
 }
 
 int osim_exhaustive(const double* durs, int n, int dma, double sigma, uint64_t rank_lo,
@@ -717,7 +744,7 @@ int osim_exhaustive_stats(const double* durs, int n, int dma, double sigma, uint
     std::vector<unsigned long long> bel(G, 0);
     std::vector<const double*> vals(G);
     std::vector<uint64_t> counts(G);
-    std::vector<unsigned*> hists(G);
+    std::vector<unsigned long long*> hists(G);
     std::vector<unsigned long long*> cbufs(G);
     uint64_t ccap = 0;  // per-device compaction capacity (values)
     std::vector<std::unique_lock<std::mutex>> locks;
@@ -732,7 +759,7 @@ int osim_exhaustive_stats(const double* durs, int n, int dma, double sigma, uint
         size_t off_sum = off_parts + align_up(mp * sizeof(Part));
         size_t off_bel = off_sum + align_up(sizeof(osim_summary));
         size_t off_hist = off_bel + 256;
-        size_t off_ms = off_hist + align_up((1u << kRadixBits) * sizeof(unsigned) + 256);
+        size_t off_ms = off_hist + align_up(((1u << kRadixBits) + 1) * sizeof(unsigned long long));
         size_t off_cb = off_ms + align_up((hi - lo) * sizeof(double) + 8);
         size_t bytes = off_cb + (median ? align_up(((hi - lo) / 8 + 1) * sizeof(double)) : 0);
         void* base;
@@ -747,7 +774,7 @@ int osim_exhaustive_stats(const double* durs, int n, int dma, double sigma, uint
         CK(cudaMemcpyAsync(&bel[gi], b + off_bel, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
         vals[gi] = (const double*)(b + off_ms);
         counts[gi] = hi - lo;
-        hists[gi] = (unsigned*)(b + off_hist);
+        hists[gi] = (unsigned long long*)(b + off_hist);
         cbufs[gi] = (unsigned long long*)(b + off_cb);
         ccap = (gi == 0 || (hi - lo) / 8 + 1 < ccap) ? (hi - lo) / 8 + 1 : ccap;
     }
@@ -791,7 +818,7 @@ int osim_exhaustive_stats(const double* durs, int n, int dma, double sigma, uint
 }
 
 int osim_radix_hist_dev(const double* d_vals, uint64_t count, uint64_t prefix, int prefix_bits, int digit_bits,
-                        uint32_t* d_hist, void* stream) {
+                        uint64_t* d_hist, void* stream) {
     if (prefix_bits < 0 || digit_bits < 1 || digit_bits > kRadixBits || prefix_bits + digit_bits > 64)
         return fail(OSIM_EINVAL, "bad radix digit (prefix %d bits, digit %d bits)", prefix_bits, digit_bits);
     DevList dl;
@@ -799,15 +826,35 @@ int osim_radix_hist_dev(const double* d_vals, uint64_t count, uint64_t prefix, i
     if (rc) return rc;
     DevCtx* c = dl.v[0];
     cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
-    CK(cudaMemsetAsync(d_hist, 0, (1u << digit_bits) * sizeof(unsigned), st));
+    CK(cudaMemsetAsync(d_hist, 0, (1u << digit_bits) * sizeof(uint64_t), st));
     if (count) {
-        const uint64_t blocks = (count + 255) / 256;
-        const int g = (int)(blocks < (uint64_t)c->sms * 8 ? blocks : (uint64_t)c->sms * 8);
+        const int g = radix_grid(count, c->sms);
         k_radix_hist<<<g, 256, 0, st>>>((const unsigned long long*)d_vals, count, prefix, prefix_bits, digit_bits,
-                                        d_hist);
+                                        (unsigned long long*)d_hist);
     }
     CK(cudaGetLastError());
     return 0;
+}
+
+int osim_select_kth_dev(const double* d_vals, uint64_t count, uint64_t k, double* kth, void* stream) {
+    if (!kth) return fail(OSIM_EINVAL, "kth is NULL");
+    if (count && !d_vals) return fail(OSIM_EINVAL, "d_vals is NULL");
+    if (k >= count) return fail(OSIM_EINVAL, "rank %llu outside [0, %llu)", (unsigned long long)k,
+                                (unsigned long long)count);
+    DevList dl;
+    int rc = pick_devs(1, dl);
+    if (rc) return rc;
+    DevCtx* c = dl.v[0];
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->dev));
+    if (stream) CK(cudaStreamSynchronize((cudaStream_t)stream));  // the values are complete
+    void* base;
+    if ((rc = scratch(c, align_up(((1u << kRadixBits) + 1) * sizeof(unsigned long long)), &base))) return rc;
+    std::vector<const double*> vals{d_vals};
+    std::vector<uint64_t> counts{count};
+    std::vector<unsigned long long*> hists{(unsigned long long*)base};
+    std::vector<unsigned long long*> nocb;
+    return select_kth(dl.v, vals, counts, hists, k, 0.0, 0.0, nocb, 0, kth, nullptr);
 }
 
 int osim_exhaustive_ex_dev(const double* d_durs, int n, int dma, double sigma, uint64_t rank_lo, uint64_t rank_hi,
@@ -1034,16 +1081,28 @@ int osim_heuristic_batch(const double* durs, const uint8_t* id_rank, uint64_t B,
                 CK(cudaMemcpyAsync(n_sims + lo + a, d_ns, mm * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         }
     }
+    // every device's streams are drained (and its error flag reset after an
+    // optimistic pass over ineligible data) before any error is returned, so
+    // no copy into the caller's buffers is still in flight
+    std::vector<std::array<unsigned long long, 4>> chk(G);
+    int sync_rc = 0;
     for (int gi = 0; gi < G; ++gi) {
         DevCtx* c = dl.v[gi];
+        chk[gi] = {~0ull, ~0ull, 0ull, 0ull};
         if (!ms_[gi]) continue;
-        CK(cudaSetDevice(c->dev));
-        CK(cudaStreamSynchronize(c->stream2));
-        CK(cudaStreamSynchronize(c->stream));
-        unsigned long long res[4];
-        CK(cudaMemcpy(res, d_chk[gi], sizeof(res), cudaMemcpyDeviceToHost));
+        if (cudaSetDevice(c->dev) != cudaSuccess || cudaStreamSynchronize(c->stream2) != cudaSuccess ||
+            cudaStreamSynchronize(c->stream) != cudaSuccess ||
+            cudaMemcpy(chk[gi].data(), d_chk[gi], sizeof(chk[gi]), cudaMemcpyDeviceToHost) != cudaSuccess) {
+            if (!sync_rc) sync_rc = fail(OSIM_ECUDA, "device %d: %s", c->dev, cudaGetErrorString(cudaGetLastError()));
+            continue;
+        }
+        const auto& res = chk[gi];
         if (res[0] != ~0ull || res[1] != ~0ull || (fast_first && res[2]))
-            CK(cudaMemset(c->d_err, 0, sizeof(int)));  // the optimistic pass ran on ineligible data
+            cudaMemset(c->d_err, 0, sizeof(int));  // the optimistic pass ran on ineligible data
+    }
+    if (sync_rc) return sync_rc;
+    for (int gi = 0; gi < G; ++gi) {
+        const auto& res = chk[gi];
         if (res[0] != ~0ull) {  // the reason, for the reference's message
             const uint64_t t = res[0];
             const double* d = durs + 3 * t;
@@ -1053,22 +1112,31 @@ int osim_heuristic_batch(const double* durs, const uint8_t* id_rank, uint64_t B,
         }
         if (res[1] != ~0ull)
             return fail(OSIM_EINVAL, "group %llu: id ranks must be a permutation (duplicate task id?)", res[1]);
-        if (fast_first && res[2]) {
-            // not fast-eligible: recompute this shard with the null-stage
-            // kernel (every stage 0 or in range) or the general one
-            const uint64_t m = ms_[gi];
-            char* b = bases[gi];
-            if ((rc = enqueue_heuristic(c, c->stream, (double*)b, (uint8_t*)(b + offs_idr[gi]), m, n, dma, sigma,
-                                        sum_mode, res[3] ? 0 : 2, (uint8_t*)(b + offs_ord[gi]),
-                                        (double*)(b + offs_ms[gi]), (uint32_t*)(b + offs_ns[gi]))))
-                return rc;
-            const uint64_t lo = los[gi];
-            CK(cudaMemcpyAsync(order + lo * n, b + offs_ord[gi], m * n, cudaMemcpyDeviceToHost, c->stream));
-            CK(cudaMemcpyAsync(makespan + lo, b + offs_ms[gi], m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-            if (n_sims)
-                CK(cudaMemcpyAsync(n_sims + lo, b + offs_ns[gi], m * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                                   c->stream));
-        }
+    }
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        const auto& res = chk[gi];
+        if (!ms_[gi] || !(fast_first && res[2])) continue;
+        CK(cudaSetDevice(c->dev));
+        // not fast-eligible: recompute this shard with the null-stage kernel
+        // (every stage 0 or in range) or the general one
+        const uint64_t m = ms_[gi];
+        char* b = bases[gi];
+        if ((rc = enqueue_heuristic(c, c->stream, (double*)b, (uint8_t*)(b + offs_idr[gi]), m, n, dma, sigma,
+                                    sum_mode, res[3] ? 0 : 2, (uint8_t*)(b + offs_ord[gi]),
+                                    (double*)(b + offs_ms[gi]), (uint32_t*)(b + offs_ns[gi]))))
+            return rc;
+        const uint64_t lo = los[gi];
+        CK(cudaMemcpyAsync(order + lo * n, b + offs_ord[gi], m * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(makespan + lo, b + offs_ms[gi], m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        if (n_sims)
+            CK(cudaMemcpyAsync(n_sims + lo, b + offs_ns[gi], m * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                               c->stream));
+    }
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        if (!ms_[gi]) continue;
+        CK(cudaSetDevice(c->dev));
         if ((rc = finish(c, c->stream))) return rc;
     }
     return 0;
@@ -1503,6 +1571,8 @@ int osim_harness_batch(const double* durs, const uint8_t* id_rank, uint64_t S, i
         char* b = (char*)base;
         CK(cudaMemcpyAsync(b, durs + lo * n * 3, m * n * 3 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(b + off_r, id_rank + lo * n, m * n, cudaMemcpyHostToDevice, c->stream));
+        // entries past a scenario's n_groups are zero (the kernels write the first n_groups)
+        CK(cudaMemsetAsync(b + off_sz, 0, m * n, c->stream));
         const unsigned blocks = (unsigned)((m + 127) / 128);
         double* d_st = tl ? (double*)(b + off_st) : nullptr;
         double* d_en = tl ? (double*)(b + off_en) : nullptr;

@@ -18,11 +18,18 @@ int exh_t(const LaunchCfg& cfg, const double* d_durs, double sigma, uint64_t lo,
     const uint64_t prefixes = (hi + LF - 1) / LF - lo / LF;
     constexpr uint64_t kPer = (uint64_t)kPfxQ * kBlock;
     const uint64_t calls = (prefixes + kPer - 1) / kPer;  // this shard's: calls shard, shard + shards, ...
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPfxDynSmem);
-    int g = grid_for_sms(k, kBlock, kPfxDynSmem, cfg.sms, calls > shard ? (calls - shard + shards - 1) / shards : 1);
+    const uint64_t mine = calls > shard ? (calls - shard + shards - 1) / shards : 1;
+    const uint64_t slots = (uint64_t)cached_ctas_per_sm((const void*)k, kBlock, kPfxDynSmem) * cfg.sms;
+    // a shard of at most half the resident CTA slots (C3 at 8 ranks: 148
+    // calls) splits every call over two CTAs of 256 prefixes each (one per
+    // thread): twice the CTAs for the same partition, half the serial work
+    // per thread
+    const unsigned split = (2 * mine <= slots) ? 2u : 1u;
+    int g = grid_for_sms(k, kBlock, kPfxDynSmem, cfg.sms, mine * split);
     if (g > max_parts) g = max_parts;
+    g -= g % (int)split;
     k<<<g, kBlock, kPfxDynSmem, cfg.st>>>(d_durs, sigma, lo, hi, thr, parts, d_ms, d_out, d_below, d_done, shard,
-                                          shards);
+                                          shards, split);
     *grid_out = g;
     return 0;
 }

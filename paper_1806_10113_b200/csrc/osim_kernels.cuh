@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
                                                            double* __restrict__ ms_out, osim_summary* __restrict__ out,
                                                            unsigned long long* __restrict__ below,
                                                            unsigned* __restrict__ done, unsigned shard,
-                                                           unsigned shards) {
+                                                           unsigned shards, unsigned split) {
     __shared__ double2 sdr[3 * kStride];
     __shared__ Part sh[32];
     extern __shared__ __align__(16) unsigned char pfx_dsm[];
@@ -596,9 +596,17 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
     // osim_exhaustive_shard_dev): this launch takes calls shard, shard +
     // shards, ... of the range, so every shard samples the whole rank space
     // and the per-shard work evens out.
-    const uint64_t stride = (uint64_t)gridDim.x * kPer * shards;
-    for (uint64_t pb = p_lo + ((uint64_t)blockIdx.x * shards + shard) * kPer; pb < p_hi; pb += stride)
-        pfx_leaves<N, DMA, SIGP2, L, STATS>(base, sigma, rsig, pb, p_hi, lo, hi, thr, acc, ms_out, lo, K, S);
+    // split = 2 (small shards): CTAs 2c and 2c + 1 share call c, 256
+    // prefixes each (the second prefix slot of every thread stays empty and
+    // sorts last), so the partition into calls is the same for any split.
+    const uint64_t per = kPer / split;
+    const uint64_t cta_call = blockIdx.x / split, half = blockIdx.x % split;
+    const uint64_t stride = (uint64_t)(gridDim.x / split) * kPer * shards;
+    for (uint64_t pc = p_lo + (cta_call * shards + shard) * kPer; pc < p_hi; pc += stride) {
+        const uint64_t pb = pc + half * per;
+        const uint64_t pe = pb + per < p_hi ? pb + per : p_hi;
+        if (pb < pe) pfx_leaves<N, DMA, SIGP2, L, STATS>(base, sigma, rsig, pb, pe, lo, hi, thr, acc, ms_out, lo, K, S);
+    }
     acc = block_reduce(acc, sh);
     if (threadIdx.x == 0) parts[blockIdx.x] = acc;
     if (out) fused_final_reduce(parts, out, below, done, sh);
@@ -1375,9 +1383,13 @@ constexpr int kRadixBits = 11;
 // carrying that prefix (bit patterns of positive doubles order like the
 // values).  With `out`, the matching values are also appended to out
 // (warp-aggregated, order unspecified), so later passes can run on them.
+// The global histogram is 64-bit: a digit bin can hold more than 2^32 values
+// (13! = 6.2e9 makespans fit one GPU).  The per-block shared counts stay
+// 32-bit; a block visits at most ceil(count / (gridDim.x * 256)) * 256
+// values, which the launchers keep below 2^32 (radix_grid).
 static __global__ void __launch_bounds__(256) k_radix_hist(const unsigned long long* __restrict__ vals,
                                                            uint64_t count, unsigned long long prefix, int pbits,
-                                                           int dbits, unsigned* __restrict__ hist,
+                                                           int dbits, unsigned long long* __restrict__ hist,
                                                            unsigned long long* __restrict__ out = nullptr,
                                                            unsigned long long* __restrict__ out_count = nullptr) {
     __shared__ unsigned sh[1 << kRadixBits];
@@ -1409,7 +1421,7 @@ static __global__ void __launch_bounds__(256) k_radix_hist(const unsigned long l
     }
     __syncthreads();
     for (int i = threadIdx.x; i < nb; i += blockDim.x)
-        if (sh[i]) atomicAdd(&hist[i], sh[i]);
+        if (sh[i]) atomicAdd(&hist[i], (unsigned long long)sh[i]);
 }
 
 // ---------------------------------------------------------------------------

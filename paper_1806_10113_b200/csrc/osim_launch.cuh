@@ -7,6 +7,8 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "osim_kernels.cuh"
 
@@ -17,16 +19,41 @@ struct LaunchCfg {
     cudaStream_t st;
 };
 
+// Per-(kernel, device, block shape) launch facts, looked up once: the
+// occupancy query, the dynamic-shared-memory opt-in and the tuning env var
+// cost a few microseconds per launch, which small searches (C3 shards at
+// N = 8, ~40 us) would otherwise pay on every call.
+struct KernelFacts {
+    const void* fn;
+    int dev, threads;
+    size_t smem;
+    int per_sm;
+};
+
+inline int cached_ctas_per_sm(const void* fn, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::vector<KernelFacts> facts;
+    static const int cap = [] {  // OSIM_CTAS_PER_SM=<k> caps the resident CTAs per SM (tuning only)
+        const char* e = std::getenv("OSIM_CTAS_PER_SM");
+        return e ? std::atoi(e) : 0;
+    }();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    for (const KernelFacts& f : facts)
+        if (f.fn == fn && f.dev == dev && f.threads == threads && f.smem == smem) return f.per_sm;
+    if (smem > 0) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    if (cap >= 1 && cap < per_sm) per_sm = cap;
+    facts.push_back({fn, dev, threads, smem, per_sm});
+    return per_sm;
+}
+
 template <class K>
 int grid_for_sms(K kernel, int threads, size_t smem, int sms, uint64_t work_blocks) {
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
-    if (per_sm < 1) per_sm = 1;
-    // OSIM_CTAS_PER_SM=<k> caps the resident CTAs per SM (tuning only)
-    if (const char* e = std::getenv("OSIM_CTAS_PER_SM")) {
-        const int k = std::atoi(e);
-        if (k >= 1 && k < per_sm) per_sm = k;
-    }
+    const int per_sm = cached_ctas_per_sm((const void*)kernel, threads, smem);
     uint64_t g = (uint64_t)per_sm * sms;
     if (work_blocks < g) g = work_blocks;
     if (g < 1) g = 1;

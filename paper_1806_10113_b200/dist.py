@@ -33,9 +33,18 @@ def shard(total: int, rank: int, world: int) -> Tuple[int, int]:
 
 
 def default_suffix_len(n: int) -> int:
-    """Suffix length L of the prefix-sharing kernel (csrc/osim_launch.cuh
+    """Default suffix length L of the prefix-sharing kernel (csrc/osim_launch.cuh
     default_pfx_l): one kernel call covers 512 prefixes x L! leaves."""
     return 1 if n <= 3 else (2 if n <= 5 else (3 if n <= 10 else 4))
+
+
+def suffix_len(n: int) -> int:
+    """The L the library actually uses for n (osim_pfx_suffix_len: the default,
+    or the OSIM_PFX_L tuning override for n in {8, 10, 12}, read once per
+    process), so the interleaved ranges below match its shards."""
+    from . import _capi
+
+    return int(_capi.load().osim_pfx_suffix_len(int(n)))
 
 
 def shard_ranges(n: int, rank: int, world: int, fast: bool = True) -> List[Tuple[int, int]]:
@@ -47,7 +56,7 @@ def shard_ranges(n: int, rank: int, world: int, fast: bool = True) -> List[Tuple
     total = math.factorial(n)
     if not fast:
         return [shard(total, rank, world)]
-    chunk = 512 * math.factorial(default_suffix_len(n))
+    chunk = 512 * math.factorial(suffix_len(n))
     calls = -(-total // chunk)
     return [(k * chunk, min(total, (k + 1) * chunk)) for k in range(rank, calls, world)]
 
@@ -111,17 +120,25 @@ def exhaustive_summary_distributed(durs, dma: int, sigma: float, group=None,
         from . import _capi
 
         local = _capi.exhaustive_shard(d, dma, sigma, rank, world)
+        part_l = suffix_len(n) if _capi.fast_eligible(d, sigma) == 1 else 0
     else:
         ranges = shard_ranges(n, rank, world, fast=interleaved)
         local = combine([local_fn(d, dma, sigma, lo, hi) for lo, hi in ranges])
+        part_l = suffix_len(n) if interleaved else 0
     backend = tdist.get_backend(group)
     dev = device if device is not None else (torch.device("cuda", torch.cuda.current_device())
                                              if backend == "nccl" else torch.device("cpu"))
-    mine = torch.from_numpy(pack(local)).to(dev)
+    # word 6: the partition this rank used (suffix length L of the interleaved
+    # calls, 0 = contiguous); ranks whose environments disagree (OSIM_PFX_L)
+    # would double-count or drop orderings, so every rank checks all of them
+    mine = torch.from_numpy(np.append(pack(local), float(part_l))).to(dev)
     bufs = [torch.empty_like(mine) for _ in range(world)]
     tdist.all_gather(bufs, mine, group=group)
-    parts = [unpack(b.cpu().numpy()) for b in bufs]
-    return summary_from_dict(combine(parts), n)
+    rows = [b.cpu().numpy() for b in bufs]
+    if len({float(r[6]) for r in rows}) != 1:
+        raise ValueError("ranks partitioned the rank space differently (suffix lengths %s); "
+                         "set OSIM_PFX_L identically on every rank" % [float(r[6]) for r in rows])
+    return summary_from_dict(combine([unpack(r[:6]) for r in rows]), n)
 
 
 # ---- batches of groups (configs 2 and 5): group-range shards, no collective
@@ -135,7 +152,9 @@ def _gather_rows(local: np.ndarray, total: int, group, world: int, device) -> np
 
     width = max(shard(total, r, world)[1] - shard(total, r, world)[0] for r in range(world))
     row = local.shape[1:]
-    raw = np.ascontiguousarray(local).view(np.uint8).reshape(local.shape[0], -1)
+    # explicit row width: reshape(0, -1) is ambiguous for a rank whose shard is empty
+    row_bytes = local.dtype.itemsize * int(np.prod(row, dtype=np.int64))
+    raw = np.ascontiguousarray(local).view(np.uint8).reshape(local.shape[0], row_bytes)
     pad = np.zeros((width, raw.shape[1]), dtype=np.uint8)
     pad[: raw.shape[0]] = raw
     t = torch.from_numpy(pad).to(device)
@@ -322,7 +341,7 @@ def _stats_on_stream(L, C, torch, tdist, _capi, d, n, dma, sigma, threshold, gro
     out = torch.zeros(6, dtype=torch.float64, device=dev)
     below = torch.zeros(1, dtype=torch.int64, device=dev)
     ms = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=dev)
-    hist = torch.empty(1 << RADIX_BITS, dtype=torch.int32, device=dev)
+    hist = torch.empty(1 << RADIX_BITS, dtype=torch.int64, device=dev)  # uint64 counts (< 2^63)
     fast = int(_capi.fast_eligible(d, sigma))
     _capi.check(L.osim_exhaustive_ex_dev(C.c_void_p(dd.data_ptr()), n, int(dma), float(sigma), lo, hi, fast,
                                          float(threshold), C.c_void_p(out.data_ptr()), C.c_void_p(below.data_ptr()),
@@ -335,7 +354,7 @@ def _stats_on_stream(L, C, torch, tdist, _capi, d, n, dma, sigma, threshold, gro
     def local_hist(prefix, pbits, dbits):
         _capi.check(L.osim_radix_hist_dev(C.c_void_p(ms.data_ptr()), hi - lo, prefix, pbits, dbits,
                                           C.c_void_p(hist.data_ptr()), sp))
-        return hist[: 1 << dbits].to(torch.int64).cpu().numpy()
+        return hist[: 1 << dbits].cpu().numpy()
 
     med = median_distributed(local_hist, summ.count, group, vmin=summ.best, vmax=summ.worst)
     return summ, int(below.item()), med

@@ -164,6 +164,69 @@ def test_gloo_batch_shards_gather_whole_batch():
         assert summ.tobytes() == want_s.tobytes()
 
 
+def test_gloo_batch_smaller_than_world():
+    # B = 2 groups over 3 ranks: one rank's group-range shard is empty; it
+    # must still join the all_gathers (no reshape error, no hang)
+    from paper_1806_10113_b200 import synth
+
+    B, n = 2, 7
+    d = np.stack([synth.real_group("K20", n, 70 + b)[1] for b in range(B)])
+    r = np.stack([np.random.default_rng(b).permutation(n) for b in range(B)]).astype(np.uint8)
+    want = O.reorder_batch(d, r, 2, 0.5, 1, threads=2)
+    want_s = _oracle_batch(d[:, :6])
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(k, world, port, d, r, q)) for k in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, order, ms, sims, summ in res:
+        assert np.array_equal(order, want[0]) and np.array_equal(ms, want[1]) and np.array_equal(sims, want[2])
+        assert summ.tobytes() == want_s.tobytes()
+
+
+def _pfx_env_worker(rank, world, port, d, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    # rank 1 overrides the suffix length of the library's partition
+    if rank == 1:
+        os.environ["OSIM_PFX_L"] = "5"
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1806_10113_b200.dist import exhaustive_summary_distributed
+
+        try:
+            exhaustive_summary_distributed(d, 2, 0.5, local_fn=_oracle_local, interleaved=True)
+            q.put((rank, "ok"))
+        except ValueError as e:
+            q.put((rank, str(e)))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_gloo_mismatched_partitions_are_rejected():
+    # OSIM_PFX_L differing between ranks would double-count or drop
+    # orderings: every rank sees every rank's partition and raises
+    d = np.stack([[1.0 + i, 2.0 + (i * 7) % 5, 1.5] for i in range(8)])
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pfx_env_worker, args=(k, world, port, d, q)) for k in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all("partitioned the rank space differently" in m for _, m in res)
+
+
 @pytest.mark.parametrize("fast", [True, False])
 def test_shard_ranges_partition_every_space(fast):
     # every ordering of n! in exactly one rank's ranges, for any world size

@@ -361,6 +361,72 @@ def test_c4_full_space_median_is_an_order_statistic():
     assert s["best"] <= med <= s["worst"]
 
 
+def test_f2_median_bin_above_2_32():
+    """13! = 6,227,020,800 makespans in HBM with one value held by 11/13 of
+    them (5.27e9 > 2^32 in the median's bin): the selection histograms count
+    in 64 bits.  Every kernel lane is busy from the first HtD on (t_k = 5 >=
+    every transfer), so makespan = first HtD + 13 * 5 + last DtH (1): 66.5 if
+    task 11 runs first, 69.0 if task 12 does, else 67.0 (sampled against the
+    oracle below)."""
+    d = np.array([[1.0, 5.0, 1.0]] * 11 + [[0.5, 5.0, 1.0], [3.0, 5.0, 1.0]])
+    rng = np.random.default_rng(13)
+    perms = np.array([rng.permutation(13) for _ in range(2000)], dtype=np.uint8)
+    _, oms = O.eval_perms(d, 2, 0.5, perms, threads=os.cpu_count() or 1)
+    first = perms[:, 0]
+    assert set(oms[first == 11]) == {66.5} and set(oms[first == 12]) == {69.0}
+    assert set(oms[(first != 11) & (first != 12)]) == {67.0}
+    total, f12 = math.factorial(13), math.factorial(12)
+    s, lt, med = _capi.exhaustive_stats(d, 2, 0.5, 0, total, threshold=67.0)
+    assert s["count"] == total and s["best"] == 66.5 and s["best_rank"] == 11 * f12 and s["worst"] == 69.0
+    assert med == 67.0
+    _, le, _ = _capi.exhaustive_stats(d, 2, 0.5, 0, total, threshold=float(np.nextafter(67.0, np.inf)),
+                                      median=False)
+    assert lt == f12 and le == total - f12
+    assert lt <= total // 2 <= le  # the order-statistic check
+    assert le - lt > 2**32
+
+
+def test_select_kth_counts_above_2_32():
+    """A synthetic device array of 2^32 + 5 values (34 GB): 2^32 + 1 ones
+    then four twos, and a constant array; 32-bit bin counts would wrap."""
+    import torch
+
+    _capi.set_device(0)
+    n = 2**32 + 5
+    v = torch.ones(n, dtype=torch.float64, device="cuda")
+    v[-4:] = 2.0
+    torch.cuda.synchronize()
+    p = v.data_ptr()
+    assert _capi.select_kth_dev(p, n, 0) == 1.0
+    assert _capi.select_kth_dev(p, n, 2**32) == 1.0
+    assert _capi.select_kth_dev(p, n, 2**32 + 1) == 2.0
+    assert _capi.select_kth_dev(p, n, n - 1) == 2.0
+    v.fill_(3.25)
+    torch.cuda.synchronize()
+    assert _capi.select_kth_dev(p, n, n // 2) == 3.25
+    with pytest.raises(ValueError):
+        _capi.select_kth_dev(p, n, n)
+    del v
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("k", [2, 4])
+def test_virtual_multi_device_paths(k):
+    """The C-ABI's in-process n_dev > 1 paths (sharding, per-device
+    validation, host-side merges and the per-device histogram sums of the
+    exact median) on one GPU: OSIM_VIRTUAL_DEVICES=k gives the library k
+    device contexts on device 0 (tests/ndev_check.py, in a subprocess)."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, OSIM_VIRTUAL_DEVICES=str(k))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "ndev_check.py")], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert f"ndev ok {list(range(2, k + 1))}" in r.stdout
+
+
 def test_heuristic_percentile_dropin():
     g = load("c3_full.json")
     p = osim.DeviceProfile("2dma", 2, 0.01, 6e6, 0.01, 6e6, overlap_sigma=0.5)
