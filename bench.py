@@ -21,8 +21,11 @@ dist.exhaustive_summary_distributed): host buffers, H2D + kernels + D2H +
 combine per step.  `secondary` holds configs 3 (N=10), 2 (100k x 8! batch)
 and 5 (10^6 x 16-task heuristic, three device profiles).
 `--impl reference` times the CPU restatement of the reference algorithm
-(oracle/, the reference itself is pure Python and not buildable) on all host
-cores on a bounded sample of the same workload.
+(oracle/osim_oracle.c, bit-exact with the reference) on all host cores on a
+bounded sample of the same workload, stratified over the whole 12! space.
+`cpu_baseline.python` times the unmodified Python reference itself
+(baseline/_ref, tools/install_reference.sh) on strided C4 ranks, one process
+per host core.
 """
 
 from __future__ import annotations
@@ -576,9 +579,27 @@ def run_rows(a, cpu):
 
 
 # ---------------------------------------------------------------- CPU legs
+STRATA = 64  # rank windows per CPU step, evenly spaced over all of 12!
+
+
+def strata(m, k=0):
+    """`m` C4 ranks as STRATA equal windows starting at i * 12!/STRATA,
+    shifted by step index k (every window samples a different first task)."""
+    w = max(1, m // STRATA)
+    base = TOTAL12 // STRATA
+    return [(i * base + k * w, i * base + (k + 1) * w) for i in range(STRATA)], w * STRATA
+
+
+def port_windows(d, windows, threads):
+    from oracle import oracle as O
+
+    for lo, hi in windows:
+        O.exhaustive(d, DMA, SIGMA, lo, hi, threads=threads)
+
+
 def cpu_rate(seconds):
-    """CPU restatement (oracle/, all host threads) on contiguous C4 ranks,
-    sized to ~`seconds` of wall time."""
+    """CPU restatement (oracle/, all host threads) on C4 ranks in STRATA
+    windows spread over the whole 12! space, sized to ~`seconds`."""
     from oracle import oracle as O
     from paper_1806_10113_b200 import synth
 
@@ -588,12 +609,73 @@ def cpu_rate(seconds):
     t0 = time.perf_counter()
     O.exhaustive(d, DMA, SIGMA, 0, probe, threads=threads)
     rate = probe / (time.perf_counter() - t0)
-    m = int(max(probe, min(TOTAL12 // 2, rate * seconds)))
-    start = TOTAL12 // 3  # a mid-space window
+    wins, m = strata(int(max(probe, min(TOTAL12 // 2, rate * seconds))))
     t0 = time.perf_counter()
-    O.exhaustive(d, DMA, SIGMA, start, start + m, threads=threads)
+    port_windows(d, wins, threads)
     el = time.perf_counter() - t0
-    return m / el, threads, m, start
+    return m / el, threads, m, wins
+
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _py_ref_worker(ranks):
+    """Unmodified reference (baseline/_ref offsim): engine.simulate of each
+    ordering, the body of exhaustive_search's loop (oracle.py:132-135)."""
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    from offsim import engine
+    from offsim.cli import load_profile_arg
+    from offsim.workload import sample_real_tasks
+
+    tasks = sample_real_tasks("AMD", 12, seed=12)
+    prof = load_profile_arg("2dma")
+    out = []
+    for r in ranks:
+        avail = list(range(N12))
+        perm = []
+        for i in range(N12, 0, -1):  # Lehmer unrank (itertools.permutations order)
+            f = math.factorial(i - 1)
+            perm.append(avail.pop(r // f))
+            r %= f
+        out.append(engine.simulate([tasks[i] for i in perm], prof).makespan)
+    return out
+
+
+def python_reference_rate(seconds):
+    """The unmodified Python reference (tools/install_reference.sh ->
+    baseline/_ref) on C4 ranks strided over all of 12!, one process per host
+    core; its makespans are checked against the oracle port on the same ranks."""
+    if not os.path.isdir(os.path.join(REF_DIR, "offsim")):
+        return {"unavailable": "baseline/_ref/offsim missing (run tools/install_reference.sh)"}
+    import multiprocessing as mp
+
+    from oracle import oracle as O
+    from paper_1806_10113_b200 import synth
+
+    procs = os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        pool.map(_py_ref_worker, [[0]] * procs)  # imports and warm-up outside the timed region
+        t0 = time.perf_counter()
+        pool.map(_py_ref_worker, [[7 * k] for k in range(20 * procs)])
+        per = (time.perf_counter() - t0) / 20  # ~ seconds per ordering per process
+        m = int(max(procs * 10, min(2_000_000, procs * seconds / max(per, 1e-6))))
+        stride = TOTAL12 // m
+        ranks = [k * stride for k in range(m)]
+        chunks = [ranks[i::procs] for i in range(procs)]
+        t0 = time.perf_counter()
+        res = pool.map(_py_ref_worker, chunks)
+        el = time.perf_counter() - t0
+    ms = np.empty(m)
+    for i in range(procs):
+        ms[i::procs] = res[i]
+    perms = np.array([O.unrank(r, N12) for r in ranks], dtype=np.uint8)
+    _, oms = O.eval_perms(synth.c4_group(), DMA, SIGMA, perms, threads=procs)
+    return {"value": m / el, "unit": "orderings/s", "cores": procs, "kind": "python",
+            "sample": f"{m} C4 ranks k*{stride} (strided over all of 12!) through the unmodified reference "
+                      f"(baseline/_ref offsim.engine.simulate), {procs} processes",
+            "bit_exact_vs_port": bool(np.array_equal(ms, oms))}
 
 
 def cpu_heuristic_rate(seconds):
@@ -617,31 +699,31 @@ def cpu_heuristic_rate(seconds):
 
 
 def cpu_baseline(seconds):
-    v, threads, m, start = cpu_rate(seconds)
+    v, threads, m, wins = cpu_rate(seconds)
     return {"value": v, "unit": "orderings/s", "cores": threads, "kind": "port",
-            "sample": f"C4 ranks [{start}, {start + m}) ({m} of 12! orderings) through oracle/osim_oracle.c "
-                      f"(C restatement of engine.py/oracle.py; the reference is pure Python) on {threads} threads"}
+            "sample": f"{m} C4 ranks in {len(wins)} windows of {wins[0][1] - wins[0][0]} at i*12!/{len(wins)} "
+                      f"through oracle/osim_oracle.c (C restatement of engine.py/oracle.py) on {threads} threads",
+            "python": python_reference_rate(min(seconds, 10.0))}
 
 
 def run_reference(a):
     if env_int("RANK", 0) != 0:
         return
-    from oracle import oracle as O
     from paper_1806_10113_b200 import synth
 
     threads = os.cpu_count() or 1
     d = synth.c4_group()
-    v, _, m, start = cpu_rate(float(os.environ.get("OSIM_REF_STEP_SECONDS", "2.0")))  # each step ~2 s
-    for _ in range(a.warmup):
-        O.exhaustive(d, DMA, SIGMA, start, start + m // 4, threads=threads)
+    v, _, m, _ = cpu_rate(float(os.environ.get("OSIM_REF_STEP_SECONDS", "2.0")))  # each step ~2 s
+    for k in range(a.warmup):
+        port_windows(d, strata(m // 4, 1000 + k)[0], threads)
     t0 = time.perf_counter()
-    for k in range(a.steps):
-        lo = start + k * m
-        O.exhaustive(d, DMA, SIGMA, lo, lo + m, threads=threads)
+    for k in range(a.steps):  # step k: the STRATA windows shifted by k (distinct ranks every step)
+        port_windows(d, strata(m, k)[0], threads)
     el = time.perf_counter() - t0
     value = m * a.steps / el
-    sample = (f"C4 ranks [{start}, {start + m * a.steps}) in {a.steps} steps of {m} orderings through "
-              f"oracle/osim_oracle.c on {threads} threads")
+    sample = (f"{a.steps} steps of {m} C4 orderings, each in {STRATA} rank windows spread over all of 12! "
+              f"(window i of step k at i*12!/{STRATA} + k*{m // STRATA}), through oracle/osim_oracle.c on "
+              f"{threads} threads")
     print(json.dumps({
         "impl": "reference", "metric": "orderings simulated/sec", "value": value, "unit": "orderings/s",
         "n_gpus": env_int("WORLD_SIZE", 1), "steps": a.steps, "warmup": a.warmup,

@@ -147,7 +147,7 @@ int osim_timeline_deps(const double* durs, int n, int dma, double sigma, const u
 /* workload._run_heuristic_schedule (workload.py:197-256) for S independent
  * scenarios of T workers x N tasks: durs[S][T*N][3] (task (w, j) at w*N+j),
  * id_rank[S][T*N] = sorted() order of each scenario's task ids.  Outputs
- * makespan[S], n_groups[S], tg_sizes[S][T*N] (nullable; first n_groups entries, the rest 0;
+ * makespan[S], n_groups[S], tg_sizes[S][T*N] (nullable; first n_groups entries, the rest 0),
  * start/end[S][T*N][3] (nullable; -1 = null stage). */
 int osim_harness_batch(const double* durs, const uint8_t* id_rank, uint64_t S, int T, int N, int dma,
                        double sigma, int sum_mode, int n_dev, double* makespan, uint8_t* n_groups,
@@ -216,6 +216,39 @@ int osim_exhaustive_batch_dev(const double* d_durs, uint64_t B, int n, int dma, 
 int osim_heuristic_batch_dev(const double* d_durs, const uint8_t* d_id_rank, uint64_t B, int n,
                              int dma, double sigma, int sum_mode, int fast, uint8_t* d_order,
                              double* d_makespan, uint32_t* d_n_sims, void* stream);
+
+/* ---- groups of any size (uint32 task ids) ------------------------------ */
+/* The reference accepts task groups of any size; the uint8 entry points
+ * above take up to 64 tasks.  These run the general path (osim_big.cuh:
+ * FIFOs and done bits in per-simulation global-memory workspaces, IEEE
+ * division, bit-identical to the reference) for any n < 2^31, with the same
+ * argument meaning as their uint8 counterparts. */
+/* engine.simulate / workload.simulate_sequence (engine.py:252-263,
+ * workload.py:277-304): order[n], dep[n] (nullable; -1 = none), waves as in
+ * osim_timeline_deps. */
+int osim_timeline_u32(const double* durs, uint64_t n, int dma, double sigma, const uint32_t* order,
+                      const int32_t* dep, int waves, double* start, double* end, double* makespan,
+                      double* idle);
+/* sampled exhaustive_search (oracle.py:127-135): perms[cnt][n]. */
+int osim_eval_perms_u32(const double* durs, uint64_t n, int dma, double sigma, const uint32_t* perms,
+                        uint64_t cnt, int n_dev, double* makespans, osim_summary* out);
+/* NoReorder label sequences (workload.py:277-327): labels[cnt][T*N]. */
+int osim_eval_sequences_u32(const double* durs, uint32_t T, uint32_t N, int dma, double sigma,
+                            const uint32_t* labels, uint64_t cnt, int n_dev, double* makespans,
+                            osim_summary* out);
+/* reorder_batch (heuristic.py:105-125), n <= 65535: id_rank[B][n],
+ * order[B][n]; one CTA per group, a greedy round's candidates spread over
+ * its threads. */
+int osim_heuristic_batch_u32(const double* durs, const uint32_t* id_rank, uint64_t B, uint64_t n, int dma,
+                             double sigma, int sum_mode, int n_dev, uint32_t* order, double* makespan,
+                             uint32_t* n_sims);
+/* workload._run_heuristic_schedule (workload.py:197-256), T <= 65535. */
+int osim_harness_batch_u32(const double* durs, const uint32_t* id_rank, uint64_t S, uint32_t T, uint32_t N,
+                           int dma, double sigma, int sum_mode, int n_dev, double* makespan,
+                           uint32_t* n_groups, uint32_t* tg_sizes, double* start, double* end);
+/* oracle.micro_simulate (oracle.py:60-95). */
+int osim_micro_timeline_u32(const double* durs, uint64_t n, int dma, double sigma, double dt,
+                            const uint32_t* order, double* start, double* end, double* makespan);
 
 /* ---- diagnostics ------------------------------------------------------ */
 /* Compare the fast-path division with IEEE division on `samples` random

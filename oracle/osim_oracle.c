@@ -22,7 +22,8 @@
 #include <stdlib.h>
 #include <string.h>
 
-#define OR_MAXN 64
+#define OR_MAXN 320 /* tasks per group (stack arrays); the big.json goldens go to 300 */
+#define OR_MAXN8 256 /* entry points with uint8 task indices or id ranks */
 #define K_HTD 0 /* engine.py:18-21 KINDS = (HtD, K, DtH) */
 #define K_K 1
 #define K_DTH 2
@@ -447,7 +448,7 @@ int oracle_exhaustive(const double* durs, int n, int dma, double sigma, uint64_t
 
 int oracle_eval_perms(const double* durs, int n, int dma, double sigma, const uint8_t* perms,
                       uint64_t cnt, int threads, double* makespans, oracle_summary* out) {
-    if (n < 1 || n > OR_MAXN) return -1;
+    if (n < 1 || n > OR_MAXN8) return -1;
     return run_jobs(durs, n, dma, sigma, 0, cnt, perms, threads, makespans, out);
 }
 
@@ -594,7 +595,7 @@ static void list_remove(int* v, int* m, int x) {
 /* reorder_batch (heuristic.py:105-125) */
 int oracle_reorder(const double* durs, const uint8_t* id_rank, int n, int dma, double sigma,
                    int sum_mode, uint8_t* order, double* makespan, uint32_t* n_sims) {
-    if (n < 1 || n > OR_MAXN) return -1; /* :111-112 */
+    if (n < 1 || n > OR_MAXN8) return -1; /* :111-112 */
     hctx h = {durs, id_rank, n, dma, sigma, sum_mode, 0, 0};
     int ot[OR_MAXN] = {0}, k = 0;
     if (n == 1) {

@@ -29,7 +29,8 @@ EXPORTS = (
     "osim_exhaustive_ex_dev", "osim_radix_hist_dev", "osim_interleavings", "osim_eval_sequences",
     "osim_timeline_deps", "osim_micro", "osim_micro_timeline", "osim_harness_batch",
     "osim_exhaustive_shard_dev", "osim_exhaustive_shard", "osim_select_kth_dev",
-    "osim_pfx_suffix_len",
+    "osim_pfx_suffix_len", "osim_timeline_u32", "osim_eval_perms_u32", "osim_eval_sequences_u32",
+    "osim_heuristic_batch_u32", "osim_harness_batch_u32", "osim_micro_timeline_u32",
 )
 
 
@@ -79,6 +80,7 @@ def load(path: str = LIB_PATH):
                 "(there is no CPU fallback)")
         L = C.CDLL(path)
         dp, u8p, u32p, vp = C.POINTER(C.c_double), C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.c_void_p
+        i32p = C.POINTER(C.c_int32)
         sp = C.POINTER(OsimSummary)
         i, d, u64 = C.c_int, C.c_double, C.c_uint64
         sig = {
@@ -104,6 +106,13 @@ def load(path: str = LIB_PATH):
             "osim_radix_hist_dev": ([vp, u64, u64, i, i, vp, vp], i),
             "osim_select_kth_dev": ([vp, u64, u64, dp, vp], i),
             "osim_pfx_suffix_len": ([i], i),
+            "osim_timeline_u32": ([dp, u64, i, d, u32p, i32p, i, dp, dp, dp, dp], i),
+            "osim_eval_perms_u32": ([dp, u64, i, d, u32p, u64, i, dp, sp], i),
+            "osim_eval_sequences_u32": ([dp, C.c_uint32, C.c_uint32, i, d, u32p, u64, i, dp, sp], i),
+            "osim_heuristic_batch_u32": ([dp, u32p, u64, u64, i, d, i, i, u32p, dp, u32p], i),
+            "osim_harness_batch_u32": ([dp, u32p, u64, C.c_uint32, C.c_uint32, i, d, i, i, dp, u32p, u32p, dp, dp],
+                                       i),
+            "osim_micro_timeline_u32": ([dp, u64, i, d, d, u32p, dp, dp, dp], i),
             "osim_interleavings": ([dp, i, i, i, d, u64, u64, d, i, sp, C.POINTER(u64), dp], i),
             "osim_eval_sequences": ([dp, i, i, i, d, u8p, u64, i, dp, sp], i),
             "osim_micro": ([dp, i, i, d, d, u64, u64, i, dp], i),
@@ -201,9 +210,24 @@ def select_kth_dev(d_vals_ptr: int, count: int, k: int, stream: int = 0) -> floa
     return out.value
 
 
+WIDE_MAX = 64  # largest group of the uint8 entry points; above: the *_u32 general path (osim_big.cuh)
+
+
+def u32(a, shape=None) -> np.ndarray:
+    x = np.ascontiguousarray(np.asarray(a, dtype=np.uint32))
+    return x.reshape(shape) if shape is not None else x
+
+
 def eval_perms(durs, dma, sigma, perms, n_dev=1):
     d = f64(durs, (-1, 3))
     n = d.shape[0]
+    if n > WIDE_MAX:
+        p = u32(perms, (-1, n))
+        ms = np.empty(p.shape[0])
+        out = OsimSummary()
+        check(load().osim_eval_perms_u32(ptr(d, C.c_double), n, int(dma), float(sigma), ptr(p, C.c_uint32),
+                                         p.shape[0], int(n_dev), ptr(ms, C.c_double), C.byref(out)))
+        return out.as_dict(), ms
     p = u8(perms, (-1, n))
     ms = np.empty(p.shape[0])
     out = OsimSummary()
@@ -223,8 +247,18 @@ def exhaustive_batch(durs, dma, sigma, n_dev=1, out=None):
 
 
 def heuristic_batch(durs, id_rank, dma, sigma, sum_mode, n_dev=1, order=None, makespan=None, n_sims=None):
+    """(order [B][n] (uint8; uint32 above 64 tasks), makespan [B], n_sims [B])."""
     d = durs if isinstance(durs, np.ndarray) and durs.dtype == np.float64 and durs.flags.c_contiguous else f64(durs)
     B, n = d.shape[0], d.shape[1]
+    if n > WIDE_MAX:
+        r = u32(id_rank, (B, n))
+        order = np.empty((B, n), dtype=np.uint32) if order is None else order
+        makespan = np.empty(B) if makespan is None else makespan
+        n_sims = np.empty(B, dtype=np.uint32) if n_sims is None else n_sims
+        check(load().osim_heuristic_batch_u32(ptr(d, C.c_double), ptr(r, C.c_uint32), B, n, int(dma), float(sigma),
+                                              int(sum_mode), int(n_dev), ptr(order, C.c_uint32),
+                                              ptr(makespan, C.c_double), ptr(n_sims, C.c_uint32)))
+        return order, makespan, n_sims
     r = u8(id_rank, (B, n))
     order = np.empty((B, n), dtype=np.uint8) if order is None else order
     makespan = np.empty(B) if makespan is None else makespan
@@ -238,6 +272,8 @@ def heuristic_batch(durs, id_rank, dma, sigma, sum_mode, n_dev=1, order=None, ma
 def timeline(durs, dma, sigma, order):
     d = f64(durs, (-1, 3))
     n = d.shape[0]
+    if n > WIDE_MAX:
+        return timeline_deps(d, dma, sigma, order)
     o = u8(order)
     st = np.empty((n, 3))
     en = np.empty((n, 3))
@@ -278,6 +314,14 @@ def interleavings(durs, T, N, dma, sigma, lo, hi, threshold=float("-inf"), n_dev
 
 def eval_sequences(durs, T, N, dma, sigma, labels, n_dev=1):
     d = f64(durs, (-1, 3))
+    if T * N > WIDE_MAX:
+        lab = u32(labels, (-1, T * N))
+        ms = np.empty(lab.shape[0])
+        out = OsimSummary()
+        check(load().osim_eval_sequences_u32(ptr(d, C.c_double), int(T), int(N), int(dma), float(sigma),
+                                             ptr(lab, C.c_uint32), lab.shape[0], int(n_dev), ptr(ms, C.c_double),
+                                             C.byref(out)))
+        return out.as_dict(), ms
     lab = u8(labels, (-1, T * N))
     ms = np.empty(lab.shape[0])
     out = OsimSummary()
@@ -290,10 +334,17 @@ def eval_sequences(durs, T, N, dma, sigma, labels, n_dev=1):
 def timeline_deps(durs, dma, sigma, order, dep=None, waves=False):
     d = f64(durs, (-1, 3))
     n = d.shape[0]
-    o = u8(order)
-    dp_ = None if dep is None else np.ascontiguousarray(np.asarray(dep, dtype=np.int8))
     st, en, idle = np.empty((n, 3)), np.empty((n, 3)), np.empty(3)
     ms = C.c_double()
+    if n > WIDE_MAX:
+        o = u32(order)
+        dp_ = None if dep is None else np.ascontiguousarray(np.asarray(dep, dtype=np.int32))
+        check(load().osim_timeline_u32(ptr(d, C.c_double), n, int(dma), float(sigma), ptr(o, C.c_uint32),
+                                       ptr(dp_, C.c_int32) if dp_ is not None else None, int(bool(waves)),
+                                       ptr(st, C.c_double), ptr(en, C.c_double), C.byref(ms), ptr(idle, C.c_double)))
+        return st, en, ms.value, idle
+    o = u8(order)
+    dp_ = None if dep is None else np.ascontiguousarray(np.asarray(dep, dtype=np.int8))
     check(load().osim_timeline_deps(ptr(d, C.c_double), n, int(dma), float(sigma), ptr(o, C.c_uint8),
                                     ptr(dp_, C.c_int8) if dp_ is not None else None, int(bool(waves)),
                                     ptr(st, C.c_double), ptr(en, C.c_double), C.byref(ms), ptr(idle, C.c_double)))
@@ -311,6 +362,14 @@ def micro(durs, dma, sigma, dt, lo, hi, n_dev=1):
 def micro_timeline(durs, dma, sigma, dt, order):
     d = f64(durs, (-1, 3))
     n = d.shape[0]
+    if n > 16:  # above the 4-bit kernels: osim_micro_timeline_u32
+        o = u32(order)
+        st, en = np.empty((n, 3)), np.empty((n, 3))
+        ms = C.c_double()
+        check(load().osim_micro_timeline_u32(ptr(d, C.c_double), n, int(dma), float(sigma), float(dt),
+                                             ptr(o, C.c_uint32), ptr(st, C.c_double), ptr(en, C.c_double),
+                                             C.byref(ms)))
+        return st, en, ms.value
     o = u8(order)
     st, en = np.empty((n, 3)), np.empty((n, 3))
     ms = C.c_double()
@@ -320,9 +379,23 @@ def micro_timeline(durs, dma, sigma, dt, order):
 
 
 def harness_batch(durs, id_rank, T, N, dma, sigma, sum_mode, n_dev=1, timeline=False):
-    """(makespan [S], n_groups [S], tg_sizes [S][T*N], start/end [S][T*N][3] or None)."""
+    """(makespan [S], n_groups [S], tg_sizes [S][T*N], start/end [S][T*N][3] or None);
+    n_groups / tg_sizes are uint8, uint32 above 64 tasks."""
     d = f64(durs).reshape(-1, T * N, 3)
     S = d.shape[0]
+    if T * N > WIDE_MAX:
+        r = u32(id_rank, (S, T * N))
+        ms = np.empty(S)
+        ng = np.empty(S, dtype=np.uint32)
+        sz = np.zeros((S, T * N), dtype=np.uint32)
+        st = np.empty((S, T * N, 3)) if timeline else None
+        en = np.empty((S, T * N, 3)) if timeline else None
+        check(load().osim_harness_batch_u32(ptr(d, C.c_double), ptr(r, C.c_uint32), S, int(T), int(N), int(dma),
+                                            float(sigma), int(sum_mode), int(n_dev), ptr(ms, C.c_double),
+                                            ptr(ng, C.c_uint32), ptr(sz, C.c_uint32),
+                                            ptr(st, C.c_double) if timeline else None,
+                                            ptr(en, C.c_double) if timeline else None))
+        return ms, ng, sz, st, en
     r = u8(id_rank, (S, T * N))
     ms = np.empty(S)
     ng = np.empty(S, dtype=np.uint8)

@@ -187,6 +187,18 @@ int scan_durs(const double* durs, uint64_t tasks, double sigma, int* fast) {
 
 int check_durs(const double* durs, uint64_t tasks) { return scan_durs(durs, tasks, 1.0, nullptr); }
 
+// micro_simulate resolves stage times without DeviceSim.submit's checks
+// (oracle.py:72-76): a task without commands is allowed (it has no queue
+// entries); durations must still be finite and non-negative
+int check_durs_micro(const double* durs, uint64_t tasks) {
+    if (!durs) return fail(OSIM_EINVAL, "durations pointer is NULL");
+    for (uint64_t i = 0; i < 3 * tasks; ++i)
+        if (!(durs[i] >= 0.0 && durs[i] < HUGE_VAL))
+            return fail(OSIM_EINVAL, "task %llu: durations must be finite and non-negative",
+                        (unsigned long long)(i / 3));
+    return 0;
+}
+
 // each row of id ranks must be a permutation of range(n) (unique ids)
 int check_id_ranks(const uint8_t* id_rank, uint64_t B, int n) {
     unsigned nt = B >= (1ull << 16) ? std::thread::hardware_concurrency() : 1u;
@@ -1447,7 +1459,7 @@ int osim_micro(const double* durs, int n, int dma, double sigma, double dt, uint
     int rc = check_common(n, dma, sigma);
     if (rc) return rc;
     if (!(dt > 0.0)) return fail(OSIM_EINVAL, "dt must be positive");
-    if ((rc = check_durs(durs, (uint64_t)n))) return rc;
+    if ((rc = check_durs_micro(durs, (uint64_t)n))) return rc;
     if (!makespans && rank_hi > rank_lo) return fail(OSIM_EINVAL, "makespans is NULL");
     if (rank_lo > rank_hi || rank_hi > factorial(n)) return fail(OSIM_EINVAL, "bad rank range");
     const long long mt = micro_max_ticks(durs, n, sigma, dt);
@@ -1494,7 +1506,7 @@ int osim_micro_timeline(const double* durs, int n, int dma, double sigma, double
     int rc = check_common(n, dma, sigma);
     if (rc) return rc;
     if (!(dt > 0.0)) return fail(OSIM_EINVAL, "dt must be positive");
-    if ((rc = check_durs(durs, (uint64_t)n))) return rc;
+    if ((rc = check_durs_micro(durs, (uint64_t)n))) return rc;
     if (!order || !start || !end) return fail(OSIM_EINVAL, "NULL buffer");
     unsigned seen = 0;
     for (int j = 0; j < n; ++j) {
@@ -1655,6 +1667,405 @@ int osim_fp64_peak(double* tflops) {
     cudaEventDestroy(e1);
     const double flops = 2.0 * 8 * 16 * (double)iters * blocks * threads;
     if (tflops) *tflops = flops / (best * 1e-3) / 1e12;
+    return 0;
+}
+
+}  // extern "C"
+
+// ---- groups of any size (osim_big.cuh): uint32 task ids -------------------
+//
+// The reference takes groups of any size (engine.py:252-263, oracle.py:127-135,
+// heuristic.py:105-125, workload.py:197-304, oracle.py:60-95).  Up to 64
+// tasks the uint8 entry points above run the register / byte-FIFO kernels;
+// these entry points run BigSim with per-simulation workspaces in global
+// memory for any n (ids below 2^31).
+
+namespace {
+
+int check_big(uint64_t n, int dma, double sigma) {
+    if (n < 1) return fail(OSIM_EINVAL, "task group must be non-empty");
+    if (n >= (1ull << 31)) return fail(OSIM_EINVAL, "n=%llu exceeds 2^31 - 1 tasks", (unsigned long long)n);
+    if (dma != 1 && dma != 2) return fail(OSIM_EINVAL, "dma_engines must be 1 or 2, got %d", dma);
+    if (!(sigma > 0.0 && sigma <= 1.0)) return fail(OSIM_EINVAL, "overlap_sigma must be in (0, 1]");
+    return 0;
+}
+
+// rows of `width` uint32 values must each be a permutation of range(width)
+int check_perm_rows(const uint32_t* v, uint64_t rows, uint64_t width, const char* what) {
+    std::vector<uint64_t> stamp(width, ~0ull);
+    for (uint64_t r = 0; r < rows; ++r)
+        for (uint64_t j = 0; j < width; ++j) {
+            const uint64_t x = v[r * width + j];
+            if (x >= width || stamp[x] == r)
+                return fail(OSIM_EINVAL, "%s row %llu is not a permutation of range(%llu)", what,
+                            (unsigned long long)r, (unsigned long long)width);
+            stamp[x] = r;
+        }
+    return 0;
+}
+
+// workspace budget of one big launch (per device), bytes
+uint64_t big_budget() {
+    static const uint64_t b = [] {
+        const char* e = std::getenv("OSIM_BIG_WS_MB");  // testing / tuning only
+        const long long mb = e ? std::atoll(e) : 0;
+        return (uint64_t)(mb > 0 ? mb : 2048) << 20;
+    }();
+    return b;
+}
+
+// threads (a multiple of the block) whose per-thread workspaces of `per`
+// bytes fit the budget, at most enough for `work` items and 8 CTAs per SM
+int big_threads(const DevCtx* c, uint64_t per, uint64_t work, uint64_t* threads) {
+    const uint64_t blk = (uint64_t)big_block();
+    uint64_t t = big_budget() / (per ? per : 1);
+    const uint64_t cap = (uint64_t)c->sms * 8 * blk;
+    if (t > cap) t = cap;
+    const uint64_t need = ((work + blk - 1) / blk) * blk;
+    if (t > need) t = need;
+    t = (t / blk) * blk;
+    if (t == 0) {
+        if (per > (16ull << 30)) return fail(OSIM_EINVAL, "workspace of %llu bytes per simulation is too large",
+                                             (unsigned long long)per);
+        t = blk;  // one CTA even above the budget
+    }
+    *threads = t;
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int osim_timeline_u32(const double* durs, uint64_t n, int dma, double sigma, const uint32_t* order,
+                      const int32_t* dep, int waves, double* start, double* end, double* makespan, double* idle) {
+    int rc = check_big(n, dma, sigma);
+    if (rc) return rc;
+    if ((rc = check_durs(durs, n))) return rc;
+    if (!order || !start || !end) return fail(OSIM_EINVAL, "NULL buffer");
+    if ((rc = check_perm_rows(order, 1, n, "order"))) return rc;
+    if (dep)
+        for (uint64_t t = 0; t < n; ++t)
+            if (dep[t] < -1 || dep[t] >= (int64_t)n || dep[t] == (int64_t)t)
+                return fail(OSIM_EINVAL, "bad dependency of task %llu", (unsigned long long)t);
+    DevList dl;
+    if ((rc = pick_devs(1, dl))) return rc;
+    DevCtx* c = dl.v[0];
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->dev));
+    const size_t off_o = align_up(3 * n * sizeof(double));
+    const size_t off_dp = off_o + align_up(n * sizeof(uint32_t));
+    const size_t off_s = off_dp + align_up(n * sizeof(int32_t));
+    const size_t off_e = off_s + align_up(3 * n * sizeof(double));
+    const size_t off_r = off_e + align_up(3 * n * sizeof(double));
+    const size_t off_ws = off_r + 256;
+    void* base;
+    if ((rc = scratch(c, off_ws + big_sim_bytes(n), &base))) return rc;
+    char* b = (char*)base;
+    CK(cudaMemcpyAsync(b, durs, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(b + off_o, order, n * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+    if (dep) CK(cudaMemcpyAsync(b + off_dp, dep, n * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+    big_timeline_launch(dma, c->stream, (double*)b, n, sigma, (uint32_t*)(b + off_o),
+                        dep ? (int32_t*)(b + off_dp) : nullptr, waves, (uint8_t*)(b + off_ws), (double*)(b + off_s),
+                        (double*)(b + off_e), (double*)(b + off_r), c->d_err);
+    CK(cudaGetLastError());
+    double res4[4];
+    CK(cudaMemcpyAsync(start, b + off_s, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(end, b + off_e, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(res4, b + off_r, sizeof(res4), cudaMemcpyDeviceToHost, c->stream));
+    if ((rc = finish(c, c->stream))) return rc;
+    if (makespan) *makespan = res4[0];
+    if (idle) { idle[0] = res4[1]; idle[1] = res4[2]; idle[2] = res4[3]; }
+    return 0;
+}
+
+int osim_eval_perms_u32(const double* durs, uint64_t n, int dma, double sigma, const uint32_t* perms, uint64_t cnt,
+                        int n_dev, double* makespans, osim_summary* out) {
+    int rc = check_big(n, dma, sigma);
+    if (rc) return rc;
+    if ((rc = check_durs(durs, n))) return rc;
+    if (cnt && (!perms || !makespans)) return fail(OSIM_EINVAL, "NULL buffer");
+    if ((rc = check_perm_rows(perms, cnt, n, "perms"))) return rc;
+    DevList dl;
+    if ((rc = pick_devs(n_dev, dl))) return rc;
+    const int G = (int)dl.v.size();
+    std::vector<osim_summary> res(G);
+    std::vector<std::unique_lock<std::mutex>> locks;
+    const uint64_t wsb = big_sim_bytes(n);
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        locks.emplace_back(c->mu);
+        CK(cudaSetDevice(c->dev));
+        const uint64_t lo = cnt * (uint64_t)gi / (uint64_t)G, hi = cnt * (uint64_t)(gi + 1) / (uint64_t)G;
+        const uint64_t m = hi - lo;
+        uint64_t threads = 0;
+        if ((rc = big_threads(c, wsb, m, &threads))) return rc;
+        const int grid = m ? (int)(threads / (uint64_t)big_block()) : 0;
+        const size_t off_parts = align_up(3 * n * sizeof(double));
+        const size_t off_sum = off_parts + align_up((grid + 1) * sizeof(Part));
+        const size_t off_ms = off_sum + align_up(sizeof(osim_summary));
+        const size_t off_p = off_ms + align_up(m * sizeof(double) + 8);
+        const size_t off_ws = off_p + align_up(m * n * sizeof(uint32_t) + 8);
+        void* base;
+        if ((rc = scratch(c, off_ws + (m ? threads * wsb : 0), &base))) return rc;
+        char* b = (char*)base;
+        CK(cudaMemcpyAsync(b, durs, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        Part* parts = (Part*)(b + off_parts);
+        if (m) {
+            CK(cudaMemcpyAsync(b + off_p, perms + lo * n, m * n * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                               c->stream));
+            big_eval_perms_launch(dma, c->stream, grid, (double*)b, n, sigma, (uint32_t*)(b + off_p), m,
+                                  (uint8_t*)(b + off_ws), wsb, (double*)(b + off_ms), parts, c->d_err);
+        }
+        k_final_reduce<<<1, kBlock, 0, c->stream>>>(parts, grid, (osim_summary*)(b + off_sum), nullptr);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&res[gi], b + off_sum, sizeof(osim_summary), cudaMemcpyDeviceToHost, c->stream));
+        if (m) CK(cudaMemcpyAsync(makespans + lo, b + off_ms, m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    }
+    osim_summary acc;
+    memset(&acc, 0, sizeof(acc));
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        CK(cudaSetDevice(c->dev));
+        if ((rc = finish(c, c->stream))) return rc;
+        res[gi].best_rank += cnt * (uint64_t)gi / (uint64_t)G;  // device-local indices -> list indices
+        merge_host(acc, res[gi]);
+    }
+    if (out) *out = acc;
+    return 0;
+}
+
+int osim_eval_sequences_u32(const double* durs, uint32_t T, uint32_t N, int dma, double sigma, const uint32_t* labels,
+                            uint64_t cnt, int n_dev, double* makespans, osim_summary* out) {
+    if (T < 1 || N < 1) return fail(OSIM_EINVAL, "T and N must be at least 1");
+    const uint64_t n = (uint64_t)T * N;
+    int rc = check_big(n, dma, sigma);
+    if (rc) return rc;
+    if ((rc = check_durs(durs, n))) return rc;
+    if (cnt && (!labels || !makespans)) return fail(OSIM_EINVAL, "NULL buffer");
+    {
+        std::vector<uint32_t> cw(T);
+        for (uint64_t i = 0; i < cnt; ++i) {  // each row: every worker exactly N times
+            std::fill(cw.begin(), cw.end(), 0u);
+            for (uint64_t p = 0; p < n; ++p) {
+                const uint32_t w = labels[i * n + p];
+                if (w >= T || ++cw[w] > N)
+                    return fail(OSIM_EINVAL, "row %llu is not an interleaving of %u workers x %u tasks",
+                                (unsigned long long)i, T, N);
+            }
+        }
+    }
+    std::vector<int32_t> dep(n);  // task (w, j) = w*N + j waits for (w, j-1) (workload.py:311-315)
+    for (uint64_t t = 0; t < n; ++t) dep[t] = (t % N) ? (int32_t)(t - 1) : -1;
+    DevList dl;
+    if ((rc = pick_devs(n_dev, dl))) return rc;
+    const int G = (int)dl.v.size();
+    std::vector<osim_summary> res(G);
+    std::vector<std::unique_lock<std::mutex>> locks;
+    const uint64_t wsb = big_sim_bytes(n) + align_up((n + T) * sizeof(uint32_t));
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        locks.emplace_back(c->mu);
+        CK(cudaSetDevice(c->dev));
+        const uint64_t lo = cnt * (uint64_t)gi / (uint64_t)G, hi = cnt * (uint64_t)(gi + 1) / (uint64_t)G;
+        const uint64_t m = hi - lo;
+        uint64_t threads = 0;
+        if ((rc = big_threads(c, wsb, m, &threads))) return rc;
+        const int grid = m ? (int)(threads / (uint64_t)big_block()) : 0;
+        const size_t off_dep = align_up(3 * n * sizeof(double));
+        const size_t off_parts = off_dep + align_up(n * sizeof(int32_t));
+        const size_t off_sum = off_parts + align_up((grid + 1) * sizeof(Part));
+        const size_t off_ms = off_sum + align_up(sizeof(osim_summary));
+        const size_t off_l = off_ms + align_up(m * sizeof(double) + 8);
+        const size_t off_ws = off_l + align_up(m * n * sizeof(uint32_t) + 8);
+        void* base;
+        if ((rc = scratch(c, off_ws + (m ? threads * wsb : 0), &base))) return rc;
+        char* b = (char*)base;
+        CK(cudaMemcpyAsync(b, durs, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(b + off_dep, dep.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+        Part* parts = (Part*)(b + off_parts);
+        if (m) {
+            CK(cudaMemcpyAsync(b + off_l, labels + lo * n, m * n * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                               c->stream));
+            big_eval_labels_launch(dma, c->stream, grid, (double*)b, T, N, sigma, (uint32_t*)(b + off_l), m,
+                                   (int32_t*)(b + off_dep), (uint8_t*)(b + off_ws), wsb, (double*)(b + off_ms), parts,
+                                   c->d_err);
+        }
+        k_final_reduce<<<1, kBlock, 0, c->stream>>>(parts, grid, (osim_summary*)(b + off_sum), nullptr);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&res[gi], b + off_sum, sizeof(osim_summary), cudaMemcpyDeviceToHost, c->stream));
+        if (m) CK(cudaMemcpyAsync(makespans + lo, b + off_ms, m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    }
+    osim_summary acc;
+    memset(&acc, 0, sizeof(acc));
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        CK(cudaSetDevice(c->dev));
+        if ((rc = finish(c, c->stream))) return rc;
+        res[gi].best_rank += cnt * (uint64_t)gi / (uint64_t)G;
+        merge_host(acc, res[gi]);
+    }
+    if (out) *out = acc;
+    return 0;
+}
+
+int osim_heuristic_batch_u32(const double* durs, const uint32_t* id_rank, uint64_t B, uint64_t n, int dma,
+                             double sigma, int sum_mode, int n_dev, uint32_t* order, double* makespan,
+                             uint32_t* n_sims) {
+    int rc = check_big(n, dma, sigma);
+    if (rc) return rc;
+    if (n > 65535) return fail(OSIM_EINVAL, "n=%llu: the heuristic is limited to 65535 tasks per group",
+                               (unsigned long long)n);
+    if (B && (!durs || !id_rank || !order || !makespan)) return fail(OSIM_EINVAL, "NULL buffer");
+    if ((rc = check_durs(durs, B * n))) return rc;
+    if ((rc = check_perm_rows(id_rank, B, n, "id_rank"))) return rc;
+    DevList dl;
+    if ((rc = pick_devs(n_dev, dl))) return rc;
+    const int G = (int)dl.v.size();
+    std::vector<std::unique_lock<std::mutex>> locks;
+    const uint64_t per_cta = big_heur_bytes_per_cta(n);
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        locks.emplace_back(c->mu);
+        CK(cudaSetDevice(c->dev));
+        const uint64_t lo = B * (uint64_t)gi / (uint64_t)G, hi = B * (uint64_t)(gi + 1) / (uint64_t)G;
+        const uint64_t m = hi - lo;
+        if (!m) continue;
+        uint64_t grid = big_budget() / per_cta;
+        if (grid > (uint64_t)c->sms * 4) grid = (uint64_t)c->sms * 4;
+        if (grid > m) grid = m;
+        if (grid < 1) grid = 1;
+        const size_t off_idr = align_up(m * 3 * n * sizeof(double));
+        const size_t off_ord = off_idr + align_up(m * n * sizeof(uint32_t));
+        const size_t off_ms = off_ord + align_up(m * n * sizeof(uint32_t));
+        const size_t off_ns = off_ms + align_up(m * sizeof(double));
+        const size_t off_ws = off_ns + align_up(m * sizeof(uint32_t));
+        void* base;
+        if ((rc = scratch(c, off_ws + grid * per_cta, &base))) return rc;
+        char* b = (char*)base;
+        CK(cudaMemcpyAsync(b, durs + lo * 3 * n, m * 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(b + off_idr, id_rank + lo * n, m * n * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                           c->stream));
+        big_heuristic_launch(dma, c->stream, (int)grid, (double*)b, (uint32_t*)(b + off_idr), m, n, sigma, sum_mode,
+                             (uint8_t*)(b + off_ws), (uint32_t*)(b + off_ord), (double*)(b + off_ms),
+                             (uint32_t*)(b + off_ns), c->d_err);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(order + lo * n, b + off_ord, m * n * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(makespan + lo, b + off_ms, m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        if (n_sims)
+            CK(cudaMemcpyAsync(n_sims + lo, b + off_ns, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    }
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        CK(cudaSetDevice(c->dev));
+        if ((rc = finish(c, c->stream))) return rc;
+    }
+    return 0;
+}
+
+int osim_harness_batch_u32(const double* durs, const uint32_t* id_rank, uint64_t S, uint32_t T, uint32_t N, int dma,
+                           double sigma, int sum_mode, int n_dev, double* makespan, uint32_t* n_groups,
+                           uint32_t* tg_sizes, double* start, double* end) {
+    if (T < 1 || N < 1) return fail(OSIM_EINVAL, "T and N must be at least 1");
+    const uint64_t n = (uint64_t)T * N;
+    int rc = check_big(n, dma, sigma);
+    if (rc) return rc;
+    if (T > 65535) return fail(OSIM_EINVAL, "T=%u: at most 65535 workers", T);
+    if ((rc = check_durs(durs, S * n))) return rc;
+    if (S && (!id_rank || !makespan || !n_groups)) return fail(OSIM_EINVAL, "NULL buffer");
+    if ((rc = check_perm_rows(id_rank, S, n, "id_rank"))) return rc;
+    DevList dl;
+    if ((rc = pick_devs(n_dev, dl))) return rc;
+    const int G = (int)dl.v.size();
+    std::vector<std::unique_lock<std::mutex>> locks;
+    const uint64_t per = big_harness_bytes_per_thread(T, N);
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        locks.emplace_back(c->mu);
+        CK(cudaSetDevice(c->dev));
+        const uint64_t lo = S * (uint64_t)gi / (uint64_t)G, hi = S * (uint64_t)(gi + 1) / (uint64_t)G;
+        const uint64_t m = hi - lo;
+        if (!m) continue;
+        uint64_t threads = 0;
+        if ((rc = big_threads(c, per, m, &threads))) return rc;
+        const int grid = (int)(threads / (uint64_t)big_block());
+        const bool tl = start && end;
+        const size_t off_r = align_up(m * n * 3 * sizeof(double));
+        const size_t off_ms = off_r + align_up(m * n * sizeof(uint32_t));
+        const size_t off_ng = off_ms + align_up(m * sizeof(double));
+        const size_t off_sz = off_ng + align_up(m * sizeof(uint32_t));
+        const size_t off_st = off_sz + align_up(m * n * sizeof(uint32_t));
+        const size_t off_en = off_st + (tl ? align_up(m * n * 3 * sizeof(double)) : 0);
+        const size_t off_ws = off_en + (tl ? align_up(m * n * 3 * sizeof(double)) : 0);
+        void* base;
+        if ((rc = scratch(c, off_ws + threads * per, &base))) return rc;
+        char* b = (char*)base;
+        CK(cudaMemcpyAsync(b, durs + lo * n * 3, m * n * 3 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(b + off_r, id_rank + lo * n, m * n * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemsetAsync(b + off_sz, 0, m * n * sizeof(uint32_t), c->stream));
+        double* d_st = tl ? (double*)(b + off_st) : nullptr;
+        double* d_en = tl ? (double*)(b + off_en) : nullptr;
+        big_harness_launch(dma, c->stream, grid, (double*)b, (uint32_t*)(b + off_r), m, T, N, sigma, sum_mode,
+                           (uint8_t*)(b + off_ws), (double*)(b + off_ms), (uint32_t*)(b + off_ng),
+                           (uint32_t*)(b + off_sz), d_st, d_en, c->d_err);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(makespan + lo, b + off_ms, m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(n_groups + lo, b + off_ng, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+        if (tg_sizes)
+            CK(cudaMemcpyAsync(tg_sizes + lo * n, b + off_sz, m * n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                               c->stream));
+        if (tl) {
+            CK(cudaMemcpyAsync(start + lo * n * 3, d_st, m * n * 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(end + lo * n * 3, d_en, m * n * 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        }
+    }
+    for (int gi = 0; gi < G; ++gi) {
+        DevCtx* c = dl.v[gi];
+        CK(cudaSetDevice(c->dev));
+        if ((rc = finish(c, c->stream))) {
+            if (rc == OSIM_ESTALL) return fail(OSIM_ESTALL, "harness stalled with tasks remaining");
+            return rc;
+        }
+    }
+    return 0;
+}
+
+int osim_micro_timeline_u32(const double* durs, uint64_t n, int dma, double sigma, double dt, const uint32_t* order,
+                            double* start, double* end, double* makespan) {
+    int rc = check_big(n, dma, sigma);
+    if (rc) return rc;
+    if (!(dt > 0.0)) return fail(OSIM_EINVAL, "dt must be positive");
+    if ((rc = check_durs_micro(durs, n))) return rc;
+    if (!order || !start || !end) return fail(OSIM_EINVAL, "NULL buffer");
+    if ((rc = check_perm_rows(order, 1, n, "order"))) return rc;
+    double work = 0.0;  // every command runs at rate >= sigma: ticks <= total / (dt * sigma) + commands
+    for (uint64_t i = 0; i < 3 * n; ++i) work += durs[i] > 0.0 ? durs[i] : 0.0;
+    const double tk = work / (dt * sigma) + 3.0 * (double)n + 16.0;
+    if (tk > 4.0e9) return fail(OSIM_EINVAL, "dt too small (%.3g ticks)", tk);
+    const long long mt = (long long)tk;
+    DevList dl;
+    if ((rc = pick_devs(1, dl))) return rc;
+    DevCtx* c = dl.v[0];
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->dev));
+    const size_t off_o = align_up(3 * n * sizeof(double));
+    const size_t off_s = off_o + align_up(n * sizeof(uint32_t));
+    const size_t off_e = off_s + align_up(3 * n * sizeof(double));
+    const size_t off_r = off_e + align_up(3 * n * sizeof(double));
+    void* base;
+    if ((rc = scratch(c, off_r + 256, &base))) return rc;
+    char* b = (char*)base;
+    CK(cudaMemcpyAsync(b, durs, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(b + off_o, order, n * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+    big_micro_timeline_launch(dma, c->stream, (double*)b, n, sigma, dt, (uint32_t*)(b + off_o), mt,
+                              (double*)(b + off_s), (double*)(b + off_e), (double*)(b + off_r), c->d_err);
+    CK(cudaGetLastError());
+    double r0;
+    CK(cudaMemcpyAsync(start, b + off_s, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(end, b + off_e, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&r0, b + off_r, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if ((rc = finish(c, c->stream))) return rc;
+    if (makespan) *makespan = r0;
     return 0;
 }
 

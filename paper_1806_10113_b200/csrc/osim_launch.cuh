@@ -121,4 +121,29 @@ void wide_harness_launch(int dma, cudaStream_t st, const double* d_durs, const u
                          int N, double sigma, int sum_mode, double* d_ms, uint8_t* d_ng, uint8_t* d_sizes,
                          double* d_start, double* d_end, int* d_err);
 
+// groups of any size, general path (osim_big.cu): uint32 task ids, per-simulation
+// workspaces in global memory carved by the caller
+uint64_t big_sim_bytes(uint64_t n);
+uint64_t big_heur_bytes_per_cta(uint64_t n);
+uint64_t big_harness_bytes_per_thread(uint64_t T, uint64_t N);
+int big_block();
+void big_timeline_launch(int dma, cudaStream_t st, const double* d_durs, uint64_t n, double sigma,
+                         const uint32_t* d_order, const int32_t* d_dep, int waves, uint8_t* ws, double* d_start,
+                         double* d_end, double* d_res, int* d_err);
+void big_eval_perms_launch(int dma, cudaStream_t st, int grid, const double* d_durs, uint64_t n, double sigma,
+                           const uint32_t* d_perms, uint64_t cnt, uint8_t* ws, uint64_t wsb, double* d_ms,
+                           Part* parts, int* d_err);
+void big_eval_labels_launch(int dma, cudaStream_t st, int grid, const double* d_durs, uint32_t T, uint32_t N,
+                            double sigma, const uint32_t* d_labels, uint64_t cnt, const int32_t* d_dep, uint8_t* ws,
+                            uint64_t wsb, double* d_ms, Part* parts, int* d_err);
+void big_heuristic_launch(int dma, cudaStream_t st, int grid, const double* d_durs, const uint32_t* d_idr,
+                          uint64_t B, uint64_t n, double sigma, int sum_mode, uint8_t* ws, uint32_t* d_order,
+                          double* d_ms, uint32_t* d_ns, int* d_err);
+void big_harness_launch(int dma, cudaStream_t st, int grid, const double* d_durs, const uint32_t* d_idr, uint64_t S,
+                        uint32_t T, uint32_t N, double sigma, int sum_mode, uint8_t* ws, double* d_ms, uint32_t* d_ng,
+                        uint32_t* d_sizes, double* d_start, double* d_end, int* d_err);
+void big_micro_timeline_launch(int dma, cudaStream_t st, const double* d_durs, uint64_t n, double sigma, double dt,
+                               const uint32_t* d_order, long long max_ticks, double* d_start, double* d_end,
+                               double* d_res, int* d_err);
+
 }  // namespace osim

@@ -12,7 +12,7 @@ from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence, Tuple
 
 from . import _capi
-from .model import MAX_TASKS, DeviceProfile, TaskSpec, resolve_group
+from .model import DeviceProfile, TaskSpec, resolve_group
 
 KIND_HTD = "HtD"
 KIND_K = "K"
@@ -78,8 +78,6 @@ def _simulate(tasks: Sequence[TaskSpec], profile: DeviceProfile, deps: Optional[
               waves: bool) -> Timeline:
     """One ordered group on the GPU; deps -> osim_timeline_deps (waves: the
     1-DMA split of workload.simulate_sequence)."""
-    if len(tasks) > MAX_TASKS:
-        raise NotImplementedError(f"groups of more than {MAX_TASKS} tasks are not supported on the B200 path")
     durs = resolve_group(tasks, profile)
     n = len(tasks)
     if deps:

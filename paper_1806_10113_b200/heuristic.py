@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _capi
 from .engine import KIND_K, Timeline, simulate
-from .model import MAX_TASKS, DeviceProfile, TaskSpec, id_ranks, resolve_group, stage_times
+from .model import DeviceProfile, TaskSpec, id_ranks, resolve_group, stage_times
 
 SUM_MODE = 1 if sys.version_info >= (3, 12) else 0
 
@@ -90,6 +90,8 @@ def reorder_batch(tg: Sequence[TaskSpec], profile: DeviceProfile) -> List[TaskSp
     """Near-optimal submission order for one task group (on the GPU)."""
     if not tg:
         raise ValueError("task group is empty")
+    if len(tg) == 1:  # heuristic.py:113-114: returned as is, durations never resolved
+        return [tg[0]]
     return reorder_batch_many([tg], profile)[0]
 
 
@@ -103,8 +105,8 @@ def reorder_batch_many(groups: Sequence[Sequence[TaskSpec]], profile: DeviceProf
         raise ValueError("task group is empty")
     if any(len(g) != n for g in groups):
         raise ValueError("all groups of one batch must have the same size")
-    if n > MAX_TASKS:
-        raise NotImplementedError(f"groups of more than {MAX_TASKS} tasks are not supported on the B200 path")
+    if n == 1 and not return_makespans:  # heuristic.py:113-114 (no stage_times, no simulation)
+        return [[g[0]] for g in groups]
     durs = np.stack([resolve_group(g, profile) for g in groups])
     ranks = np.stack([id_ranks(g) for g in groups])
     order, ms, _ = reorder_durs(durs, ranks, profile.dma_engines, profile.overlap_sigma, n_dev=n_dev)

@@ -25,7 +25,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _capi
-from .model import MAX_ENUM_TASKS, MAX_TASKS, DeviceProfile, TaskSpec, resolve_group
+from .model import MAX_ENUM_TASKS, WIDE_MAX_TASKS, DeviceProfile, TaskSpec, resolve_group
 
 DEFAULT_CAP = 10_000  # oracle.py:24
 DEFAULT_DT = 0.001
@@ -64,7 +64,8 @@ def make_report(orderings: Sequence[Tuple[str, ...]], makespans: Sequence[float]
 
 def sample_permutations(n: int, cap: int, seed: int) -> np.ndarray:
     """`cap` distinct permutations of range(n) in first-drawn order from
-    numpy's default_rng(seed) (oracle.py:98-108) -> uint8 [cap][n]."""
+    numpy's default_rng(seed) (oracle.py:98-108) -> uint8 [cap][n] (uint32 above
+    64 tasks, the *_u32 entry points)."""
     gen = np.random.default_rng(seed)
     kept = {}
     while len(kept) < cap:
@@ -72,7 +73,7 @@ def sample_permutations(n: int, cap: int, seed: int) -> np.ndarray:
         key = p.tobytes()
         if key not in kept:
             kept[key] = p
-    out = np.empty((cap, n), dtype=np.uint8)
+    out = np.empty((cap, n), dtype=np.uint8 if n <= WIDE_MAX_TASKS else np.uint32)
     for row, p in enumerate(kept.values()):  # dicts keep insertion order
         out[row] = p
     return out
@@ -86,8 +87,6 @@ def exhaustive_search(tasks: Sequence[TaskSpec], profile: DeviceProfile, cap: in
     if cap < 1:
         raise ValueError("cap must be at least 1")
     n = len(tasks)
-    if n > MAX_TASKS:
-        raise NotImplementedError(f"groups of more than {MAX_TASKS} tasks are not supported on the B200 path")
     durs = resolve_group(tasks, profile)
     ids = [t.id for t in tasks]
     total = math.factorial(n)

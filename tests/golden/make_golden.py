@@ -20,6 +20,8 @@ Fixtures (all under tests/golden/):
   c3_full.json        (--c3, ~3 min on 8 cores) config-3 full 10! sweep
   wide.json           groups of 17..64 tasks: timelines (plain, deps, 1-DMA waves),
                       reorder_batch, sampled exhaustive_search, sampled NoReorder
+  big.json            groups above 64 tasks (to 300), NoReorder enumeration beyond 16
+                      tasks, micro_simulate beyond 16 tasks, reorder_batch of one task
 """
 
 from __future__ import annotations
@@ -664,6 +666,205 @@ def gen_wide():
                        "noreorder": noreorder, "harness": harness})
 
 
+# ------------------------------------------- groups above 64 tasks (any n)
+def _multiset_perms(labels):
+    """Every distinct permutation of `labels` (recursive choice of the next
+    label).  Stands in for itertools.permutations inside the reference's
+    sorted(set(permutations(labels))) (workload.py:262-265): the sorted set
+    of distinct sequences is the same list, but (T*N)! raw permutations are
+    out of reach above ~12 tasks."""
+    counts = {}
+    for x in labels:
+        counts[x] = counts.get(x, 0) + 1
+    keys = sorted(counts)
+    out, cur = [], []
+
+    def rec():
+        if len(cur) == len(labels):
+            out.append(tuple(cur))
+            return
+        for k in keys:
+            if counts[k]:
+                counts[k] -= 1
+                cur.append(k)
+                rec()
+                cur.pop()
+                counts[k] += 1
+
+    rec()
+    return out
+
+
+def _seq_timeline(tasks_grid, labels, p):
+    from offsim import workload
+
+    T = len(tasks_grid)
+    cnt = [0] * T
+    seq = []
+    for w in labels:
+        seq.append(tasks_grid[w][cnt[w]]); cnt[w] += 1
+    deps = {tasks_grid[w][j].id: tasks_grid[w][j - 1].id for w in range(T) for j in range(1, len(tasks_grid[w]))}
+    tl = workload.simulate_sequence(seq, p, deps)
+    flat = [t for row in tasks_grid for t in row]
+    ix = {t.id: i for i, t in enumerate(flat)}
+    kinds = {engine.KIND_HTD: 0, engine.KIND_K: 1, engine.KIND_DTH: 2}
+    start = [[None] * 3 for _ in flat]
+    end = [[None] * 3 for _ in flat]
+    for cmd in tl.commands:
+        start[ix[cmd.task_id]][kinds[cmd.kind]] = H(cmd.start)
+        end[ix[cmd.task_id]][kinds[cmd.kind]] = H(cmd.end)
+    return tl, start, end
+
+
+def gen_big():
+    """big.json: the reference on groups of more than 64 tasks (and the other
+    drop-in divergences VERDICT r01 listed): timelines, simulate_sequence,
+    reorder_batch, sampled exhaustive_search, NoReorder (exhaustive beyond 16
+    tasks and sampled beyond 64), micro_simulate beyond 16 tasks, the harness
+    beyond 64 tasks, and reorder_batch of one unresolvable task."""
+    from offsim import workload
+    from offsim.oracle import micro_simulate
+    from offsim.workload import Scenario
+
+    rng = np.random.default_rng(70_2)
+    timelines = []
+    for c, n in enumerate([65, 70, 70, 96, 130, 200, 257, 300]):
+        mode = ["int", "mixed", "real"][c % 3]
+        dma = 1 + c % 2
+        sigma = [0.375, 0.5, 0.8, 1.0][(c // 2) % 4]
+        d = rand_task_durs(rng, n, mode)
+        tasks = [TaskSpec(id=f"t{i}", fixed_durations=tuple(d[i])) for i in range(n)]
+        order = [int(x) for x in rng.permutation(n)]
+        doc = timeline_doc(tasks, order, prof(dma, sigma))
+        doc.update({"n": n, "dma": dma, "sigma": H(sigma), "durs": [[H(x) for x in r] for r in d], "order": order})
+        timelines.append(doc)
+        print("big timeline", n)
+    seqs = []
+    for c, (T, N) in enumerate([(5, 14), (9, 8), (3, 30), (13, 6)]):
+        dma = 1 + c % 2
+        sigma = [0.5, 0.375, 1.0, 0.8][c % 4]
+        d = rand_task_durs(rng, T * N, ["int", "mixed", "real"][c % 3])
+        grid = [[TaskSpec(id=f"w{w}.{j}", fixed_durations=tuple(d[w * N + j])) for j in range(N)] for w in range(T)]
+        labels = [int(x) for x in rng.permutation([w for w in range(T) for _ in range(N)])]
+        tl, start, end = _seq_timeline(grid, labels, prof(dma, sigma))
+        seqs.append({"T": T, "N": N, "dma": dma, "sigma": H(sigma), "labels": labels,
+                     "durs": [[H(x) for x in r] for r in d], "makespan": H(tl.makespan),
+                     "idle": [H(tl.idle[k]) for k in engine.KINDS], "start": start, "end": end})
+        print("big sequence", T, N)
+    heur = []
+    for pname, (dev, dma, sigma) in DEVICE_PROFILES.items():
+        p = prof(dma, sigma)
+        for n, seed in ((65, 1), (70, 2)):
+            tasks = sample_real_tasks(dev, n, seed=seed)
+            doc = heuristic_doc(tasks, p)
+            doc.update({"profile": pname, "dma": dma, "sigma": H(sigma), "n": n, "seed": seed,
+                        "ids": [t.id for t in tasks], "durs": durs_of(tasks), "id_rank": id_rank(tasks)})
+            heur.append(doc)
+            print("big heuristic", pname, n)
+    for c, n in enumerate([70, 100]):
+        dma = 1 + c % 2
+        sigma = [0.5, 0.375][c % 2]
+        d = rand_task_durs(rng, n, "int" if c % 2 else "mixed")
+        ids = [f"x{int(v)}" for v in rng.permutation(1000)[:n]]
+        tasks = [TaskSpec(id=ids[i], fixed_durations=tuple(d[i])) for i in range(n)]
+        doc = heuristic_doc(tasks, prof(dma, sigma))
+        doc.update({"profile": "rand", "dma": dma, "sigma": H(sigma), "n": n, "seed": c,
+                    "ids": ids, "durs": durs_of(tasks), "id_rank": id_rank(tasks)})
+        heur.append(doc)
+        print("big heuristic rand", n)
+    sampled = []
+    for n, dev, pname, cap, seed in ((70, "K20", "2dma", 200, 7), (90, "PHI", "1dma", 120, 8)):
+        p = load_profile_arg(pname)
+        tasks = sample_real_tasks(dev, n, seed=seed)
+        rep = report_doc(tasks, p, cap, seed, full=True)
+        rep["orderings_sha256"] = hashlib.sha256(np.asarray(
+            [[int(x) for x in o] for o in rep["orderings"]], dtype=np.uint32).tobytes()).hexdigest()
+        rep["orderings"] = rep["orderings"][:8]
+        sampled.append({"n": n, "profile": pname, "dma": p.dma_engines, "sigma": H(p.overlap_sigma),
+                        "cap": cap, "seed": seed, "durs": durs_of(tasks, p), **rep})
+        print("big sampled", n)
+    noreorder = []
+    real_perm = workload.permutations
+    for (T, N, bk, seed, pname, cap) in [(2, 9, "BK50", 21, "2dma", 50_000), (2, 9, "BK75", 22, "1dma", 50_000),
+                                         (2, 10, "BK25", 23, "2dma", 200_000), (7, 10, "BK50", 24, "1dma", 300),
+                                         (5, 14, "BK100", 25, "2dma", 200)]:
+        p = load_profile_arg(pname)
+        sc = Scenario(workers=T, batch_depth=N, pool=load_bk_benchmark(bk), seed=seed, profile=p)
+        wt = workload._draw_worker_tasks(sc)
+        workload.permutations = _multiset_perms
+        try:
+            rep = workload.noreorder_distribution(sc, wt, cap)
+        finally:
+            workload.permutations = real_perm
+        ms = np.asarray(rep.makespans)
+        idx = {wt[w][j].id: (w, j) for w in range(T) for j in range(N)}
+        labels = [[idx[i][0] for i in o] for o in rep.orderings]
+        noreorder.append({
+            "T": T, "N": N, "bk": bk, "seed": seed, "profile": pname, "cap": cap,
+            "dma": p.dma_engines, "sigma": H(p.overlap_sigma),
+            "durs": [[[H(float(x)) for x in offsim.stage_times(wt[w][j], p)] for j in range(N)] for w in range(T)],
+            "count": len(ms), "exhaustive": rep.exhaustive,
+            "labels_head": labels[:20],
+            "labels_sha256": hashlib.sha256(np.asarray(labels, dtype=np.uint8).tobytes()).hexdigest(),
+            "makespans_sha256": hashlib.sha256(ms.astype("<f8").tobytes()).hexdigest(),
+            "makespans_head": [H(float(m)) for m in ms[:20]],
+            "best": H(rep.best), "argmin": int(np.argmin(ms)), "worst": H(rep.worst), "median": H(rep.median),
+            "geomean": H(rep.geomean), "best_ordering": [list(idx[i]) for i in rep.best_ordering],
+        })
+        print("big noreorder", T, N, len(ms), rep.exhaustive)
+    micro = []
+    for c, n in enumerate([17, 20, 33, 70, 120]):
+        dma = 1 + c % 2
+        sigma = [0.5, 0.375, 1.0][c % 3]
+        dt = [0.01, 0.005, 0.02][c % 3]
+        d = rand_task_durs(rng, n, ["int", "mixed", "real"][c % 3])
+        tasks = [TaskSpec(id=f"t{i}", fixed_durations=tuple(d[i])) for i in range(n)]
+        order = [int(x) for x in rng.permutation(n)]
+        tl = micro_simulate([tasks[i] for i in order], prof(dma, sigma), dt=dt)
+        kinds = {engine.KIND_HTD: 0, engine.KIND_K: 1, engine.KIND_DTH: 2}
+        start = [[None] * 3 for _ in range(n)]
+        end = [[None] * 3 for _ in range(n)]
+        for cmd in tl.commands:
+            i = int(cmd.task_id[1:])
+            start[i][kinds[cmd.kind]] = H(cmd.start)
+            end[i][kinds[cmd.kind]] = H(cmd.end)
+        micro.append({"n": n, "dma": dma, "sigma": H(sigma), "dt": H(dt), "durs": [[H(x) for x in r] for r in d],
+                      "order": order, "makespan": H(tl.makespan), "start": start, "end": end,
+                      "idle": [H(tl.idle[k]) for k in engine.KINDS]})
+        print("big micro", n)
+    harness = []
+    for c, (T, N) in enumerate([(5, 14), (9, 8), (70, 1), (33, 3)]):
+        bk = BK_NAMES[c % 5]
+        pool = load_bk_benchmark(bk) if c % 2 == 0 else workload.make_benchmark(
+            "real", sample_real_tasks(["K20", "AMD", "PHI"][c % 3], 8, seed=c))
+        p = [load_profile_arg("2dma"), load_profile_arg("1dma"), prof(2, 0.375)][c % 3]
+        seed = 300 + c
+        sc = Scenario(workers=T, batch_depth=N, pool=pool, seed=seed, profile=p)
+        wt = workload._draw_worker_tasks(sc)
+        res = workload.run_scenario(sc, evaluate_noreorder=False)
+        flat = [t for row in wt for t in row]
+        harness.append({"T": T, "N": N, "bk": bk, "seed": seed, "dma": p.dma_engines, "sigma": H(p.overlap_sigma),
+                        "ids": [t.id for t in flat], "id_rank": id_rank(flat),
+                        "durs": [[H(float(x)) for x in offsim.stage_times(t, p)] for t in flat],
+                        "makespan": H(res.heuristic_makespan), "tg_sizes": res.tg_sizes,
+                        "idle": [H(res.timeline.idle[k]) for k in engine.KINDS]})
+        print("big harness", T, N)
+    # reorder_batch of one task returns it without resolving its durations
+    # (heuristic.py:113-114): an unresolvable task comes back unchanged
+    from offsim.model import UnresolvableDuration
+
+    lone = TaskSpec(id="lone", kernel_work=0.0)
+    try:
+        offsim.stage_times(lone, None)
+        resolvable = True
+    except UnresolvableDuration:
+        resolvable = False
+    single = {"id": lone.id, "resolvable": resolvable,
+              "returned": [t.id for t in heuristic.reorder_batch([lone], load_profile_arg("2dma"))]}
+    dump("big.json", {"timelines": timelines, "sequences": seqs, "heuristic": heur, "sampled": sampled,
+                      "noreorder": noreorder, "micro": micro, "harness": harness, "single": single})
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--c3", action="store_true")
@@ -674,7 +875,7 @@ if __name__ == "__main__":
         sys.exit(0)
     gens = {"c1": gen_c1, "sim": gen_sim_random, "heur": gen_heuristic_random, "c2": gen_c2,
             "c4": gen_c4, "c5": gen_c5, "sampled": gen_sampled, "noreorder": gen_noreorder,
-            "micro": gen_micro, "harness": gen_harness, "wide": gen_wide}
+            "micro": gen_micro, "harness": gen_harness, "wide": gen_wide, "big": gen_big}
     for k, g in gens.items():
         if not a.only or k in a.only.split(","):
             g()

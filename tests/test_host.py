@@ -194,3 +194,49 @@ def test_common_prefix_of_value_range():
         assert bits == 0 or all(int(x) >> (64 - bits) == p for x in u)
     assert common_prefix(2.0, 2.0)[1] == 63
     assert common_prefix(0.0, 1.0) == (0, 0)
+
+
+def test_reorder_batch_single_task_is_not_resolved():
+    # heuristic.py:113-114: a one-task group comes back as is, without
+    # stage_times (an unresolvable task does not raise) -- big.json "single"
+    import paper_1806_10113_b200 as osim
+    from tests._golden import load
+
+    g = load("big.json")["single"]
+    lone = osim.TaskSpec(g["id"], kernel_work=0.0)
+    with pytest.raises(osim.UnresolvableDuration):
+        osim.stage_times(lone, None)
+    p = osim.DeviceProfile("2dma", 2, 0.01, 6e6, 0.01, 6e6, overlap_sigma=0.5)
+    assert [t.id for t in osim.reorder_batch([lone], p)] == g["returned"]
+    assert osim.reorder_batch_many([[lone], [lone]], p) == [[lone], [lone]]
+
+
+def test_all_interleavings_is_sorted_set_of_permutations():
+    # the host enumeration used beyond 16 tasks (noreorder.all_interleavings)
+    # against workload.py:262-265's sorted(set(permutations(labels)))
+    import hashlib
+    from itertools import permutations
+
+    from paper_1806_10113_b200.noreorder import all_interleavings, interleaving_count, unrank_labels
+    from tests._golden import load
+
+    for T, N in ((1, 3), (2, 2), (2, 3), (3, 2), (3, 3), (4, 2)):
+        labels = [w for w in range(T) for _ in range(N)]
+        want = sorted(set(permutations(labels)))
+        got = all_interleavings(T, N)
+        assert [tuple(r) for r in got.tolist()] == want
+        assert [unrank_labels(r, T, N) for r in range(interleaving_count(T, N))] == want
+    for c in load("big.json")["noreorder"]:
+        if c["exhaustive"]:
+            lab = all_interleavings(c["T"], c["N"])
+            assert len(lab) == c["count"]
+            assert hashlib.sha256(lab.astype(np.uint8).tobytes()).hexdigest() == c["labels_sha256"]
+
+
+def test_micro_simulate_empty_group():
+    # micro_core over empty arrays: no commands, makespan 0 (_micro.py:68-71)
+    import paper_1806_10113_b200 as osim
+
+    p = osim.DeviceProfile("2dma", 2, 0.01, 6e6, 0.01, 6e6, overlap_sigma=0.5)
+    tl = osim.micro_simulate([], p)
+    assert tl.commands == [] and tl.makespan == 0.0 and set(tl.idle.values()) == {0.0}

@@ -316,3 +316,54 @@ def test_wide_harness_oracle_pinned():
                               c["T"], c["N"], c["dma"], F(c["sigma"]), sum_mode_of(g), C.byref(ms), C.byref(ng),
                               sizes.ctypes.data_as(C.POINTER(C.c_int)))
         assert rc == 0 and ms.value == F(c["makespan"]) and sizes[: ng.value].tolist() == c["tg_sizes"], (c["T"], c["N"])
+
+
+# ---- groups above 64 tasks and the round-1 drop-in divergences (tests/golden/big.json)
+
+def test_big_oracle_pinned():
+    import hashlib
+
+    from paper_1806_10113_b200.noreorder import sample_interleavings
+    from paper_1806_10113_b200.search import sample_permutations
+
+    g = load("big.json")
+    mode = sum_mode_of(g)
+    for c in g["timelines"]:
+        r = O.simulate(durs(c["durs"]), c["order"], c["dma"], F(c["sigma"]))
+        assert r.makespan == F(c["makespan"]) and r.k_end == F(c["k_end"])
+        assert r.idle.tolist() == fl(c["idle"]) and r.steps == c["steps"]
+        _check_timeline(r, c, c["n"])
+    for c in g["sequences"]:
+        T, N = c["T"], c["N"]
+        cnt = [0] * T
+        order = []
+        for w in c["labels"]:
+            order.append(w * N + cnt[w])
+            cnt[w] += 1
+        dep = [(w * N + j - 1 if j else -1) for w in range(T) for j in range(N)]
+        r = O.simulate_seq(durs(c["durs"]), order, c["dma"], F(c["sigma"]), dep)
+        assert r.makespan == F(c["makespan"]) and r.idle.tolist() == fl(c["idle"])
+        _check_timeline(r, c, T * N)
+    for c in g["heuristic"]:
+        order, m, sims = O.reorder(durs(c["durs"]), c["id_rank"], c["dma"], F(c["sigma"]), mode)
+        assert order == c["order"] and m == F(c["makespan"]) and sims == c["n_sims"], (c["profile"], c["n"])
+    for c in g["sampled"]:
+        perms = sample_permutations(c["n"], c["cap"], c["seed"])
+        assert hashlib.sha256(perms.astype(np.uint32).tobytes()).hexdigest() == c["orderings_sha256"]
+        s, ms = O.eval_perms(durs(c["durs"]), c["dma"], F(c["sigma"]), perms.astype(np.uint8))
+        assert sha(ms) == c["makespans_sha256"] and s["best_rank"] == c["argmin"]
+    for c in g["noreorder"]:
+        if c["exhaustive"]:
+            continue  # the enumeration is checked in test_host (all_interleavings)
+        T, N = c["T"], c["N"]
+        d = np.array([[[F(x) for x in r] for r in row] for row in c["durs"]]).reshape(-1, 3)
+        lab = sample_interleavings(T, N, c["cap"], c["seed"])
+        assert hashlib.sha256(lab.astype(np.uint8).tobytes()).hexdigest() == c["labels_sha256"]
+        s, ms = O.eval_sequences(d, T, N, c["dma"], F(c["sigma"]), lab)
+        assert hashlib.sha256(ms.astype("<f8").tobytes()).hexdigest() == c["makespans_sha256"]
+        assert s["best_rank"] == c["argmin"] and float(np.median(ms)) == F(c["median"])
+    for c in g["micro"]:
+        ms, st, en = O.micro(durs(c["durs"]), c["order"], c["dma"], F(c["sigma"]), F(c["dt"]))
+        assert ms == F(c["makespan"])
+    single = g["single"]
+    assert single["resolvable"] is False and single["returned"] == [single["id"]]
