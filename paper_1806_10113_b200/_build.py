@@ -49,8 +49,8 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in SOURCES + HEADERS)
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(OBJDIR, os.path.basename(src).replace(".cu", ".o"))
+def _compile(src: str, objdir: str, verbose: bool) -> str:
+    obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
     extra = os.environ.get("OSIM_NVCC_EXTRA", "").split()  # tuning only, e.g. -DOSIM_PFX_MINB=3
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", "-o", obj, src]
     if verbose:
@@ -63,17 +63,33 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 0) -> str:
     """Compile the translation units in parallel, link the shared library."""
     if not force and not stale():
         return LIB
+    return _build_to(LIB, OBJDIR, verbose, jobs)
+
+
+def build_variant(name: str, extra: list, verbose: bool = False) -> str:
+    """A/B tuning build: liboffsim_b200_<name>.so with extra nvcc flags
+    (e.g. -DOSIM_HSPLIT=0); load it with OSIM_LIB=<path>."""
+    out = os.path.join(PKG, f"liboffsim_b200_{name}.so")
+    os.environ["OSIM_NVCC_EXTRA"] = " ".join(extra)
+    return _build_to(out, OBJDIR + "_" + name, verbose, 0)
+
+
+def _build_to(lib: str, objdir: str, verbose: bool, jobs: int) -> str:
     from concurrent.futures import ThreadPoolExecutor
 
-    os.makedirs(OBJDIR, exist_ok=True)
+    os.makedirs(objdir, exist_ok=True)
     jobs = jobs or min(len(SOURCES), os.cpu_count() or 1)
     with ThreadPoolExecutor(jobs) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
-    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp", *objs]
+        objs = list(ex.map(lambda s: _compile(s, objdir, verbose), SOURCES))
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib + ".tmp", *objs]
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:], verbose=True))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

@@ -16,7 +16,7 @@ import numpy as np
 from .model import UnresolvableDuration
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "liboffsim_b200.so")
+LIB_PATH = os.environ.get("OSIM_LIB") or os.path.join(PKG, "liboffsim_b200.so")  # OSIM_LIB: A/B builds (tuning only)
 
 OSIM_OK, OSIM_EINVAL, OSIM_ENODEV, OSIM_ECUDA, OSIM_ENCCL, OSIM_ESTALL = 0, -1, -2, -3, -4, -5
 

@@ -1037,9 +1037,12 @@ constexpr int kHGF = kWG * kWPB;       // groups per CTA (fast kernel)
 constexpr int kHTF = 32 * kWPB;        // threads per CTA (fast kernel)
 static_assert(kLPG * kWG == 32 && kWG <= 16, "groups per warp");
 
+#ifndef OSIM_HSPLIT
+#define OSIM_HSPLIT 1  // k_heuristic_fast: command starts as three 8-byte loads (see start_if_split)
+#endif
 template <int DMA, bool SP2>
 struct HeurWarpShared {
-    using FS = FastSim<DMA, SP2, true, false>;
+    using FS = FastSim<DMA, SP2, true, false, false, OSIM_HSPLIT != 0>;
     double2 dr[kWG * kHS];
     typename FS::Ck ck[kWG];
 #ifndef OSIM_HKREG
@@ -1220,9 +1223,11 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
 #endif
         }
         __syncwarp();
-        // argmin of the key over the m candidates: kLPG lanes per group, each
-        // scanning every kLPG-th candidate, then a shuffle reduction
-        // (the key is a strict total order, so the tree order is immaterial)
+        // argmin of the key over the m candidates (a strict total order, so the
+        // reduction order is immaterial).  Register path (default): each lane
+        // already holds the best key of its candidates j = lane / kWG + kLPG *
+        // it of group lane % kWG; shuffles across the lanes with the same
+        // lane % kWG leave group g's argmin on lane g.
         int bj;
 #ifdef OSIM_HKREG
         {
@@ -1236,6 +1241,9 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restric
             bj = lj;  // lane < kWG holds group `lane`'s argmin
         }
 #else
+        // shared-key path (-DOSIM_HKSHARED): kLPG lanes per group, each
+        // scanning every kLPG-th candidate's key in shared memory, then a
+        // shuffle reduction over the group's kLPG lanes
         {
             const int g = lane / kLPG, part = lane % kLPG;
             int lj = -1;

@@ -339,6 +339,16 @@ __device__ __forceinline__ void start_if(bool p, uint32_t addr, double& nd, doub
         : "+d"(nd), "+d"(rc), "+d"(rem)
         : "r"(addr), "r"((int)p));
 }
+// the same with three 8-byte loads: no 16-byte register-pair alignment for
+// {nd, 1/nd}, so under register pressure the compiler needs no predicated
+// moves from a temporary quad (k_heuristic_fast: -6 instructions per step)
+__device__ __forceinline__ void start_if_split(bool p, uint32_t addr, double& nd, double& rc, double& rem) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+        "@q ld.shared.f64 %0, [%3];\n\t@q ld.shared.f64 %1, [%3+8];\n\t@q ld.shared.f64 %2, [%3];\n\t}"
+        : "+d"(nd), "+d"(rc), "+d"(rem)
+        : "r"(addr), "r"((int)p));
+}
 __device__ __forceinline__ void mul_if(bool p, double& x, double y) {
     asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q mul.rn.f64 %0, %0, %1;\n\t}"
         : "+d"(x) : "d"(y), "r"((int)p));
@@ -375,8 +385,13 @@ __device__ __forceinline__ uint32_t task_off(uint64_t seq, int sh) {
 // like `seq`.  With every stage non-null a task is finished exactly when its
 // DtH finalized, and DtHs finalize in sequence order, so the gate is one
 // extra condition on the HtD start: s1 >= 4 * (1 + prerequisite position).
-template <int DMA, bool SIGP2, bool TRACK, bool PRE, bool DEPS = false>
+template <int DMA, bool SIGP2, bool TRACK, bool PRE, bool DEPS = false, bool SPLIT = false>
 struct FastSim {
+    // a command start: {nd, 1/nd} and rem = nd from shared memory (SPLIT: three 8-byte loads)
+    __device__ __forceinline__ static void st_(bool p, uint32_t addr, double& nd, double& rc, double& rem) {
+        if constexpr (SPLIT) start_if_split(p, addr, nd, rc, rem);
+        else start_if(p, addr, nd, rc, rem);
+    }
     uint32_t base;
     uint64_t seq;   // packed ordering (pre-shifted by 4 when PRE)
     uint64_t dseq;  // DEPS: packed 1 + prerequisite position (pre-shifted like seq)
@@ -403,7 +418,7 @@ struct FastSim {
     __device__ __forceinline__ void set_seq(uint64_t sq) { seq = PRE ? (sq << 4) : sq; }
     // start the HtD at the queue head now (the HtD lane is idle and an HtD
     // is always ready): what the next step's start phase would do
-    __device__ __forceinline__ void start_htd() { start_if(true, base + task_off<PRE>(seq, s0), d0, c0, r0); }
+    __device__ __forceinline__ void start_htd() { st_(true, base + task_off<PRE>(seq, s0), d0, c0, r0); }
     __device__ __forceinline__ int finalized() const { return (s0 + s1 + s2) >> 2; }
 
     // checkpoint image (prefix sharing across calls, e.g. in shared memory)
@@ -443,8 +458,8 @@ struct FastSim {
         const bool st2 = idle(r2) && s2 < n4;
         const bool st1 = idle(r1) && s1 < s2;
         k_idle_gap(st2);
-        start_if(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
-        start_if(st1, base + 512 + task_off<PRE>(seq, s1), d1, c1, r1);
+        st_(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
+        st_(st1, base + 512 + task_off<PRE>(seq, s1), d1, c1, r1);
         const double dt = dmin(r1, r2);
         now = __dadd_rn(now, dt);
         r2 = upd(r2, dt, d2, c2);
@@ -461,7 +476,7 @@ struct FastSim {
     __device__ __forceinline__ void step_d() {
         static_assert(DMA == 2, "2-DMA only");
         const bool st1 = idle(r1) && s1 < n4;
-        start_if(st1, base + 512 + task_off<PRE>(seq, s1), d1, c1, r1);
+        st_(st1, base + 512 + task_off<PRE>(seq, s1), d1, c1, r1);
         const double dt = r1;  // the only lane that can run (rem ~0 once drained)
         now = __dadd_rn(now, dt);
         r1 = upd(r1, dt, d1, c1);
@@ -481,8 +496,8 @@ struct FastSim {
         const bool st0 = idle(r0) && s0 < 2 * n4 && s2 > ps;
         const bool st2 = idle(r2) && s2 < n4;
         k_idle_gap(st2);
-        start_if(st0, base + 512u + task_off<PRE>(seq, ps), d0, c0, r0);
-        start_if(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
+        st_(st0, base + 512u + task_off<PRE>(seq, ps), d0, c0, r0);
+        st_(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
         const double dt = dmin(r0, r2);
         now = __dadd_rn(now, dt);
         r0 = upd(r0, dt, d0, c0);
@@ -505,8 +520,8 @@ struct FastSim {
         const bool st0 = idle(r0) && s0 < 2 * n4 && s2 > ps;
         const bool st2 = idle(r2) && s2 < n4 && s2 < s0;
         k_idle_gap(st2);
-        start_if(st0, base + 512u + task_off<PRE>(seq, ps), d0, c0, r0);
-        start_if(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
+        st_(st0, base + 512u + task_off<PRE>(seq, ps), d0, c0, r0);
+        st_(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
         const double dt = dmin(r0, r2);
         now = __dadd_rn(now, dt);
         r0 = upd(r0, dt, d0, c0);
@@ -523,7 +538,7 @@ struct FastSim {
     __device__ __forceinline__ void step_1dd() {
         static_assert(DMA == 1, "1-DMA only");
         const bool st0 = idle(r0) && s0 < 2 * n4;
-        start_if(st0, base + 512u + task_off<PRE>(seq, s0 - n4), d0, c0, r0);
+        st_(st0, base + 512u + task_off<PRE>(seq, s0 - n4), d0, c0, r0);
         const double dt = r0;  // the only lane that can run (rem ~0 once drained)
         now = __dadd_rn(now, dt);
         r0 = upd(r0, dt, d0, c0);
@@ -602,17 +617,17 @@ struct FastSim {
             const bool st2 = idle(r2) && s2 < s0;
             const bool st1 = idle(r1) && s1 < s2;
             k_idle_gap(st2);
-            if constexpr (H0) start_if(st0, base + task_off<PRE>(seq, s0), d0, c0, r0);
-            start_if(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
-            start_if(st1, base + 512 + task_off<PRE>(seq, s1), d1, c1, r1);
+            if constexpr (H0) st_(st0, base + task_off<PRE>(seq, s0), d0, c0, r0);
+            st_(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
+            st_(st1, base + 512 + task_off<PRE>(seq, s1), d1, c1, r1);
         } else {
             const bool isH = s0 < n4;
             const int ps = isH ? s0 : s0 - n4;
             const bool st0 = idle(r0) && s0 < 2 * n4 && (isH || s2 > ps);
             const bool st2 = idle(r2) && s2 < n4 && s2 < s0;
             k_idle_gap(st2);
-            start_if(st0, base + (isH ? 0u : 512u) + task_off<PRE>(seq, ps), d0, c0, r0);
-            start_if(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
+            st_(st0, base + (isH ? 0u : 512u) + task_off<PRE>(seq, ps), d0, c0, r0);
+            st_(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
         }
         // ---- dt (engine.py:200-210)
         double dt, dd;
