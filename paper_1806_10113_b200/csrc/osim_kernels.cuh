@@ -1038,11 +1038,12 @@ constexpr int kHTF = 32 * kWPB;        // threads per CTA (fast kernel)
 static_assert(kLPG * kWG == 32 && kWG <= 16, "groups per warp");
 
 #ifndef OSIM_HSPLIT
-#define OSIM_HSPLIT 1  // k_heuristic_fast: command starts as three 8-byte loads (see start_if_split)
+#define OSIM_HSPLIT 1  // k_heuristic_fast, 2-DMA: command starts as three 8-byte loads (start_if_split;
+                       // C5 NVIDIA 147.4 -> 150.4, AMD 143.1 -> 147.9 M decisions/s; PHI 172.3 -> 168.6)
 #endif
 template <int DMA, bool SP2>
 struct HeurWarpShared {
-    using FS = FastSim<DMA, SP2, true, false, false, OSIM_HSPLIT != 0>;
+    using FS = FastSim<DMA, SP2, true, false, false, OSIM_HSPLIT != 0 && DMA == 2>;  // 1-DMA: measured slower
     double2 dr[kWG * kHS];
     typename FS::Ck ck[kWG];
 #ifndef OSIM_HKREG
@@ -1072,8 +1073,16 @@ __device__ __forceinline__ bool key_less(double e, double d, int r, double be, d
     return r < br;
 }
 
+#ifndef OSIM_HMINB
+#define OSIM_HMINB 0  // min resident CTAs per SM for k_heuristic_fast (0: unspecified; register budget, tuning)
+#endif
+#if OSIM_HMINB > 0
+#define OSIM_HLB __launch_bounds__(kHTF, OSIM_HMINB)
+#else
+#define OSIM_HLB __launch_bounds__(kHTF)
+#endif
 template <int DMA, bool SP2>
-__global__ void __launch_bounds__(kHTF) k_heuristic_fast(const double* __restrict__ durs,
+__global__ void OSIM_HLB k_heuristic_fast(const double* __restrict__ durs,
                                                         const uint8_t* __restrict__ id_rank, uint64_t B, int n,
                                                         double sigma, int sum_mode,
                                                         uint8_t* __restrict__ order_out,
