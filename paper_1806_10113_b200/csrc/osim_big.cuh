@@ -69,7 +69,10 @@ struct BigSim {
     __device__ __forceinline__ double dur(int k, uint32_t t) const { return d[3ull * t + k]; }
     __device__ __forceinline__ bool nonnull(int k, uint32_t t) const { return dur(k, t) > 0.0; }
     __device__ __forceinline__ int64_t depof(uint32_t t) const { return dep ? (int64_t)dep[t] : -1; }
-    __device__ __forceinline__ void push(int l, uint32_t e) { q[(uint64_t)l * qcap + len[l]++] = e; }
+    __device__ __forceinline__ void push(int l, uint32_t e) {
+        OSIM_DCHECK(len[l] < qcap && (e & ~kBigDtH) < qcap / 2);
+        q[(uint64_t)l * qcap + len[l]++] = e;
+    }
     // k_end of heuristic.py:46: the latest K end, 0.0 without any K
     __device__ __forceinline__ double k_end() const { return seen[1] ? pend[1] : 0.0; }
 
@@ -143,6 +146,7 @@ struct BigSim {
     __device__ bool step(TimelineOut* tl) {
         for (int l = 0; l < 3; ++l) {  // start phase (engine.py:188-194)
             if (run[l] || h[l] >= len[l]) continue;
+            OSIM_DCHECK(h[l] < len[l] && len[l] <= qcap);
             const uint32_t e = q[(uint64_t)l * qcap + h[l]], t = e & ~kBigDtH;
             const int kind = (l == 2) ? 1 : ((l == 1) ? 2 : ((e & kBigDtH) ? 2 : 0));
             if (!ready(kind, t)) continue;
@@ -315,6 +319,7 @@ __device__ double big_reorder(const Team& tm, const double* gd, const uint32_t* 
         }
         best = tm.argmin(best);
         if (me == 0) {
+            OSIM_DCHECK(best.valid && best.slot < m && k < n);
             ot[k] = best.task;
             for (uint64_t j = best.slot; j + 1 < m; ++j) rt[j] = rt[j + 1];
         }
@@ -536,6 +541,7 @@ __global__ void __launch_bounds__(kBigBlock) k_big_harness(const double* __restr
             s.last_htd = -1;
             s.submit(BigSeq{ord, m, 0u, 0u, 0}, false);  // DeviceSim.submit (engine.py:125-156)
             watched = s.last_htd;
+            OSIM_DCHECK(ng < n && m >= 1 && m <= T);
             if (sizes_out) sizes_out[sc * n + ng] = (uint32_t)m;
             ++ng;
             polling = watched < 0;

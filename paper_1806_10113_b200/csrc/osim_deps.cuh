@@ -23,6 +23,7 @@ struct Queue32 {  // up to 32 entries: 4-bit task id + 1 kind bit (XFER: 1 = DtH
     int len;
     __device__ __forceinline__ void clear() { t[0] = t[1] = 0; kind = 0; len = 0; }
     __device__ __forceinline__ void push(int task, int isD) {
+        OSIM_DCHECK(len >= 0 && len < 32 && task >= 0 && task < 16);
         t[len >> 4] |= (uint64_t)task << (4 * (len & 15));
         kind |= (uint32_t)isD << len;
         ++len;

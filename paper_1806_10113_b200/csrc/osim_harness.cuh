@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(128) k_harness(const double* __restrict__ durs
                 const int u = tg[ord[i]];
                 if (s.nonnull(2, u)) { s.q[0].push(u, 1); ++s.ncmd; }
             }
+        OSIM_DCHECK(ng < n && m >= 1);
         if (sizes_out) sizes_out[sc * n + ng] = (uint8_t)m;
         ++ng;
         polling = watched < 0;

@@ -408,10 +408,14 @@ __device__ __forceinline__ int2 pfx_sort(PfxSort& S, int sa0, int sa1) {
         if (ww < w) r0 += S.cnt[0][ww][sa0];
         r1 += S.cnt[0][ww][sa1] + (ww < w ? S.cnt[1][ww][sa1] : 0);
     }
+    OSIM_DCHECK(sa0 >= 0 && sa0 < kSaBins && sa1 >= 0 && sa1 < kSaBins);
+    OSIM_DCHECK(r0 >= 0 && r0 < kPfxQ * kBlock && r1 >= 0 && r1 < kPfxQ * kBlock && r0 != r1);
     S.order[r0] = (short)ti;
     S.order[r1] = (short)(kBlock + ti);
     __syncthreads();
-    return make_int2(S.order[32 * w + lane], S.order[32 * (2 * kNW - 1 - w) + lane]);
+    const int2 e = make_int2(S.order[32 * w + lane], S.order[32 * (2 * kNW - 1 - w) + lane]);
+    OSIM_DCHECK(e.x >= 0 && e.x < kPfxQ * kBlock && e.y >= 0 && e.y < kPfxQ * kBlock);
+    return e;
 }
 
 // Simulate this CTA's prefixes P0 + t and P0 + 256 + t (t = thread) of
@@ -443,6 +447,7 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
             a = advance_to(s, valid ? M : 0, sigma, rsig);
             ck_store(K, q, ti, s);
         }
+        OSIM_DCHECK(a >= 0 && a < kSaBins - 1);
         sa[q] = valid ? a : kSaBins - 1;
         S.seq[q * kBlock + ti] = seq0;
         S.P[q * kBlock + ti] = valid ? P : ~0ull;
@@ -518,6 +523,7 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
             if (all_in || (any_in && r >= lo && r < hi)) {
                 leaf_add<STATS>(acc, s.now, r, thr);
                 if constexpr (STATS) {
+                    OSIM_DCHECK(r >= ms_base && r >= lo && r < hi);
                     if (ms_out) ms_out[r - ms_base] = s.now;
                 }
             }
@@ -543,7 +549,9 @@ __device__ __forceinline__ void fused_final_reduce(const Part* parts, osim_summa
     __syncthreads();  // this CTA's partial is written (thread 0 wrote it)
     if (threadIdx.x == 0) {
         __threadfence();
-        last = atomicAdd(done, 1u) == gridDim.x - 1;
+        const unsigned prev = atomicAdd(done, 1u);
+        OSIM_DCHECK(prev < gridDim.x);  // the counter starts at 0 and is reset by the last CTA
+        last = prev == gridDim.x - 1;
     }
     __syncthreads();
     if (!last) return;
@@ -1185,6 +1193,8 @@ __global__ void OSIM_HLB k_heuristic_fast(const double* __restrict__ durs,
 #endif
             const uint64_t cl0 = S.cand[g];
             const int c = rt_at(cl0, j);
+            OSIM_DCHECK(g >= 0 && g < kWG && j >= 0 && j < m && c >= 0 && c < n);
+            OSIM_DCHECK(!valid || ((S.ot[g] >> (4 * k)) == 0ull));  // position k is still free
             FS s;
             s.init(gbase(g), S.ot[g] | ((uint64_t)c << (4 * k)), k + 1);
             s.load(S.ck[g]);
@@ -1279,6 +1289,7 @@ __global__ void OSIM_HLB k_heuristic_fast(const double* __restrict__ durs,
             const int g = lane;
             const int c = rt_at(S.cand[g], bj);
             S.ot[g] |= (uint64_t)c << (4 * k);
+            OSIM_DCHECK(bj >= 0 && bj < m);
             S.cand[g] = rt_drop(S.cand[g], bj);
             // advance the checkpoint by the chosen task (prefix length k+1)
             FS s;
@@ -1423,6 +1434,7 @@ static __global__ void __launch_bounds__(256) k_radix_hist(const unsigned long l
         const unsigned long long u = valid ? vals[i] : 0ull;
         const bool match = valid && (pbits == 0 || (u >> (64 - pbits)) == prefix);
         const unsigned digit = (unsigned)(u >> shift) & mask;
+        OSIM_DCHECK(digit < (unsigned)nb);
         const unsigned key = match ? digit : 0xFFFFFFFFu;
         const unsigned peers = __match_any_sync(kFull, key);
         if (match && lane == __ffs(peers) - 1) atomicAdd(&sh[digit], (unsigned)__popc(peers));

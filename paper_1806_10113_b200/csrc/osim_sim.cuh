@@ -31,6 +31,28 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
+
+// Device-side bounds and invariant checks, compiled in only for the
+// checking build (python -m paper_1806_10113_b200._build --variant dcheck
+// -DOSIM_DEBUG_CHECKS; tools/dcheck_run.py).  compute-sanitizer is not
+// available on the GPU pool, so shared-memory / global indices and the
+// kernels' own invariants are asserted in the code: a violation prints the
+// site and traps (the launch fails with cudaErrorLaunchFailure).
+#ifdef OSIM_DEBUG_CHECKS
+#define OSIM_DCHECK(cond)                                                                          \
+    do {                                                                                           \
+        if (!(cond)) {                                                                             \
+            printf("OSIM_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                             \
+            __trap();                                                                              \
+        }                                                                                          \
+    } while (0)
+#else
+#define OSIM_DCHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
 
 namespace osim {
 

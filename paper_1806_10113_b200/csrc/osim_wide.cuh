@@ -40,7 +40,10 @@ struct WideSim {
     __device__ __forceinline__ double dur(int k, int t) const { return d[3 * t + k]; }
     __device__ __forceinline__ bool nonnull(int k, int t) const { return dur(k, t) > 0.0; }
     __device__ __forceinline__ int depof(int t) const { return dep ? (int)dep[t] : -1; }
-    __device__ __forceinline__ void push(int l, int task, int isD) { q[l][len[l]++] = (uint8_t)(task | (isD << 7)); }
+    __device__ __forceinline__ void push(int l, int task, int isD) {
+        OSIM_DCHECK(len[l] < 2 * kWideMax && task >= 0 && task < kWideMax);
+        q[l][len[l]++] = (uint8_t)(task | (isD << 7));
+    }
 
     // order: task ids of the len positions; ntask: tasks in the group
     __device__ void init(const double* dd, int ntask, double sg, const uint8_t* order, int n, const int8_t* dp,
@@ -418,6 +421,7 @@ __global__ void __launch_bounds__(kWideBlock) k_wide_harness(const double* __res
                 const int u = tg[ord[i]];
                 if (s.nonnull(2, u)) { s.push(0, u, 1); ++s.ncmd; }
             }
+        OSIM_DCHECK(ng < n && m >= 1);
         if (sizes_out) sizes_out[sc * n + ng] = (uint8_t)m;
         ++ng;
         polling = watched < 0;
