@@ -254,6 +254,10 @@ int osim_micro_timeline_u32(const double* durs, uint64_t n, int dma, double sigm
 /* Compare the fast-path division with IEEE division on `samples` random
  * operand pairs drawn from the fast-path range; *mismatches = count. */
 int osim_selftest_div(uint64_t samples, uint64_t seed, uint64_t* mismatches);
+/* mode 0: as osim_selftest_div; mode 1: adversarial operands (mantissas on
+ * rounding boundaries, quotients at binade edges, rounded products
+ * y * (1 - 2^-k)) over the fast-path range of divisors [2^-60, 2^22). */
+int osim_selftest_div_mode(uint64_t samples, uint64_t seed, int mode, uint64_t* mismatches);
 /* Measured FP64 FMA-pipe throughput of the current device, TFLOP/s
  * (2 flops per DFMA). */
 int osim_fp64_peak(double* tflops);

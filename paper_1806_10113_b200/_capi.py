@@ -30,7 +30,7 @@ EXPORTS = (
     "osim_timeline_deps", "osim_micro", "osim_micro_timeline", "osim_harness_batch",
     "osim_exhaustive_shard_dev", "osim_exhaustive_shard", "osim_select_kth_dev",
     "osim_pfx_suffix_len", "osim_timeline_u32", "osim_eval_perms_u32", "osim_eval_sequences_u32",
-    "osim_heuristic_batch_u32", "osim_harness_batch_u32", "osim_micro_timeline_u32",
+    "osim_heuristic_batch_u32", "osim_harness_batch_u32", "osim_micro_timeline_u32", "osim_selftest_div_mode",
 )
 
 
@@ -101,6 +101,7 @@ def load(path: str = LIB_PATH):
             "osim_exhaustive_batch_dev": ([vp, u64, i, i, d, i, vp, vp], i),
             "osim_heuristic_batch_dev": ([vp, vp, u64, i, i, d, i, i, vp, vp, vp, vp], i),
             "osim_selftest_div": ([u64, u64, C.POINTER(u64)], i),
+            "osim_selftest_div_mode": ([u64, u64, i, C.POINTER(u64)], i),
             "osim_exhaustive_stats": ([dp, i, i, d, u64, u64, d, i, sp, C.POINTER(u64), dp], i),
             "osim_exhaustive_ex_dev": ([vp, i, i, d, u64, u64, i, d, vp, vp, vp, vp], i),
             "osim_radix_hist_dev": ([vp, u64, u64, i, i, vp, vp], i),
@@ -289,9 +290,11 @@ def fast_eligible(durs, sigma) -> bool:
     return bool(load().osim_fast_eligible(ptr(d, C.c_double), d.size // 3, float(sigma)))
 
 
-def selftest_div(samples: int, seed: int = 1) -> int:
+def selftest_div(samples: int, seed: int = 1, mode: int = 0) -> int:
+    """Mismatches of the fast-path division against IEEE division over
+    `samples` operand pairs (mode 0 random, 1 adversarial)."""
     m = C.c_uint64()
-    check(load().osim_selftest_div(int(samples), int(seed), C.byref(m)))
+    check(load().osim_selftest_div_mode(int(samples), int(seed), int(mode), C.byref(m)))
     return m.value
 
 

@@ -1639,6 +1639,27 @@ int osim_selftest_div(uint64_t samples, uint64_t seed, uint64_t* mismatches) {
     return 0;
 }
 
+int osim_selftest_div_mode(uint64_t samples, uint64_t seed, int mode, uint64_t* mismatches) {
+    if (mode != 0 && mode != 1) return fail(OSIM_EINVAL, "mode must be 0 (random) or 1 (adversarial)");
+    if (mode == 0) return osim_selftest_div(samples, seed, mismatches);
+    DevList dl;
+    int rc = pick_devs(1, dl);
+    if (rc) return rc;
+    DevCtx* c = dl.v[0];
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->dev));
+    void* base;
+    if ((rc = scratch(c, 256, &base))) return rc;
+    CK(cudaMemsetAsync(base, 0, 8, c->stream));
+    k_selftest_div_hard<<<c->sms * 8, 256, 0, c->stream>>>(samples, seed, (unsigned long long*)base);
+    CK(cudaGetLastError());
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, base, 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (mismatches) *mismatches = h;
+    return 0;
+}
+
 int osim_fp64_peak(double* tflops) {
     DevList dl;
     int rc = pick_devs(1, dl);

@@ -1493,6 +1493,48 @@ static __global__ void k_selftest_div(uint64_t samples, uint64_t seed, unsigned 
     if ((threadIdx.x & 31) == 0 && bad) atomicAdd(mism, bad);
 }
 
+// Adversarial operands for the fast-path division (mode 1 of
+// osim_selftest_div_mode): mantissas that sit on rounding boundaries --
+// all ones, all ones minus a few ulps, one plus a few ulps, runs of ones --
+// for divisor and dividend, exponents placing the quotient on both sides of
+// a binade boundary, and dividends that are rounded products y * (1 - 2^-k).
+__device__ __forceinline__ uint64_t hard_mant(uint64_t a, uint64_t b) {
+    const uint64_t full = 0xFFFFFFFFFFFFFull;
+    switch (a & 7) {
+        case 0: return full;
+        case 1: return full - (b & 0xFFF);
+        case 2: return b & 0xFFF;
+        case 3: return full & ~((1ull << (b % 52)) - 1ull);  // ones down to bit b % 52
+        case 4: return (1ull << (b % 52)) - 1ull;           // ones below bit b % 52
+        case 5: return (b & full) | 0xFFFFFull;             // random, low 20 bits set
+        case 6: return (b & full) & ~0xFFFFFull;            // random, low 20 bits clear
+        default: return b & full;
+    }
+}
+
+static __global__ void k_selftest_div_hard(uint64_t samples, uint64_t seed, unsigned long long* mism) {
+    uint64_t st = seed ^ ((uint64_t)(blockIdx.x * blockDim.x + threadIdx.x) * 0x9E3779B97F4A7C15ull);
+    unsigned long long bad = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < samples; i += stride) {
+        const uint64_t a = splitmix(st), b = splitmix(st), c = splitmix(st), d = splitmix(st);
+        const int ey = (int)(a % 82) - 60;  // y in [2^-60, 2^22): the fast range of durations
+        const double y = __longlong_as_double(((long long)(1023 + ey) << 52) | (long long)hard_mant(a >> 8, b));
+        double x;
+        if ((c & 3) == 0) {  // a rounded product y * (1 - 2^-k): remaining work just below a duration
+            const double frac = 1.0 - __longlong_as_double((long long)(1023 - 1 - (int)(d % 60)) << 52);
+            x = __dmul_rn(y, frac);
+        } else {
+            const int ex = ey + (int)((c >> 2) % 7) - 3 - (((c >> 5) & 7) == 0 ? (int)(d % 40) : 0);
+            x = __longlong_as_double(((long long)(1023 + ex) << 52) | (long long)hard_mant(c >> 8, d));
+        }
+        const double ry = __ddiv_rn(1.0, y);
+        if (divq<true>(x, y, ry) != __ddiv_rn(x, y)) ++bad;
+    }
+    for (int m = 16; m >= 1; m >>= 1) bad += __shfl_xor_sync(kFull, bad, m);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(mism, bad);
+}
+
 // DFMA throughput: 8 independent chains per thread.
 static __global__ void __launch_bounds__(256) k_fp64_peak(double* sink, int iters, double a, double b) {
     double x0 = threadIdx.x * 1e-9, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;

@@ -35,6 +35,8 @@ def test_device_present_and_library_loaded():
 def test_fast_division_matches_ieee():
     assert _capi.selftest_div(200_000_000, seed=7) == 0
     assert _capi.selftest_div(50_000_000, seed=12345) == 0
+    # adversarial operands: rounding-boundary mantissas, binade edges
+    assert _capi.selftest_div(500_000_000, seed=99, mode=1) == 0
 
 
 def test_timelines_bit_exact():
