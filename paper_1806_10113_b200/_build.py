@@ -22,7 +22,7 @@ SOURCES = [os.path.join(CSRC, f) for f in (
     "osim_batch_d2.cu", "osim_batch_d1.cu", "osim_heur.cu", "osim_null.cu", "osim_wide.cu",
     "osim_big.cu")]
 HEADERS = [os.path.join(CSRC, f) for f in (
-    "osim_sim.cuh", "osim_kernels.cuh", "osim_launch.cuh", "osim_deps.cuh", "osim_micro.cuh", "osim_harness.cuh", "osim_exh_impl.cuh", "osim_batch_impl.cuh", "osim_suftab.h", "osim_null.cuh", "osim_wide.cuh", "osim_heur_null.cuh", "osim_big.cuh")] + [
+    "osim_sim.cuh", "osim_kernels.cuh", "osim_launch.cuh", "osim_deps.cuh", "osim_micro.cuh", "osim_harness.cuh", "osim_exh_impl.cuh", "osim_batch_impl.cuh", "osim_suftab.h", "osim_null.cuh", "osim_wide.cuh", "osim_heur_null.cuh", "osim_big.cuh", "osim_heur_lane.cuh")] + [
     os.path.join(ROOT, "include", "offsim_b200.h")
 ]
 OBJDIR = os.path.join(PKG, "build")

@@ -1,16 +1,48 @@
 // osim_heur.cu -- instantiations and launch of the heuristic kernel.
 #include <cmath>
+#include <cstdlib>
 
 #include "osim_launch.cuh"
+#include "osim_heur_lane.cuh"
 #include "osim_heur_null.cuh"
 
 namespace osim {
+
+#ifndef OSIM_HEUR_LANE_DEFAULT
+#define OSIM_HEUR_LANE_DEFAULT 0
+#endif
+// which all-non-null heuristic kernel runs: k_heuristic_lane (one group per
+// lane) or k_heuristic_fast (8 groups per warp); OSIM_HEUR_LANE=0/1 overrides
+// the default (tuning only)
+static bool lane_kernel() {
+    static const bool v = [] {
+        const char* e = std::getenv("OSIM_HEUR_LANE");
+        return e ? std::atoi(e) != 0 : (OSIM_HEUR_LANE_DEFAULT != 0);
+    }();
+    return v;
+}
 
 void heuristic_launch(int dma, int mode, const LaunchCfg& cfg, const double* d_durs, const uint8_t* d_idr,
                       uint64_t B, int n, double sigma, int sum_mode, uint8_t* d_order, double* d_ms,
                       uint32_t* d_ns, int* d_err) {
     const unsigned grid = (unsigned)((B + kHG - 1) / kHG);
     const size_t sm = sizeof(HeurShared);
+    if (mode == 1 && lane_kernel()) {
+        const unsigned gl = (unsigned)((B + kHLT - 1) / kHLT);
+        const size_t sml = kHLW * kHLWarpSmem;
+        int e;
+        const bool sp2 = std::frexp(sigma, &e) == 0.5;
+#define OSIM_HLN(D, P)                                                                               \
+    do {                                                                                             \
+        auto kf = k_heuristic_lane<D, P>;                                                            \
+        cached_ctas_per_sm((const void*)kf, kHLT, sml); /* opts in to > 48 KB dynamic smem */        \
+        kf<<<gl, kHLT, sml, cfg.st>>>(d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms, d_ns);   \
+    } while (0)
+        if (dma == 2) { if (sp2) OSIM_HLN(2, true); else OSIM_HLN(2, false); }
+        else OSIM_HLN(1, false);
+#undef OSIM_HLN
+        return;
+    }
     if (mode == 1) {
         const unsigned gridf = (unsigned)((B + kHGF - 1) / kHGF);
         int e;

@@ -1051,7 +1051,7 @@ static_assert(kLPG * kWG == 32 && kWG <= 16, "groups per warp");
 #endif
 template <int DMA, bool SP2>
 struct HeurWarpShared {
-    using FS = FastSim<DMA, SP2, true, false, false, OSIM_HSPLIT != 0 && DMA == 2>;  // 1-DMA: measured slower
+    using FS = FastSim<DMA, SP2, true, false, false, (OSIM_HSPLIT != 0 && DMA == 2) ? 1 : 0>;  // 1-DMA: measured slower
     double2 dr[kWG * kHS];
     typename FS::Ck ck[kWG];
 #ifndef OSIM_HKREG

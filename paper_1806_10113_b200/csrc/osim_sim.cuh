@@ -371,6 +371,14 @@ __device__ __forceinline__ void start_if_split(bool p, uint32_t addr, double& nd
         : "+d"(nd), "+d"(rc), "+d"(rem)
         : "r"(addr), "r"((int)p));
 }
+// LAYOUT 2 of FastSim: nd and 1/nd in separate lane-interleaved arrays
+__device__ __forceinline__ void start_if_lanes(bool p, uint32_t addr, double& nd, double& rc, double& rem) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+        "@q ld.shared.f64 %0, [%3];\n\t@q ld.shared.f64 %1, [%3+12288];\n\t@q ld.shared.f64 %2, [%3];\n\t}"
+        : "+d"(nd), "+d"(rc), "+d"(rem)
+        : "r"(addr), "r"((int)p));
+}
 __device__ __forceinline__ void mul_if(bool p, double& x, double y) {
     asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q mul.rn.f64 %0, %0, %1;\n\t}"
         : "+d"(x) : "d"(y), "r"((int)p));
@@ -407,11 +415,28 @@ __device__ __forceinline__ uint32_t task_off(uint64_t seq, int sh) {
 // like `seq`.  With every stage non-null a task is finished exactly when its
 // DtH finalized, and DtHs finalize in sequence order, so the gate is one
 // extra condition on the HtD start: s1 >= 4 * (1 + prerequisite position).
-template <int DMA, bool SIGP2, bool TRACK, bool PRE, bool DEPS = false, bool SPLIT = false>
+// LAYOUT of the durations in shared memory:
+//  0: double2 {nd, 1/nd} rows [3][16] at `base` (kind k, task t at base + k*256 + t*16),
+//     one 16-byte + one 8-byte load per command start;
+//  1: the same rows, three 8-byte loads (start_if_split);
+//  2: lane-interleaved arrays nd[48][32], rc[48][32] (one group per lane; kind
+//     k, task t of lane l at base + (k*16 + t)*256 with base = array + 8*l,
+//     1/nd 12288 bytes above): a warp's 8-byte loads of 32 different
+//     (kind, task) entries are bank-conflict free.
+template <int DMA, bool SIGP2, bool TRACK, bool PRE, bool DEPS = false, int LAYOUT = 0>
 struct FastSim {
-    // a command start: {nd, 1/nd} and rem = nd from shared memory (SPLIT: three 8-byte loads)
+    static_assert(LAYOUT == 0 || !PRE, "pre-shifted sequences assume the double2 rows");
+    static constexpr int kDma = DMA;
+    static constexpr uint32_t KS = (LAYOUT == 2) ? 4096u : 256u;  // bytes per kind row
+    static constexpr uint32_t kRcOff = 48u * 256u;               // LAYOUT 2: 1/nd above nd
+    __device__ __forceinline__ static uint32_t toff(uint64_t sq, int sh) {
+        if constexpr (LAYOUT == 2) return ((uint32_t)(sq >> sh) & 0xFu) << 8;
+        else return task_off<PRE>(sq, sh);
+    }
+    // a command start: {nd, 1/nd} and rem = nd from shared memory
     __device__ __forceinline__ static void st_(bool p, uint32_t addr, double& nd, double& rc, double& rem) {
-        if constexpr (SPLIT) start_if_split(p, addr, nd, rc, rem);
+        if constexpr (LAYOUT == 1) start_if_split(p, addr, nd, rc, rem);
+        else if constexpr (LAYOUT == 2) start_if_lanes(p, addr, nd, rc, rem);
         else start_if(p, addr, nd, rc, rem);
     }
     uint32_t base;
@@ -440,7 +465,7 @@ struct FastSim {
     __device__ __forceinline__ void set_seq(uint64_t sq) { seq = PRE ? (sq << 4) : sq; }
     // start the HtD at the queue head now (the HtD lane is idle and an HtD
     // is always ready): what the next step's start phase would do
-    __device__ __forceinline__ void start_htd() { st_(true, base + task_off<PRE>(seq, s0), d0, c0, r0); }
+    __device__ __forceinline__ void start_htd() { st_(true, base + toff(seq, s0), d0, c0, r0); }
     __device__ __forceinline__ int finalized() const { return (s0 + s1 + s2) >> 2; }
 
     // checkpoint image (prefix sharing across calls, e.g. in shared memory)
@@ -480,8 +505,8 @@ struct FastSim {
         const bool st2 = idle(r2) && s2 < n4;
         const bool st1 = idle(r1) && s1 < s2;
         k_idle_gap(st2);
-        st_(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
-        st_(st1, base + 512 + task_off<PRE>(seq, s1), d1, c1, r1);
+        st_(st2, base + KS + toff(seq, s2), d2, c2, r2);
+        st_(st1, base + 2 * KS + toff(seq, s1), d1, c1, r1);
         const double dt = dmin(r1, r2);
         now = __dadd_rn(now, dt);
         r2 = upd(r2, dt, d2, c2);
@@ -498,7 +523,7 @@ struct FastSim {
     __device__ __forceinline__ void step_d() {
         static_assert(DMA == 2, "2-DMA only");
         const bool st1 = idle(r1) && s1 < n4;
-        st_(st1, base + 512 + task_off<PRE>(seq, s1), d1, c1, r1);
+        st_(st1, base + 2 * KS + toff(seq, s1), d1, c1, r1);
         const double dt = r1;  // the only lane that can run (rem ~0 once drained)
         now = __dadd_rn(now, dt);
         r1 = upd(r1, dt, d1, c1);
@@ -518,8 +543,8 @@ struct FastSim {
         const bool st0 = idle(r0) && s0 < 2 * n4 && s2 > ps;
         const bool st2 = idle(r2) && s2 < n4;
         k_idle_gap(st2);
-        st_(st0, base + 512u + task_off<PRE>(seq, ps), d0, c0, r0);
-        st_(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
+        st_(st0, base + 2 * KS + toff(seq, ps), d0, c0, r0);
+        st_(st2, base + KS + toff(seq, s2), d2, c2, r2);
         const double dt = dmin(r0, r2);
         now = __dadd_rn(now, dt);
         r0 = upd(r0, dt, d0, c0);
@@ -542,8 +567,8 @@ struct FastSim {
         const bool st0 = idle(r0) && s0 < 2 * n4 && s2 > ps;
         const bool st2 = idle(r2) && s2 < n4 && s2 < s0;
         k_idle_gap(st2);
-        st_(st0, base + 512u + task_off<PRE>(seq, ps), d0, c0, r0);
-        st_(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
+        st_(st0, base + 2 * KS + toff(seq, ps), d0, c0, r0);
+        st_(st2, base + KS + toff(seq, s2), d2, c2, r2);
         const double dt = dmin(r0, r2);
         now = __dadd_rn(now, dt);
         r0 = upd(r0, dt, d0, c0);
@@ -560,7 +585,7 @@ struct FastSim {
     __device__ __forceinline__ void step_1dd() {
         static_assert(DMA == 1, "1-DMA only");
         const bool st0 = idle(r0) && s0 < 2 * n4;
-        st_(st0, base + 512u + task_off<PRE>(seq, s0 - n4), d0, c0, r0);
+        st_(st0, base + 2 * KS + toff(seq, s0 - n4), d0, c0, r0);
         const double dt = r0;  // the only lane that can run (rem ~0 once drained)
         now = __dadd_rn(now, dt);
         r0 = upd(r0, dt, d0, c0);
@@ -639,17 +664,17 @@ struct FastSim {
             const bool st2 = idle(r2) && s2 < s0;
             const bool st1 = idle(r1) && s1 < s2;
             k_idle_gap(st2);
-            if constexpr (H0) st_(st0, base + task_off<PRE>(seq, s0), d0, c0, r0);
-            st_(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
-            st_(st1, base + 512 + task_off<PRE>(seq, s1), d1, c1, r1);
+            if constexpr (H0) st_(st0, base + toff(seq, s0), d0, c0, r0);
+            st_(st2, base + KS + toff(seq, s2), d2, c2, r2);
+            st_(st1, base + 2 * KS + toff(seq, s1), d1, c1, r1);
         } else {
             const bool isH = s0 < n4;
             const int ps = isH ? s0 : s0 - n4;
             const bool st0 = idle(r0) && s0 < 2 * n4 && (isH || s2 > ps);
             const bool st2 = idle(r2) && s2 < n4 && s2 < s0;
             k_idle_gap(st2);
-            st_(st0, base + (isH ? 0u : 512u) + task_off<PRE>(seq, ps), d0, c0, r0);
-            st_(st2, base + 256 + task_off<PRE>(seq, s2), d2, c2, r2);
+            st_(st0, base + (isH ? 0u : 2 * KS) + toff(seq, ps), d0, c0, r0);
+            st_(st2, base + KS + toff(seq, s2), d2, c2, r2);
         }
         // ---- dt (engine.py:200-210)
         double dt, dd;
