@@ -5,9 +5,10 @@
 // 8*m candidates over the 32 lanes: ceil(m/4) iterations leave 15 % of the
 // lane slots empty, and the per-group serial phases (key argmin, checkpoint
 // advance) run on 8 of 32 lanes.  Here every lane owns a group and walks its
-// round's m candidates itself, two at a time (two independent simulations
-// interleaved in one instruction stream for ILP), so only odd m wastes a
-// slot (6 %) and every serial phase runs on all 32 lanes.  The checkpoint of
+// round's m candidates itself, kHLILP at a time (independent simulations
+// interleaved in one instruction stream for ILP: with 9 warps per SM the
+// kernel needs it to keep the issue slots busy), so only the last partial
+// set of a round wastes slots and every serial phase runs on all 32 lanes.  The checkpoint of
 // simulate(ot) (prefix sharing) lives in registers; the
 // group's durations live in shared memory in FastSim LAYOUT 2 (nd and 1/nd
 // arrays interleaved by lane, bank-conflict free).  Shared memory per warp:
@@ -26,70 +27,84 @@ constexpr int kHLW = 3;                                     // warps per CTA
 constexpr int kHLT = 32 * kHLW;                             // threads per CTA
 constexpr size_t kHLWarpSmem = 2 * 48 * 32 * sizeof(double);  // nd + 1/nd, [48][32] each
 
-// Two simulations stepped in one loop (independent instruction streams):
-// FastSim::run_phased for a pair of lanes' worth of work.
-template <bool H0, class FS>
-__device__ __forceinline__ void run_pair(FS& a, FS& b, int rest, double sigma, double rsig) {
+#ifndef OSIM_HL_ILP
+#define OSIM_HL_ILP 3
+#endif
+constexpr int kHLILP = OSIM_HL_ILP;  // candidates per lane stepped together
+
+// ILP simulations stepped in one loop (independent instruction streams):
+// FastSim::run_phased for several candidates of a lane at once.
+template <bool H0, int P, class FS>
+__device__ __forceinline__ void run_multi(FS (&s)[P], int rest, double sigma, double rsig) {
     int st = 0;
     constexpr int DMA = FS::kDma;
+    auto all_h = [&]() {
+        bool d = true;
+#pragma unroll
+        for (int i = 0; i < P; ++i) d = d && s[i].s0 >= s[i].n4;
+        return __all_sync(kFull, d);
+    };
+    auto all_k = [&]() {
+        bool d = true;
+#pragma unroll
+        for (int i = 0; i < P; ++i) d = d && s[i].s2 >= s[i].n4;
+        return __all_sync(kFull, d);
+    };
     if constexpr (DMA == 2) {
 #pragma unroll 1
         for (; st < rest; st += 2) {
-            if (__all_sync(kFull, a.s0 >= a.n4 && b.s0 >= b.n4)) break;
-            a.template step<H0>(sigma, rsig);
-            b.template step<H0>(sigma, rsig);
-            a.template step<H0>(sigma, rsig);
-            b.template step<H0>(sigma, rsig);
+            if (all_h()) break;
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int i = 0; i < P; ++i) s[i].template step<H0>(sigma, rsig);
         }
 #pragma unroll 1
         for (; st < rest; st += 2) {
-            if (__all_sync(kFull, a.s2 >= a.n4 && b.s2 >= b.n4)) break;
-            a.step_kd();
-            b.step_kd();
-            a.step_kd();
-            b.step_kd();
+            if (all_k()) break;
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int i = 0; i < P; ++i) s[i].step_kd();
         }
 #pragma unroll 1
-        for (; st < rest; ++st) {
-            a.step_d();
-            b.step_d();
-        }
+        for (; st < rest; ++st)
+#pragma unroll
+            for (int i = 0; i < P; ++i) s[i].step_d();
     } else if constexpr (H0) {
 #pragma unroll 1
         for (; st < rest; st += 2) {
-            if (__all_sync(kFull, a.s0 >= a.n4 && b.s0 >= b.n4)) break;
-            a.step(sigma, rsig);
-            b.step(sigma, rsig);
-            a.step(sigma, rsig);
-            b.step(sigma, rsig);
+            if (all_h()) break;
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int i = 0; i < P; ++i) s[i].step(sigma, rsig);
         }
 #pragma unroll 1
         for (; st < rest; st += 2) {
-            if (__all_sync(kFull, a.s2 >= a.n4 && b.s2 >= b.n4)) break;
-            a.step_1d();
-            b.step_1d();
-            a.step_1d();
-            b.step_1d();
+            if (all_k()) break;
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int i = 0; i < P; ++i) s[i].step_1d();
         }
 #pragma unroll 1
-        for (; st < rest; ++st) {
-            a.step_1dd();
-            b.step_1dd();
-        }
+        for (; st < rest; ++st)
+#pragma unroll
+            for (int i = 0; i < P; ++i) s[i].step_1dd();
     } else {
 #pragma unroll 1
         for (; st < rest; st += 2) {
-            if (__all_sync(kFull, a.s2 >= a.n4 && b.s2 >= b.n4)) break;
-            a.step_1dk();
-            b.step_1dk();
-            a.step_1dk();
-            b.step_1dk();
+            if (all_k()) break;
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int i = 0; i < P; ++i) s[i].step_1dk();
         }
 #pragma unroll 1
-        for (; st < rest; ++st) {
-            a.step_1dd();
-            b.step_1dd();
-        }
+        for (; st < rest; ++st)
+#pragma unroll
+            for (int i = 0; i < P; ++i) s[i].step_1dd();
     }
 }
 
@@ -110,15 +125,15 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
     const uint64_t g = g0 + lane;
     const bool live = g < B;
     const int Gv = (int)((B - g0) < 32 ? (B - g0) : 32);
-    // stage the warp's groups (contiguous in HBM) with coalesced loads: entry
-    // (kind k, task t) of lane gi at [(k*16 + t)*32 + gi]; tasks >= n get 1.0
-    for (int e = lane; e < 48 * 32; e += 32) {
-        const int gi = e / 48, r = e % 48, t = r / 3, k = r % 3;
-        const int idx = (k * 16 + t) * 32 + gi;
-        double v = 1.0;
-        if (gi < Gv && t < n) v = durs[(g0 + gi) * 3 * (uint64_t)n + 3 * t + k];
-        nd[idx] = v;  // every (k, t, gi) exactly once
-        rcp[idx] = __ddiv_rn(1.0, v);
+    // stage this lane's group: entry (kind k, task t) at [(k*16 + t)*32 + lane]
+    // (bank-conflict-free stores; the strided loads hit L1 after the first
+    // touch of each line); tasks >= n get 1.0
+    (void)Gv;
+    for (int kt = 0; kt < 48; ++kt) {
+        const int k = kt >> 4, t = kt & 15;
+        const double v = (live && t < n) ? durs[g * 3 * (uint64_t)n + 3 * t + k] : 1.0;
+        nd[kt * 32 + lane] = v;
+        rcp[kt * 32 + lane] = __ddiv_rn(1.0, v);
     }
     __syncwarp();
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(nd) + 8u * (uint32_t)lane;
@@ -171,46 +186,50 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
         int bj = -1;
         double be = 0, bd = 0;
         int br = 0;
-        for (int j = 0; j < m; j += 2) {
-            const bool two = j + 1 < m;
-            const int ja = j, jb = two ? j + 1 : j;
-            const int ca = rt_at(cand, ja), cb = rt_at(cand, jb);
-            FS sa, sb;
-            sa.init(base, ot | ((uint64_t)ca << (4 * k)), k + 1);
-            sb.init(base, ot | ((uint64_t)cb << (4 * k)), k + 1);
-            sa.load(ck);
-            sb.load(ck);
-            sa.start_htd();
-            sb.start_htd();
-            run_pair<false>(sa, sb, rest, sigma, rsig);
-            // _completion_estimate (heuristic.py:34-49) of both: CPython's sum of the
-            // rest's t_k in rt order, min t_dth
-            double fa = 0.0, ea = 0.0, ta = kBig, fb = 0.0, eb = 0.0, tb = kBig;
-            uint64_t la = rt_drop(cand, ja), lb = rt_drop(cand, jb);
-#pragma unroll 2
-            for (int i = 0; i < m - 1; ++i, la >>= 4, lb >>= 4) {
-                const int ua = (int)(la & 0xF), ub = (int)(lb & 0xF);
-                const double xa = DV(1, ua), xb = DV(1, ub);
-                const double sa_ = __dadd_rn(fa, xa), sb_ = __dadd_rn(fb, xb);
-                if (sum_mode) {  // Neumaier (CPython >= 3.12): TwoSum error of f + x
-                    const double pa = __dsub_rn(sa_, fa), pb = __dsub_rn(sb_, fb);
-                    ea = __dadd_rn(ea, __dadd_rn(__dsub_rn(fa, __dsub_rn(sa_, pa)), __dsub_rn(xa, pa)));
-                    eb = __dadd_rn(eb, __dadd_rn(__dsub_rn(fb, __dsub_rn(sb_, pb)), __dsub_rn(xb, pb)));
-                }
-                fa = sa_;
-                fb = sb_;
-                ta = dmin(DV(2, ua), ta);
-                tb = dmin(DV(2, ub), tb);
+        for (int j = 0; j < m; j += kHLILP) {
+            int cj[kHLILP], cc[kHLILP];
+            FS sim[kHLILP];
+#pragma unroll
+            for (int i = 0; i < kHLILP; ++i) {
+                cj[i] = (j + i < m) ? j + i : m - 1;  // a surplus slot repeats the last candidate
+                cc[i] = rt_at(cand, cj[i]);
+                sim[i].init(base, ot | ((uint64_t)cc[i] << (4 * k)), k + 1);
+                sim[i].load(ck);
+                sim[i].start_htd();
             }
-            if (sum_mode && ea != 0.0 && isfinite(ea)) fa = __dadd_rn(fa, ea);
-            if (sum_mode && eb != 0.0 && isfinite(eb)) fb = __dadd_rn(fb, eb);
-            const double bound_a = __dadd_rn(__dadd_rn(sa.kEnd, fa), ta);
-            const double bound_b = __dadd_rn(__dadd_rn(sb.kEnd, fb), tb);
-            const double est_a = (bound_a > sa.now) ? bound_a : sa.now;
-            const double est_b = (bound_b > sb.now) ? bound_b : sb.now;
-            const int ra = IR(ca), rb = IR(cb);
-            if (bj < 0 || key_less(est_a, sa.idleK, ra, be, bd, br)) { bj = ja; be = est_a; bd = sa.idleK; br = ra; }
-            if (two && key_less(est_b, sb.idleK, rb, be, bd, br)) { bj = jb; be = est_b; bd = sb.idleK; br = rb; }
+            run_multi<false>(sim, rest, sigma, rsig);
+            // _completion_estimate (heuristic.py:34-49): CPython's sum of the
+            // rest's t_k in rt order, min t_dth
+            double f[kHLILP], e[kHLILP], tl[kHLILP];
+            uint64_t rl[kHLILP];
+#pragma unroll
+            for (int i = 0; i < kHLILP; ++i) { f[i] = 0.0; e[i] = 0.0; tl[i] = kBig; rl[i] = rt_drop(cand, cj[i]); }
+#pragma unroll 2
+            for (int q = 0; q < m - 1; ++q) {
+#pragma unroll
+                for (int i = 0; i < kHLILP; ++i) {
+                    const int u = (int)(rl[i] & 0xF);
+                    rl[i] >>= 4;
+                    const double x = DV(1, u);
+                    const double t = __dadd_rn(f[i], x);
+                    if (sum_mode) {  // Neumaier (CPython >= 3.12): TwoSum error of f + x
+                        const double p = __dsub_rn(t, f[i]);
+                        e[i] = __dadd_rn(e[i], __dadd_rn(__dsub_rn(f[i], __dsub_rn(t, p)), __dsub_rn(x, p)));
+                    }
+                    f[i] = t;
+                    tl[i] = dmin(DV(2, u), tl[i]);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < kHLILP; ++i) {
+                if (sum_mode && e[i] != 0.0 && isfinite(e[i])) f[i] = __dadd_rn(f[i], e[i]);
+                const double bound = __dadd_rn(__dadd_rn(sim[i].kEnd, f[i]), tl[i]);
+                const double est = (bound > sim[i].now) ? bound : sim[i].now;
+                const int r = IR(cc[i]);
+                if (j + i < m && (bj < 0 || key_less(est, sim[i].idleK, r, be, bd, br))) {
+                    bj = cj[i]; be = est; bd = sim[i].idleK; br = r;
+                }
+            }
         }
         OSIM_DCHECK(bj >= 0 && bj < m);
         const int c = rt_at(cand, bj);
@@ -234,14 +253,14 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
     if (n >= 2) {
         int a = rt_at(cand, 0), b = rt_at(cand, 1);
         if (IR(b) < IR(a)) { const int x = a; a = b; b = x; }
-        FS sa, sb;
-        sa.init(base, ot | ((uint64_t)a << (4 * kl)) | ((uint64_t)b << (4 * (kl + 1))), n);
-        sb.init(base, ot | ((uint64_t)b << (4 * kl)) | ((uint64_t)a << (4 * (kl + 1))), n);
-        sa.load(ck);
-        sb.load(ck);
-        const int rest = __reduce_max_sync(kFull, 3 * n - sa.finalized());
-        run_pair<true>(sa, sb, rest, sigma, rsig);
-        const double m_ab = sa.now, m_ba = sb.now;
+        FS sp[2];
+        sp[0].init(base, ot | ((uint64_t)a << (4 * kl)) | ((uint64_t)b << (4 * (kl + 1))), n);
+        sp[1].init(base, ot | ((uint64_t)b << (4 * kl)) | ((uint64_t)a << (4 * (kl + 1))), n);
+        sp[0].load(ck);
+        sp[1].load(ck);
+        const int rest = __reduce_max_sync(kFull, 3 * n - sp[0].finalized());
+        run_multi<true>(sp, rest, sigma, rsig);
+        const double m_ab = sp[0].now, m_ba = sp[1].now;
         bool ab;
         if (m_ab < m_ba) ab = true;
         else if (m_ba < m_ab) ab = false;
