@@ -9,7 +9,7 @@
 namespace osim {
 
 #ifndef OSIM_HEUR_LANE_DEFAULT
-#define OSIM_HEUR_LANE_DEFAULT 0
+#define OSIM_HEUR_LANE_DEFAULT 1
 #endif
 // which all-non-null heuristic kernel runs: k_heuristic_lane (one group per
 // lane) or k_heuristic_fast (8 groups per warp); OSIM_HEUR_LANE=0/1 overrides

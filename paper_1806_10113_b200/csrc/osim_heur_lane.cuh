@@ -23,14 +23,21 @@
 
 namespace osim {
 
-constexpr int kHLW = 3;                                     // warps per CTA
+#ifndef OSIM_HL_W
+#define OSIM_HL_W 1
+#endif
+// warps per CTA: one, so a finished warp's slot is refilled at once (the
+// warps of a CTA are independent; a CTA's slot frees only when all finish)
+constexpr int kHLW = OSIM_HL_W;
 constexpr int kHLT = 32 * kHLW;                             // threads per CTA
 constexpr size_t kHLWarpSmem = 2 * 48 * 32 * sizeof(double);  // nd + 1/nd, [48][32] each
 
 #ifndef OSIM_HL_ILP
-#define OSIM_HL_ILP 3
+#define OSIM_HL_ILP 0  // 0: the measured best per DMA mode
 #endif
-constexpr int kHLILP = OSIM_HL_ILP;  // candidates per lane stepped together
+// candidates per lane stepped together (2-DMA: 2, 1-DMA: 3 measured best)
+template <int DMA>
+__host__ __device__ constexpr int hl_ilp() { return OSIM_HL_ILP > 0 ? OSIM_HL_ILP : (DMA == 2 ? 2 : 3); }
 
 // ILP simulations stepped in one loop (independent instruction streams):
 // FastSim::run_phased for several candidates of a lane at once.
@@ -116,6 +123,7 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
                                                          double* __restrict__ ms_out,
                                                          uint32_t* __restrict__ nsims_out) {
     using FS = FastSim<DMA, SP2, true, false, false, 2>;
+    constexpr int kHLILP = hl_ilp<DMA>();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* nd = reinterpret_cast<double*>(smem_raw + warp * kHLWarpSmem);  // [48][32]
