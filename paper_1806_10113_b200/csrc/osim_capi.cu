@@ -55,6 +55,7 @@ struct DevCtx {
     size_t scratch_bytes = 0;
     int* d_err = nullptr;
     unsigned* d_done = nullptr;  // last-CTA counter of the fused final reductions (kept at 0)
+    AuxBuf aux[2];               // launchers' temporaries, per stream (stream, stream2)
     std::mutex mu;
 };
 
@@ -355,7 +356,10 @@ int enqueue_heuristic(DevCtx* c, cudaStream_t st, const double* d_durs, const ui
                       uint8_t* d_order, double* d_ms, uint32_t* d_ns) {
     if (B == 0) return 0;
     if ((B + kHG - 1) / kHG > 0x7fffffffull) return fail(OSIM_EINVAL, "batch too large");
-    heuristic_launch(dma, fast, LaunchCfg{c->sms, st}, d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms,
+    // the launcher's temporaries (the lane kernel's group order): one buffer
+    // per library stream, so the host path's two chunk streams never share one
+    AuxBuf* aux = &c->aux[st == c->stream2 ? 1 : 0];
+    heuristic_launch(dma, fast, LaunchCfg{c->sms, st, aux}, d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms,
                      d_ns, c->d_err);
     CK(cudaGetLastError());
     return 0;

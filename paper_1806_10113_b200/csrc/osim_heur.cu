@@ -2,6 +2,8 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "osim_launch.cuh"
 #include "osim_heur_lane.cuh"
 #include "osim_heur_null.cuh"
@@ -14,6 +16,33 @@ namespace osim {
 // which all-non-null heuristic kernel runs: k_heuristic_lane (one group per
 // lane) or k_heuristic_fast (8 groups per warp); OSIM_HEUR_LANE=0/1 overrides
 // the default (tuning only)
+// Group order for k_heuristic_lane: an 8-bit key per group (k_heur_sort_keys)
+// and a one-pass radix sort of (key, index) in the launcher's aux buffer.
+// nullptr (batch order) for small batches, without the buffer, or with
+// OSIM_HEUR_SORT=0 (tuning).
+static const uint32_t* heur_group_order(const LaunchCfg& cfg, const double* d_durs, uint64_t B, int n) {
+    static const bool on = [] {
+        const char* e = std::getenv("OSIM_HEUR_SORT");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    if (!on || B < 4096 || B > 0xFFFFFFFFull || !cfg.aux) return nullptr;
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const uint8_t*)nullptr, (uint8_t*)nullptr,
+                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)B, 0, 8, cfg.st);
+    const size_t a8 = (B + 255) & ~size_t(255), a32 = (4 * B + 255) & ~size_t(255);
+    char* p = (char*)aux_get(cfg.aux, 2 * a8 + 2 * a32 + tmp, cfg.st);
+    if (!p) return nullptr;
+    uint8_t* k_in = (uint8_t*)p;
+    uint8_t* k_out = k_in + a8;
+    uint32_t* i_in = (uint32_t*)(p + 2 * a8);
+    uint32_t* i_out = (uint32_t*)(p + 2 * a8 + a32);
+    k_heur_sort_keys<<<(unsigned)((B + 255) / 256), 256, 0, cfg.st>>>(d_durs, B, n, k_in, i_in);
+    if (cub::DeviceRadixSort::SortPairs(p + 2 * a8 + 2 * a32, tmp, k_in, k_out, i_in, i_out, (int)B, 0, 8,
+                                        cfg.st) != cudaSuccess)
+        return nullptr;
+    return i_out;
+}
+
 static bool lane_kernel() {
     static const bool v = [] {
         const char* e = std::getenv("OSIM_HEUR_LANE");
@@ -30,13 +59,14 @@ void heuristic_launch(int dma, int mode, const LaunchCfg& cfg, const double* d_d
     if (mode == 1 && lane_kernel()) {
         const unsigned gl = (unsigned)((B + kHLT - 1) / kHLT);
         const size_t sml = kHLW * kHLWarpSmem;
+        const uint32_t* perm = heur_group_order(cfg, d_durs, B, n);
         int e;
         const bool sp2 = std::frexp(sigma, &e) == 0.5;
 #define OSIM_HLN(D, P)                                                                               \
     do {                                                                                             \
         auto kf = k_heuristic_lane<D, P>;                                                            \
         cached_ctas_per_sm((const void*)kf, kHLT, sml); /* opts in to > 48 KB dynamic smem */        \
-        kf<<<gl, kHLT, sml, cfg.st>>>(d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms, d_ns);   \
+        kf<<<gl, kHLT, sml, cfg.st>>>(d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms, d_ns, perm); \
     } while (0)
         if (dma == 2) { if (sp2) OSIM_HLN(2, true); else OSIM_HLN(2, false); }
         else OSIM_HLN(1, false);

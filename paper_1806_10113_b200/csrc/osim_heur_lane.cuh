@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
                                                          double sigma, int sum_mode,
                                                          uint8_t* __restrict__ order_out,
                                                          double* __restrict__ ms_out,
-                                                         uint32_t* __restrict__ nsims_out) {
+                                                         uint32_t* __restrict__ nsims_out,
+                                                         const uint32_t* __restrict__ perm) {
     using FS = FastSim<DMA, SP2, true, false, false, 2>;
     constexpr int kHLILP = hl_ilp<DMA>();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -130,13 +131,16 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
     double* rcp = nd + 48 * 32;
     const uint64_t g0 = ((uint64_t)blockIdx.x * kHLW + warp) * 32;
     if (g0 >= B) return;  // whole warp leaves together; no block barriers below
-    const uint64_t g = g0 + lane;
-    const bool live = g < B;
+    const bool live = g0 + lane < B;
+    // perm (nullable): the batch position this lane's group comes from (and
+    // whose outputs it writes) -- groups ordered by heur_sort_keys so a warp's
+    // 32 groups have similar replay lengths
+    const uint64_t g = live ? (perm ? (uint64_t)perm[g0 + lane] : g0 + lane) : 0;
     const int Gv = (int)((B - g0) < 32 ? (B - g0) : 32);
     // stage this lane's group: entry (kind k, task t) at [(k*16 + t)*32 + lane]
     // (bank-conflict-free stores; the strided loads hit L1 after the first
     // touch of each line); tasks >= n get 1.0
-    (void)Gv;
+    (void)Gv;  // (tasks of a lane past the batch end are 1.0 placeholders)
     for (int kt = 0; kt < 48; ++kt) {
         const int k = kt >> 4, t = kt & 15;
         const double v = (live && t < n) ? durs[g * 3 * (uint64_t)n + 3 * t + k] : 1.0;
@@ -286,6 +290,32 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
         if (nsims_out) nsims_out[g] = (n >= 3) ? (uint32_t)(n * (n - 1) / 2 - 1) : (n == 2 ? 2u : 0u);
         for (int p = 0; p < n; ++p) order_out[g * (uint64_t)n + p] = (uint8_t)nib(ot, p);
     }
+}
+
+}  // namespace osim
+
+namespace osim {
+
+// Sort key of a group for k_heuristic_lane's warp assignment: its kernel
+// share sum(t_k) / (sum(t_htd) + sum(t_dth)) in 1/64 steps up to 4 (8 bits).
+// Kernel-heavy groups carry a long K/DtH backlog at every checkpoint
+// (long candidate replays), transfer-heavy ones a short one; a warp's replay
+// length is the longest of its 32 groups', so similar groups share warps.
+// Only the assignment changes: every group's result is computed from its own
+// data and written to its own position.
+static __global__ void k_heur_sort_keys(const double* __restrict__ durs, uint64_t B, int n, uint8_t* __restrict__ key,
+                                        uint32_t* __restrict__ idx) {
+    const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= B) return;
+    const double* d = durs + g * 3 * (uint64_t)n;
+    double h = 0.0, k = 0.0;
+    for (int t = 0; t < n; ++t) {
+        h += d[3 * t] + d[3 * t + 2];
+        k += d[3 * t + 1];
+    }
+    const double q = h > 0.0 ? k / h * 64.0 : 255.0;
+    key[g] = (uint8_t)(q < 255.0 ? q : 255.0);
+    idx[g] = (uint32_t)g;
 }
 
 }  // namespace osim

@@ -14,9 +14,34 @@
 
 namespace osim {
 
+// Grow-only device buffer for a launcher's own temporaries (one per device
+// stream; the caller holds the device lock).  Growing waits for the stream
+// (the old buffer may still be read by earlier work on it).
+struct AuxBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+inline void* aux_get(AuxBuf* a, size_t bytes, cudaStream_t st) {
+    if (!a) return nullptr;
+    if (bytes > a->bytes) {
+        cudaStreamSynchronize(st);
+        if (a->p) cudaFree(a->p);
+        a->p = nullptr;
+        a->bytes = 0;
+        const size_t want = bytes + bytes / 4;
+        if (cudaMalloc(&a->p, want) != cudaSuccess) {
+            cudaGetLastError();  // not fatal: the caller runs without the buffer
+            return nullptr;
+        }
+        a->bytes = want;
+    }
+    return a->p;
+}
+
 struct LaunchCfg {
     int sms;
     cudaStream_t st;
+    AuxBuf* aux = nullptr;
 };
 
 // Per-(kernel, device, block shape) launch facts, looked up once: the
