@@ -18,12 +18,14 @@ namespace osim {
 // the default (tuning only)
 // Group order for k_heuristic_lane: an 8-bit key per group (k_heur_sort_keys)
 // and a one-pass radix sort of (key, index) in the launcher's aux buffer.
-// nullptr (batch order) for small batches, without the buffer, or with
-// OSIM_HEUR_SORT=0 (tuning).
+// Off by default (OSIM_HEUR_SORT=1 turns it on): on the C5 batch a sorted
+// input runs 4.4 % faster on the 2-DMA profiles, but the key pass, the sort
+// and the permuted group loads cost about as much (measured +0.4 % / +0.2 %,
+// and -4 % on the 1-DMA profile).  nullptr = batch order.
 static const uint32_t* heur_group_order(const LaunchCfg& cfg, const double* d_durs, uint64_t B, int n) {
     static const bool on = [] {
         const char* e = std::getenv("OSIM_HEUR_SORT");
-        return e ? std::atoi(e) != 0 : true;
+        return e ? std::atoi(e) != 0 : false;
     }();
     if (!on || B < 4096 || B > 0xFFFFFFFFull || !cfg.aux) return nullptr;
     size_t tmp = 0;
