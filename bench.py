@@ -142,7 +142,6 @@ class Dist:
             # NCCL's init lines (communicator size, transport) on stderr, so
             # the run log shows every rank joined one communicator
             os.environ.setdefault("NCCL_DEBUG", "INFO")
-            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             tdist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
