@@ -39,6 +39,11 @@ constexpr size_t kHLWarpSmem = 2 * 48 * 32 * sizeof(double);  // nd + 1/nd, [48]
 template <int DMA>
 __host__ __device__ constexpr int hl_ilp() { return OSIM_HL_ILP > 0 ? OSIM_HL_ILP : (DMA == 2 ? 2 : 3); }
 
+#ifndef OSIM_HL_UNR
+#define OSIM_HL_UNR 2
+#endif
+constexpr int kHLU = OSIM_HL_UNR;  // steps per phase test (warp vote)
+
 // ILP simulations stepped in one loop (independent instruction streams):
 // FastSim::run_phased for several candidates of a lane at once.
 template <bool H0, int P, class FS>
@@ -59,18 +64,18 @@ __device__ __forceinline__ void run_multi(FS (&s)[P], int rest, double sigma, do
     };
     if constexpr (DMA == 2) {
 #pragma unroll 1
-        for (; st < rest; st += 2) {
+        for (; st < rest; st += kHLU) {
             if (all_h()) break;
 #pragma unroll
-            for (int r = 0; r < 2; ++r)
+            for (int r = 0; r < kHLU; ++r)
 #pragma unroll
                 for (int i = 0; i < P; ++i) s[i].template step<H0>(sigma, rsig);
         }
 #pragma unroll 1
-        for (; st < rest; st += 2) {
+        for (; st < rest; st += kHLU) {
             if (all_k()) break;
 #pragma unroll
-            for (int r = 0; r < 2; ++r)
+            for (int r = 0; r < kHLU; ++r)
 #pragma unroll
                 for (int i = 0; i < P; ++i) s[i].step_kd();
         }
@@ -80,18 +85,18 @@ __device__ __forceinline__ void run_multi(FS (&s)[P], int rest, double sigma, do
             for (int i = 0; i < P; ++i) s[i].step_d();
     } else if constexpr (H0) {
 #pragma unroll 1
-        for (; st < rest; st += 2) {
+        for (; st < rest; st += kHLU) {
             if (all_h()) break;
 #pragma unroll
-            for (int r = 0; r < 2; ++r)
+            for (int r = 0; r < kHLU; ++r)
 #pragma unroll
                 for (int i = 0; i < P; ++i) s[i].step(sigma, rsig);
         }
 #pragma unroll 1
-        for (; st < rest; st += 2) {
+        for (; st < rest; st += kHLU) {
             if (all_k()) break;
 #pragma unroll
-            for (int r = 0; r < 2; ++r)
+            for (int r = 0; r < kHLU; ++r)
 #pragma unroll
                 for (int i = 0; i < P; ++i) s[i].step_1d();
         }
@@ -101,10 +106,10 @@ __device__ __forceinline__ void run_multi(FS (&s)[P], int rest, double sigma, do
             for (int i = 0; i < P; ++i) s[i].step_1dd();
     } else {
 #pragma unroll 1
-        for (; st < rest; st += 2) {
+        for (; st < rest; st += kHLU) {
             if (all_k()) break;
 #pragma unroll
-            for (int r = 0; r < 2; ++r)
+            for (int r = 0; r < kHLU; ++r)
 #pragma unroll
                 for (int i = 0; i < P; ++i) s[i].step_1dk();
         }
