@@ -25,10 +25,12 @@ from paper_1806_10113_b200.heuristic import SUM_MODE  # noqa: E402
 SIGMAS = (1.0, 0.5, 0.375, 0.8, 0.25, 0.125, 0.9999999999999999)
 
 
-def durations(rng, n):
+def durations(rng, n, nulls=True):
+    """Random stage durations in four regimes; nulls=False keeps every stage
+    non-null (the all-non-null kernels: k_exhaustive_pfx, k_heuristic_lane)."""
     mode = rng.integers(4)
     if mode == 0:
-        d = rng.integers(0, 5, (n, 3)).astype(np.float64)
+        d = rng.integers(0 if nulls else 1, 5, (n, 3)).astype(np.float64)
     elif mode == 1:
         d = np.where(rng.random((n, 3)) < 0.5, rng.integers(1, 4, (n, 3)).astype(np.float64),
                      rng.uniform(0.1, 5.0, (n, 3)))
@@ -36,7 +38,8 @@ def durations(rng, n):
         d = rng.uniform(0.01, 10.0, (n, 3))
     else:
         d = np.exp(rng.uniform(np.log(1e-6), np.log(1e8), (n, 3)))  # wide range (above 2^22 ms: general path)
-    d[rng.random((n, 3)) < (0.15 if mode else 0.0)] = 0.0
+    if nulls:
+        d[rng.random((n, 3)) < (0.15 if mode else 0.0)] = 0.0
     empty = d.sum(axis=1) == 0.0
     d[empty, 1] = 1.0  # every task keeps a command (the reference rejects empty tasks)
     return d
@@ -111,7 +114,7 @@ def main():
         sigma = 1.0 if dma == 1 else float(SIGMAS[rng.integers(len(SIGMAS))])
         # exhaustive summary (every ordering, or a window for n >= 10)
         n = int(rng.integers(1, 13))
-        d = durations(rng, n)
+        d = durations(rng, n, rng.random() < 0.5)
         total = math.factorial(n)
         lo, hi = 0, total
         if n >= 10:
@@ -127,12 +130,15 @@ def main():
         if not ok:
             stats["mismatches"].append({"kind": "exhaustive", "n": n, "dma": dma, "sigma": sigma, "lo": lo,
                                         "durs": d.tolist()})
-        # heuristic batch of 64 groups of one size (up to 40 tasks: the wide path above 16)
-        n = int(rng.integers(1, 41)) if rng.random() < 0.3 else int(rng.integers(1, 17))
-        B = 64
-        dd = np.stack([durations(rng, n) for _ in range(B)])
+        # heuristic batch of one group size: up to 16 tasks (half of the batches
+        # without null stages: the lane kernel), 17..40 (wide path), 65..90 (any-size path)
+        u = rng.random()
+        n = int(rng.integers(65, 91)) if u < 0.05 else (int(rng.integers(1, 41)) if u < 0.3 else int(rng.integers(1, 17)))
+        B = 8 if n > 64 else 64
+        nulls = rng.random() < 0.5
+        dd = np.stack([durations(rng, n, nulls) for _ in range(B)])
         rr = np.stack([rng.permutation(n) for _ in range(B)]).astype(np.uint8)
-        go, gms, gs = _capi.heuristic_batch(dd, rr, dma, sigma, SUM_MODE)
+        go, gms, gs = _capi.heuristic_batch(dd, rr.astype(np.uint32) if n > 64 else rr, dma, sigma, SUM_MODE)
         oo, oms, osims = O.reorder_batch(dd, rr, dma, sigma, SUM_MODE, threads=threads)
         stats["heuristic_groups"] += B
         if not (np.array_equal(go, oo) and np.array_equal(gms.view(np.uint64), oms.view(np.uint64))
@@ -140,8 +146,9 @@ def main():
             bad = int(np.nonzero((go != oo).any(axis=1) | (gms != oms) | (gs != osims))[0][0])
             stats["mismatches"].append({"kind": "heuristic", "n": n, "dma": dma, "sigma": sigma,
                                         "durs": dd[bad].tolist(), "id_rank": rr[bad].tolist()})
-        # one timeline
-        n = int(rng.integers(1, 65)) if rng.random() < 0.2 else int(rng.integers(1, 17))
+        # one timeline (up to 300 tasks: the any-size path above 64)
+        u = rng.random()
+        n = int(rng.integers(65, 301)) if u < 0.05 else (int(rng.integers(1, 65)) if u < 0.25 else int(rng.integers(1, 17)))
         d = durations(rng, n)
         order = [int(x) for x in rng.permutation(n)]
         st, en, ms, idle = _capi.timeline(d, dma, sigma, order)
