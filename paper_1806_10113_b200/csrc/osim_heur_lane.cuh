@@ -216,26 +216,57 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
             }
             run_multi<false>(sim, rest, sigma, rsig);
             // _completion_estimate (heuristic.py:34-49): CPython's sum of the
-            // rest's t_k in rt order, min t_dth
+            // rest's t_k in rt order and min t_dth.  The set's candidates are
+            // the rt slots j .. j+P-1 (a surplus one has virtual slot j+i >= m,
+            // its result unused), so every rest shares the slots before j: their
+            // running sum state is computed once and forked; inside [j, j+P)
+            // each candidate skips its own slot (a warp-uniform test); after
+            // it every candidate continues its own state, and the tail minimum
+            // (order-free) over those slots is shared.
             double f[kHLILP], e[kHLILP], tl[kHLILP];
-            uint64_t rl[kHLILP];
-#pragma unroll
-            for (int i = 0; i < kHLILP; ++i) { f[i] = 0.0; e[i] = 0.0; tl[i] = kBig; rl[i] = rt_drop(cand, cj[i]); }
-#pragma unroll 2
-            for (int q = 0; q < m - 1; ++q) {
-#pragma unroll
-                for (int i = 0; i < kHLILP; ++i) {
-                    const int u = (int)(rl[i] & 0xF);
-                    rl[i] >>= 4;
-                    const double x = DV(1, u);
-                    const double t = __dadd_rn(f[i], x);
-                    if (sum_mode) {  // Neumaier (CPython >= 3.12): TwoSum error of f + x
-                        const double p = __dsub_rn(t, f[i]);
-                        e[i] = __dadd_rn(e[i], __dadd_rn(__dsub_rn(f[i], __dsub_rn(t, p)), __dsub_rn(x, p)));
-                    }
-                    f[i] = t;
-                    tl[i] = dmin(DV(2, u), tl[i]);
+            auto nadd = [&](double& fs, double& es, double x) {
+                const double t = __dadd_rn(fs, x);
+                if (sum_mode) {  // Neumaier (CPython >= 3.12): TwoSum error of f + x
+                    const double p = __dsub_rn(t, fs);
+                    es = __dadd_rn(es, __dadd_rn(__dsub_rn(fs, __dsub_rn(t, p)), __dsub_rn(x, p)));
                 }
+                fs = t;
+            };
+            {
+                double pf = 0.0, pe = 0.0, ptl = kBig;
+                uint64_t rl = cand;
+#pragma unroll 2
+                for (int q = 0; q < j; ++q, rl >>= 4) {  // common prefix
+                    const int u = (int)(rl & 0xF);
+                    nadd(pf, pe, DV(1, u));
+                    ptl = dmin(DV(2, u), ptl);
+                }
+#pragma unroll
+                for (int i = 0; i < kHLILP; ++i) { f[i] = pf; e[i] = pe; tl[i] = ptl; }
+#pragma unroll
+                for (int q2 = 0; q2 < kHLILP; ++q2) {  // the set's own slots
+                    if (j + q2 >= m) break;
+                    const int u = (int)((rl >> (4 * q2)) & 0xF);
+                    const double x = DV(1, u), y = DV(2, u);
+#pragma unroll
+                    for (int i = 0; i < kHLILP; ++i) {
+                        if (i == q2) continue;
+                        nadd(f[i], e[i], x);
+                        tl[i] = dmin(y, tl[i]);
+                    }
+                }
+                double stl = kBig;
+                rl >>= 4 * kHLILP;
+#pragma unroll 2
+                for (int q = j + kHLILP; q < m; ++q, rl >>= 4) {  // common suffix, separate sums
+                    const int u = (int)(rl & 0xF);
+                    const double x = DV(1, u);
+                    stl = dmin(DV(2, u), stl);
+#pragma unroll
+                    for (int i = 0; i < kHLILP; ++i) nadd(f[i], e[i], x);
+                }
+#pragma unroll
+                for (int i = 0; i < kHLILP; ++i) tl[i] = dmin(stl, tl[i]);
             }
 #pragma unroll
             for (int i = 0; i < kHLILP; ++i) {
