@@ -578,7 +578,10 @@ int osim_shutdown(void) {
     std::lock_guard<std::mutex> lk(g_init_mu);
     for (DevCtx* c : g_devs) {
         cudaSetDevice(c->dev);
+        cudaDeviceSynchronize();
         if (c->scratch) cudaFree(c->scratch);
+        for (AuxBuf& a : c->aux)
+            if (a.p) cudaFree(a.p);
         if (c->d_err) cudaFree(c->d_err);
         if (c->d_done) cudaFree(c->d_done);
         if (c->stream) cudaStreamDestroy(c->stream);

@@ -59,7 +59,7 @@ void heuristic_launch(int dma, int mode, const LaunchCfg& cfg, const double* d_d
     const unsigned grid = (unsigned)((B + kHG - 1) / kHG);
     const size_t sm = sizeof(HeurShared);
     if (mode == 1 && lane_kernel()) {
-        const unsigned gl = (unsigned)((B + kHLT - 1) / kHLT);
+        const unsigned gl = (unsigned)((B + kHLW * kHLGPW - 1) / (kHLW * kHLGPW));
         const size_t sml = kHLW * kHLWarpSmem;
         const uint32_t* perm = heur_group_order(cfg, d_durs, B, n);
         int e;

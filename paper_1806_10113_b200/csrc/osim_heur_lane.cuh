@@ -30,14 +30,21 @@ namespace osim {
 // warps of a CTA are independent; a CTA's slot frees only when all finish)
 constexpr int kHLW = OSIM_HL_W;
 constexpr int kHLT = 32 * kHLW;                             // threads per CTA
-constexpr size_t kHLWarpSmem = 2 * 48 * 32 * sizeof(double);  // nd + 1/nd, [48][32] each
+#ifndef OSIM_HL_LPG
+#define OSIM_HL_LPG 1
+#endif
+constexpr int kHLLPG = OSIM_HL_LPG;  // lanes per group (1: a group per lane; 2: lanes l, l + 16)
+constexpr int kHLGPW = 32 / kHLLPG;  // groups per warp
+constexpr size_t kHLWarpSmem = 2 * 48 * kHLGPW * sizeof(double);  // nd + 1/nd, [48][groups] each
 
 #ifndef OSIM_HL_ILP
 #define OSIM_HL_ILP 0  // 0: the measured best per DMA mode
 #endif
 // candidates per lane stepped together (2-DMA: 2, 1-DMA: 3 measured best)
 template <int DMA>
-__host__ __device__ constexpr int hl_ilp() { return OSIM_HL_ILP > 0 ? OSIM_HL_ILP : (DMA == 2 ? 2 : 3); }
+__host__ __device__ constexpr int hl_ilp() {
+    return OSIM_HL_ILP > 0 ? OSIM_HL_ILP : (kHLLPG == 2 ? (DMA == 2 ? 1 : 2) : (DMA == 2 ? 2 : 3));
+}
 
 #ifndef OSIM_HL_UNR
 #define OSIM_HL_UNR 2
@@ -128,33 +135,36 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
                                                          double* __restrict__ ms_out,
                                                          uint32_t* __restrict__ nsims_out,
                                                          const uint32_t* __restrict__ perm) {
-    using FS = FastSim<DMA, SP2, true, false, false, 2>;
+    using FS = FastSim<DMA, SP2, true, false, false, kHLLPG == 1 ? 2 : 3>;
     constexpr int kHLILP = hl_ilp<DMA>();
+    constexpr int W = kHLGPW;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* nd = reinterpret_cast<double*>(smem_raw + warp * kHLWarpSmem);  // [48][32]
-    double* rcp = nd + 48 * 32;
-    const uint64_t g0 = ((uint64_t)blockIdx.x * kHLW + warp) * 32;
+    const int warp = threadIdx.x >> 5, lane0 = threadIdx.x & 31;
+    const int lane = lane0 % W;    // this lane's group within the warp
+    const int sub = lane0 / W;     // which of the group's lanes (kHLLPG = 2: candidate sets alternate)
+    double* nd = reinterpret_cast<double*>(smem_raw + warp * kHLWarpSmem);  // [48][W]
+    double* rcp = nd + 48 * W;
+    const uint64_t g0 = ((uint64_t)blockIdx.x * kHLW + warp) * W;
     if (g0 >= B) return;  // whole warp leaves together; no block barriers below
     const bool live = g0 + lane < B;
     // perm (nullable): the batch position this lane's group comes from (and
     // whose outputs it writes) -- groups ordered by heur_sort_keys so a warp's
     // 32 groups have similar replay lengths
     const uint64_t g = live ? (perm ? (uint64_t)perm[g0 + lane] : g0 + lane) : 0;
-    const int Gv = (int)((B - g0) < 32 ? (B - g0) : 32);
+    const int Gv = (int)((B - g0) < (uint64_t)W ? (B - g0) : (uint64_t)W);
     // stage this lane's group: entry (kind k, task t) at [(k*16 + t)*32 + lane]
     // (bank-conflict-free stores; the strided loads hit L1 after the first
     // touch of each line); tasks >= n get 1.0
     (void)Gv;  // (tasks of a lane past the batch end are 1.0 placeholders)
-    for (int kt = 0; kt < 48; ++kt) {
+    for (int kt = sub * (48 / kHLLPG); kt < (sub + 1) * (48 / kHLLPG); ++kt) {  // a group's lanes split it
         const int k = kt >> 4, t = kt & 15;
         const double v = (live && t < n) ? durs[g * 3 * (uint64_t)n + 3 * t + k] : 1.0;
-        nd[kt * 32 + lane] = v;
-        rcp[kt * 32 + lane] = __ddiv_rn(1.0, v);
+        nd[kt * W + lane] = v;
+        rcp[kt * W + lane] = __ddiv_rn(1.0, v);
     }
     __syncwarp();
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(nd) + 8u * (uint32_t)lane;
-    auto DV = [&](int k, int t) { return nd[(k * 16 + t) * 32 + lane]; };
+    auto DV = [&](int k, int t) { return nd[(k * 16 + t) * W + lane]; };
     uint64_t idr = 0;  // id rank per task, 4 bits each
     for (int t = 0; t < n; ++t) idr |= (uint64_t)(live ? id_rank[g * (uint64_t)n + t] : (uint8_t)t) << (4 * t);
     auto IR = [&](int t) { return (int)((idr >> (4 * t)) & 0xF); };
@@ -203,7 +213,8 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
         int bj = -1;
         double be = 0, bd = 0;
         int br = 0;
-        for (int j = 0; j < m; j += kHLILP) {
+        for (int j0 = 0; j0 < m; j0 += kHLLPG * kHLILP) {
+            const int j = j0 + sub * kHLILP;  // this lane's candidates j .. j + P - 1 (>= m: surplus)
             int cj[kHLILP], cc[kHLILP];
             FS sim[kHLILP];
 #pragma unroll
@@ -279,6 +290,14 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
                 }
             }
         }
+        if constexpr (kHLLPG > 1) {  // the group's lanes exchange their best keys
+#pragma unroll
+            for (int off = W; off < 32; off <<= 1) {
+                const int oj = __shfl_xor_sync(kFull, bj, off), orr = __shfl_xor_sync(kFull, br, off);
+                const double oe = __shfl_xor_sync(kFull, be, off), od = __shfl_xor_sync(kFull, bd, off);
+                if (oj >= 0 && (bj < 0 || key_less(oe, od, orr, be, bd, br))) { bj = oj; be = oe; bd = od; br = orr; }
+            }
+        }
         OSIM_DCHECK(bj >= 0 && bj < m);
         const int c = rt_at(cand, bj);
         ot |= (uint64_t)c << (4 * k);
@@ -321,7 +340,7 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
         for (int st = 0; st < 3; ++st) s.step(sigma, rsig);
         ms = s.now;
     }
-    if (live) {
+    if (live && sub == 0) {
         ms_out[g] = ms;
         if (nsims_out) nsims_out[g] = (n >= 3) ? (uint32_t)(n * (n - 1) / 2 - 1) : (n == 2 ? 2u : 0u);
         for (int p = 0; p < n; ++p) order_out[g * (uint64_t)n + p] = (uint8_t)nib(ot, p);

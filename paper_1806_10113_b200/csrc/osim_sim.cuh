@@ -371,13 +371,15 @@ __device__ __forceinline__ void start_if_split(bool p, uint32_t addr, double& nd
         : "+d"(nd), "+d"(rc), "+d"(rem)
         : "r"(addr), "r"((int)p));
 }
-// LAYOUT 2 of FastSim: nd and 1/nd in separate lane-interleaved arrays
+// LAYOUTs 2 and 3 of FastSim: nd and 1/nd in separate lane-interleaved
+// arrays, 1/nd RCOFF bytes above nd
+template <int RCOFF>
 __device__ __forceinline__ void start_if_lanes(bool p, uint32_t addr, double& nd, double& rc, double& rem) {
     asm volatile(
         "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
-        "@q ld.shared.f64 %0, [%3];\n\t@q ld.shared.f64 %1, [%3+12288];\n\t@q ld.shared.f64 %2, [%3];\n\t}"
+        "@q ld.shared.f64 %0, [%3];\n\t@q ld.shared.f64 %1, [%3+%5];\n\t@q ld.shared.f64 %2, [%3];\n\t}"
         : "+d"(nd), "+d"(rc), "+d"(rem)
-        : "r"(addr), "r"((int)p));
+        : "r"(addr), "r"((int)p), "n"(RCOFF));
 }
 __device__ __forceinline__ void mul_if(bool p, double& x, double y) {
     asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q mul.rn.f64 %0, %0, %1;\n\t}"
@@ -422,21 +424,25 @@ __device__ __forceinline__ uint32_t task_off(uint64_t seq, int sh) {
 //  2: lane-interleaved arrays nd[48][32], rc[48][32] (one group per lane; kind
 //     k, task t of lane l at base + (k*16 + t)*256 with base = array + 8*l,
 //     1/nd 12288 bytes above): a warp's 8-byte loads of 32 different
-//     (kind, task) entries are bank-conflict free.
+//     (kind, task) entries are bank-conflict free;
+//  3: the same with 16 groups per row (two lanes per group, l and l + 16):
+//     task stride 128 bytes, 1/nd 6144 bytes above; each half-warp's 8-byte
+//     loads touch 16 different groups, again conflict free.
 template <int DMA, bool SIGP2, bool TRACK, bool PRE, bool DEPS = false, int LAYOUT = 0>
 struct FastSim {
     static_assert(LAYOUT == 0 || !PRE, "pre-shifted sequences assume the double2 rows");
     static constexpr int kDma = DMA;
-    static constexpr uint32_t KS = (LAYOUT == 2) ? 4096u : 256u;  // bytes per kind row
-    static constexpr uint32_t kRcOff = 48u * 256u;               // LAYOUT 2: 1/nd above nd
+    static constexpr int kTSh = (LAYOUT == 2) ? 8 : 7;  // LAYOUTs 2/3: log2 bytes per task row
+    static constexpr uint32_t KS = (LAYOUT >= 2) ? (16u << kTSh) : 256u;  // bytes per kind row
+    static constexpr int kRcOff = 48 << kTSh;                 // LAYOUTs 2/3: 1/nd above nd
     __device__ __forceinline__ static uint32_t toff(uint64_t sq, int sh) {
-        if constexpr (LAYOUT == 2) return ((uint32_t)(sq >> sh) & 0xFu) << 8;
+        if constexpr (LAYOUT >= 2) return ((uint32_t)(sq >> sh) & 0xFu) << kTSh;
         else return task_off<PRE>(sq, sh);
     }
     // a command start: {nd, 1/nd} and rem = nd from shared memory
     __device__ __forceinline__ static void st_(bool p, uint32_t addr, double& nd, double& rc, double& rem) {
         if constexpr (LAYOUT == 1) start_if_split(p, addr, nd, rc, rem);
-        else if constexpr (LAYOUT == 2) start_if_lanes(p, addr, nd, rc, rem);
+        else if constexpr (LAYOUT >= 2) start_if_lanes<kRcOff>(p, addr, nd, rc, rem);
         else start_if(p, addr, nd, rc, rem);
     }
     uint32_t base;
