@@ -58,6 +58,10 @@ namespace osim {
 
 constexpr double kEndEps = 1e-9;  // engine.py:26 _END_EPS
 
+#ifndef OSIM_EXPSHIFT
+#define OSIM_EXPSHIFT 1  // FastSim, power-of-two sigma: rate factors as exponent shifts (see step())
+#endif
+
 // Step bounds.  The command that sets dt leaves left = rem - RN(RN(rem/r)*r),
 // which is 0 for rate 1 and at most 2^-52 * rem for rate sigma; with every
 // duration below kFastHi = 2^22 ms that is < 1e-9, so each step finalizes at
@@ -688,6 +692,21 @@ struct FastSim {
             const bool ov = !idle(r0) && !idle(r1);
             double m = dmin(r0, r1);
             if constexpr (SIGP2) {
+#if OSIM_EXPSHIFT
+                // sigma = 2^-e: with both transfers running (ov) m = min of two
+                // running commands' rem, a normal double in [2^-60, 2^22] (a
+                // command starts with rem = nd >= 2^-60 and finalizes once rem
+                // <= 1e-9), so m / sigma is m with e added to its exponent, and
+                // dt * sigma (dt = min(m / sigma, rem_K) >= 2^-60) is dt with e
+                // subtracted: exact, and one integer add on the high word each
+                // instead of a select, a zeroed low word and a multiply.  Without
+                // ov the factors are 1.0 (unchanged values; drained or idle
+                // lanes' sentinels never get shifted).
+                const int sh = ov ? __double2hiint(rsig) - 0x3FF00000 : 0;
+                m = __hiloint2double(__double2hiint(m) + sh, __double2loint(m));
+                dt = dmin(m, r2);
+                dd = __hiloint2double(__double2hiint(dt) - sh, __double2loint(dt));
+#else
                 // sigma, 1/sigma and 1.0 are powers of two (low word 0): select
                 // the factor's high word and multiply unconditionally
                 // (x * 1.0 == x exactly), one integer select instead of a
@@ -695,6 +714,7 @@ struct FastSim {
                 m = __dmul_rn(m, __hiloint2double(ov ? __double2hiint(rsig) : 0x3FF00000, 0));
                 dt = dmin(m, r2);
                 dd = __dmul_rn(dt, __hiloint2double(ov ? __double2hiint(sigma) : 0x3FF00000, 0));
+#endif
             } else {
                 if (ov) m = divq<true>(m, sigma, rsig);
                 dt = dmin(m, r2);
