@@ -57,6 +57,17 @@
 namespace osim {
 
 constexpr double kEndEps = 1e-9;  // engine.py:26 _END_EPS
+#ifndef OSIM_CEPS
+#define OSIM_CEPS 1
+#endif
+#if OSIM_CEPS
+// the same value in the constant bank: FastSim's finalize compares take it as
+// a direct operand instead of rematerializing it in the replay loops
+static __constant__ double c_end_eps = 1e-9;
+#define OSIM_FIN_EPS c_end_eps
+#else
+#define OSIM_FIN_EPS kEndEps
+#endif
 
 #ifndef OSIM_EXPSHIFT
 #define OSIM_EXPSHIFT 1  // FastSim, power-of-two sigma: rate factors as exponent shifts (see step())
@@ -521,10 +532,10 @@ struct FastSim {
         now = __dadd_rn(now, dt);
         r2 = upd(r2, dt, d2, c2);
         r1 = upd(r1, dt, d1, c1);
-        const bool f1 = r1 <= kEndEps;
+        const bool f1 = r1 <= OSIM_FIN_EPS;
         r1 = retire_or_drain(f1, r1, s1 + 4 >= n4);
         s1 += f1 ? 4 : 0;
-        if (r2 <= kEndEps) {
+        if (r2 <= OSIM_FIN_EPS) {
             r2 = retire(r2);
             s2 += 4;
             if constexpr (TRACK) kEnd = now;
@@ -537,7 +548,7 @@ struct FastSim {
         const double dt = r1;  // the only lane that can run (rem ~0 once drained)
         now = __dadd_rn(now, dt);
         r1 = upd(r1, dt, d1, c1);
-        const bool f1 = r1 <= kEndEps;
+        const bool f1 = r1 <= OSIM_FIN_EPS;
         r1 = retire_or_drain(f1, r1, s1 + 4 >= n4);
         s1 += f1 ? 4 : 0;
     }
@@ -559,10 +570,10 @@ struct FastSim {
         now = __dadd_rn(now, dt);
         r0 = upd(r0, dt, d0, c0);
         r2 = upd(r2, dt, d2, c2);
-        const bool f0 = r0 <= kEndEps;
+        const bool f0 = r0 <= OSIM_FIN_EPS;
         r0 = retire_or_drain(f0, r0, s0 + 4 >= 2 * n4);
         s0 += f0 ? 4 : 0;
-        if (r2 <= kEndEps) {
+        if (r2 <= OSIM_FIN_EPS) {
             r2 = retire(r2);
             s2 += 4;
             if constexpr (TRACK) kEnd = now;
@@ -583,10 +594,10 @@ struct FastSim {
         now = __dadd_rn(now, dt);
         r0 = upd(r0, dt, d0, c0);
         r2 = upd(r2, dt, d2, c2);
-        const bool f0 = r0 <= kEndEps;
+        const bool f0 = r0 <= OSIM_FIN_EPS;
         r0 = retire_or_drain(f0, r0, s0 + 4 >= 2 * n4);
         s0 += f0 ? 4 : 0;
-        if (r2 <= kEndEps) {
+        if (r2 <= OSIM_FIN_EPS) {
             r2 = retire(r2);
             s2 += 4;
             if constexpr (TRACK) kEnd = now;
@@ -599,7 +610,7 @@ struct FastSim {
         const double dt = r0;  // the only lane that can run (rem ~0 once drained)
         now = __dadd_rn(now, dt);
         r0 = upd(r0, dt, d0, c0);
-        const bool f0 = r0 <= kEndEps;
+        const bool f0 = r0 <= OSIM_FIN_EPS;
         r0 = retire_or_drain(f0, r0, s0 + 4 >= 2 * n4);
         s0 += f0 ? 4 : 0;
     }
@@ -735,16 +746,16 @@ struct FastSim {
         r2 = upd(r2, dt, d2, c2);
         if constexpr (DMA == 2) r1 = upd(r1, dd, d1, c1);
         if constexpr (DMA == 2) {
-            if (r0 <= kEndEps) { r0 = retire(r0); s0 += 4; }
-            const bool f1 = r1 <= kEndEps;
+            if (r0 <= OSIM_FIN_EPS) { r0 = retire(r0); s0 += 4; }
+            const bool f1 = r1 <= OSIM_FIN_EPS;
             r1 = retire_or_drain(f1, r1, s1 + 4 >= n4);
             s1 += f1 ? 4 : 0;
         } else {
-            const bool f0 = r0 <= kEndEps;
+            const bool f0 = r0 <= OSIM_FIN_EPS;
             r0 = retire_or_drain(f0, r0, s0 + 4 >= 2 * n4);
             s0 += f0 ? 4 : 0;
         }
-        if (r2 <= kEndEps) {
+        if (r2 <= OSIM_FIN_EPS) {
             r2 = retire(r2);
             s2 += 4;
             if constexpr (TRACK) kEnd = now;
@@ -849,9 +860,17 @@ struct NullSim {
             const bool ov = !idle(r0) && !idle(r1);
             double m = dmin(r0, r1);
             if constexpr (SIGP2) {
+#if OSIM_EXPSHIFT
+                // as FastSim::step: exponent shifts of running commands' rems (ov)
+                const int sh = ov ? __double2hiint(rsig) - 0x3FF00000 : 0;
+                m = __hiloint2double(__double2hiint(m) + sh, __double2loint(m));
+                dt = dmin(m, r2);
+                dd = __hiloint2double(__double2hiint(dt) - sh, __double2loint(dt));
+#else
                 m = __dmul_rn(m, __hiloint2double(ov ? __double2hiint(rsig) : 0x3FF00000, 0));
                 dt = dmin(m, r2);
                 dd = __dmul_rn(dt, __hiloint2double(ov ? __double2hiint(sigma) : 0x3FF00000, 0));
+#endif
             } else {
                 if (ov) m = divq<true>(m, sigma, rsig);
                 dt = dmin(m, r2);
