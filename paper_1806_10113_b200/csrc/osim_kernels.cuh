@@ -356,6 +356,17 @@ __device__ __forceinline__ int advance_to(FS& s, int target, double sigma, doubl
 // Entries without a prefix (range tails) sort last; all-empty chunks are
 // skipped.
 constexpr int kSaBins = 64;  // sa <= 3 * kMaxN; bin kSaBins - 1 = no prefix
+// FastSim LAYOUT of the prefix kernels' duration rows: 0 (address = register
+// base + kind offset + task offset) or 4 (base | task offset, one LOP3); both
+// with the base in a register the compiler cannot rematerialize (opaque_u32).
+// Measured (tools/exh_ab.py): C4 20.80 G (0) vs 20.62 G (4); C2 22.20 G (0) vs
+// 22.86 G (4); with the base rematerialized each iteration (round 1) 20.35 / 22.50.
+#ifndef OSIM_PFX_LAYOUT
+#define OSIM_PFX_LAYOUT 0  // k_exhaustive_pfx
+#endif
+#ifndef OSIM_BATCH_LAYOUT
+#define OSIM_BATCH_LAYOUT 4  // k_exhaustive_batch_pfx
+#endif
 constexpr int kPfxQ = 2;
 constexpr int kNW = kBlock / 32;
 struct PfxSort {
@@ -424,14 +435,14 @@ __device__ __forceinline__ int2 pfx_sort(PfxSort& S, int sa0, int sa1) {
 // (A second checkpoint level two positions later was measured slower on B200:
 // its middle segment runs in divergent advance loops shared by only two
 // leaves.)
-template <int N, int DMA, bool SIGP2, int L, bool STATS>
+template <int N, int DMA, bool SIGP2, int L, bool STATS, int LAY>
 __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double rsig, uint64_t P0, uint64_t p_end,
                                            uint64_t lo, uint64_t hi, double thr, Part& acc,
                                            double* __restrict__ ms_out, uint64_t ms_base, CkSlots<kPfxQ>& K,
                                            PfxSort& S) {
     constexpr int M = N - L;
     constexpr uint64_t LF = Fact<L>::v;
-    using FS = FastSim<DMA, SIGP2, false, (N <= 15)>;
+    using FS = FastSim<DMA, SIGP2, false, (N <= 15), false, LAY>;
     const int ti = threadIdx.x;
     FS s;
     // ---- phase A: both prefixes to their checkpoints
@@ -573,6 +584,18 @@ __device__ __forceinline__ void fused_final_reduce(const Part* parts, osim_summa
     }
 }
 
+// a value the compiler cannot rematerialize inside the replay loops (it keeps
+// the register instead of recomputing the shared-window base every iteration)
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
+#ifndef OSIM_NO_OPAQUE
+    uint32_t y;
+    asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+#else
+    return x;
+#endif
+}
+
 // dynamic shared memory of the prefix kernels (checkpoint slots + sort)
 constexpr size_t kPfxDynSmem = sizeof(CkSlots<kPfxQ>) + sizeof(PfxSort);
 
@@ -583,14 +606,14 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
                                                            unsigned long long* __restrict__ below,
                                                            unsigned* __restrict__ done, unsigned shard,
                                                            unsigned shards, unsigned split) {
-    __shared__ double2 sdr[3 * kStride];
+    __shared__ __align__(256) double2 sdr[3 * kStride];  // 256-aligned: FastSim LAYOUT 4
     __shared__ Part sh[32];
     extern __shared__ __align__(16) unsigned char pfx_dsm[];
     CkSlots<kPfxQ>& K = *reinterpret_cast<CkSlots<kPfxQ>*>(pfx_dsm);
     PfxSort& S = *reinterpret_cast<PfxSort*>(pfx_dsm + sizeof(CkSlots<kPfxQ>));
     stage_dr(durs, N, sdr);
     __syncthreads();
-    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
+    const uint32_t base = opaque_u32((uint32_t)__cvta_generic_to_shared(sdr));
     const double rsig = __ddiv_rn(1.0, sigma);
     constexpr uint64_t LF = Fact<L>::v;
     const uint64_t p_lo = lo / LF, p_hi = (hi + LF - 1) / LF;
@@ -613,7 +636,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
     for (uint64_t pc = p_lo + (cta_call * shards + shard) * kPer; pc < p_hi; pc += stride) {
         const uint64_t pb = pc + half * per;
         const uint64_t pe = pb + per < p_hi ? pb + per : p_hi;
-        if (pb < pe) pfx_leaves<N, DMA, SIGP2, L, STATS>(base, sigma, rsig, pb, pe, lo, hi, thr, acc, ms_out, lo, K, S);
+        if (pb < pe) pfx_leaves<N, DMA, SIGP2, L, STATS, OSIM_PFX_LAYOUT>(base, sigma, rsig, pb, pe, lo, hi, thr, acc, ms_out, lo, K, S);
     }
     acc = block_reduce(acc, sh);
     if (threadIdx.x == 0) parts[blockIdx.x] = acc;
@@ -624,7 +647,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
 template <int N, int DMA, bool SIGP2, int L>
 __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_batch_pfx(const double* __restrict__ durs, uint64_t B,
                                                                  double sigma, osim_summary* __restrict__ out) {
-    __shared__ double2 sdr[3 * kStride];
+    __shared__ __align__(256) double2 sdr[3 * kStride];  // 256-aligned: FastSim LAYOUT 4
     __shared__ Part sh[32];
     extern __shared__ __align__(16) unsigned char pfx_dsm[];
     CkSlots<kPfxQ>& K = *reinterpret_cast<CkSlots<kPfxQ>*>(pfx_dsm);
@@ -632,7 +655,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_batch_pfx(
     constexpr uint64_t total = Fact<N>::v;
     constexpr uint64_t NP = total / Fact<L>::v;
     constexpr uint64_t kPer = (uint64_t)kPfxQ * kBlock;
-    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
+    const uint32_t base = opaque_u32((uint32_t)__cvta_generic_to_shared(sdr));
     const double rsig = __ddiv_rn(1.0, sigma);
     for (uint64_t b = blockIdx.x; b < B; b += gridDim.x) {
         stage_dr(durs + b * 3 * N, N, sdr);
@@ -640,7 +663,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_batch_pfx(
         Part acc;
         part_init(acc);
         for (uint64_t pb = 0; pb < NP; pb += kPer)
-            pfx_leaves<N, DMA, SIGP2, L, false>(base, sigma, rsig, pb, NP, 0, total, -kBig, acc, nullptr, 0, K, S);
+            pfx_leaves<N, DMA, SIGP2, L, false, OSIM_BATCH_LAYOUT>(base, sigma, rsig, pb, NP, 0, total, -kBig, acc, nullptr, 0, K, S);
         acc = block_reduce(acc, sh);  // ends with __syncthreads: smem reusable
         if (threadIdx.x == 0) out[b] = part_to_summary(acc);
     }

@@ -445,19 +445,28 @@ __device__ __forceinline__ uint32_t task_off(uint64_t seq, int sh) {
 //     loads touch 16 different groups, again conflict free.
 template <int DMA, bool SIGP2, bool TRACK, bool PRE, bool DEPS = false, int LAYOUT = 0>
 struct FastSim {
-    static_assert(LAYOUT == 0 || !PRE, "pre-shifted sequences assume the double2 rows");
+    static_assert(LAYOUT == 0 || LAYOUT == 4 || !PRE, "pre-shifted sequences assume the double2 rows");
     static constexpr int kDma = DMA;
+    static constexpr bool kLanes = LAYOUT == 2 || LAYOUT == 3;  // lane-interleaved arrays
     static constexpr int kTSh = (LAYOUT == 2) ? 8 : 7;  // LAYOUTs 2/3: log2 bytes per task row
-    static constexpr uint32_t KS = (LAYOUT >= 2) ? (16u << kTSh) : 256u;  // bytes per kind row
+    static constexpr uint32_t KS = kLanes ? (16u << kTSh) : 256u;  // bytes per kind row
     static constexpr int kRcOff = 48 << kTSh;                 // LAYOUTs 2/3: 1/nd above nd
     __device__ __forceinline__ static uint32_t toff(uint64_t sq, int sh) {
-        if constexpr (LAYOUT >= 2) return ((uint32_t)(sq >> sh) & 0xFu) << kTSh;
+        if constexpr (kLanes) return ((uint32_t)(sq >> sh) & 0xFu) << kTSh;
         else return task_off<PRE>(sq, sh);
+    }
+    // address of the (kind offset kofs, task offset t) entry; LAYOUT 4 (the
+    // double2 rows at a 256-byte-aligned base held in a register): base | t
+    // is one LOP3 with the task-offset mask and kofs folds into the load's
+    // immediate -- no shared-window base rematerialized in the loops
+    __device__ __forceinline__ uint32_t adr(uint32_t kofs, uint32_t t) const {
+        if constexpr (LAYOUT == 4) return (base | t) + kofs;
+        else return base + kofs + t;
     }
     // a command start: {nd, 1/nd} and rem = nd from shared memory
     __device__ __forceinline__ static void st_(bool p, uint32_t addr, double& nd, double& rc, double& rem) {
         if constexpr (LAYOUT == 1) start_if_split(p, addr, nd, rc, rem);
-        else if constexpr (LAYOUT >= 2) start_if_lanes<kRcOff>(p, addr, nd, rc, rem);
+        else if constexpr (kLanes) start_if_lanes<kRcOff>(p, addr, nd, rc, rem);
         else start_if(p, addr, nd, rc, rem);
     }
     uint32_t base;
@@ -486,7 +495,7 @@ struct FastSim {
     __device__ __forceinline__ void set_seq(uint64_t sq) { seq = PRE ? (sq << 4) : sq; }
     // start the HtD at the queue head now (the HtD lane is idle and an HtD
     // is always ready): what the next step's start phase would do
-    __device__ __forceinline__ void start_htd() { st_(true, base + toff(seq, s0), d0, c0, r0); }
+    __device__ __forceinline__ void start_htd() { st_(true, adr(0, toff(seq, s0)), d0, c0, r0); }
     __device__ __forceinline__ int finalized() const { return (s0 + s1 + s2) >> 2; }
 
     // checkpoint image (prefix sharing across calls, e.g. in shared memory)
@@ -526,8 +535,8 @@ struct FastSim {
         const bool st2 = idle(r2) && s2 < n4;
         const bool st1 = idle(r1) && s1 < s2;
         k_idle_gap(st2);
-        st_(st2, base + KS + toff(seq, s2), d2, c2, r2);
-        st_(st1, base + 2 * KS + toff(seq, s1), d1, c1, r1);
+        st_(st2, adr(KS, toff(seq, s2)), d2, c2, r2);
+        st_(st1, adr(2 * KS, toff(seq, s1)), d1, c1, r1);
         const double dt = dmin(r1, r2);
         now = __dadd_rn(now, dt);
         r2 = upd(r2, dt, d2, c2);
@@ -544,7 +553,7 @@ struct FastSim {
     __device__ __forceinline__ void step_d() {
         static_assert(DMA == 2, "2-DMA only");
         const bool st1 = idle(r1) && s1 < n4;
-        st_(st1, base + 2 * KS + toff(seq, s1), d1, c1, r1);
+        st_(st1, adr(2 * KS, toff(seq, s1)), d1, c1, r1);
         const double dt = r1;  // the only lane that can run (rem ~0 once drained)
         now = __dadd_rn(now, dt);
         r1 = upd(r1, dt, d1, c1);
@@ -564,8 +573,8 @@ struct FastSim {
         const bool st0 = idle(r0) && s0 < 2 * n4 && s2 > ps;
         const bool st2 = idle(r2) && s2 < n4;
         k_idle_gap(st2);
-        st_(st0, base + 2 * KS + toff(seq, ps), d0, c0, r0);
-        st_(st2, base + KS + toff(seq, s2), d2, c2, r2);
+        st_(st0, adr(2 * KS, toff(seq, ps)), d0, c0, r0);
+        st_(st2, adr(KS, toff(seq, s2)), d2, c2, r2);
         const double dt = dmin(r0, r2);
         now = __dadd_rn(now, dt);
         r0 = upd(r0, dt, d0, c0);
@@ -588,8 +597,8 @@ struct FastSim {
         const bool st0 = idle(r0) && s0 < 2 * n4 && s2 > ps;
         const bool st2 = idle(r2) && s2 < n4 && s2 < s0;
         k_idle_gap(st2);
-        st_(st0, base + 2 * KS + toff(seq, ps), d0, c0, r0);
-        st_(st2, base + KS + toff(seq, s2), d2, c2, r2);
+        st_(st0, adr(2 * KS, toff(seq, ps)), d0, c0, r0);
+        st_(st2, adr(KS, toff(seq, s2)), d2, c2, r2);
         const double dt = dmin(r0, r2);
         now = __dadd_rn(now, dt);
         r0 = upd(r0, dt, d0, c0);
@@ -606,7 +615,7 @@ struct FastSim {
     __device__ __forceinline__ void step_1dd() {
         static_assert(DMA == 1, "1-DMA only");
         const bool st0 = idle(r0) && s0 < 2 * n4;
-        st_(st0, base + 2 * KS + toff(seq, s0 - n4), d0, c0, r0);
+        st_(st0, adr(2 * KS, toff(seq, s0 - n4)), d0, c0, r0);
         const double dt = r0;  // the only lane that can run (rem ~0 once drained)
         now = __dadd_rn(now, dt);
         r0 = upd(r0, dt, d0, c0);
@@ -685,17 +694,17 @@ struct FastSim {
             const bool st2 = idle(r2) && s2 < s0;
             const bool st1 = idle(r1) && s1 < s2;
             k_idle_gap(st2);
-            if constexpr (H0) st_(st0, base + toff(seq, s0), d0, c0, r0);
-            st_(st2, base + KS + toff(seq, s2), d2, c2, r2);
-            st_(st1, base + 2 * KS + toff(seq, s1), d1, c1, r1);
+            if constexpr (H0) st_(st0, adr(0, toff(seq, s0)), d0, c0, r0);
+            st_(st2, adr(KS, toff(seq, s2)), d2, c2, r2);
+            st_(st1, adr(2 * KS, toff(seq, s1)), d1, c1, r1);
         } else {
             const bool isH = s0 < n4;
             const int ps = isH ? s0 : s0 - n4;
             const bool st0 = idle(r0) && s0 < 2 * n4 && (isH || s2 > ps);
             const bool st2 = idle(r2) && s2 < n4 && s2 < s0;
             k_idle_gap(st2);
-            st_(st0, base + (isH ? 0u : 2 * KS) + toff(seq, ps), d0, c0, r0);
-            st_(st2, base + KS + toff(seq, s2), d2, c2, r2);
+            st_(st0, adr(isH ? 0u : 2 * KS, toff(seq, ps)), d0, c0, r0);
+            st_(st2, adr(KS, toff(seq, s2)), d2, c2, r2);
         }
         // ---- dt (engine.py:200-210)
         double dt, dd;
