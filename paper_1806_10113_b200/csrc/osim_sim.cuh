@@ -69,6 +69,12 @@ static __constant__ double c_end_eps = 1e-9;
 #define OSIM_FIN_EPS kEndEps
 #endif
 
+#ifndef OSIM_PH_FULL
+#define OSIM_PH_FULL 2  // FastSim::run_phased (2-DMA): steps per phase vote, full / K+DtH phases
+#endif
+#ifndef OSIM_PH_KD
+#define OSIM_PH_KD 2
+#endif
 #ifndef OSIM_EXPSHIFT
 #define OSIM_EXPSHIFT 1  // FastSim, power-of-two sigma: rate factors as exponent shifts (see step())
 #endif
@@ -633,16 +639,16 @@ struct FastSim {
         int st = 0;
         if constexpr (DMA == 2) {
 #pragma unroll 1
-            for (; st < rest; st += 2) {
+            for (; st < rest; st += OSIM_PH_FULL) {
                 if (__all_sync(0xffffffffu, s0 >= n4)) break;
-                step<H0>(sigma, rsig);
-                step<H0>(sigma, rsig);
+#pragma unroll
+                for (int r = 0; r < OSIM_PH_FULL; ++r) step<H0>(sigma, rsig);
             }
 #pragma unroll 1
-            for (; st < rest; st += 2) {
+            for (; st < rest; st += OSIM_PH_KD) {
                 if (__all_sync(0xffffffffu, s2 >= n4)) break;
-                step_kd();
-                step_kd();
+#pragma unroll
+                for (int r = 0; r < OSIM_PH_KD; ++r) step_kd();
             }
 #pragma unroll 2
             for (; st < rest; ++st) step_d();
