@@ -229,6 +229,7 @@ def run_ours(a):
     # ---- headline: C4 ------------------------------------------------------
     durs = synth.c4_group()
     fast = int(_capi.fast_eligible(durs, SIGMA))
+    assert fast == 1, "the C4 group is fast-path eligible (every duration in [2^-60, 2^22) ms)"
     d_durs = torch.from_numpy(durs).to(dev)
     d_out = torch.zeros(6, dtype=torch.float64, device=dev)
     gathered = [torch.zeros(6, dtype=torch.float64, device=dev) for _ in range(D.world)]
@@ -322,11 +323,7 @@ def run_ours(a):
             "metric": "orderings simulated/sec", "value": value, "unit": "orderings/s", "n_gpus": D.world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": t_max / a.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "orderings_per_step": TOTAL12, "n_tasks": N12,
-                       "parallelism": f"interleaved Lehmer-rank shards x{D.world}" + (" + NCCL all_gather of 48-B summaries"
-                                                                          if D.pg else ""),
-                       "l2": "256 MiB buffer zeroed before every timed step (excluded from timing); inputs 288 B",
-                       "fast_path": bool(fast)},
+            "config": arm_config(D.world, D.pg is not None),
             "result": {"best": res.best, "best_rank": res.best_rank, "best_ordering": list(res.best_ordering),
                        "worst": res.worst, "mean": res.mean, "geomean": res.geomean},
             "roofline": roof, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches_per_step * a.steps,
@@ -710,6 +707,16 @@ def cpu_baseline(seconds):
             "python": python_reference_rate(min(seconds, 10.0))}
 
 
+def arm_config(world, pg):
+    """The workload both arms report (the reference arm times a bounded
+    sample of it per step, described in its cpu_baseline.sample)."""
+    return {"workload": WORKLOAD, "orderings_per_step": TOTAL12, "n_tasks": N12,
+            "parallelism": f"interleaved Lehmer-rank shards x{world}" + (" + NCCL all_gather of 48-B summaries"
+                                                                         if pg else ""),
+            "l2": "256 MiB buffer zeroed before every timed step (excluded from timing); inputs 288 B",
+            "fast_path": True}
+
+
 def run_reference(a):
     if env_int("RANK", 0) != 0:
         return
@@ -733,8 +740,9 @@ def run_reference(a):
         "n_gpus": env_int("WORLD_SIZE", 1), "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": el / a.steps * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "orderings_per_step": m, "n_tasks": N12},
-        "cpu_baseline": {"value": value, "unit": "orderings/s", "cores": threads, "kind": "port", "sample": sample},
+        "config": arm_config(env_int("WORLD_SIZE", 1), env_int("WORLD_SIZE", 1) > 1),
+        "cpu_baseline": {"value": value, "unit": "orderings/s", "cores": threads, "kind": "port", "sample": sample,
+                         "orderings_per_step": m},
         "e2e": {"value": value, "unit": "orderings/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
