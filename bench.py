@@ -139,9 +139,6 @@ class Dist:
         if self.world > 1 or os.environ.get("OSIM_BENCH_FORCE_PG") == "1":
             import torch.distributed as tdist
 
-            # NCCL's init lines (communicator size, transport) on stderr, so
-            # the run log shows every rank joined one communicator
-            os.environ.setdefault("NCCL_DEBUG", "INFO")
 
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             tdist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
@@ -760,6 +757,11 @@ def main():
     if a.warmup < 3:
         print("note: --warmup raised to 3 (timing rules)", file=sys.stderr)
         a.warmup = 3
+    if env_int("WORLD_SIZE", 1) > 1 or os.environ.get("OSIM_BENCH_FORCE_PG") == "1":
+        # NCCL's init lines (communicator size, transport) on stderr, so the
+        # run log shows every rank joined one communicator; set before torch
+        # (and with it NCCL) is first imported
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
     if a.impl == "reference":
         run_reference(a)
     else:
