@@ -118,6 +118,17 @@ int scratch(DevCtx* c, size_t bytes, void** p) {
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Give back a scratch buffer that one call grew past `keep` bytes (the exact
+// median of a 13-task space holds 56 GB of makespans): later calls
+// re-allocate what they need.  Caller holds c->mu; the device is idle.
+void trim_scratch(DevCtx* c, size_t keep = size_t(4) << 30) {
+    if (c->scratch && c->scratch_bytes > keep) {
+        cudaFree(c->scratch);
+        c->scratch = nullptr;
+        c->scratch_bytes = 0;
+    }
+}
+
 // ---- validation (model.py:63-71, 91-100; engine.py:129-130, 258-259) -----
 int check_common(int n, int dma, double sigma, int maxn = kMaxN) {
     if (n < 1) return fail(OSIM_EINVAL, "task group must be non-empty");
@@ -833,6 +844,7 @@ int osim_exhaustive_stats(const double* durs, int n, int dma, double sigma, uint
             *median = s / 2.0;
         }
     }
+    for (DevCtx* c : dl.v) trim_scratch(c);
     return 0;
 }
 
