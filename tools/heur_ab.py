@@ -1,5 +1,6 @@
-"""A/B of the all-non-null heuristic kernels (k_heuristic_fast vs
-k_heuristic_lane, OSIM_HEUR_LANE=0/1): device-resident rate on the C5 batch
+"""A/B of the heuristic kernels (k_heuristic_fast / k_heuristic_nullck vs
+k_heuristic_lane / k_heuristic_null_lane, OSIM_HEUR_LANE=0/1; AB_NULL=1: one
+null DtH per group, the null-stage kernels): device-resident rate on the C5 batch
 (10^6 x 16 tasks, three device profiles) and a hash of the outputs, which
 must be identical.
 
@@ -30,14 +31,17 @@ def child():
     for prof in ("nvidia", "amd", "phi"):
         _, dma, sigma = synth.PROFILES[prof]
         d, r = synth.c5_batch_fast(prof, B)
+        if os.environ.get("AB_NULL") == "1":  # one null DtH per group: the null-stage kernels
+            d[:, 5, 2] = 0.0
         dd, rr = torch.from_numpy(d).to(dev), torch.from_numpy(r).to(dev)
         oo = torch.empty((B, 16), dtype=torch.uint8, device=dev)
         mm = torch.empty(B, dtype=torch.float64, device=dev)
         ns = torch.empty(B, dtype=torch.int32, device=dev)
 
         def run():
+            mode = 2 if os.environ.get("AB_NULL") == "1" else 1
             _capi.check(L.osim_heuristic_batch_dev(C.c_void_p(dd.data_ptr()), C.c_void_p(rr.data_ptr()), B, 16, dma,
-                                                   sigma, 1, 1, C.c_void_p(oo.data_ptr()), C.c_void_p(mm.data_ptr()),
+                                                   sigma, 1, mode, C.c_void_p(oo.data_ptr()), C.c_void_p(mm.data_ptr()),
                                                    C.c_void_p(ns.data_ptr()), C.c_void_p(st.cuda_stream)))
         run()
         torch.cuda.synchronize()
