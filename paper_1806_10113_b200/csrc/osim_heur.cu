@@ -89,22 +89,6 @@ void heuristic_launch(int dma, int mode, const LaunchCfg& cfg, const double* d_d
     }
 #define OSIM_HL(D, M) \
     k_heuristic<D, M><<<grid, kHT, sm, cfg.st>>>(d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms, d_ns, d_err)
-    if (mode == 2 && lane_kernel()) {  // null stages, one group per lane
-        const unsigned gl = (unsigned)((B + kHLW * 32 - 1) / (kHLW * 32));
-        const size_t sml = kHLW * kHLWarpSmem;
-        int e;
-        const bool sp2 = std::frexp(sigma, &e) == 0.5;
-#define OSIM_HNL(D, P)                                                                               \
-    do {                                                                                             \
-        auto kf = k_heuristic_null_lane<D, P>;                                                       \
-        cached_ctas_per_sm((const void*)kf, kHLT, sml);                                              \
-        kf<<<gl, kHLT, sml, cfg.st>>>(d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms, d_ns, d_err); \
-    } while (0)
-        if (dma == 2) { if (sp2) OSIM_HNL(2, true); else OSIM_HNL(2, false); }
-        else OSIM_HNL(1, false);
-#undef OSIM_HNL
-        return;
-    }
     if (mode == 2) {  // null stages in the fast range: NullSim with prefix-world checkpoints
         const unsigned gridf = (unsigned)((B + kHGF - 1) / kHGF);
         int e;

@@ -17,7 +17,6 @@
 // makespans and orders are bit-identical to k_heuristic<DMA, 2>.
 #pragma once
 
-#include "osim_heur_lane.cuh"
 #include "osim_null.cuh"
 
 namespace osim {
@@ -282,203 +281,6 @@ __global__ void __launch_bounds__(kHTF) k_heuristic_nullck(const double* __restr
     for (int i = lane; i < Gv * n; i += 32) {
         const int g = i / n, p = i % n;
         order_out[(g0 + g) * (uint64_t)n + p] = (uint8_t)nib(S.ot[g], p);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// The same algorithm with one group per lane (k_heuristic_lane's mapping,
-// osim_heur_lane.cuh): durations in FastSim/NullSim LAYOUT 2 (lane-
-// interleaved nd and 1/nd), the prefix-world checkpoint in registers, a
-// lane's round candidates kHNILP at a time as independent simulations, every
-// serial phase on all 32 lanes.  Same operations per simulation as
-// k_heuristic_nullck, so the same bits.
-// ---------------------------------------------------------------------------
-#ifndef OSIM_HN_ILP
-#define OSIM_HN_ILP 2
-#endif
-constexpr int kHNILP = OSIM_HN_ILP;
-
-template <int DMA, bool SP2>
-__global__ void __launch_bounds__(kHLT) k_heuristic_null_lane(const double* __restrict__ durs,
-                                                              const uint8_t* __restrict__ id_rank, uint64_t B, int n,
-                                                              double sigma, int sum_mode,
-                                                              uint8_t* __restrict__ order_out,
-                                                              double* __restrict__ ms_out,
-                                                              uint32_t* __restrict__ nsims_out,
-                                                              int* __restrict__ err) {
-    static_assert(kHLLPG == 1, "one group per lane");
-    using NS = NullSim<DMA, SP2, true, 2>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* nd = reinterpret_cast<double*>(smem_raw + warp * kHLWarpSmem);  // [48][32]
-    double* rcp = nd + 48 * 32;
-    const uint64_t g0 = ((uint64_t)blockIdx.x * kHLW + warp) * 32;
-    if (g0 >= B) return;  // whole warp leaves together; no block barriers below
-    const bool live = g0 + lane < B;
-    const uint64_t g = live ? g0 + lane : 0;
-    for (int kt = 0; kt < 48; ++kt) {  // entry (kind k, task t) at [(k*16 + t)*32 + lane]
-        const int k = kt >> 4, t = kt & 15;
-        const double v = (live && t < n) ? durs[g * 3 * (uint64_t)n + 3 * t + k] : 1.0;
-        nd[kt * 32 + lane] = v;
-        rcp[kt * 32 + lane] = __ddiv_rn(1.0, v);  // 1/0 = inf for a null stage (never loaded)
-    }
-    __syncwarp();
-    const uint32_t base = (uint32_t)__cvta_generic_to_shared(nd) + 8u * (uint32_t)lane;
-    auto DV = [&](int k, int t) { return nd[(k * 16 + t) * 32 + lane]; };
-    uint64_t idr = 0;
-    for (int t = 0; t < n; ++t) idr |= (uint64_t)(live ? id_rank[g * (uint64_t)n + t] : (uint8_t)t) << (4 * t);
-    auto IR = [&](int t) { return (int)((idr >> (4 * t)) & 0xF); };
-    const double rsig = __ddiv_rn(1.0, sigma);
-    unsigned tH = 0, tK = 0, tD = 0;  // task null masks
-    for (int t = 0; t < n; ++t) {
-        tH |= (DV(0, t) > 0.0 ? 0u : 1u) << t;
-        tK |= (DV(1, t) > 0.0 ? 0u : 1u) << t;
-        tD |= (DV(2, t) > 0.0 ? 0u : 1u) << t;
-    }
-    bool ok = true;
-
-    // select_first_task (heuristic.py:22-31) and the first prefix-world checkpoint
-    NullHeurCk ck;
-    uint64_t ot = 0, cand = 0;
-    {
-        const unsigned all = (1u << n) - 1u;
-        unsigned rm = all;
-        NS s;
-        int steps = 0;
-        if (n >= 3) {
-            int best = 0;
-            double b1 = 0, b2 = 0;
-            for (int t = 0; t < n; ++t) {
-                const double k1 = -__dsub_rn(DV(1, t), DV(0, t));
-                const double k2 = -DV(2, t);
-                bool less;
-                if (t == 0) less = true;
-                else if (k1 < b1) less = true;
-                else if (b1 < k1) less = false;
-                else if (k2 < b2) less = true;
-                else if (b2 < k2) less = false;
-                else less = IR(t) < IR(best);
-                if (less) { best = t; b1 = k1; b2 = k2; }
-            }
-            ot = (uint64_t)best;
-            rm = all & ~(1u << best);
-            s.init(base, ot, 1, tH, tK, tD);  // the 1-position world
-            for (; steps < 3 * kMaxN && !null_at_ck(s); ++steps) s.step(sigma, rsig);
-        } else {
-            s.init(base, 0, 0, tH, tK, tD);  // the empty world: the initial state
-        }
-        nh_save(s, steps, ck);
-        for (int t = n - 1; t >= 0; --t)
-            if ((rm >> t) & 1u) cand = (cand << 4) | (uint64_t)t;
-    }
-
-    const int k0 = (n >= 3) ? 1 : 0;
-    for (int k = k0; n - k > 2; ++k) {  // heuristic.py:120-123
-        const int m = n - k;
-        const int rest = __reduce_max_sync(kFull, 3 * (k + 1) - ck.steps);
-        int bj = -1;
-        double be = 0, bd = 0;
-        int br = 0;
-        for (int j = 0; j < m; j += kHNILP) {
-            int cj[kHNILP], cc[kHNILP];
-            NS sim[kHNILP];
-#pragma unroll
-            for (int i = 0; i < kHNILP; ++i) {
-                cj[i] = (j + i < m) ? j + i : m - 1;  // a surplus slot repeats the last candidate
-                cc[i] = rt_at(cand, cj[i]);
-                nh_load<DMA>(sim[i], ck, k, base, ot | ((uint64_t)cc[i] << (4 * k)), k + 1, tH, tK, tD);
-            }
-#pragma unroll 1
-            for (int st = 0; st < rest; st += 2) {
-                bool dr = true;
-#pragma unroll
-                for (int i = 0; i < kHNILP; ++i) dr = dr && sim[i].drained();
-                if (__all_sync(kFull, dr)) break;
-#pragma unroll
-                for (int r = 0; r < 2; ++r)
-#pragma unroll
-                    for (int i = 0; i < kHNILP; ++i) sim[i].step(sigma, rsig);
-            }
-#pragma unroll
-            for (int i = 0; i < kHNILP; ++i) ok = ok && (sim[i].drained() || !live);
-            // _completion_estimate (heuristic.py:34-49): CPython's sum of the rest's
-            // t_k in rt order, min t_dth (per candidate, as k_heuristic_nullck)
-#pragma unroll
-            for (int i = 0; i < kHNILP; ++i) {
-                double f = 0.0, e = 0.0, tail = kBig;
-                uint64_t rl = rt_drop(cand, cj[i]);
-#pragma unroll 2
-                for (int q = 0; q < m - 1; ++q, rl >>= 4) {
-                    const int u = (int)(rl & 0xF);
-                    const double x = DV(1, u);
-                    const double t = __dadd_rn(f, x);
-                    if (sum_mode) {
-                        const double p = __dsub_rn(t, f);
-                        e = __dadd_rn(e, __dadd_rn(__dsub_rn(f, __dsub_rn(t, p)), __dsub_rn(x, p)));
-                    }
-                    f = t;
-                    tail = dmin(DV(2, u), tail);
-                }
-                if (sum_mode && e != 0.0 && isfinite(e)) f = __dadd_rn(f, e);
-                const double bound = __dadd_rn(__dadd_rn(sim[i].kEnd, f), tail);
-                const double est = (bound > sim[i].now) ? bound : sim[i].now;
-                const int r = IR(cc[i]);
-                if (j + i < m && (bj < 0 || key_less(est, sim[i].idleK, r, be, bd, br))) {
-                    bj = cj[i]; be = est; bd = sim[i].idleK; br = r;
-                }
-            }
-        }
-        OSIM_DCHECK(bj >= 0 && bj < m);
-        const int c = rt_at(cand, bj);
-        ot |= (uint64_t)c << (4 * k);
-        cand = rt_drop(cand, bj);
-        NS s;  // advance the checkpoint into the (k+1)-world
-        nh_load<DMA>(s, ck, k, base, ot, k + 1, tH, tK, tD);
-        int steps = ck.steps;
-        for (; steps < 3 * kMaxN && !null_at_ck(s); ++steps) s.step(sigma, rsig);
-        nh_save(s, steps, ck);
-    }
-
-    const int kl = n - 2;  // select_last_tasks (heuristic.py:81-102)
-    double ms;
-    if (n >= 2) {
-        int a = rt_at(cand, 0), b = rt_at(cand, 1);
-        if (IR(b) < IR(a)) { const int x = a; a = b; b = x; }
-        NS sp[2];
-        nh_load<DMA>(sp[0], ck, kl, base, ot | ((uint64_t)a << (4 * kl)) | ((uint64_t)b << (4 * (kl + 1))), n, tH,
-                     tK, tD);
-        nh_load<DMA>(sp[1], ck, kl, base, ot | ((uint64_t)b << (4 * kl)) | ((uint64_t)a << (4 * (kl + 1))), n, tH,
-                     tK, tD);
-        const int rest = __reduce_max_sync(kFull, 3 * n - ck.steps);
-#pragma unroll 1
-        for (int st = 0; st < rest; st += 2) {
-            if (__all_sync(kFull, sp[0].drained() && sp[1].drained())) break;
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                sp[0].step(sigma, rsig);
-                sp[1].step(sigma, rsig);
-            }
-        }
-        ok = ok && ((sp[0].drained() && sp[1].drained()) || !live);
-        const double m_ab = sp[0].now, m_ba = sp[1].now;
-        bool ab;
-        if (m_ab < m_ba) ab = true;
-        else if (m_ba < m_ab) ab = false;
-        else ab = !(DV(2, a) <= DV(2, b));  // tie: shorter DtH last
-        ot |= ((uint64_t)(ab ? a : b) << (4 * kl)) | ((uint64_t)(ab ? b : a) << (4 * (kl + 1)));
-        ms = ab ? m_ab : m_ba;
-    } else {  // n == 1: reorder_batch returns [tg[0]] without simulating
-        NS s;
-        s.init(base, 0, 1, tH, tK, tD);
-        for (int st = 0; st < 3 && !s.drained(); ++st) s.step(sigma, rsig);
-        ok = ok && s.drained();
-        ms = s.now;
-    }
-    if (!__all_sync(kFull, ok) && lane == 0) atomicExch(err, OSIM_ESTALL);
-    if (live) {
-        ms_out[g] = ms;
-        if (nsims_out) nsims_out[g] = (n >= 3) ? (uint32_t)(n * (n - 1) / 2 - 1) : (n == 2 ? 2u : 0u);
-        for (int p = 0; p < n; ++p) order_out[g * (uint64_t)n + p] = (uint8_t)nib(ot, p);
     }
 }
 

@@ -37,8 +37,8 @@ namespace osim {
 // each head that sat at M to the first non-null slot >= M of the full
 // ordering (1-DMA: the prefix world's XFER slot M is the full world's HtD(M)).
 // ---------------------------------------------------------------------------
-template <int DMA, bool SIGP2, bool TRACK, int LAY>
-__device__ __forceinline__ bool null_at_ck(const NullSim<DMA, SIGP2, TRACK, LAY>& s) {
+template <int DMA, bool SIGP2, bool TRACK>
+__device__ __forceinline__ bool null_at_ck(const NullSim<DMA, SIGP2, TRACK>& s) {
     const bool a = idle(s.r0) && s.s0 >= s.n4;  // 1-DMA prefix world: XFER at its DtH part
     const bool c = idle(s.r2) && s.s2 >= s.n4;
     if constexpr (DMA == 2) return a || c || (idle(s.r1) && s.s1 >= s.n4);

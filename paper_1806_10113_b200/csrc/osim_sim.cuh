@@ -781,19 +781,8 @@ struct FastSim {
 // FastSim generalized to null stages (see osim_null.cuh for the contract):
 // position heads, find-first-set skipping over per-sequence null masks,
 // "head passed or stage null" readiness, dt clamped to 0 once all lanes idle.
-template <int DMA, bool SIGP2, bool TRACK = false, int LAYOUT = 0>
+template <int DMA, bool SIGP2, bool TRACK = false>
 struct NullSim {
-    // LAYOUT: 0 = double2 rows at `base`; 2 = lane-interleaved arrays (see FastSim)
-    static_assert(LAYOUT == 0 || LAYOUT == 2, "NullSim layouts");
-    static constexpr uint32_t KS = (LAYOUT == 2) ? 4096u : 256u;
-    __device__ __forceinline__ static uint32_t toff(uint64_t sq, int sh) {
-        if constexpr (LAYOUT == 2) return ((uint32_t)(sq >> sh) & 0xFu) << 8;
-        else return task_off<false>(sq, sh);
-    }
-    __device__ __forceinline__ static void st_(bool p, uint32_t addr, double& nd, double& rc, double& rem) {
-        if constexpr (LAYOUT == 2) start_if_lanes<48 * 256>(p, addr, nd, rc, rem);
-        else start_if(p, addr, nd, rc, rem);
-    }
     uint32_t base;
     uint64_t seq;
     int n, n4;
@@ -868,17 +857,17 @@ struct NullSim {
             const bool st2 = idle(r2) && s2 < n4 && (s2 < s0 || nul(mH, s2));
             const bool st1 = idle(r1) && s1 < n4 && (s1 < s2 || nul(mK, s1)) && (s1 < s0 || nul(mH, s1));
             k_idle_gap(st2);
-            st_(st0, base + toff(seq, s0), d0, c0, r0);
-            st_(st2, base + KS + toff(seq, s2), d2, c2, r2);
-            st_(st1, base + 2 * KS + toff(seq, s1), d1, c1, r1);
+            start_if(st0, base + task_off<false>(seq, s0), d0, c0, r0);
+            start_if(st2, base + 256 + task_off<false>(seq, s2), d2, c2, r2);
+            start_if(st1, base + 512 + task_off<false>(seq, s1), d1, c1, r1);
         } else {
             const bool isH = s0 < n4;
             const int ps = isH ? s0 : s0 - n4;
             const bool st0 = idle(r0) && s0 < 2 * n4 && (isH || ps < s2 || nul(mK, ps));
             const bool st2 = idle(r2) && s2 < n4 && (s2 < s0 || nul(mH, s2));
             k_idle_gap(st2);
-            st_(st0, base + (isH ? 0u : 2 * KS) + toff(seq, ps), d0, c0, r0);
-            st_(st2, base + KS + toff(seq, s2), d2, c2, r2);
+            start_if(st0, base + (isH ? 0u : 512u) + task_off<false>(seq, ps), d0, c0, r0);
+            start_if(st2, base + 256 + task_off<false>(seq, s2), d2, c2, r2);
         }
         // ---- dt (engine.py:200-210); every lane idle (drained): dt = 0
         double dt, dd;
