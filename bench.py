@@ -269,6 +269,15 @@ def run_ours(a):
                              if k in ("issue_active_pct", "fp64_pipe_active_pct", "alu_pipe_active_pct",
                                       "warp_exec_efficiency", "achieved_occupancy_pct",
                                       "theoretical_occupancy_pct", "source")}}
+    # the same against the nominal FP64 pipe rate (64 FP64 lanes per SM x SMs x
+    # the SM clock sampled during the timed region): MEASURED_PEAKS.json has no
+    # FP64 entry, so both denominators are reported
+    sm_mhz_fp = clk.summary().get("sm_mhz")
+    if sm_mhz_fp:
+        sms_fp = torch.cuda.get_device_properties(dev).multi_processor_count
+        nominal = 64.0 * sms_fp * sm_mhz_fp * 1e6 / 1e12
+        roof["peak_nominal"] = nominal
+        roof["frac_nominal"] = achieved / nominal
     # the issue roofline (SURVEY 8(d) ii): warp instructions the kernel executes
     # per launch (the committed ncu capture of the same kernel on the whole
     # 12! space, scaled to this rank's shard) over 4 issues/clk/SM x SMs x the
