@@ -770,7 +770,10 @@ def main():
         # NCCL's init lines (communicator size, transport) on stderr, so the
         # run log shows every rank joined one communicator; set before torch
         # (and with it NCCL) is first imported
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        # (the GPU image sets NCCL_DEBUG=VERSION, which prints only the banner)
+        if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION", "WARN"):
+            os.environ["NCCL_DEBUG"] = "INFO"
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if a.impl == "reference":
         run_reference(a)
     else:
