@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_F1_MINB) k_interleave_pfx(const d
     const int n = T * N;
     stage_dr(durs, n, sdr);
     __syncthreads();
-    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
+    const uint32_t base = opaque_u32((uint32_t)__cvta_generic_to_shared(sdr));  // kept in a register
     const double rsig = __ddiv_rn(1.0, sigma);
     const int ti = threadIdx.x;
     Part acc;
@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_F1_MINB) k_interleave_pfx1(const 
     const int n = T * N;
     stage_dr(durs, n, sdr);
     __syncthreads();
-    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
+    const uint32_t base = opaque_u32((uint32_t)__cvta_generic_to_shared(sdr));  // kept in a register
     const int ti = threadIdx.x;
     Part acc;
     part_init(acc);

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kBlock) k_exhaustive_null_pfx(const double* __
     __syncthreads();
     unsigned tH, tK, tD;
     null_masks_dr(sdr, N, tH, tK, tD);
-    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
+    const uint32_t base = opaque_u32((uint32_t)__cvta_generic_to_shared(sdr));  // kept in a register
     const double rsig = __ddiv_rn(1.0, sigma);
     const uint64_t p_lo = lo / LF, p_hi = (hi + LF - 1) / LF;
     Part acc;
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kBlock) k_exhaustive_batch_null_pfx(const doub
     __shared__ double2 sdr[3 * kStride];
     __shared__ Part sh[32];
     __shared__ NullCk K;
-    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sdr);
+    const uint32_t base = opaque_u32((uint32_t)__cvta_generic_to_shared(sdr));  // kept in a register
     const double rsig = __ddiv_rn(1.0, sigma);
     for (uint64_t b = blockIdx.x; b < B; b += gridDim.x) {
         stage_dr(durs + b * 3 * N, N, sdr);
