@@ -35,7 +35,14 @@ constexpr int kHLT = 32 * kHLW;                             // threads per CTA
 #endif
 constexpr int kHLLPG = OSIM_HL_LPG;  // lanes per group (1: a group per lane; 2: lanes l, l + 16)
 constexpr int kHLGPW = 32 / kHLLPG;  // groups per warp
-constexpr size_t kHLWarpSmem = 2 * 48 * kHLGPW * sizeof(double);  // nd + 1/nd, [48][groups] each
+#ifndef OSIM_HL_LAYOUT
+#define OSIM_HL_LAYOUT 6
+#endif
+// FastSim layout: 2 (all three kinds in shared memory) or 6 (K and DtH in
+// shared memory, a candidate's HtD durations loaded from global memory)
+constexpr int kHLLay = kHLLPG == 1 ? OSIM_HL_LAYOUT : 3;
+constexpr int kHLRows = kHLLay == 6 ? 32 : 48;  // shared rows per group
+constexpr size_t kHLWarpSmem = 2 * kHLRows * kHLGPW * sizeof(double);  // nd + 1/nd, [rows][groups] each
 
 #ifndef OSIM_HL_ILP
 #define OSIM_HL_ILP 0  // 0: the measured best per DMA mode
@@ -135,7 +142,9 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
                                                          double* __restrict__ ms_out,
                                                          uint32_t* __restrict__ nsims_out,
                                                          const uint32_t* __restrict__ perm) {
-    using FS = FastSim<DMA, SP2, true, false, false, kHLLPG == 1 ? 2 : 3>;
+    using FS = FastSim<DMA, SP2, true, false, false, kHLLay>;
+    constexpr bool kRH = kHLLay == 6;
+    constexpr int kK0 = kRH ? 1 : 0;  // first kind held in shared memory
     constexpr int kHLILP = hl_ilp<DMA>();
     constexpr int W = kHLGPW;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -143,7 +152,7 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
     const int lane = lane0 % W;    // this lane's group within the warp
     const int sub = lane0 / W;     // which of the group's lanes (kHLLPG = 2: candidate sets alternate)
     double* nd = reinterpret_cast<double*>(smem_raw + warp * kHLWarpSmem);  // [48][W]
-    double* rcp = nd + 48 * W;
+    double* rcp = nd + kHLRows * W;
     const uint64_t g0 = ((uint64_t)blockIdx.x * kHLW + warp) * W;
     if (g0 >= B) return;  // whole warp leaves together; no block barriers below
     const bool live = g0 + lane < B;
@@ -156,15 +165,17 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
     // (bank-conflict-free stores; the strided loads hit L1 after the first
     // touch of each line); tasks >= n get 1.0
     (void)Gv;  // (tasks of a lane past the batch end are 1.0 placeholders)
-    for (int kt = sub * (48 / kHLLPG); kt < (sub + 1) * (48 / kHLLPG); ++kt) {  // a group's lanes split it
-        const int k = kt >> 4, t = kt & 15;
+    for (int kt = sub * (kHLRows / kHLLPG); kt < (sub + 1) * (kHLRows / kHLLPG); ++kt) {  // a group's lanes split it
+        const int k = (kt >> 4) + kK0, t = kt & 15;
         const double v = (live && t < n) ? durs[g * 3 * (uint64_t)n + 3 * t + k] : 1.0;
         nd[kt * W + lane] = v;
         rcp[kt * W + lane] = __ddiv_rn(1.0, v);
     }
     __syncwarp();
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(nd) + 8u * (uint32_t)lane;
-    auto DV = [&](int k, int t) { return nd[(k * 16 + t) * W + lane]; };
+    auto DV = [&](int k, int t) { return nd[((k - kK0) * 16 + t) * W + lane]; };
+    const double* gH = durs + g * 3 * (uint64_t)n;  // LAYOUT 6: HtD durations of task t at gH[3t]
+    auto HV = [&](int t) { return kRH ? ((live && t < n) ? gH[3 * t] : 1.0) : DV(0, t); };
     uint64_t idr = 0;  // id rank per task, 4 bits each
     for (int t = 0; t < n; ++t) idr |= (uint64_t)(live ? id_rank[g * (uint64_t)n + t] : (uint8_t)t) << (4 * t);
     auto IR = [&](int t) { return (int)((idr >> (4 * t)) & 0xF); };
@@ -181,7 +192,7 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
             int best = 0;
             double b1 = 0, b2 = 0;
             for (int t = 0; t < n; ++t) {
-                const double k1 = -__dsub_rn(DV(1, t), DV(0, t));
+                const double k1 = -__dsub_rn(DV(1, t), HV(t));
                 const double k2 = -DV(2, t);
                 bool less;
                 if (t == 0) less = true;
@@ -195,6 +206,7 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
             ot = (uint64_t)best;
             rm = all & ~(1u << best);
             s.init(base, ot, 1);
+            if constexpr (kRH) { const double h = HV(best); s.set_htd(h, __ddiv_rn(1.0, h)); }
             for (int q = 0; q < 3 * kMaxN && s.htd_done() < 1; ++q) s.step(sigma, rsig);
         } else {
             s.init(base, 0, 1);  // empty prefix: the initial state
@@ -223,6 +235,7 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
                 cc[i] = rt_at(cand, cj[i]);
                 sim[i].init(base, ot | ((uint64_t)cc[i] << (4 * k)), k + 1);
                 sim[i].load(ck);
+                if constexpr (kRH) { const double h = HV(cc[i]); sim[i].set_htd(h, __ddiv_rn(1.0, h)); }
                 sim[i].start_htd();
             }
             run_multi<false>(sim, rest, sigma, rsig);
@@ -306,6 +319,7 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
         FS s;
         s.init(base, ot, k + 1);
         s.load(ck);
+        if constexpr (kRH) { const double h = HV(c); s.set_htd(h, __ddiv_rn(1.0, h)); }
         s.start_htd();  // the chosen task's HtD, the queue's last
         if constexpr (DMA == 2) {
             for (int q = 0; q < 3 * kMaxN && s.htd_done() < k + 1; ++q) s.template step<false>(sigma, rsig);
@@ -325,6 +339,11 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
         sp[1].init(base, ot | ((uint64_t)b << (4 * kl)) | ((uint64_t)a << (4 * (kl + 1))), n);
         sp[0].load(ck);
         sp[1].load(ck);
+        if constexpr (kRH) {  // the two queued HtDs, in each ordering's order
+            const double ha = HV(a), hb = HV(b), ra = __ddiv_rn(1.0, ha), rb = __ddiv_rn(1.0, hb);
+            sp[0].set_htd(ha, ra, hb, rb);
+            sp[1].set_htd(hb, rb, ha, ra);
+        }
         const int rest = __reduce_max_sync(kFull, 3 * n - sp[0].finalized());
         run_multi<true>(sp, rest, sigma, rsig);
         const double m_ab = sp[0].now, m_ba = sp[1].now;
@@ -337,6 +356,7 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
     } else {
         FS s;  // n == 1: reorder_batch returns [tg[0]] without simulating
         s.init(base, 0, 1);
+        if constexpr (kRH) { const double h = HV(0); s.set_htd(h, __ddiv_rn(1.0, h)); }
         for (int st = 0; st < 3; ++st) s.step(sigma, rsig);
         ms = s.now;
     }

@@ -453,10 +453,13 @@ template <int DMA, bool SIGP2, bool TRACK, bool PRE, bool DEPS = false, int LAYO
 struct FastSim {
     static_assert(LAYOUT == 0 || LAYOUT == 4 || !PRE, "pre-shifted sequences assume the double2 rows");
     static constexpr int kDma = DMA;
-    static constexpr bool kLanes = LAYOUT == 2 || LAYOUT == 3;  // lane-interleaved arrays
-    static constexpr int kTSh = (LAYOUT == 2) ? 8 : 7;  // LAYOUTs 2/3: log2 bytes per task row
+    static constexpr bool kLanes = LAYOUT == 2 || LAYOUT == 3 || LAYOUT == 6;  // lane-interleaved arrays
+    static constexpr bool kRegH = LAYOUT == 6;  // HtD durations from registers (set_htd), not shared memory
+    static constexpr int kTSh = (LAYOUT == 3) ? 7 : 8;  // LAYOUTs 2/3/6: log2 bytes per task row
     static constexpr uint32_t KS = kLanes ? (16u << kTSh) : 256u;  // bytes per kind row
-    static constexpr int kRcOff = 48 << kTSh;                 // LAYOUTs 2/3: 1/nd above nd
+    static constexpr int kRcOff = (kRegH ? 32 : 48) << kTSh;  // LAYOUTs 2/3/6: 1/nd above nd
+    static constexpr uint32_t KO_K = kRegH ? 0u : KS;       // kind row offsets (LAYOUT 6 stores K, DtH only)
+    static constexpr uint32_t KO_D = kRegH ? KS : 2 * KS;
     __device__ __forceinline__ static uint32_t toff(uint64_t sq, int sh) {
         if constexpr (kLanes) return ((uint32_t)(sq >> sh) & 0xFu) << kTSh;
         else return task_off<PRE>(sq, sh);
@@ -476,6 +479,7 @@ struct FastSim {
         else start_if(p, addr, nd, rc, rem);
     }
     uint32_t base;
+    double hnd, hrc, hnd2, hrc2;  // LAYOUT 6: {nd, 1/nd} of the next two HtDs to start (set_htd)
     uint64_t seq;   // packed ordering (pre-shifted by 4 when PRE)
     uint64_t dseq;  // DEPS: packed 1 + prerequisite position (pre-shifted like seq)
     int n4;         // 4*n
@@ -501,7 +505,18 @@ struct FastSim {
     __device__ __forceinline__ void set_seq(uint64_t sq) { seq = PRE ? (sq << 4) : sq; }
     // start the HtD at the queue head now (the HtD lane is idle and an HtD
     // is always ready): what the next step's start phase would do
-    __device__ __forceinline__ void start_htd() { st_(true, adr(0, toff(seq, s0)), d0, c0, r0); }
+    __device__ __forceinline__ void start_htd() {
+        if constexpr (kRegH) reg_htd(true);
+        else st_(true, adr(0, toff(seq, s0)), d0, c0, r0);
+    }
+    // LAYOUT 6: the durations of the next HtD the queue will start
+    __device__ __forceinline__ void set_htd(double nd, double rc, double nd2 = 1.0, double rc2 = 1.0) {
+        hnd = nd; hrc = rc; hnd2 = nd2; hrc2 = rc2;
+    }
+    __device__ __forceinline__ void reg_htd(bool st) {  // LAYOUT 6: start the pending HtD if st
+        d0 = st ? hnd : d0; c0 = st ? hrc : c0; r0 = st ? hnd : r0;
+        hnd = st ? hnd2 : hnd; hrc = st ? hrc2 : hrc;
+    }
     __device__ __forceinline__ int finalized() const { return (s0 + s1 + s2) >> 2; }
 
     // checkpoint image (prefix sharing across calls, e.g. in shared memory)
@@ -541,8 +556,8 @@ struct FastSim {
         const bool st2 = idle(r2) && s2 < n4;
         const bool st1 = idle(r1) && s1 < s2;
         k_idle_gap(st2);
-        st_(st2, adr(KS, toff(seq, s2)), d2, c2, r2);
-        st_(st1, adr(2 * KS, toff(seq, s1)), d1, c1, r1);
+        st_(st2, adr(KO_K, toff(seq, s2)), d2, c2, r2);
+        st_(st1, adr(KO_D, toff(seq, s1)), d1, c1, r1);
         const double dt = dmin(r1, r2);
         now = __dadd_rn(now, dt);
         r2 = upd(r2, dt, d2, c2);
@@ -559,7 +574,7 @@ struct FastSim {
     __device__ __forceinline__ void step_d() {
         static_assert(DMA == 2, "2-DMA only");
         const bool st1 = idle(r1) && s1 < n4;
-        st_(st1, adr(2 * KS, toff(seq, s1)), d1, c1, r1);
+        st_(st1, adr(KO_D, toff(seq, s1)), d1, c1, r1);
         const double dt = r1;  // the only lane that can run (rem ~0 once drained)
         now = __dadd_rn(now, dt);
         r1 = upd(r1, dt, d1, c1);
@@ -579,8 +594,8 @@ struct FastSim {
         const bool st0 = idle(r0) && s0 < 2 * n4 && s2 > ps;
         const bool st2 = idle(r2) && s2 < n4;
         k_idle_gap(st2);
-        st_(st0, adr(2 * KS, toff(seq, ps)), d0, c0, r0);
-        st_(st2, adr(KS, toff(seq, s2)), d2, c2, r2);
+        st_(st0, adr(KO_D, toff(seq, ps)), d0, c0, r0);
+        st_(st2, adr(KO_K, toff(seq, s2)), d2, c2, r2);
         const double dt = dmin(r0, r2);
         now = __dadd_rn(now, dt);
         r0 = upd(r0, dt, d0, c0);
@@ -603,8 +618,8 @@ struct FastSim {
         const bool st0 = idle(r0) && s0 < 2 * n4 && s2 > ps;
         const bool st2 = idle(r2) && s2 < n4 && s2 < s0;
         k_idle_gap(st2);
-        st_(st0, adr(2 * KS, toff(seq, ps)), d0, c0, r0);
-        st_(st2, adr(KS, toff(seq, s2)), d2, c2, r2);
+        st_(st0, adr(KO_D, toff(seq, ps)), d0, c0, r0);
+        st_(st2, adr(KO_K, toff(seq, s2)), d2, c2, r2);
         const double dt = dmin(r0, r2);
         now = __dadd_rn(now, dt);
         r0 = upd(r0, dt, d0, c0);
@@ -621,7 +636,7 @@ struct FastSim {
     __device__ __forceinline__ void step_1dd() {
         static_assert(DMA == 1, "1-DMA only");
         const bool st0 = idle(r0) && s0 < 2 * n4;
-        st_(st0, adr(2 * KS, toff(seq, s0 - n4)), d0, c0, r0);
+        st_(st0, adr(KO_D, toff(seq, s0 - n4)), d0, c0, r0);
         const double dt = r0;  // the only lane that can run (rem ~0 once drained)
         now = __dadd_rn(now, dt);
         r0 = upd(r0, dt, d0, c0);
@@ -700,17 +715,28 @@ struct FastSim {
             const bool st2 = idle(r2) && s2 < s0;
             const bool st1 = idle(r1) && s1 < s2;
             k_idle_gap(st2);
-            if constexpr (H0) st_(st0, adr(0, toff(seq, s0)), d0, c0, r0);
-            st_(st2, adr(KS, toff(seq, s2)), d2, c2, r2);
-            st_(st1, adr(2 * KS, toff(seq, s1)), d1, c1, r1);
+            if constexpr (H0) {
+                if constexpr (kRegH) {  // the pending HtD's durations (set_htd)
+                    reg_htd(st0);
+                } else {
+                    st_(st0, adr(0, toff(seq, s0)), d0, c0, r0);
+                }
+            }
+            st_(st2, adr(KO_K, toff(seq, s2)), d2, c2, r2);
+            st_(st1, adr(KO_D, toff(seq, s1)), d1, c1, r1);
         } else {
             const bool isH = s0 < n4;
             const int ps = isH ? s0 : s0 - n4;
             const bool st0 = idle(r0) && s0 < 2 * n4 && (isH || s2 > ps);
             const bool st2 = idle(r2) && s2 < n4 && s2 < s0;
             k_idle_gap(st2);
-            st_(st0, adr(isH ? 0u : 2 * KS, toff(seq, ps)), d0, c0, r0);
-            st_(st2, adr(KS, toff(seq, s2)), d2, c2, r2);
+            if constexpr (kRegH) {  // an XFER HtD from the pending registers, a DtH from shared memory
+                st_(st0 && !isH, adr(KO_D, toff(seq, ps)), d0, c0, r0);
+                reg_htd(st0 && isH);
+            } else {
+                st_(st0, adr(isH ? 0u : 2 * KS, toff(seq, ps)), d0, c0, r0);
+            }
+            st_(st2, adr(KO_K, toff(seq, s2)), d2, c2, r2);
         }
         // ---- dt (engine.py:200-210)
         double dt, dd;
