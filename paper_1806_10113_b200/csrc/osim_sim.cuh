@@ -438,6 +438,9 @@ __device__ __forceinline__ uint32_t task_off(uint64_t seq, int sh) {
 // like `seq`.  With every stage non-null a task is finished exactly when its
 // DtH finalized, and DtHs finalize in sequence order, so the gate is one
 // extra condition on the HtD start: s1 >= 4 * (1 + prerequisite position).
+#ifndef OSIM_LANE_MAD
+#define OSIM_LANE_MAD 1
+#endif
 // LAYOUT of the durations in shared memory:
 //  0: double2 {nd, 1/nd} rows [3][16] at `base` (kind k, task t at base + k*256 + t*16),
 //     one 16-byte + one 8-byte load per command start;
@@ -460,8 +463,9 @@ struct FastSim {
     static constexpr int kRcOff = (kRegH ? 32 : 48) << kTSh;  // LAYOUTs 2/3/6: 1/nd above nd
     static constexpr uint32_t KO_K = kRegH ? 0u : KS;       // kind row offsets (LAYOUT 6 stores K, DtH only)
     static constexpr uint32_t KO_D = kRegH ? KS : 2 * KS;
+    // LAYOUTs 2/3/6: the task index (times the row stride in adr()); else the byte offset
     __device__ __forceinline__ static uint32_t toff(uint64_t sq, int sh) {
-        if constexpr (kLanes) return ((uint32_t)(sq >> sh) & 0xFu) << kTSh;
+        if constexpr (kLanes) return (uint32_t)(sq >> sh) & 0xFu;
         else return task_off<PRE>(sq, sh);
     }
     // address of the (kind offset kofs, task offset t) entry; LAYOUT 4 (the
@@ -470,7 +474,17 @@ struct FastSim {
     // immediate -- no shared-window base rematerialized in the loops
     __device__ __forceinline__ uint32_t adr(uint32_t kofs, uint32_t t) const {
         if constexpr (LAYOUT == 4) return (base | t) + kofs;
-        else return base + kofs + t;
+        else if constexpr (kLanes) {
+#if OSIM_LANE_MAD
+            // one multiply-add for row * stride + base (the compiler otherwise
+            // emits shift, mask and add for the masked-then-shifted index)
+            uint32_t a;
+            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(a) : "r"(t), "n"(1 << kTSh), "r"(base));
+            return a + kofs;
+#else
+            return base + kofs + (t << kTSh);
+#endif
+        } else return base + kofs + t;
     }
     // a command start: {nd, 1/nd} and rem = nd from shared memory
     __device__ __forceinline__ static void st_(bool p, uint32_t addr, double& nd, double& rc, double& rem) {
