@@ -6,13 +6,15 @@
 // lane slots empty, and the per-group serial phases (key argmin, checkpoint
 // advance) run on 8 of 32 lanes.  Here every lane owns a group and walks its
 // round's m candidates itself, kHLILP at a time (independent simulations
-// interleaved in one instruction stream for ILP: with 9 warps per SM the
+// interleaved in one instruction stream for ILP: with 13 warps per SM the
 // kernel needs it to keep the issue slots busy), so only the last partial
 // set of a round wastes slots and every serial phase runs on all 32 lanes.  The checkpoint of
 // simulate(ot) (prefix sharing) lives in registers; the
-// group's durations live in shared memory in FastSim LAYOUT 2 (nd and 1/nd
-// arrays interleaved by lane, bank-conflict free).  Shared memory per warp:
-// 24 KB, so 9 warps per SM; the ILP makes up for the fewer warps.
+// group's kernel and DtH durations live in shared memory in FastSim LAYOUT 6
+// (nd and 1/nd arrays interleaved by lane, bank-conflict free), its HtD
+// durations are read from global memory as a replay is set up (a replay
+// starts at most two queued HtDs).  Shared memory per warp: 16 KB, so 13
+// warps per SM (LAYOUT 2 with all three kinds: 24 KB, 9 warps).
 // The per-candidate operation sequence is the one k_heuristic_fast runs
 // (same FastSim steps from the same checkpoint, CPython's sum over `rest` in
 // rt order, the (estimate, idle_K, id) key, select_last_tasks' tie rule), so
