@@ -516,7 +516,9 @@ struct FastSim {
         kEnd = 0.0;
         idleK = 0.0;
     }
-    __device__ __forceinline__ void set_seq(uint64_t sq) { seq = PRE ? (sq << 4) : sq; }
+    __device__ __forceinline__ void set_seq(uint64_t sq) { seq = pack_seq(sq); }
+    static constexpr bool kPre = PRE;
+    __device__ __forceinline__ static uint64_t pack_seq(uint64_t sq) { return PRE ? (sq << 4) : sq; }
     // start the HtD at the queue head now (the HtD lane is idle and an HtD
     // is always ready): what the next step's start phase would do
     __device__ __forceinline__ void start_htd() {
