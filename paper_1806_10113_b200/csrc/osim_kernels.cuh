@@ -82,14 +82,32 @@ __device__ __forceinline__ void part_add(Part& a, double ms, unsigned long long 
     a.count += 1;
 }
 
+#ifndef OSIM_LEAF_LEAN
+#define OSIM_LEAF_LEAN 1
+#endif
 // prefix-kernel leaf: part_add without the count (added per prefix) and the
-// renormalization (every 4 leaves); the threshold count only when STATS
-template <bool STATS>
+// renormalization (every 8 leaves); the threshold count only when STATS.
+// LEAN (makespans are positive and finite): ranks compared in 32 bits when
+// every rank fits (R32: n <= 12), the maximum without fmax's NaN handling,
+// and the running sum compensated by Fast2Sum (t = s + x, error x - (t - s),
+// exact whenever s >= x, i.e. from the second or third leaf of a thread on;
+// the mean is not bit-exact anyway, see the reduction note in DESIGN.md)
+template <bool STATS, bool R32 = false>
 __device__ __forceinline__ void leaf_add(Part& a, double ms, unsigned long long r, double thr) {
+#if OSIM_LEAF_LEAN
+    const bool rl = R32 ? ((uint32_t)r < (uint32_t)a.rank) : (r < a.rank);
+    if (ms < a.best || (ms == a.best && rl)) { a.best = ms; a.rank = r; }
+    if constexpr (STATS) a.below += (ms < thr) ? 1ull : 0ull;
+    a.worst = (a.worst < ms) ? ms : a.worst;
+    const double t = __dadd_rn(a.sum, ms);
+    a.csum = __dadd_rn(a.csum, __dsub_rn(ms, __dsub_rn(t, a.sum)));
+    a.sum = t;
+#else
     if (ms < a.best || (ms == a.best && r < a.rank)) { a.best = ms; a.rank = r; }
     if constexpr (STATS) a.below += (ms < thr) ? 1ull : 0ull;
     a.worst = fmax(a.worst, ms);
     neumaier(a.sum, a.csum, ms);
+#endif
     a.lpm = __dmul_rn(a.lpm, ms);
 }
 
@@ -554,11 +572,12 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
 #pragma unroll 1
         for (int j = 0; j < (int)LF; ++j) {
 #if OSIM_SJT
-            // (2-DMA: the table load stays here, ahead of the replay, instead
-            // of being sunk to the rank's first use after it -- measured
-            // +0.1 to +0.2 % on 2-DMA, -0.9 % on 1-DMA)
-            const uint32_t tj = (OSIM_SJT_PIN && DMA == 2) ? opaque_u32(sjt_tab<L>(j)) : sjt_tab<L>(j);
-            const uint64_t r = r0 + (uint64_t)(tj & 0xFFu);
+            // (the rank is taken here, ahead of the replay, instead of
+            // the table load being sunk to its first use after it; pinning the
+            // whole entry instead moved the swap off the uniform datapath)
+            const uint32_t tj = sjt_tab<L>(j);
+            const uint32_t rj = OSIM_SJT_PIN ? opaque_u32(tj & 0xFFu) : (tj & 0xFFu);
+            const uint64_t r = r0 + (uint64_t)rj;  // (the swap below keeps tj uniform)
             if constexpr (M > 0) ck_load(K, q, ti, s, M);
             else s.init(base, 0, N);
             s.seq = cur;
@@ -589,16 +608,18 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
 #endif
             s.run_phased(rest, sigma, rsig);
             if (all_in || (any_in && r >= lo && r < hi)) {
-                leaf_add<STATS>(acc, s.now, r, thr);
+                leaf_add<STATS, (N <= 12)>(acc, s.now, r, thr);
                 if constexpr (STATS) {
                     OSIM_DCHECK(r >= ms_base && r >= lo && r < hi);
                     if (ms_out) ms_out[r - ms_base] = s.now;
                 }
             }
-            // the log-product's exponent is split off every 4 leaves (exact:
-            // only the binary exponent moves; 4 fast-path makespans stay
-            // within [2^-240, 2^120])
-            if ((j & 3) == 3 || j == (int)LF - 1) renorm<false>(acc.lpm, acc.lpe);
+            // the log-product's exponent is split off every 8 leaves (exact:
+            // only the binary exponent moves; a fast-path makespan lies in
+            // [2^-60, 2^88] -- durations in [2^-60, 2^22), sigma >= 2^-60,
+            // n <= 16 -- so 8 of them times the mantissa in [1, 2) stay within
+            // [2^-480, 2^705], inside the normal range)
+            if ((j & 7) == 7 || j == (int)LF - 1) renorm<false>(acc.lpm, acc.lpe);
         }
     }
     // No trailing barrier: after the copy above every K slot is read only by
