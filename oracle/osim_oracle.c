@@ -931,8 +931,8 @@ int oracle_harness(const double* durs, const uint8_t* id_rank, int T, int N, int
             for (int a = 0; a < n_avail; ++a)                                               \
                 if (avail[a] == w) ws[m++] = w;                                             \
         int tg[16];                                                                         \
-        double td[16 * 3];                                                                  \
-        uint8_t tr[16], sub[16], order8[16];                                                \
+        double td[16 * 3] = {0};                                                            \
+        uint8_t tr[16] = {0}, sub[16], order8[16];                                          \
         for (int i = 0; i < m; ++i) {                                                       \
             tg[i] = ws[i] * N + next_idx[ws[i]];                                            \
             next_idx[ws[i]]++;                                                              \
