@@ -346,6 +346,55 @@ __device__ __forceinline__ void ck_load(const CkSlots<SLOTS>& K, int slot, int i
     s.s0 = 4 * hdone;
 }
 
+constexpr int kPfxQ = 2;  // prefixes per thread and prefix-kernel call
+#ifndef OSIM_SUBCK
+#define OSIM_SUBCK 1
+#endif
+#ifndef OSIM_SUB_MINN
+#define OSIM_SUB_MINN 11  // sub-checkpoints for groups of at least this many tasks
+#endif
+#ifndef OSIM_SUB_D1
+#define OSIM_SUB_D1 0     // ... and on 1-DMA devices
+#endif
+// Checkpoint slots of the prefix kernels, two kinds.  Full (CkSlots): the
+// clock, the K/DtH rems and their {nd, 1/nd} (7 doubles + 2 ints per slot).
+// Compact (PfxCkC, 2-DMA when OSIM_SUBCK): only the clock, the rems and the
+// heads (3 doubles + 2 ints); the running commands' {nd, 1/nd} are reloaded
+// from the duration rows by their task (the K/DtH heads), which needs the
+// sequence set first -- and one more slot per thread holds the
+// sub-checkpoint one HtD later (see pfx_leaves).  Both fit the same dynamic
+// shared memory (kPfxCkBytes).
+struct PfxCkC {
+    double v[kPfxQ + 1][3][kBlock];  // now, r1, r2; slot kPfxQ: the sub-checkpoint
+    int h[kPfxQ + 1][2][kBlock];     // s1, s2
+};
+template <class T> struct CkNV { static constexpr int v = 7; };
+template <> struct CkNV<PfxCkC> { static constexpr int v = 3; };
+template <bool C> struct PfxCkSel { using T = CkSlots<kPfxQ>; };
+template <> struct PfxCkSel<true> { using T = PfxCkC; };
+constexpr size_t kPfxCkBytes =
+    sizeof(PfxCkC) > sizeof(CkSlots<kPfxQ>) ? sizeof(PfxCkC) : sizeof(CkSlots<kPfxQ>);
+template <class FS>
+__device__ __forceinline__ void pk_store(PfxCkC& K, int slot, int i, const FS& s) {
+    K.v[slot][0][i] = s.now; K.v[slot][1][i] = s.r1; K.v[slot][2][i] = s.r2;
+    K.h[slot][0][i] = s.s1; K.h[slot][1][i] = s.s2;
+}
+// restore (s.seq set): the HtD lane idle with `hdone` HtDs finalized
+template <class FS>
+__device__ __forceinline__ void pk_load(const PfxCkC& K, int slot, int i, FS& s, int hdone) {
+    s.now = K.v[slot][0][i]; s.r1 = K.v[slot][1][i]; s.r2 = K.v[slot][2][i];
+    s.s1 = K.h[slot][0][i]; s.s2 = K.h[slot][1][i];
+    s.r0 = kBig;
+    s.s0 = 4 * hdone;
+    s.reload_kd();
+}
+template <class FS>
+__device__ __forceinline__ void pk_store(CkSlots<kPfxQ>& K, int slot, int i, const FS& s) { ck_store(K, slot, i, s); }
+template <class FS>
+__device__ __forceinline__ void pk_load(const CkSlots<kPfxQ>& K, int slot, int i, FS& s, int hdone) {
+    ck_load(K, slot, i, s, hdone);
+}
+
 // Advance every lane of the warp to the checkpoint "htd_done() == target";
 // returns this lane's step count.
 template <class FS>
@@ -422,7 +471,6 @@ constexpr int kSaBins = 64;  // sa <= 3 * kMaxN; bin kSaBins - 1 = no prefix
 #ifndef OSIM_BATCH_LAYOUT
 #define OSIM_BATCH_LAYOUT 4  // k_exhaustive_batch_pfx
 #endif
-constexpr int kPfxQ = 2;
 constexpr int kNW = kBlock / 32;
 struct PfxSort {
     uint64_t seq[kPfxQ * kBlock];
@@ -487,15 +535,19 @@ __device__ __forceinline__ int2 pfx_sort(PfxSort& S, int sa0, int sa1) {
 // Simulate this CTA's prefixes P0 + t and P0 + 256 + t (t = thread) of
 // length M and every suffix; accumulate leaves that fall inside [lo, hi) and
 // below prefix p_end.  All threads of the CTA must call together.
-// (A second checkpoint level two positions later was measured slower on B200:
+// (A further checkpoint level two positions later was measured slower on B200:
 // its middle segment runs in divergent advance loops shared by only two
 // leaves.)
 template <int N, int DMA, bool SIGP2, int L, bool STATS, int LAY>
 __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double rsig, uint64_t P0, uint64_t p_end,
                                            uint64_t lo, uint64_t hi, double thr, Part& acc,
-                                           double* __restrict__ ms_out, uint64_t ms_base, CkSlots<kPfxQ>& K,
+                                           double* __restrict__ ms_out, uint64_t ms_base, unsigned char* dsm,
                                            PfxSort& S) {
     constexpr int M = N - L;
+    constexpr bool kC = OSIM_SUBCK && (DMA == 2 || OSIM_SUB_D1);  // compact slots (+ sub-checkpoints)
+    using CK = typename PfxCkSel<kC>::T;
+    constexpr int kCkV = CkNV<CK>::v;
+    CK& K = *reinterpret_cast<CK*>(dsm);
     constexpr uint64_t LF = Fact<L>::v;
     using FS = FastSim<DMA, SIGP2, false, (N <= 15), false, LAY>;
     const int ti = threadIdx.x;
@@ -511,7 +563,7 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
         int a = 0;
         if constexpr (M > 0) {
             a = advance_to(s, valid ? M : 0, sigma, rsig);
-            ck_store(K, q, ti, s);
+            pk_store(K, q, ti, s);
         }
         OSIM_DCHECK(a >= 0 && a < kSaBins - 1);
         sa[q] = valid ? a : kSaBins - 1;
@@ -522,28 +574,40 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
     // ---- reassign: this thread replays entries e.x then e.y
     const int2 e = pfx_sort(S, sa[0], sa[1]);
     uint64_t seqq[kPfxQ], Pq[kPfxQ];
-    double tv[7];
-    int th[2];
+    double tu[kCkV], tv[kCkV];
+    int tg[2], th[2];
     {
         const int ex = e.x & (kBlock - 1), qx = e.x >> 8;
         const int ey = e.y & (kBlock - 1), qy = e.y >> 8;
         static_assert(kBlock == 256, "entry index split");
         seqq[0] = S.seq[e.x]; Pq[0] = S.P[e.x]; sa[0] = S.sa[e.x];
         seqq[1] = S.seq[e.y]; Pq[1] = S.P[e.y]; sa[1] = S.sa[e.y];
-        if constexpr (M > 0) {
+        if constexpr (kC && M > 0) {  // raw copies (a compact restore needs the sequence)
+#pragma unroll
+            for (int k = 0; k < kCkV; ++k) { tu[k] = K.v[qx][k][ex]; tv[k] = K.v[qy][k][ey]; }
+            tg[0] = K.h[qx][0][ex]; tg[1] = K.h[qx][1][ex];
+            th[0] = K.h[qy][0][ey]; th[1] = K.h[qy][1][ey];
+            __syncthreads();  // every source slot has been read
+#pragma unroll
+            for (int k = 0; k < kCkV; ++k) { K.v[0][k][ti] = tu[k]; K.v[1][k][ti] = tv[k]; }
+            K.h[0][0][ti] = tg[0]; K.h[0][1][ti] = tg[1];
+            K.h[1][0][ti] = th[0]; K.h[1][1][ti] = th[1];
+        } else if constexpr (M > 0) {
+            (void)tu; (void)tg;
             ck_load(K, qx, ex, s, M);
 #pragma unroll
-            for (int k = 0; k < 7; ++k) tv[k] = K.v[qy][k][ey];
+            for (int k = 0; k < kCkV; ++k) tv[k] = K.v[qy][k][ey];
             th[0] = K.h[qy][0][ey];
             th[1] = K.h[qy][1][ey];
-        }
-        __syncthreads();  // every source slot has been read
-        if constexpr (M > 0) {
+            __syncthreads();  // every source slot has been read
             ck_store(K, 0, ti, s);
 #pragma unroll
-            for (int k = 0; k < 7; ++k) K.v[1][k][ti] = tv[k];
+            for (int k = 0; k < kCkV; ++k) K.v[1][k][ti] = tv[k];
             K.h[1][0][ti] = th[0];
             K.h[1][1][ti] = th[1];
+        } else {
+            (void)tu; (void)tg; (void)tv; (void)th;
+            __syncthreads();
         }
     }
     // ---- phase B: replay the L! suffixes of each taken prefix
@@ -561,6 +625,48 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
         const bool any_in = validP && r0 + LF > lo && r0 < hi;
         const bool all_in = validP && r0 >= lo && r0 + LF <= hi;
         if (any_in) acc.count += (r0 + LF < hi ? r0 + LF : hi) - (r0 > lo ? r0 : lo);
+        // sub-checkpoints: the (L-1)! leaves that share the first suffix task
+        // f also share the replay up to f's HtD finalize, so it runs once per
+        // f (lock-step advance, stored in the thread's sub slot) and each
+        // leaf replays only from there; the L-1 later tasks in adjacent-swap
+        // order, ranks f * (L-1)! + the table's
+        if constexpr (kC && L >= 3 && M > 0 && N >= OSIM_SUB_MINN) {
+            constexpr int L1 = L - 1;
+            constexpr uint64_t LF1 = Fact<L1>::v;
+            constexpr int kSh1 = 4 * (M + 1) + (FS::kPre ? 4 : 0);  // bit of suffix position 1
+#pragma unroll 1
+            for (int f = 0; f < L; ++f) {
+                const uint64_t lowm = (1ull << (4 * f)) - 1ull;
+                const uint64_t others = (rem & lowm) | ((rem >> (4 * (f + 1))) << (4 * f));  // ascending
+                const uint64_t suf = ((rem >> (4 * f)) & 0xFull) | (others << 4);
+                uint64_t cur = FS::pack_seq(pre | (suf << (4 * M)));
+                s.seq = cur;
+                pk_load(K, q, ti, s, M);
+                const int af = advance_to(s, validP ? M + 1 : 0, sigma, rsig);
+                pk_store(K, kPfxQ, ti, s);
+                const int restf = 3 * N - __reduce_min_sync(kFull, validP ? sa[q] + af : 3 * N);
+#pragma unroll 1
+                for (int j = 0; j < (int)LF1; ++j) {
+                    const uint32_t tj = sjt_tab<L1>(j);
+                    const int lj = f * (int)LF1 + (int)(tj & 0xFFu);  // lexicographic leaf index
+                    const uint64_t r = r0 + (uint64_t)(OSIM_SJT_PIN ? opaque_u32((uint32_t)lj) : (uint32_t)lj);
+                    s.seq = cur;
+                    pk_load(K, kPfxQ, ti, s, M + 1);
+                    swap_nibbles<kSh1, L1>(cur, (int)(tj >> 8));
+                    s.run_phased(restf, sigma, rsig);
+                    if (all_in || (any_in && r >= lo && r < hi)) {
+                        leaf_add<STATS, (N <= 12)>(acc, s.now, r, thr);
+                        if constexpr (STATS) {
+                            OSIM_DCHECK(r >= ms_base && r >= lo && r < hi);
+                            if (ms_out) ms_out[r - ms_base] = s.now;
+                        }
+                    }
+                    const int k = f * (int)LF1 + j;  // leaves done in this prefix, minus one
+                    if ((k & 7) == 7 || k == (int)LF - 1) renorm<false>(acc.lpm, acc.lpe);
+                }
+            }
+            continue;
+        }
 #if OSIM_SJT
         // the L! suffixes in adjacent-swap (Steinhaus-Johnson-Trotter) order:
         // each leaf's sequence is the previous one with two neighbouring
@@ -578,9 +684,13 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
             const uint32_t tj = sjt_tab<L>(j);
             const uint32_t rj = OSIM_SJT_PIN ? opaque_u32(tj & 0xFFu) : (tj & 0xFFu);
             const uint64_t r = r0 + (uint64_t)rj;  // (the swap below keeps tj uniform)
-            if constexpr (M > 0) ck_load(K, q, ti, s, M);
-            else s.init(base, 0, N);
-            s.seq = cur;
+            if constexpr (M > 0) {
+                s.seq = cur;
+                pk_load(K, q, ti, s, M);
+            } else {
+                s.init(base, 0, N);
+                s.seq = cur;
+            }
             swap_nibbles<kSh0, L>(cur, (int)(tj >> 8));  // the next leaf's sequence
 #else
             // suffix order: for L >= 4 a constant-table load replaces ~35
@@ -596,9 +706,9 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
                 const uint32_t id = (uint32_t)(idx >> (4 * i)) & 0xFu;
                 suf |= ((rem >> (4 * id)) & 0xFull) << (4 * (M + i));
             }
-            if constexpr (M > 0) ck_load(K, q, ti, s, M);
-            else s.init(base, 0, N);
             s.set_seq(pre | suf);
+            if constexpr (M > 0) pk_load(K, q, ti, s, M);
+            else s.init(base, 0, N), s.set_seq(pre | suf);
             const uint64_t r = r0 + (uint64_t)j;
 #endif
             // full steps while any lane of the warp still has an HtD to run, then
@@ -663,7 +773,7 @@ __device__ __forceinline__ void fused_final_reduce(const Part* parts, osim_summa
 }
 
 // dynamic shared memory of the prefix kernels (checkpoint slots + sort)
-constexpr size_t kPfxDynSmem = sizeof(CkSlots<kPfxQ>) + sizeof(PfxSort);
+constexpr size_t kPfxDynSmem = kPfxCkBytes + sizeof(PfxSort);
 
 template <int N, int DMA, bool SIGP2, int L, bool STATS>
 __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const double* __restrict__ durs, double sigma,
@@ -675,8 +785,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
     __shared__ __align__(256) double2 sdr[3 * kStride];  // 256-aligned: FastSim LAYOUT 4
     __shared__ Part sh[32];
     extern __shared__ __align__(16) unsigned char pfx_dsm[];
-    CkSlots<kPfxQ>& K = *reinterpret_cast<CkSlots<kPfxQ>*>(pfx_dsm);
-    PfxSort& S = *reinterpret_cast<PfxSort*>(pfx_dsm + sizeof(CkSlots<kPfxQ>));
+    PfxSort& S = *reinterpret_cast<PfxSort*>(pfx_dsm + kPfxCkBytes);
     stage_dr(durs, N, sdr);
     __syncthreads();
     const uint32_t base = opaque_u32((uint32_t)__cvta_generic_to_shared(sdr));
@@ -702,7 +811,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_pfx(const 
     for (uint64_t pc = p_lo + (cta_call * shards + shard) * kPer; pc < p_hi; pc += stride) {
         const uint64_t pb = pc + half * per;
         const uint64_t pe = pb + per < p_hi ? pb + per : p_hi;
-        if (pb < pe) pfx_leaves<N, DMA, SIGP2, L, STATS, OSIM_PFX_LAYOUT>(base, sigma, rsig, pb, pe, lo, hi, thr, acc, ms_out, lo, K, S);
+        if (pb < pe) pfx_leaves<N, DMA, SIGP2, L, STATS, OSIM_PFX_LAYOUT>(base, sigma, rsig, pb, pe, lo, hi, thr, acc, ms_out, lo, pfx_dsm, S);
     }
     acc = block_reduce(acc, sh);
     if (threadIdx.x == 0) parts[blockIdx.x] = acc;
@@ -716,8 +825,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_batch_pfx(
     __shared__ __align__(256) double2 sdr[3 * kStride];  // 256-aligned: FastSim LAYOUT 4
     __shared__ Part sh[32];
     extern __shared__ __align__(16) unsigned char pfx_dsm[];
-    CkSlots<kPfxQ>& K = *reinterpret_cast<CkSlots<kPfxQ>*>(pfx_dsm);
-    PfxSort& S = *reinterpret_cast<PfxSort*>(pfx_dsm + sizeof(CkSlots<kPfxQ>));
+    PfxSort& S = *reinterpret_cast<PfxSort*>(pfx_dsm + kPfxCkBytes);
     constexpr uint64_t total = Fact<N>::v;
     constexpr uint64_t NP = total / Fact<L>::v;
     constexpr uint64_t kPer = (uint64_t)kPfxQ * kBlock;
@@ -729,7 +837,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_PFX_MINB) k_exhaustive_batch_pfx(
         Part acc;
         part_init(acc);
         for (uint64_t pb = 0; pb < NP; pb += kPer)
-            pfx_leaves<N, DMA, SIGP2, L, false, OSIM_BATCH_LAYOUT>(base, sigma, rsig, pb, NP, 0, total, -kBig, acc, nullptr, 0, K, S);
+            pfx_leaves<N, DMA, SIGP2, L, false, OSIM_BATCH_LAYOUT>(base, sigma, rsig, pb, NP, 0, total, -kBig, acc, nullptr, 0, pfx_dsm, S);
         acc = block_reduce(acc, sh);  // ends with __syncthreads: smem reusable
         if (threadIdx.x == 0) out[b] = part_to_summary(acc);
     }

@@ -517,6 +517,19 @@ struct FastSim {
         idleK = 0.0;
     }
     __device__ __forceinline__ void set_seq(uint64_t sq) { seq = pack_seq(sq); }
+    // {nd, 1/nd} of the K and DtH heads (the running commands, if any) from
+    // the duration rows: restoring a checkpoint that stores only the rems
+    __device__ __forceinline__ void reload_kd() {
+        ld_dc(adr(KO_D, toff(seq, s1)), d1, c1);
+        ld_dc(adr(KO_K, toff(seq, s2)), d2, c2);
+    }
+    __device__ __forceinline__ static void ld_dc(uint32_t addr, double& nd, double& rc) {
+        if constexpr (kLanes) {
+            asm("ld.shared.f64 %0, [%2];\n\tld.shared.f64 %1, [%2+%3];" : "=d"(nd), "=d"(rc) : "r"(addr), "n"(kRcOff));
+        } else {
+            asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(nd), "=d"(rc) : "r"(addr));
+        }
+    }
     static constexpr bool kPre = PRE;
     __device__ __forceinline__ static uint64_t pack_seq(uint64_t sq) { return PRE ? (sq << 4) : sq; }
     // start the HtD at the queue head now (the HtD lane is idle and an HtD
