@@ -545,6 +545,10 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
                                            PfxSort& S) {
     constexpr int M = N - L;
     constexpr bool kC = OSIM_SUBCK && (DMA == 2 || OSIM_SUB_D1);  // compact slots (+ sub-checkpoints)
+    // steps per phase vote in the full phase: 3 measured best for the
+    // cheaper power-of-two-sigma step at n >= 10 (C4 +0.9 %), 2 otherwise
+    // (sigma 0.375: 3 is -1.5 %; C2, n = 8: -0.4 %)
+    constexpr int kPhF = (SIGP2 && N >= 10) ? OSIM_PH_FULL_P2 : OSIM_PH_FULL;
     using CK = typename PfxCkSel<kC>::T;
     constexpr int kCkV = CkNV<CK>::v;
     CK& K = *reinterpret_cast<CK*>(dsm);
@@ -653,7 +657,7 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
                     s.seq = cur;
                     pk_load(K, kPfxQ, ti, s, M + 1);
                     swap_nibbles<kSh1, L1>(cur, (int)(tj >> 8));
-                    s.run_phased(restf, sigma, rsig);
+                    s.template run_phased<true, kPhF>(restf, sigma, rsig);
                     if (all_in || (any_in && r >= lo && r < hi)) {
                         leaf_add<STATS, (N <= 12)>(acc, s.now, r, thr);
                         if constexpr (STATS) {
@@ -716,7 +720,7 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
 #ifdef OSIM_HSTATS
             hstats_replay(s, rest, validP, sigma, rsig);
 #endif
-            s.run_phased(rest, sigma, rsig);
+            s.template run_phased<true, kPhF>(rest, sigma, rsig);
             if (all_in || (any_in && r >= lo && r < hi)) {
                 leaf_add<STATS, (N <= 12)>(acc, s.now, r, thr);
                 if constexpr (STATS) {

@@ -75,6 +75,9 @@ static __constant__ double c_end_eps = 1e-9;
 #ifndef OSIM_PH_KD
 #define OSIM_PH_KD 2
 #endif
+#ifndef OSIM_PH_FULL_P2
+#define OSIM_PH_FULL_P2 3  // the prefix kernels' full phase at power-of-two sigma, n >= 10
+#endif
 #ifndef OSIM_EXPSHIFT
 #define OSIM_EXPSHIFT 1  // FastSim, power-of-two sigma: rate factors as exponent shifts (see step())
 #endif
@@ -678,15 +681,15 @@ struct FastSim {
     // soon as the whole warp has drained its HtD (then K) lanes
     // H0 = false: see step(); the heuristic's candidate replays start the
     // candidate's HtD (the queue's last) before the first step
-    template <bool H0 = true>
+    template <bool H0 = true, int PHF = OSIM_PH_FULL>
     __device__ __forceinline__ void run_phased(int rest, double sigma, double rsig) {
         int st = 0;
         if constexpr (DMA == 2) {
 #pragma unroll 1
-            for (; st < rest; st += OSIM_PH_FULL) {
+            for (; st < rest; st += PHF) {
                 if (__all_sync(0xffffffffu, s0 >= n4)) break;
 #pragma unroll
-                for (int r = 0; r < OSIM_PH_FULL; ++r) step<H0>(sigma, rsig);
+                for (int r = 0; r < PHF; ++r) step<H0>(sigma, rsig);
             }
 #pragma unroll 1
             for (; st < rest; st += OSIM_PH_KD) {
