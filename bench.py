@@ -424,9 +424,11 @@ def run_secondary(a, D, torch, dev, sp, flush, ops, peak_ops, L):
         d4 = synth.c4_group()
         _capi.exhaustive_stats(d4, 2, 0.5, 0, TOTAL12, threshold=60.0)  # warm-up (allocates 3.8 GB)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        st4, below4, med4 = _capi.exhaustive_stats(d4, 2, 0.5, 0, TOTAL12, threshold=60.0)
-        tw = time.perf_counter() - t0
+        tw = float("inf")
+        for _ in range(3):  # host wall clock of single calls: the best of three
+            t0 = time.perf_counter()
+            st4, below4, med4 = _capi.exhaustive_stats(d4, 2, 0.5, 0, TOTAL12, threshold=60.0)
+            tw = min(tw, time.perf_counter() - t0)
         out["c4_full_stats"] = {"value": TOTAL12 / tw, "unit": "orderings/s", "seconds": tw,
                                 "workload": "C4 12! with exact median (radix selection over 3.8 GB of makespans "
                                             "in HBM) and count below 60 ms, host API wall clock",
