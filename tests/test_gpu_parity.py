@@ -21,7 +21,9 @@ REL = 1e-12
 
 def assert_summary_vs_oracle(s, o):
     assert s["count"] == o["count"]
-    assert s["best"] == o["best"] and s["best_rank"] == o["best_rank"]
+    # an empty range (a shard with no calls, e.g. under an OSIM_PFX_L override)
+    # has no argmin: only the identities are compared
+    assert s["best"] == o["best"] and (s["count"] == 0 or s["best_rank"] == o["best_rank"])
     assert s["worst"] == o["worst"]
     assert close(s["sum"], o["sum"], REL)
     assert close(s["sum_log"], o["sum_log"], REL)
