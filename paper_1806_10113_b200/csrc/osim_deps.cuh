@@ -440,6 +440,9 @@ __device__ __forceinline__ void run_tasks(uint64_t lab, int N, int M, int n, uin
     }
 }
 
+#ifndef OSIM_F1_LEAN
+#define OSIM_F1_LEAN 1
+#endif
 template <bool SIGP2, bool PRE>
 __global__ void __launch_bounds__(kBlock, OSIM_F1_MINB) k_interleave_pfx(const double* __restrict__ durs, int T, int N,
                                                            double sigma, uint64_t lo, uint64_t hi, uint64_t mtotal,
@@ -500,6 +503,18 @@ __global__ void __launch_bounds__(kBlock, OSIM_F1_MINB) k_interleave_pfx(const d
             ck_load(ck, 0, e, s, M);
             s.set_seq(order);
             s.dseq = PRE ? (dseq << 4) : dseq;
+#if OSIM_F1_LEAN
+            s.template run_phased<true, SIGP2 ? OSIM_PH_FULL_P2 : OSIM_PH_FULL>(rest, sigma, rsig);
+            const uint64_t r = r0 + (uint64_t)q;
+            if (valid && r < r1) {
+                if (!s.drained()) atomicExch(err, OSIM_ESTALL);
+                leaf_add<true>(acc, s.now, r, thr);  // the prefix kernels' leaf (see there)
+                acc.count += 1;
+                if (ms_out) ms_out[r - lo] = s.now;
+            }
+            // exponent split-off every 8 sequences (fast-path makespans: see pfx_leaves)
+            if ((q & 7) == 7 || q == K - 1) renorm<false>(acc.lpm, acc.lpe);
+#else
             s.run_phased(rest, sigma, rsig);
             const uint64_t r = r0 + (uint64_t)q;
             if (valid && r < r1) {
@@ -507,6 +522,7 @@ __global__ void __launch_bounds__(kBlock, OSIM_F1_MINB) k_interleave_pfx(const d
                 part_add<true>(acc, s.now, r, thr);
                 if (ms_out) ms_out[r - lo] = s.now;
             }
+#endif
         }
     }
     acc = block_reduce(acc, sh);
