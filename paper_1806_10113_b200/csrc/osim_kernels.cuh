@@ -356,6 +356,9 @@ constexpr int kPfxQ = 2;  // prefixes per thread and prefix-kernel call
 #ifndef OSIM_SUB_D1
 #define OSIM_SUB_D1 0     // ... and on 1-DMA devices
 #endif
+#ifndef OSIM_SUB_SNAP
+#define OSIM_SUB_SNAP 1   // the sub-checkpoint is stored by the group's first leaf (no separate advance)
+#endif
 // Checkpoint slots of the prefix kernels, two kinds.  Full (CkSlots): the
 // clock, the K/DtH rems and their {nd, 1/nd} (7 doubles + 2 ints per slot).
 // Compact (PfxCkC, 2-DMA when OSIM_SUBCK): only the clock, the rems and the
@@ -644,20 +647,43 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
                 const uint64_t others = (rem & lowm) | ((rem >> (4 * (f + 1))) << (4 * f));  // ascending
                 const uint64_t suf = ((rem >> (4 * f)) & 0xFull) | (others << 4);
                 uint64_t cur = FS::pack_seq(pre | (suf << (4 * M)));
+#if OSIM_SUB_SNAP
+                // the group's first leaf replays from the prefix checkpoint and
+                // leaves the sub-checkpoint behind as it passes it
+                int af = 0;
+                int restf = rest;
+#else
                 s.seq = cur;
                 pk_load(K, q, ti, s, M);
                 const int af = advance_to(s, validP ? M + 1 : 0, sigma, rsig);
                 pk_store(K, kPfxQ, ti, s);
                 const int restf = 3 * N - __reduce_min_sync(kFull, validP ? sa[q] + af : 3 * N);
+#endif
 #pragma unroll 1
                 for (int j = 0; j < (int)LF1; ++j) {
                     const uint32_t tj = sjt_tab<L1>(j);
                     const int lj = f * (int)LF1 + (int)(tj & 0xFFu);  // lexicographic leaf index
                     const uint64_t r = r0 + (uint64_t)(OSIM_SJT_PIN ? opaque_u32((uint32_t)lj) : (uint32_t)lj);
                     s.seq = cur;
+#if OSIM_SUB_SNAP
+                    if (j == 0) {
+                        pk_load(K, q, ti, s, M);
+                        swap_nibbles<kSh1, L1>(cur, (int)(tj >> 8));
+                        s.template run_phased_snap<kPhF>(rest, sigma, rsig, M + 1, [&](int stp) {
+                            pk_store(K, kPfxQ, ti, s);
+                            af = stp;
+                        });
+                    } else {
+                        if (j == 1) restf = 3 * N - __reduce_min_sync(kFull, validP ? sa[q] + af : 3 * N);
+                        pk_load(K, kPfxQ, ti, s, M + 1);
+                        swap_nibbles<kSh1, L1>(cur, (int)(tj >> 8));
+                        s.template run_phased<true, kPhF>(restf, sigma, rsig);
+                    }
+#else
                     pk_load(K, kPfxQ, ti, s, M + 1);
                     swap_nibbles<kSh1, L1>(cur, (int)(tj >> 8));
                     s.template run_phased<true, kPhF>(restf, sigma, rsig);
+#endif
                     if (all_in || (any_in && r >= lo && r < hi)) {
                         leaf_add<STATS, (N <= 12)>(acc, s.now, r, thr);
                         if constexpr (STATS) {

@@ -677,6 +677,36 @@ struct FastSim {
         s0 += f0 ? 4 : 0;
     }
 
+    // run_phased (2-DMA) that also calls snap(steps so far) right after the
+    // step in which this lane's HtD count reaches `target` (the state a
+    // lock-step advance_to(target) would stop at)
+    template <int PHF, class F>
+    __device__ __forceinline__ void run_phased_snap(int rest, double sigma, double rsig, int target, F&& snap) {
+        static_assert(DMA == 2, "2-DMA only");
+        int st = 0;
+        bool got = false;
+#pragma unroll 1
+        for (; st < rest; st += PHF) {
+            if (__all_sync(0xffffffffu, s0 >= n4)) break;
+#pragma unroll
+            for (int r = 0; r < PHF; ++r) {
+                step<true>(sigma, rsig);
+                if (!got && (s0 >> 2) == target) {
+                    got = true;
+                    snap(st + r + 1);
+                }
+            }
+        }
+#pragma unroll 1
+        for (; st < rest; st += OSIM_PH_KD) {
+            if (__all_sync(0xffffffffu, s2 >= n4)) break;
+#pragma unroll
+            for (int r = 0; r < OSIM_PH_KD; ++r) step_kd();
+        }
+#pragma unroll 2
+        for (; st < rest; ++st) step_d();
+    }
+
     // `rest` steps in warp lock-step, switching to the specialized steps as
     // soon as the whole warp has drained its HtD (then K) lanes
     // H0 = false: see step(); the heuristic's candidate replays start the
