@@ -682,14 +682,14 @@ struct FastSim {
     // lock-step advance_to(target) would stop at)
     template <int PHF, class F>
     __device__ __forceinline__ void run_phased_snap(int rest, double sigma, double rsig, int target, F&& snap) {
-        static_assert(DMA == 2, "2-DMA only");
+        constexpr int kF = DMA == 2 ? PHF : 2;  // full steps per vote
         int st = 0;
         bool got = false;
 #pragma unroll 1
-        for (; st < rest; st += PHF) {
+        for (; st < rest; st += kF) {
             if (__all_sync(0xffffffffu, s0 >= n4)) break;
 #pragma unroll
-            for (int r = 0; r < PHF; ++r) {
+            for (int r = 0; r < kF; ++r) {
                 step<true>(sigma, rsig);
                 if (!got && (s0 >> 2) == target) {
                     got = true;
@@ -697,14 +697,25 @@ struct FastSim {
                 }
             }
         }
+        if constexpr (DMA == 2) {
 #pragma unroll 1
-        for (; st < rest; st += OSIM_PH_KD) {
-            if (__all_sync(0xffffffffu, s2 >= n4)) break;
+            for (; st < rest; st += OSIM_PH_KD) {
+                if (__all_sync(0xffffffffu, s2 >= n4)) break;
 #pragma unroll
-            for (int r = 0; r < OSIM_PH_KD; ++r) step_kd();
-        }
+                for (int r = 0; r < OSIM_PH_KD; ++r) step_kd();
+            }
 #pragma unroll 2
-        for (; st < rest; ++st) step_d();
+            for (; st < rest; ++st) step_d();
+        } else {
+#pragma unroll 1
+            for (; st < rest; st += 2) {
+                if (__all_sync(0xffffffffu, s2 >= n4)) break;
+                step_1d();
+                step_1d();
+            }
+#pragma unroll 2
+            for (; st < rest; ++st) step_1dd();
+        }
     }
 
     // `rest` steps in warp lock-step, switching to the specialized steps as
