@@ -634,9 +634,10 @@ __device__ __forceinline__ void pfx_leaves(uint32_t base, double sigma, double r
         if (any_in) acc.count += (r0 + LF < hi ? r0 + LF : hi) - (r0 > lo ? r0 : lo);
         // sub-checkpoints: the (L-1)! leaves that share the first suffix task
         // f also share the replay up to f's HtD finalize, so it runs once per
-        // f (lock-step advance, stored in the thread's sub slot) and each
-        // leaf replays only from there; the L-1 later tasks in adjacent-swap
-        // order, ranks f * (L-1)! + the table's
+        // f -- the group's first leaf stores the state in the thread's sub
+        // slot as it passes it (OSIM_SUB_SNAP; else a lock-step advance) --
+        // and the other leaves replay only from there; the L-1 later tasks in
+        // adjacent-swap order, ranks f * (L-1)! + the table's
         if constexpr (kC && L >= 3 && M > 0 && N >= OSIM_SUB_MINN) {
             constexpr int L1 = L - 1;
             constexpr uint64_t LF1 = Fact<L1>::v;
