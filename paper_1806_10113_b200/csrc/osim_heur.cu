@@ -22,7 +22,8 @@ namespace osim {
 // input runs 4.4 % faster on the 2-DMA profiles, but the key pass, the sort
 // and the permuted group loads cost about as much (measured +0.4 % / +0.2 %,
 // and -4 % on the 1-DMA profile).  nullptr = batch order.
-static const uint32_t* heur_group_order(const LaunchCfg& cfg, const double* d_durs, uint64_t B, int n) {
+static const uint32_t* heur_group_order(const LaunchCfg& cfg, const double* d_durs, uint64_t B, int n,
+                                        size_t skip, char** base) {
     static const bool on = [] {
         const char* e = std::getenv("OSIM_HEUR_SORT");
         return e ? std::atoi(e) != 0 : false;
@@ -32,8 +33,10 @@ static const uint32_t* heur_group_order(const LaunchCfg& cfg, const double* d_du
     cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const uint8_t*)nullptr, (uint8_t*)nullptr,
                                     (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)B, 0, 8, cfg.st);
     const size_t a8 = (B + 255) & ~size_t(255), a32 = (4 * B + 255) & ~size_t(255);
-    char* p = (char*)aux_get(cfg.aux, 2 * a8 + 2 * a32 + tmp, cfg.st);
+    char* p = (char*)aux_get(cfg.aux, skip + 2 * a8 + 2 * a32 + tmp, cfg.st);
     if (!p) return nullptr;
+    *base = p;
+    p += skip;
     uint8_t* k_in = (uint8_t*)p;
     uint8_t* k_out = k_in + a8;
     uint32_t* i_in = (uint32_t*)(p + 2 * a8);
@@ -61,14 +64,20 @@ void heuristic_launch(int dma, int mode, const LaunchCfg& cfg, const double* d_d
     if (mode == 1 && lane_kernel()) {
         const unsigned gl = (unsigned)((B + kHLW * kHLGPW - 1) / (kHLW * kHLGPW));
         const size_t sml = kHLW * kHLWarpSmem;
-        const uint32_t* perm = heur_group_order(cfg, d_durs, B, n);
+        // LAYOUT 6: {t_htd, 1/t_htd} per task in the aux buffer ahead of the
+        // sort's arrays (nullptr: the kernel loads and divides per candidate)
+        const size_t hrb = (kHLLay == 6 && OSIM_HL_HR) ? ((B * 16 * sizeof(double2) + 255) & ~size_t(255)) : 0;
+        char* abase = nullptr;
+        const uint32_t* perm = heur_group_order(cfg, d_durs, B, n, hrb, &abase);
+        if (hrb && !abase) abase = (char*)aux_get(cfg.aux, hrb, cfg.st);
+        double2* hr = hrb ? (double2*)abase : nullptr;
         int e;
         const bool sp2 = std::frexp(sigma, &e) == 0.5;
 #define OSIM_HLN(D, P)                                                                               \
     do {                                                                                             \
         auto kf = k_heuristic_lane<D, P>;                                                            \
         cached_ctas_per_sm((const void*)kf, kHLT, sml); /* opts in to > 48 KB dynamic smem */        \
-        kf<<<gl, kHLT, sml, cfg.st>>>(d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms, d_ns, perm); \
+        kf<<<gl, kHLT, sml, cfg.st>>>(d_durs, d_idr, B, n, sigma, sum_mode, d_order, d_ms, d_ns, perm, hr); \
     } while (0)
         if (dma == 2) { if (sp2) OSIM_HLN(2, true); else OSIM_HLN(2, false); }
         else OSIM_HLN(1, false);

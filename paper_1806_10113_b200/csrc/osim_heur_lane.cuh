@@ -40,6 +40,9 @@ constexpr int kHLGPW = 32 / kHLLPG;  // groups per warp
 #ifndef OSIM_HL_LAYOUT
 #define OSIM_HL_LAYOUT 6
 #endif
+#ifndef OSIM_HL_HR
+#define OSIM_HL_HR 1  // LAYOUT 6: {t_htd, 1/t_htd} pairs staged in global scratch
+#endif
 // FastSim layout: 2 (all three kinds in shared memory) or 6 (K and DtH in
 // shared memory, a candidate's HtD durations loaded from global memory)
 constexpr int kHLLay = kHLLPG == 1 ? OSIM_HL_LAYOUT : 3;
@@ -143,7 +146,8 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
                                                          uint8_t* __restrict__ order_out,
                                                          double* __restrict__ ms_out,
                                                          uint32_t* __restrict__ nsims_out,
-                                                         const uint32_t* __restrict__ perm) {
+                                                         const uint32_t* __restrict__ perm,
+                                                         double2* __restrict__ hr) {
     using FS = FastSim<DMA, SP2, true, false, false, kHLLay>;
     constexpr bool kRH = kHLLay == 6;
     constexpr int kK0 = kRH ? 1 : 0;  // first kind held in shared memory
@@ -178,6 +182,20 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
     auto DV = [&](int k, int t) { return nd[((k - kK0) * 16 + t) * W + lane]; };
     const double* gH = durs + g * 3 * (uint64_t)n;  // LAYOUT 6: HtD durations of task t at gH[3t]
     auto HV = [&](int t) { return kRH ? ((live && t < n) ? gH[3 * t] : 1.0) : DV(0, t); };
+    // a candidate's HtD {nd, 1/nd}: from the staged pairs (hr), else loaded
+    // and divided here
+    double2* hrg = hr ? hr + g * 16 : nullptr;
+    if (kRH && hrg && live) {
+        for (int t = 0; t < n; ++t) {
+            const double h = gH[3 * t];
+            hrg[t] = make_double2(h, __ddiv_rn(1.0, h));
+        }
+    }
+    auto HR = [&](int t) {
+        if (hrg && live) return hrg[t];
+        const double h = HV(t);
+        return make_double2(h, __ddiv_rn(1.0, h));
+    };
     uint64_t idr = 0;  // id rank per task, 4 bits each
     for (int t = 0; t < n; ++t) idr |= (uint64_t)(live ? id_rank[g * (uint64_t)n + t] : (uint8_t)t) << (4 * t);
     auto IR = [&](int t) { return (int)((idr >> (4 * t)) & 0xF); };
@@ -237,7 +255,7 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
                 cc[i] = rt_at(cand, cj[i]);
                 sim[i].init(base, ot | ((uint64_t)cc[i] << (4 * k)), k + 1);
                 sim[i].load(ck);
-                if constexpr (kRH) { const double h = HV(cc[i]); sim[i].set_htd(h, __ddiv_rn(1.0, h)); }
+                if constexpr (kRH) { const double2 h = HR(cc[i]); sim[i].set_htd(h.x, h.y); }
                 sim[i].start_htd();
             }
             run_multi<false>(sim, rest, sigma, rsig);
@@ -321,7 +339,7 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
         FS s;
         s.init(base, ot, k + 1);
         s.load(ck);
-        if constexpr (kRH) { const double h = HV(c); s.set_htd(h, __ddiv_rn(1.0, h)); }
+        if constexpr (kRH) { const double2 h = HR(c); s.set_htd(h.x, h.y); }
         s.start_htd();  // the chosen task's HtD, the queue's last
         if constexpr (DMA == 2) {
             for (int q = 0; q < 3 * kMaxN && s.htd_done() < k + 1; ++q) s.template step<false>(sigma, rsig);
@@ -342,9 +360,9 @@ __global__ void __launch_bounds__(kHLT) k_heuristic_lane(const double* __restric
         sp[0].load(ck);
         sp[1].load(ck);
         if constexpr (kRH) {  // the two queued HtDs, in each ordering's order
-            const double ha = HV(a), hb = HV(b), ra = __ddiv_rn(1.0, ha), rb = __ddiv_rn(1.0, hb);
-            sp[0].set_htd(ha, ra, hb, rb);
-            sp[1].set_htd(hb, rb, ha, ra);
+            const double2 pa = HR(a), pb = HR(b);
+            sp[0].set_htd(pa.x, pa.y, pb.x, pb.y);
+            sp[1].set_htd(pb.x, pb.y, pa.x, pa.y);
         }
         const int rest = __reduce_max_sync(kFull, 3 * n - sp[0].finalized());
         run_multi<true>(sp, rest, sigma, rsig);
