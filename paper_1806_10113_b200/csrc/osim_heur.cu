@@ -70,7 +70,11 @@ void heuristic_launch(int dma, int mode, const LaunchCfg& cfg, const double* d_d
         char* abase = nullptr;
         const uint32_t* perm = heur_group_order(cfg, d_durs, B, n, hrb, &abase);
         if (hrb && !abase) abase = (char*)aux_get(cfg.aux, hrb, cfg.st);
-        double2* hr = hrb ? (double2*)abase : nullptr;
+        static const bool no_hr = [] {  // OSIM_HL_NO_HR=1: test hook for the kernel's fallback path
+            const char* e = std::getenv("OSIM_HL_NO_HR");
+            return e && std::atoi(e) != 0;
+        }();
+        double2* hr = (hrb && !no_hr) ? (double2*)abase : nullptr;
         int e;
         const bool sp2 = std::frexp(sigma, &e) == 0.5;
 #define OSIM_HLN(D, P)                                                                               \

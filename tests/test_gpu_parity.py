@@ -243,6 +243,37 @@ def test_c5_heuristic_vs_oracle_many(profile):
     assert np.array_equal(sims, o_sims)
 
 
+_HR_CHILD = """
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1806_10113_b200 as osim
+from paper_1806_10113_b200 import _capi, synth
+for prof in ("nvidia", "amd", "phi"):
+    d, r = synth.c5_batch_fast(prof, 50_000)
+    _, dma, sigma = synth.PROFILES[prof]
+    o, m, n = _capi.heuristic_batch(d, r, dma, sigma, osim.SUM_MODE)
+    print(prof, hashlib.sha256(o.tobytes() + m.tobytes() + n.tobytes()).hexdigest())
+"""
+
+
+def test_heuristic_lane_htd_pair_fallback():
+    """k_heuristic_lane reads each candidate's {t_htd, 1/t_htd} from pairs it
+    staged in the launcher's aux buffer; without the buffer it loads and
+    divides per candidate.  OSIM_HL_NO_HR=1 forces that path: same outputs."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for v in ("0", "1"):
+        r = subprocess.run([sys.executable, "-c", _HR_CHILD, root], env=dict(os.environ, OSIM_HL_NO_HR=v),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        outs.append([ln for ln in r.stdout.splitlines() if ln.split(" ")[0] in ("nvidia", "amd", "phi")])
+    assert len(outs[0]) == 3 and outs[0] == outs[1]
+
+
 def test_heuristic_random_goldens():
     g = load("heuristic_random.json")
     for c in g["cases"]:
