@@ -594,8 +594,10 @@ int osim_shutdown(void) {
         cudaSetDevice(c->dev);
         cudaDeviceSynchronize();
         if (c->scratch) cudaFree(c->scratch);
-        for (AuxBuf& a : c->aux)
+        for (AuxBuf& a : c->aux) {
             if (a.p) cudaFree(a.p);
+            if (a.ev) cudaEventDestroy(a.ev);
+        }
         if (c->d_err) cudaFree(c->d_err);
         if (c->d_done) cudaFree(c->d_done);
         if (c->stream) cudaStreamDestroy(c->stream);

@@ -86,6 +86,7 @@ void heuristic_launch(int dma, int mode, const LaunchCfg& cfg, const double* d_d
         if (dma == 2) { if (sp2) OSIM_HLN(2, true); else OSIM_HLN(2, false); }
         else OSIM_HLN(1, false);
 #undef OSIM_HLN
+        if (hr || perm) aux_done(cfg.aux, cfg.st);
         return;
     }
     if (mode == 1) {

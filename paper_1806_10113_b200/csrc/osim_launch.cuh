@@ -14,16 +14,22 @@
 
 namespace osim {
 
-// Grow-only device buffer for a launcher's own temporaries (one per device
-// stream; the caller holds the device lock).  Growing waits for the stream
-// (the old buffer may still be read by earlier work on it).
+// Grow-only device buffer for a launcher's own temporaries (one per library
+// stream; the caller holds the device lock).  Work that used it is marked by
+// an event (aux_done), and the next user -- on any stream, e.g. a _dev call's
+// own stream -- waits for that event first; growing waits for it and for the
+// stream (the old buffer may still be read).
 struct AuxBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    cudaEvent_t ev = nullptr;
+    bool pending = false;
 };
 inline void* aux_get(AuxBuf* a, size_t bytes, cudaStream_t st) {
     if (!a) return nullptr;
+    if (a->pending) cudaStreamWaitEvent(st, a->ev, 0);
     if (bytes > a->bytes) {
+        if (a->pending) cudaEventSynchronize(a->ev);
         cudaStreamSynchronize(st);
         if (a->p) cudaFree(a->p);
         a->p = nullptr;
@@ -36,6 +42,18 @@ inline void* aux_get(AuxBuf* a, size_t bytes, cudaStream_t st) {
         a->bytes = want;
     }
     return a->p;
+}
+
+// the work using the buffer has been enqueued on `st`
+inline void aux_done(AuxBuf* a, cudaStream_t st) {
+    if (!a || !a->p) return;
+    if (!a->ev && cudaEventCreateWithFlags(&a->ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        cudaStreamSynchronize(st);  // no event: finish the work instead
+        return;
+    }
+    cudaEventRecord(a->ev, st);
+    a->pending = true;
 }
 
 struct LaunchCfg {
